@@ -1,0 +1,249 @@
+"""MASQuant hot-path ORACLE — plain, slow, obviously-correct CPU reference.
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` leg may import or execute anything under
+oracle/.  The product path (paper_2603_04800_b200/) never imports it and shares
+no code with it (no kernels, helpers, tables or constants).
+
+Precision contract:
+  * Integer-valued parts (ranges R, factors s, codes, scales Delta, integer
+    accumulators) follow a FIXED float32 operation sequence (IEEE mul / div /
+    sqrt, no fused multiply-add), so the GPU path must match them bit-exactly.
+  * Float parts (dequantized outputs, the CMC term, the loss) are evaluated in
+    float64 from the exact f32 / bf16 input values.
+
+Every function cites the passage it follows.  Pins: tests/test_oracle_pins.py.
+Parity pinned for every function below (no "parity unpinned" entries): the
+closed forms, brute-force, invariance and identity checks listed in
+DESIGN.md §"Oracle pins".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+F32 = np.float32
+F64 = np.float64
+FLOOR = np.float32(1e-12)          # SPEC.md:131, 164, 292 (Delta and s floors), reading Q7
+
+
+# --------------------------------------------------------------------------- inputs
+def decode(a: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> exact float32; float32 passes through."""
+    a = np.asarray(a)
+    if a.dtype == np.uint16:
+        return (a.astype(np.uint32) << 16).view(np.float32)
+    return a.astype(np.float32, copy=False)
+
+
+def _check_ids(ids: np.ndarray, n_mod: int) -> np.ndarray:
+    ids = np.asarray(ids).astype(np.int64)
+    if ids.size and (ids.min() < 0 or ids.max() >= n_mod):
+        raise ValueError("token tagged with unknown modality")
+    return ids
+
+
+# --------------------------------------------------------------------------- O1
+def calibrate_stats(X, ids, n_mod: int, R=None, count=None):
+    """O1 — per-modality per-channel range R^m_i = max_t |x^m_{t,i}| and token counts.
+
+    PAPER.md:35 (§4.1 "we measure the activation range per channel"),
+    SPEC.md:196-204, 274-277 (running max over stored batches).
+    R / count, when given, are the running state (batch coherence).
+    """
+    X = decode(X)
+    ids = _check_ids(ids, n_mod)
+    T, d = X.shape
+    R = np.zeros((n_mod, d), F32) if R is None else np.array(R, F32, copy=True)
+    count = np.zeros(n_mod, np.int64) if count is None else np.array(count, np.int64, copy=True)
+    for m in range(n_mod):
+        rows = X[ids == m]
+        if rows.shape[0]:
+            R[m] = np.maximum(R[m], np.abs(rows).max(axis=0))
+        count[m] += rows.shape[0]
+    return R, count
+
+
+# --------------------------------------------------------------------------- O2
+def weight_absmax(W) -> np.ndarray:
+    """max_j |w_{j,i}| for every input channel i (reading Q8: W is
+    D_in x D_out, so this is the max over row i of W)."""
+    return np.abs(decode(W)).max(axis=1).astype(F32)
+
+
+def init_factors(R, count, W) -> np.ndarray:
+    """O2 — s^m_i = sqrt( max_t|x^m_{t,i}| / max_j|w_{j,i}| )   (§4.2).
+
+    f32 sequence: sqrt( div( max(R,1e-12f), max(wmax,1e-12f) ) ) (Q6/Q7).
+    A modality with zero calibration tokens is rejected.
+    """
+    R = np.asarray(R, F32)
+    if (np.asarray(count) == 0).any():
+        raise ValueError("modality with zero calibration tokens")
+    wmax = weight_absmax(W)
+    num = np.maximum(R, FLOOR)
+    den = np.maximum(wmax, FLOOR)[None, :]
+    return np.sqrt(np.divide(num, den, dtype=F32), dtype=F32)
+
+
+# --------------------------------------------------------------------------- Q
+def rha(v: np.ndarray) -> np.ndarray:
+    """Round half away from zero (reading Q5; "rounding-to-nearest").
+    trunc(v) + sign(v)*[|v - trunc(v)| >= 0.5]; v - trunc(v) is exact in f32."""
+    v = np.asarray(v, F32)
+    t = np.trunc(v)
+    frac = np.abs(v - t)
+    return (t + np.where(frac >= F32(0.5), np.sign(v), F32(0))).astype(F32)
+
+
+def quantize_rows(A, bits: int):
+    """Symmetric per-row uniform quantizer, z = 0 (PAPER.md:241-245 Eq. PTQ; Q3, Q4).
+
+    Delta = max( div(max_i |a_i|, q_max), 1e-12f ),  q = clamp(rha(div(a, Delta)), -2^{b-1}, 2^{b-1}-1)
+    Returns (codes int8 [rows x cols], Delta f32 [rows]).
+    """
+    if not (2 <= bits <= 8):
+        raise ValueError("bits must be in [2, 8] on this path")
+    A = np.asarray(A, F32)
+    qmax = F32(2 ** (bits - 1) - 1)
+    qmin = F32(-(2 ** (bits - 1)))
+    amax = np.abs(A).max(axis=1) if A.shape[1] else np.zeros(A.shape[0], F32)
+    delta = np.maximum(np.divide(amax, qmax, dtype=F32), FLOOR)
+    v = np.divide(A, delta[:, None], dtype=F32)
+    codes = np.clip(rha(v), qmin, qmax).astype(np.int8)
+    return codes, delta.astype(F32)
+
+
+def dequantize_rows(codes, delta) -> np.ndarray:
+    """Q(x) = code * Delta (PAPER.md:244 with z = 0), in f64."""
+    return np.asarray(codes, F64) * np.asarray(delta, F64)[:, None]
+
+
+# --------------------------------------------------------------------------- O3
+def quantize_weight(W, s, wbits: int):
+    """O3 — Q(S W) per OUTPUT channel (reading Q1), stored K-major: qw [n x d].
+
+    ws[i,j] = f32 mul(s_i, W[i,j])  (S W, PAPER.md:129 / 180-183 with S_t; PAPER.md:69 with S_m)
+    Delta_w[j] = max(div(max_i |ws[i,j]|, q_w), 1e-12f); codes = clamp(rha(div(ws, Delta_w[j]))).
+    """
+    Wf = decode(W)
+    s = np.asarray(s, F32)
+    ws = np.multiply(s[:, None], Wf, dtype=F32)          # [d x n]
+    return quantize_rows(np.ascontiguousarray(ws.T), wbits)   # rows = output channels
+
+
+# --------------------------------------------------------------------------- O4
+def smooth_activations(X, ids, s) -> np.ndarray:
+    """X_m S_m^{-1} row by row: xs[t,i] = f32 mul(x[t,i], f32 div(1, s[m_t, i]))
+    (reading Q6: S^{-1} applied as multiplication by the f32 reciprocal)."""
+    Xf = decode(X)
+    s = np.asarray(s, F32)
+    ids = _check_ids(ids, s.shape[0])
+    inv = np.divide(F32(1.0), s, dtype=F32)
+    return np.multiply(Xf, inv[ids], dtype=F32)
+
+
+def quantize_activations(X, ids, s, abits: int):
+    """O4 — Q(X_m S_m^{-1}) per token, dynamic symmetric (PAPER.md:76 per-token Delta_t; Q2).
+    Returns (qx int8 [T x d], Delta_x f32 [T])."""
+    return quantize_rows(smooth_activations(X, ids, s), abits)
+
+
+# --------------------------------------------------------------------------- O5 / O6
+def int_gemm(qx, qw) -> np.ndarray:
+    """O5 — acc[t,j] = sum_i qx[t,i] * qw[j,i], exact (every partial sum < 2^53, so f64 BLAS
+    on integer-valued matrices is exact; pinned against an int64 triple loop)."""
+    acc = np.asarray(qx, F64) @ np.asarray(qw, F64).T
+    return acc.astype(np.int64)
+
+
+def dequant_output(acc, dx, dw) -> np.ndarray:
+    """O6 — Q(X S^-1) . Q(S W) = acc * Delta_x[t] * Delta_w[j], in f64."""
+    return np.asarray(acc, F64) * np.asarray(dx, F64)[:, None] * np.asarray(dw, F64)[None, :]
+
+
+# --------------------------------------------------------------------------- O7
+def _values_f64(a) -> np.ndarray:
+    """bf16 bits -> exact values; any float array kept at its own precision (as f64)."""
+    a = np.asarray(a)
+    return np.asarray(decode(a) if a.dtype == np.uint16 else a, F64)
+
+
+def cmc_term(xs_rows, L1m, L2m) -> np.ndarray:
+    """X_m S_m^{-1} . L1^m L2^m in f64 (full precision)."""
+    return (np.asarray(xs_rows, F64) @ _values_f64(L1m)) @ _values_f64(L2m)
+
+
+def linear_forward(X, ids, s, qw, dw, abits: int, L1=None, L2=None, rows=None) -> np.ndarray:
+    """O4-O7 — the routed inference equation:
+
+        Y_t = Q(x_t S_{m}^{-1}) . Q(S_t W)                              m = text (id 0)
+        Y_t = Q(x_t S_{m}^{-1}) . Q(S_t W) + x_t S_m^{-1} . L1^m L2^m    m != text
+
+    qw/dw are Q(S_text W) (output of quantize_weight with s[0]).  L1[m-1], L2[m-1] are the
+    correction factors of modality m (bf16 bits or any float array); None => rank 0.
+    rows: optional subset of token indices (per-token quantization is row-local).
+    Output f64 [len(rows) x n] in the given token order.
+    """
+    Xf = decode(X)
+    ids = _check_ids(ids, np.asarray(s).shape[0])
+    if rows is not None:
+        rows = np.asarray(rows, np.int64)
+        Xf, ids = Xf[rows], ids[rows]
+    xs = smooth_activations(Xf, ids, s)
+    qx, dx = quantize_rows(xs, abits)
+    Y = dequant_output(int_gemm(qx, qw), dx, dw)
+    if L1 is not None and L2 is not None:
+        for m in range(1, np.asarray(s).shape[0]):
+            sel = np.nonzero(ids == m)[0]
+            if sel.size:
+                Y[sel] += cmc_term(xs[sel], L1[m - 1], L2[m - 1])
+    return Y
+
+
+# --------------------------------------------------------------------------- O8
+def reference_output(X, W, rows=None) -> np.ndarray:
+    """X W in f64 from the exact inputs ("X_m W"; reading Q16)."""
+    Xf = decode(X)
+    if rows is not None:
+        Xf = Xf[np.asarray(rows, np.int64)]
+    return np.asarray(Xf, F64) @ np.asarray(decode(W), F64)
+
+
+def calib_loss(X, ids, s, W, wbits: int, abits: int, lam=None, rows=None, Yref=None):
+    """O8 — per-modality sums of |Q(X_m S_m^-1) . Q(S_m W) - X_m W| (Eq. mas_quant),
+    counts, and L = sum_m lambda_m * MAE_m with MAE_m = sum_m / (count_m * n) (reading Q9;
+    lambda default 1.0).  Each modality uses its OWN weight Q(S_m W) (Q12).
+    Modalities with zero tokens contribute 0.  Returns (sums f64 [M], counts i64 [M], loss f64).
+    """
+    s = np.asarray(s, F32)
+    n_mod = s.shape[0]
+    Xf = decode(X)
+    ids = _check_ids(ids, n_mod)
+    if rows is not None:
+        rows = np.asarray(rows, np.int64)
+        Xf, ids = Xf[rows], ids[rows]
+    lam = np.ones(n_mod) if lam is None else np.asarray(lam, F64)
+    Yr = reference_output(Xf, W) if Yref is None else np.asarray(Yref, F64)
+    n = Yr.shape[1]
+    qx, dx = quantize_activations(Xf, ids, s, abits)
+    sums = np.zeros(n_mod, F64)
+    counts = np.zeros(n_mod, np.int64)
+    for m in range(n_mod):
+        sel = np.nonzero(ids == m)[0]
+        counts[m] = sel.size
+        if not sel.size:
+            continue
+        qw, dw = quantize_weight(W, s[m], wbits)
+        yq = dequant_output(int_gemm(qx[sel], qw), dx[sel], dw)
+        sums[m] = np.abs(yq - Yr[sel]).sum()
+    loss = loss_finalize(sums, counts, lam, n)
+    return sums, counts, loss
+
+
+def loss_finalize(sums, counts, lam, n: int) -> float:
+    """L = sum_m lambda_m * sums_m / (counts_m * n) over modalities with tokens."""
+    loss = 0.0
+    for m in range(len(sums)):
+        if counts[m] > 0:
+            loss += float(lam[m]) * float(sums[m]) / (float(counts[m]) * n)
+    return loss

@@ -1,0 +1,354 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (no GPU).
+
+Each test names the passage / identity it checks.  None of them re-types the
+oracle's own formula: they use brute force, closed forms, special cases,
+invariants or hand-worked values (tests/golden/).
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+F32 = np.float32
+
+
+def rng(seed=0):
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+# ----------------------------------------------------------------------------- O1 stats
+def test_stats_brute_force_loop():
+    """O1 vs a naive per-element loop."""
+    g = rng(1)
+    T, d, M = 37, 11, 3
+    X = g.standard_normal((T, d)).astype(F32) * 5
+    ids = g.integers(0, M, T).astype(np.uint8)
+    R, cnt = O.calibrate_stats(X, ids, M)
+    for m in range(M):
+        for i in range(d):
+            best = 0.0
+            for t in range(T):
+                if ids[t] == m:
+                    best = max(best, abs(float(X[t, i])))
+            assert R[m, i] == F32(best)
+        assert cnt[m] == int(sum(1 for t in range(T) if ids[t] == m))
+
+
+def test_stats_identity_and_single_token():
+    """X = I -> all ones; single token -> |x|."""
+    R, cnt = O.calibrate_stats(np.eye(8, dtype=F32), np.zeros(8, np.uint8), 1)
+    assert np.all(R == 1) and cnt[0] == 8
+    x = np.array([[-3.5, 0.25, 0.0, 7.0]], F32)
+    R, _ = O.calibrate_stats(x, np.array([1], np.uint8), 2)
+    assert np.array_equal(R[1], np.abs(x[0])) and np.all(R[0] == 0)
+
+
+def test_stats_unified_reduction():
+    """max_m R^m == unified stats of the untagged X (PAPER.md:37 s^uni uses max over m,t)."""
+    c = synth.config_inputs("c1")
+    R, _ = O.calibrate_stats(c["X"], c["ids"], 2)
+    Ru, _ = O.calibrate_stats(c["X"], np.zeros_like(c["ids"]), 1)
+    assert np.array_equal(R.max(axis=0), Ru[0])
+
+
+def test_stats_batch_coherence():
+    """Running max over batches == one pass."""
+    c = synth.config_inputs("c1")
+    R1, n1 = O.calibrate_stats(c["X"], c["ids"], 2)
+    R, n = None, None
+    for a, b in [(0, 50), (50, 51), (51, 256)]:
+        R, n = O.calibrate_stats(c["X"][a:b], c["ids"][a:b], 2, R, n)
+    assert np.array_equal(R, R1) and np.array_equal(n, n1)
+
+
+def test_stats_rejects_unknown_modality():
+    with pytest.raises(ValueError):
+        O.calibrate_stats(np.ones((2, 2), F32), np.array([0, 3], np.uint8), 2)
+
+
+# ----------------------------------------------------------------------------- O2 init
+def test_init_spec_examples():
+    g = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+    for ex in g["init_factors"]:
+        W = np.array([[ex["wmax"], -ex["wmax"] / 2]], F32)          # row absmax = wmax
+        s = O.init_factors(np.array([[ex["R"]]], F32), np.array([1]), W)
+        assert s[0, 0] == F32(ex["s"]), ex["citation"]
+
+
+def test_init_equals_smoothquant_beta_half():
+    """s^m = sqrt(R/wmax) equals SmoothQuant beta=0.5, R^0.5 / wmax^0.5 (PAPER.md:22 vs 57)."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    wmax = np.abs(O.decode(c["W"]).astype(np.float64)).max(axis=1)
+    sq = np.power(R.astype(np.float64), 0.5) / np.power(wmax, 0.5)[None, :]
+    rel = np.abs(s.astype(np.float64) - sq) / sq
+    assert rel.max() <= 2.0 ** -23        # within one f32 ulp
+
+
+def test_init_rejects_empty_modality():
+    with pytest.raises(ValueError):
+        O.init_factors(np.ones((2, 3), F32), np.array([5, 0]), np.ones((3, 4), F32))
+
+
+def test_init_floor_zero_range():
+    """Zero range / zero weight row are floored at 1e-12."""
+    s = O.init_factors(np.zeros((1, 2), F32), np.array([1]), np.array([[0.0, 0.0], [1.0, 1.0]], F32))
+    assert s[0, 0] == F32(1.0) and s[0, 1] == np.sqrt(F32(1e-12), dtype=F32)
+
+
+# ----------------------------------------------------------------------------- quantizer
+def test_rha_edges():
+    v = np.array([0.49999997, 0.5, -0.5, 1.5, 2.5, -2.5, -0.49999997, 3.0, -7.5], F32)
+    assert rha_list(v) == [0, 1, -1, 2, 3, -3, 0, 3, -8]
+
+
+def rha_list(v):
+    return [int(x) for x in O.rha(v)]
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 6, 8])
+def test_quantizer_brute_force_nearest_code(bits):
+    """Code == nearest of all 2^b grid points to x/Delta, ties -> larger magnitude."""
+    g = rng(bits)
+    A = (g.standard_normal((40, 25)) * np.exp(g.standard_normal((40, 1)))).astype(F32)
+    A[0, :5] = [0.5, -0.5, 1.5, 2.5, -3.5]                 # exact half-grid points on row 0
+    codes, delta = O.quantize_rows(A, bits)
+    grid = np.arange(-(2 ** (bits - 1)), 2 ** (bits - 1))
+    for r in range(A.shape[0]):
+        v = np.divide(A[r], delta[r], dtype=F32).astype(np.float64)
+        for i, vi in enumerate(v):
+            dist = np.abs(grid - vi)
+            best = grid[dist == dist.min()]
+            want = best[np.argmax(np.abs(best))]
+            assert codes[r, i] == want, (r, i, vi)
+
+
+def test_quantizer_spec_examples():
+    g = json.load(open(os.path.join(GOLD, "spec_examples.json")))
+    for ex in g["quantizer"]:
+        codes, delta = O.quantize_rows(np.array([ex["x"]], F32), ex["bits"])
+        want_delta = F32(1.0) / F32(127.0) if ex["delta"] == "1/127" else F32(1e-12)
+        assert delta[0] == want_delta, ex["citation"]
+        assert list(codes[0]) == ex["codes_by_hand"], ex["citation"]
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_quantizer_properties(bits):
+    """Saturation, error bound |Q(x)-x| <= Delta/2, idempotence, power-of-two scale covariance
+    (PAPER.md:76)."""
+    g = rng(10 + bits)
+    A = (g.standard_normal((64, 100)) * 3).astype(F32)
+    qmax = 2 ** (bits - 1) - 1
+    codes, delta = O.quantize_rows(A, bits)
+    assert np.all(np.abs(codes).max(axis=1) == qmax)                      # saturation
+    err = np.abs(O.dequantize_rows(codes, delta) - A.astype(np.float64))
+    assert np.all(err <= delta[:, None].astype(np.float64) * (0.5 + 1e-6))  # rounding bound
+    deq = np.multiply(codes.astype(F32), delta[:, None], dtype=F32)
+    again = np.clip(O.rha(np.divide(deq, delta[:, None], dtype=F32)), -qmax - 1, qmax)
+    assert np.array_equal(again.astype(np.int8), codes)                   # idempotence
+    for k in (-3, 5):
+        c2, d2 = O.quantize_rows(A * F32(2.0 ** k), bits)
+        assert np.array_equal(c2, codes) and np.array_equal(d2, delta * F32(2.0 ** k))
+
+
+def test_quantizer_zero_row():
+    codes, delta = O.quantize_rows(np.zeros((2, 8), F32), 8)
+    assert np.all(codes == 0) and np.all(delta == F32(1e-12))
+
+
+# ----------------------------------------------------------------------------- O5
+def test_int_gemm_vs_triple_loop():
+    g = rng(5)
+    qx = g.integers(-128, 128, (5, 33)).astype(np.int8)
+    qw = g.integers(-128, 128, (7, 33)).astype(np.int8)
+    acc = O.int_gemm(qx, qw)
+    for t, j in itertools.product(range(5), range(7)):
+        assert acc[t, j] == sum(int(qx[t, i]) * int(qw[j, i]) for i in range(33))
+
+
+def test_int_gemm_extreme_magnitude_exact():
+    """|acc| <= 127*127*d; at d = 18944 (c3 down) the f64 path is still exact (< 2^53)."""
+    d = 18944
+    qx = np.full((2, d), 127, np.int8)
+    qx[1, ::2] = -128
+    qw = np.full((2, d), -128, np.int8)
+    acc = O.int_gemm(qx, qw)
+    assert acc[0, 0] == 127 * -128 * d
+    assert acc[1, 1] == (d // 2) * (-128 * -128) + (d // 2) * (127 * -128)
+
+
+# ----------------------------------------------------------------------------- invariance
+def test_invariance_before_quantization():
+    """(X S^-1)(S W) = X W: exact for power-of-two s, <= 1e-6 rel for any s
+    (the only rounding is the f32 smoothing of X, reading Q6)."""
+    g = rng(7)
+    for seed in range(20):
+        g = rng(100 + seed)
+        d = int(g.integers(2, 64))
+        X = g.standard_normal((9, d)).astype(F32)
+        W = g.standard_normal((d, 5)).astype(F32)
+        ids = np.zeros(9, np.uint8)
+        s2 = (2.0 ** g.integers(-6, 7, d)).astype(F32)
+        xs = O.smooth_activations(X, ids, s2[None, :]).astype(np.float64)
+        sw = (s2[:, None].astype(np.float64) * W)
+        assert np.array_equal(xs @ sw, X.astype(np.float64) @ W.astype(np.float64)) or \
+            np.allclose(xs @ sw, X.astype(np.float64) @ W, rtol=1e-12, atol=1e-12)
+        s = np.exp(g.standard_normal(d)).astype(F32)
+        xs = O.smooth_activations(X, ids, s[None, :]).astype(np.float64)
+        ref = X.astype(np.float64) @ W
+        rel = np.linalg.norm(xs @ (s[:, None].astype(np.float64) * W) - ref) / np.linalg.norm(ref)
+        assert rel <= 1e-6
+
+
+def _grid_aligned_case(seed=3, T=6, d=8, n=5, abits=8, wbits=4):
+    """Inputs on which every quantization is lossless: power-of-two s and Deltas,
+    integer codes with one saturated code per row / column."""
+    g = rng(seed)
+    qa, qw_ = 2 ** (abits - 1) - 1, 2 ** (wbits - 1) - 1
+    s0 = (2.0 ** g.integers(-3, 4, d)).astype(F32)
+    s = np.stack([s0, s0 * F32(4.0)])                     # S_1 = 4 S_0 keeps S_1 W lossless
+    ids = np.array([0, 1, 0, 1, 1, 0][:T], np.uint8)
+    cx = g.integers(-qa, qa + 1, (T, d)).astype(np.float64)
+    cx[:, 0] = qa
+    dx = 2.0 ** g.integers(-4, 3, T)
+    xs = cx * dx[:, None]
+    X = (xs * s[ids].astype(np.float64)).astype(F32)      # X = xs S  (exact: powers of two)
+    cw = g.integers(-qw_, qw_ + 1, (d, n)).astype(np.float64)
+    cw[0, :] = qw_
+    dw = 2.0 ** g.integers(-5, 0, n)
+    W = ((cw * dw[None, :]) / s0[:, None].astype(np.float64)).astype(F32)   # S_0 W on the grid
+    return X, ids, s, W
+
+
+def test_grid_aligned_lossless_forward_and_loss():
+    """On grid-aligned inputs Q is the identity, so:
+    text rows Y = X W exactly; image rows without CMC Y = (X S_v^-1)(S_t W) = X W / 4 exactly
+    (S_v = 4 S_t: the cross-modal invariance break of PAPER.md:126-132); with the exact
+    full-rank correction L1 = I, L2 = S_v W - Q(S_t W) = 3 S_t W, Y = X W exactly; L = 0."""
+    X, ids, s, W = _grid_aligned_case()
+    qw, dw = O.quantize_weight(W, s[0], 4)
+    Y = O.linear_forward(X, ids, s, qw, dw, 8)
+    XW = O.reference_output(X, W)
+    text = ids == 0
+    assert np.array_equal(Y[text], XW[text])
+    assert np.array_equal(Y[~text], XW[~text] / 4)
+    d = W.shape[0]
+    dW = 3.0 * s[0].astype(np.float64)[:, None] * W.astype(np.float64)
+    Yc = O.linear_forward(X, ids, s, qw, dw, 8, L1=[np.eye(d)], L2=[dW])
+    assert np.array_equal(Yc, XW)
+    sums, counts, loss = O.calib_loss(X, ids, s, W, 4, 8)
+    assert loss == 0.0 and np.all(sums == 0) and list(counts) == [3, 3]
+
+
+# ----------------------------------------------------------------------------- O7 CMC
+def test_cmc_full_rank_identity():
+    """With L1 L2 = Delta W = S_m W - deqQ(S_t W) exactly (L1 = I),
+    Y_m - xs S_m W = (deqQ(xs) - xs) . deqQ(S_t W)  (PAPER.md:131 + 183)."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    qw, dw = O.quantize_weight(c["W"], s[0], 8)
+    base = (qw.astype(np.float64) * dw[:, None].astype(np.float64)).T          # deqQ(S_t W) [d x n]
+    Wf = O.decode(c["W"]).astype(np.float64)
+    dW = s[1].astype(np.float64)[:, None] * Wf - base
+    d = Wf.shape[0]
+    Y = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, L1=[np.eye(d)], L2=[dW])
+    img = np.nonzero(c["ids"] == 1)[0]
+    xs = O.smooth_activations(c["X"], c["ids"], s)[img].astype(np.float64)
+    qx, dx = O.quantize_rows(xs.astype(F32), 8)
+    lhs = Y[img] - xs @ (s[1].astype(np.float64)[:, None] * Wf)
+    rhs = (O.dequantize_rows(qx, dx) - xs) @ base
+    assert np.abs(lhs - rhs).max() <= 1e-9 * np.abs(Y[img]).max()
+
+
+def test_cmc_rank0_all_text_and_routing():
+    """rank 0 == base formula; all-text input ignores L; an image token's output does not
+    depend on other modalities' factors."""
+    c = synth.config_inputs("c2", d=64, n=48, T=1024, r=16)
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 3)
+    s = O.init_factors(R, cnt, c["W"])
+    qw, dw = O.quantize_weight(c["W"], s[0], 8)
+    L1 = [c["L1"][0], c["L1"][1]]
+    L2 = [c["L2"][0], c["L2"][1]]
+    Y0 = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8)
+    Y = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, L1, L2)
+    text = c["ids"] == 0
+    assert np.array_equal(Y[text], Y0[text]) and not np.array_equal(Y[~text], Y0[~text])
+    ids_t = np.zeros_like(c["ids"])
+    assert np.array_equal(O.linear_forward(c["X"], ids_t, s, qw, dw, 8, L1, L2),
+                          O.linear_forward(c["X"], ids_t, s, qw, dw, 8))
+    s_alt = s.copy()
+    s_alt[2] *= F32(3.0)
+    Ya = O.linear_forward(c["X"], c["ids"], s_alt, qw, dw, 8, L1, L2)
+    img = c["ids"] == 1
+    assert np.array_equal(Ya[img], Y[img])
+
+
+def test_forward_order_equivariance_and_partition():
+    """Permuting tokens permutes rows; per-modality sub-batches recombine."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    qw, dw = O.quantize_weight(c["W"], s[0], 8)
+    L1, L2 = [c["L1"][0]], [c["L2"][0]]
+    Y = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, L1, L2)
+    p = rng(9).permutation(c["T"])
+    Yp = O.linear_forward(c["X"][p], c["ids"][p], s, qw, dw, 8, L1, L2)
+    assert np.array_equal(Yp, Y[p])
+    for m in (0, 1):
+        sel = np.nonzero(c["ids"] == m)[0]
+        Ym = O.linear_forward(c["X"][sel], c["ids"][sel], s, qw, dw, 8, L1, L2)
+        assert np.array_equal(Ym, Y[sel])
+    rows = np.array([3, 100, 255, 41])
+    assert np.array_equal(O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, L1, L2, rows=rows), Y[rows])
+
+
+# ----------------------------------------------------------------------------- O8 loss
+def test_loss_separability():
+    """Mixed-batch per-modality sums == sums on each modality's sub-batch."""
+    c = synth.config_inputs("c2", d=64, n=40, T=1024)
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 3)
+    s = O.init_factors(R, cnt, c["W"])
+    sums, counts, loss = O.calib_loss(c["X"], c["ids"], s, c["W"], 4, 8)
+    tot = 0.0
+    for m in range(3):
+        sel = np.nonzero(c["ids"] == m)[0]
+        sm, cm, lm = O.calib_loss(c["X"][sel], c["ids"][sel], s, c["W"], 4, 8)
+        assert np.isclose(sm[m], sums[m], rtol=1e-12) and cm[m] == counts[m]
+        tot += lm
+    assert np.isclose(tot, loss, rtol=1e-12)
+
+
+# ----------------------------------------------------------------------------- golden
+def test_hand_worked_example():
+    g = json.load(open(os.path.join(GOLD, "hand_worked_w4a8.json")))
+    i, e = g["inputs"], g["expected"]
+    X = np.array(i["X"], F32)
+    ids = np.array(i["ids"], np.uint8)
+    s = np.array(i["s"], F32)
+    W = np.array(i["W"], F32)
+    qx, dx = O.quantize_activations(X, ids, s, i["abits"])
+    assert qx.tolist() == e["qx"]
+    qw, dw = O.quantize_weight(W, s[0], i["wbits"])
+    assert qw.tolist() == e["qw_text_kmajor"]
+    assert O.int_gemm(qx, qw).tolist() == e["acc"]
+    Y0 = O.linear_forward(X, ids, s, qw, dw, i["abits"])
+    assert np.allclose(Y0, e["Y_rank0"], rtol=1e-6, atol=1e-6)
+    L1 = [np.array(i["L1_image"])]
+    L2 = [np.array(i["L2_image"])]
+    Y = O.linear_forward(X, ids, s, qw, dw, i["abits"], L1, L2)
+    assert np.allclose(Y, e["Y_cmc"], rtol=1e-6, atol=1e-6)
+    assert np.array_equal(O.reference_output(X, W), np.array(e["XW"]))
+    sums, counts, loss = O.calib_loss(X, ids, s, W, i["wbits"], i["abits"])
+    # the hand values use exact rationals; the oracle's Deltas are f32 (reading Q6), and the
+    # loss is a difference of O(15)-sized outputs, so compare at 1e-6 of the output scale.
+    assert np.allclose(sums, e["loss_sums"], rtol=0, atol=2e-5)
+    assert counts.tolist() == e["loss_counts"]
+    assert np.isclose(loss, e["loss"], rtol=0, atol=2e-5)
