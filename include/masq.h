@@ -1,0 +1,204 @@
+/*
+ * masq.h — C ABI of the B200-native MASQuant hot path (arXiv 2603.04800).
+ *
+ * The library implements the data-parallel hot path of MASQuant's
+ * modality-aware smoothed quantized linear layer on sm_100a:
+ *
+ *   A1  masq_calibrate_stats   R^m_i = max_t |x^m_{t,i}|                  PAPER.md:35  (§4.1)
+ *   A2  masq_init_factors      s^m_i = sqrt(R^m_i / max_j |w_{j,i}|)       PAPER.md:55-58 (§4.2)
+ *   A3  masq_quantize_weight   Q(S W), per output channel                  PAPER.md:129, 244 (Eq. PTQ)
+ *   A4  masq_quantize_activations  Q(X_m S_m^{-1}), per token
+ *   A4-A7 masq_linear_forward  Y = Q(X_m S_m^-1) Q(S_t W) [+ X_m S_m^-1 L1^m L2^m if m != text]
+ *                                                                          PAPER.md:177-185
+ *   A8  masq_calib_loss        sum_m lambda_m MAE(Q(X_m S_m^-1) Q(S_m W), X_m W)
+ *                                                                          PAPER.md:62-70
+ *       masq_reference_output  X W (f32), the loss target, computed once per batch
+ *
+ * Conventions (apply to every entry point unless stated):
+ *  - Shapes follow the paper's problem statement: X is [T x d]
+ *    row-major (token rows), W is [d x d_out] row-major (D_in x D_out), one
+ *    modality id per token (uint8, 0 = text = the base modality, PAPER.md:129,
+ *    561), n_mod = |M| in [1, 8].
+ *  - Every array pointer is a DEVICE pointer owned by the caller, except
+ *    `lambda` (host).  The library allocates nothing and keeps no global
+ *    state; scratch comes from the caller's workspace `ws` (size from
+ *    masq_workspace_size, 256-byte aligned).  Calls on the same ws must be
+ *    stream-ordered; concurrent calls need distinct ws.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream).  Argument errors (NULL, shape, bits, alignment,
+ *    workspace) are returned synchronously and nothing is launched.  Data
+ *    errors found on the device (a modality id >= n_mod, a modality with no
+ *    calibration tokens) set a sticky status word inside ws; masq_check()
+ *    synchronizes the stream and returns/clears it.  CUDA launch errors ->
+ *    MASQ_ERR_CUDA.  Nothing throws across the ABI.
+ *  - Limits: d % 16 == 0, d_out % 32 == 0, T >= 0 (T == 0 is a no-op),
+ *    bits in [2, 8] (A16 / W16 -> MASQ_ERR_UNSUPPORTED), r % 16 == 0 and
+ *    r <= 256 (r == 0 disables CMC), all pointers 16-byte aligned.
+ *  - Quantizer (readings Q1-Q7 in DESIGN.md): symmetric,
+ *    z = 0, Delta = max(absmax / (2^{b-1}-1), 1e-12f), codes =
+ *    clamp(round-half-away(x / Delta), -2^{b-1}, 2^{b-1}-1), all in IEEE f32
+ *    with the operation order documented per call; integer codes and f32
+ *    scales are bit-exact against the CPU oracle.
+ */
+#ifndef MASQ_H
+#define MASQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum masq_status {
+  MASQ_OK = 0,
+  MASQ_ERR_NULL = 1,            /* a required pointer is NULL */
+  MASQ_ERR_SHAPE = 2,           /* a dimension violates the limits above */
+  MASQ_ERR_BITS = 3,            /* bit-width outside [2, 16] */
+  MASQ_ERR_ALIGN = 4,           /* a pointer or leading dimension is misaligned */
+  MASQ_ERR_WORKSPACE = 5,       /* ws NULL or ws_bytes < masq_workspace_size(...) */
+  MASQ_ERR_BAD_MODALITY = 6,    /* (sticky) a token id >= n_mod */
+  MASQ_ERR_EMPTY_MODALITY = 7,  /* (sticky) count[m] == 0 at init */
+  MASQ_ERR_UNSUPPORTED = 8,     /* valid request outside this path (e.g. A16) */
+  MASQ_ERR_CUDA = 9             /* a CUDA runtime / driver call failed */
+} masq_status;
+
+typedef enum masq_dtype { MASQ_F32 = 0, MASQ_BF16 = 1 } masq_dtype;
+
+typedef void* masq_stream;      /* cudaStream_t */
+
+/* Workspace queries: op is one of the MASQ_OP_* values. */
+enum {
+  MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
+  MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6
+};
+size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
+                           int32_t n_mod, int32_t r);
+
+/*
+ * A1 — per-modality channel absmax.
+ *   R[m*d + i]  = max(R_in[m*d+i], max_{t: id_t = m} |X[t*ld_x + i]|)     (f32, exact)
+ *   count[m]   += #{t : id_t = m}                                          (int64)
+ * reset != 0 zeroes R and count first (a new calibration set); reset == 0
+ * continues a running max over batches (resumable calibration).
+ * X: [T x d] (row stride ld_x elements) of dtype xt (bf16 or f32).
+ * Tokens with id >= n_mod are skipped and raise MASQ_ERR_BAD_MODALITY (sticky).
+ */
+masq_status masq_calibrate_stats(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                                 int64_t T, int64_t d, int32_t n_mod,
+                                 float* R, int64_t* count, int32_t reset,
+                                 void* ws, size_t ws_bytes, masq_stream stream);
+
+/*
+ * A2 — closed-form modality-aware factors (reading Q8: the
+ * weight max is over output channels j of row i of W[d x d_out]).
+ *   wmax[i]    = max_j |W[i*d_out + j]|
+ *   s[m*d + i] = sqrtf( fmaxf(R[m*d+i], 1e-12f) / fmaxf(wmax[i], 1e-12f) )   (IEEE div, sqrt)
+ * wmax_out (optional, may be NULL) receives wmax [d].
+ * count[m] == 0 for some m raises MASQ_ERR_EMPTY_MODALITY (sticky).
+ */
+masq_status masq_init_factors(const float* R, const int64_t* count, const void* W, masq_dtype wt,
+                              int64_t d, int64_t d_out, int32_t n_mod,
+                              float* s, float* wmax_out,
+                              void* ws, size_t ws_bytes, masq_stream stream);
+
+/*
+ * A3 — smoothing + per-output-channel quantization of the weight (reading Q1),
+ * stored K-major for the integer GEMM:
+ *   ws[i,j]   = s[i] * W[i*d_out + j]                               (f32 mul)
+ *   dw[j]     = fmaxf( max_i |ws[i,j]| / (2^{wbits-1}-1), 1e-12f )
+ *   qw[j*d+i] = clamp(rha(ws[i,j] / dw[j]), -2^{wbits-1}, 2^{wbits-1}-1)   (int8 container)
+ * With s = s^text this is the single stored weight Q(S_t W).
+ */
+masq_status masq_quantize_weight(const void* W, masq_dtype wt, const float* s,
+                                 int64_t d, int64_t d_out, int32_t wbits,
+                                 int8_t* qw, float* dw,
+                                 void* ws, size_t ws_bytes, masq_stream stream);
+
+/*
+ * A4 — routed smoothing + per-token quantization:
+ *   inv[m,i]  = 1.0f / s[m*d+i];  xs = X[t,i] * inv[id_t, i]            (f32)
+ *   dx[t]     = fmaxf( max_i |xs| / (2^{abits-1}-1), 1e-12f )
+ *   qx[t*d+i] = clamp(rha(xs / dx[t]))                                   (int8)
+ * tile_mask (optional, [ceil(T/128)] uint32, zeroed by the call) receives,
+ * per 128-token tile, the bit set {1 << m} of modalities present.
+ */
+masq_status masq_quantize_activations(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                                      int64_t T, int64_t d, int32_t n_mod, const float* s,
+                                      int32_t abits, int8_t* qx, float* dx, uint32_t* tile_mask,
+                                      void* ws, size_t ws_bytes, masq_stream stream);
+
+/* Optional debug taps for masq_linear_forward (parity tests). */
+typedef struct masq_debug {
+  int32_t* acc;        /* if non-NULL: write the int32 accumulators sum_i qx*qw [T x ld_acc]
+                          instead of Y (CMC skipped) */
+  int64_t ld_acc;
+} masq_debug;
+
+/*
+ * A4-A7 — the routed inference equation:
+ *   Y[t,:] = dx[t] * dw[:] * (qx[t,:] . qw[:,:]^T)                        m_t == 0 (text)
+ *   Y[t,:] = same + (X_t S_m^-1) . L1^m . L2^m                             m_t != 0
+ * s: [n_mod x d] factors (row m = s^m); qw/dw: the output of
+ * masq_quantize_weight with s^text (qw [d_out x d] K-major, dw [d_out]).
+ * L1: bf16 [(n_mod-1) x d x r] (L1^m = T^-1 U_r), row-major per modality;
+ * L2: bf16 [(n_mod-1) x r x ld_l2] (L2^m = Sigma_r V_r^T), row-major per modality.
+ * L1/L2 may be NULL iff r == 0.  The CMC term is computed in full precision
+ * from the f32 smoothed activations (split-bf16 tensor-core products, fp32
+ * accumulation, reading Q13).  Y: f32 [T x ld_y], original token order.
+ * Column sharding: pass qw + j0*d, dw + j0, L2 + j0, Y + j0 and d_out = shard width.
+ */
+masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                                int64_t T, int64_t d, int64_t d_out, int32_t n_mod,
+                                const float* s, const int8_t* qw, const float* dw,
+                                int32_t wbits, int32_t abits,
+                                const void* L1, const void* L2, int64_t ld_l2, int32_t r,
+                                float* Y, int64_t ld_y,
+                                void* ws, size_t ws_bytes, const masq_debug* dbg, masq_stream stream);
+
+/*
+ * Loss target X W ("X_m W"; reading Q16): bf16 tensor-core
+ * products accumulated in fp32.  X bf16 [T x ld_x], W bf16 [d x d_out];
+ * Yref f32 [T x ld_ref].  Computed once per calibration batch and reused by
+ * every masq_calib_loss pass of the S optimisation.
+ */
+masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, int64_t T, int64_t d,
+                                  int64_t d_out, float* Yref, int64_t ld_ref,
+                                  void* ws, size_t ws_bytes, masq_stream stream);
+
+/*
+ * A8 — fused calibration loss (Eq. mas_quant; readings Q9, Q10, Q12):
+ *   for every modality m: qw^m = Q(S_m W) (A3 with s^m), qx = A4 (each token with its own s^m),
+ *   sums[m]   = sum_{t: id_t = m} sum_j | dx[t] dw^m[j] (qx[t] . qw^m[j]) - Yref[t,j] |   (f64)
+ *   counts[m] = #{t : id_t = m}
+ *   loss[0]   = sum_m lambda[m] * sums[m] / (counts[m] * d_out)   over m with counts[m] > 0
+ * lambda: HOST array [n_mod] (NULL -> all 1.0).  Yref: f32 [T x ld_ref]
+ * from masq_reference_output.  sums/counts/loss are device pointers; the sums are
+ * reduced in a fixed order (deterministic).  For token-sharded multi-GPU use,
+ * all-reduce sums and counts (SUM) and call masq_loss_finalize.
+ */
+masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                            int64_t T, int64_t d, int64_t d_out, int32_t n_mod,
+                            const float* s, const void* W, masq_dtype wt,
+                            int32_t wbits, int32_t abits, const float* lambda,
+                            const float* Yref, int64_t ld_ref,
+                            double* sums, int64_t* counts, double* loss,
+                            void* ws, size_t ws_bytes, masq_stream stream);
+
+/* loss[0] = sum_m lambda[m] * sums[m] / (counts[m] * d_out) on the device (after an all-reduce). */
+masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const float* lambda,
+                               int32_t n_mod, int64_t d_out, double* loss, masq_stream stream);
+
+/* Synchronizes `stream`, returns the sticky device status stored in ws and clears it. */
+masq_status masq_check(void* ws, masq_stream stream);
+
+const char* masq_status_string(masq_status s);
+
+/* Library identification: "<version> sm_100a". */
+const char* masq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MASQ_H */

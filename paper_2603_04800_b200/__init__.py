@@ -1,0 +1,9 @@
+"""B200-native MASQuant hot path (arXiv 2603.04800): modality-aware smoothed quantized linear.
+
+C ABI: include/masq.h (libmasq.so, sm_100a kernels in csrc/).  Python binding: masq.py.
+"""
+from . import masq  # noqa: F401
+from .masq import (  # noqa: F401
+    MasqError, Workspace, calib_loss, calibrate_stats, check, init_factors, linear_forward, loss_finalize,
+    quantize_activations, quantize_weight, reference_output, workspace_size,
+)

@@ -1,0 +1,67 @@
+"""ctypes loader for libmasq.so (the C ABI declared in include/masq.h).
+
+The product path has no fallback: if the shared library is missing or does not load,
+every call raises.  Build it with `python -c "import __graft_entry__ as g; g.build()"`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmasq.so")
+
+c_void_p = ctypes.c_void_p
+c_int32 = ctypes.c_int32
+c_int64 = ctypes.c_int64
+c_size_t = ctypes.c_size_t
+
+# name -> (restype, argtypes) — mirrors include/masq.h exactly
+SIGNATURES = {
+    "masq_workspace_size": (c_size_t, [c_int32, c_int64, c_int64, c_int64, c_int32, c_int32]),
+    "masq_calibrate_stats": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32,
+                                       c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
+    "masq_init_factors": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32,
+                                    c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "masq_quantize_weight": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int64, c_int32,
+                                       c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "masq_quantize_activations": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32,
+                                            c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_size_t, c_void_p]),
+    "masq_linear_forward": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32,
+                                      c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                                      c_void_p, c_void_p, c_int64, c_int32,
+                                      c_void_p, c_int64, c_void_p, c_size_t, c_void_p, c_void_p]),
+    "masq_reference_output": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                        c_void_p, c_int64, c_void_p, c_size_t, c_void_p]),
+    "masq_calib_loss": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32,
+                                  c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p,
+                                  c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_size_t, c_void_p]),
+    "masq_loss_finalize": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]),
+    "masq_check": (c_int32, [c_void_p, c_void_p]),
+    "masq_status_string": (ctypes.c_char_p, [c_int32]),
+    "masq_version": (ctypes.c_char_p, []),
+}
+
+
+class MasqDebug(ctypes.Structure):
+    _fields_ = [("acc", c_void_p), ("ld_acc", c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmasq.so once; raise loudly when it is missing (no CPU fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libmasq.so not built at {LIB_PATH}; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib

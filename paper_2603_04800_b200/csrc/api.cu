@@ -1,0 +1,366 @@
+// api.cu — the C ABI (include/masq.h): argument validation, workspace carving and the launch
+// sequence of every entry point.  All compute runs in the kernels of elem.cu, zgemm.cu, gemm.cu.
+#include <cstring>
+
+#include "internal.h"
+
+namespace masq {
+
+WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r) {
+  WsLayout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const int64_t tiles_m = ceil_div(std::max<int64_t>(T, 1), kTileM);
+  const int64_t rp = rpad_of(r);
+  const int64_t nnt = std::max(n_mod - 1, 0);
+  L.status = take(kStatusBytes);
+  switch (op) {
+    case MASQ_OP_STATS:
+    case MASQ_OP_INIT:
+      break;
+    case MASQ_OP_QWEIGHT:
+      L.amax = take(sizeof(uint32_t) * n);
+      break;
+    case MASQ_OP_QACT:
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      break;
+    case MASQ_OP_FORWARD:
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      L.qx = take((size_t)T * d);
+      L.dx = take(sizeof(float) * T);
+      L.mask = take(sizeof(uint32_t) * tiles_m);
+      if (rp > 0 && nnt > 0) {
+        L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
+        L.l1t = take(sizeof(uint16_t) * (size_t)nnt * rp * d);
+        L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
+      }
+      break;
+    case MASQ_OP_LOSS:
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      L.qx = take((size_t)T * d);
+      L.dx = take(sizeof(float) * T);
+      L.mask = take(sizeof(uint32_t) * tiles_m);
+      L.qw_all = take((size_t)n_mod * n * d);
+      L.dw_all = take(sizeof(float) * n_mod * n);
+      L.amax = take(sizeof(uint32_t) * n_mod * n);
+      L.partials = take(sizeof(double) * n_mod * tiles_m * ceil_div(n, kTileN) * 4);
+      break;
+    case MASQ_OP_REFERENCE:
+      L.wt = take(sizeof(uint16_t) * (size_t)n * d);
+      break;
+    default:
+      break;
+  }
+  L.total = off;
+  return L;
+}
+
+}  // namespace masq
+
+using namespace masq;
+
+namespace {
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t S(masq_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+inline uint8_t* W8(void* ws, size_t off) { return static_cast<uint8_t*>(ws) + off; }
+inline uint32_t* status_of(void* ws) { return static_cast<uint32_t*>(ws); }
+#define MASQ_CK(x)                                   \
+  do {                                               \
+    if ((x) != cudaSuccess) return MASQ_ERR_CUDA;    \
+  } while (0)
+
+masq_status check_bits(int32_t b) {
+  if (b >= 2 && b <= 8) return MASQ_OK;
+  if (b > 8 && b <= 16) return MASQ_ERR_UNSUPPORTED;
+  return MASQ_ERR_BITS;
+}
+masq_status check_common(int64_t T, int64_t d, int32_t n_mod) {
+  if (T < 0 || d <= 0 || d % 16 != 0 || d >= (1LL << 31) || T >= (1LL << 31)) return MASQ_ERR_SHAPE;
+  if (n_mod < 1 || n_mod > kMaxMod) return MASQ_ERR_SHAPE;
+  return MASQ_OK;
+}
+masq_status check_x(const void* X, masq_dtype xt, int64_t ld_x, int64_t d) {
+  if (!X) return MASQ_ERR_NULL;
+  if (xt != MASQ_BF16 && xt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (ld_x < d) return MASQ_ERR_SHAPE;
+  const int64_t bytes = ld_x * (xt == MASQ_BF16 ? 2 : 4);
+  if (bytes % 16 != 0 || !al16(X)) return MASQ_ERR_ALIGN;
+  return MASQ_OK;
+}
+masq_status check_ws(void* ws, size_t ws_bytes, const WsLayout& L) {
+  if (!ws) return MASQ_ERR_WORKSPACE;
+  if (ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return MASQ_ERR_WORKSPACE;
+  return MASQ_OK;
+}
+#define MASQ_TRY(x)                  \
+  do {                               \
+    masq_status s_ = (x);            \
+    if (s_ != MASQ_OK) return s_;    \
+  } while (0)
+}  // namespace
+
+extern "C" {
+
+size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out, int32_t n_mod, int32_t r) {
+  return ws_layout(op, T, d, d_out, n_mod, r).total;
+}
+
+masq_status masq_calibrate_stats(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                                 int64_t d, int32_t n_mod, float* R, int64_t* count, int32_t reset, void* ws,
+                                 size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  if (!R || !count) return MASQ_ERR_NULL;
+  if (T > 0) {
+    MASQ_TRY(check_x(X, xt, ld_x, d));
+    if (!mod_id) return MASQ_ERR_NULL;
+  }
+  const WsLayout L = ws_layout(MASQ_OP_STATS, T, d, 0, n_mod, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  if (reset) {
+    MASQ_CK(cudaMemsetAsync(R, 0, sizeof(float) * n_mod * d, S(stream)));
+    MASQ_CK(cudaMemsetAsync(count, 0, sizeof(int64_t) * n_mod, S(stream)));
+  }
+  MASQ_CK(launch_stats(X, xt, ld_x, mod_id, T, d, n_mod, R, count, status_of(ws), S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_init_factors(const float* R, const int64_t* count, const void* W, masq_dtype wt, int64_t d,
+                              int64_t d_out, int32_t n_mod, float* s, float* wmax_out, void* ws, size_t ws_bytes,
+                              masq_stream stream) {
+  MASQ_TRY(check_common(0, d, n_mod));
+  if (!R || !count || !W || !s) return MASQ_ERR_NULL;
+  if (d_out <= 0 || d_out % 32 != 0) return MASQ_ERR_SHAPE;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (!al16(W)) return MASQ_ERR_ALIGN;
+  MASQ_TRY(check_ws(ws, ws_bytes, ws_layout(MASQ_OP_INIT, 0, d, d_out, n_mod, 0)));
+  MASQ_CK(launch_init(R, count, W, wt, d, d_out, n_mod, s, wmax_out, status_of(ws), S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_quantize_weight(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t d_out,
+                                 int32_t wbits, int8_t* qw, float* dw, void* ws, size_t ws_bytes,
+                                 masq_stream stream) {
+  MASQ_TRY(check_common(0, d, 1));
+  MASQ_TRY(check_bits(wbits));
+  if (!W || !s || !qw || !dw) return MASQ_ERR_NULL;
+  if (d_out <= 0 || d_out % 32 != 0) return MASQ_ERR_SHAPE;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (!al16(W) || !al16(qw)) return MASQ_ERR_ALIGN;
+  const WsLayout L = ws_layout(MASQ_OP_QWEIGHT, 0, d, d_out, 1, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  MASQ_CK(launch_wquant(W, wt, s, 1, d, d_out, wbits, qw, dw, reinterpret_cast<uint32_t*>(W8(ws, L.amax)),
+                        S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_quantize_activations(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                                      int64_t d, int32_t n_mod, const float* s, int32_t abits, int8_t* qx,
+                                      float* dx, uint32_t* tile_mask, void* ws, size_t ws_bytes,
+                                      masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  MASQ_TRY(check_bits(abits));
+  if (T == 0) return MASQ_OK;
+  MASQ_TRY(check_x(X, xt, ld_x, d));
+  if (!mod_id || !s || !qx || !dx) return MASQ_ERR_NULL;
+  if (!al16(qx) || !al16(s)) return MASQ_ERR_ALIGN;
+  const WsLayout L = ws_layout(MASQ_OP_QACT, T, d, 0, n_mod, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, S(stream)));
+  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, tile_mask, status_of(ws), S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                                int64_t d, int64_t d_out, int32_t n_mod, const float* s, const int8_t* qw,
+                                const float* dw, int32_t wbits, int32_t abits, const void* L1, const void* L2,
+                                int64_t ld_l2, int32_t r, float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
+                                const masq_debug* dbg, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  MASQ_TRY(check_bits(wbits));
+  MASQ_TRY(check_bits(abits));
+  if (d_out <= 0 || d_out % 32 != 0 || d_out >= (1LL << 31)) return MASQ_ERR_SHAPE;
+  if (r < 0 || r > 256 || r % 16 != 0) return MASQ_ERR_SHAPE;
+  const bool use_acc = dbg && dbg->acc;
+  if (!s || !qw || !dw || (!Y && !use_acc)) return MASQ_ERR_NULL;
+  const bool cmc = r > 0 && n_mod > 1 && !use_acc;
+  if (cmc) {
+    if (!L1 || !L2) return MASQ_ERR_NULL;
+    if (ld_l2 < d_out || !al16(L1) || !al16(L2) || (ld_l2 % 8) != 0) return MASQ_ERR_ALIGN;
+  }
+  float* out = use_acc ? reinterpret_cast<float*>(dbg->acc) : Y;
+  const int64_t ld_out = use_acc ? dbg->ld_acc : ld_y;
+  if (ld_out < d_out || ld_out % 4 != 0 || !al16(out)) return MASQ_ERR_ALIGN;
+  if (!al16(qw) || !al16(dw)) return MASQ_ERR_ALIGN;
+  if (T == 0) return MASQ_OK;
+  MASQ_TRY(check_x(X, xt, ld_x, d));
+  if (!mod_id) return MASQ_ERR_NULL;
+  const WsLayout L = ws_layout(MASQ_OP_FORWARD, T, d, d_out, n_mod, cmc ? r : 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
+  float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
+  uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
+  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
+  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, mask, status_of(ws), st));
+  GemmArgs g{};
+  g.mode = use_acc ? kModeAcc : kModeFwd;
+  g.T = T;
+  g.n = d_out;
+  g.d = d;
+  g.qx = qx;
+  g.b = qw;
+  g.b_rows = d_out;
+  g.dx = dx;
+  g.dw = dw;
+  g.tile_mask = mask;
+  g.ids = mod_id;
+  g.n_mod = n_mod;
+  g.out = out;
+  g.ld_out = ld_out;
+  if (cmc) {
+    const int rp = (int)rpad_of(r);
+    uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
+    uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
+    uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
+    MASQ_CK(launch_pack_lowrank(static_cast<const uint16_t*>(L1), static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1,
+                                d, d_out, r, rp, l1t, l2t, st));
+    MASQ_CK(launch_zgemm(X, xt, ld_x, mod_id, T, d, n_mod, inv, l1t, rp, mask, z, st));
+    g.rpad = rp;
+    g.z = z;
+    g.l2t = l2t;
+  }
+  MASQ_CK(launch_gemm(g, st));
+  return MASQ_OK;
+}
+
+masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, int64_t T, int64_t d, int64_t d_out,
+                                  float* Yref, int64_t ld_ref, void* ws, size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, 1));
+  if (d_out <= 0 || d_out % 32 != 0) return MASQ_ERR_SHAPE;
+  if (!W || !Yref) return MASQ_ERR_NULL;
+  if (ld_ref < d_out || ld_ref % 4 != 0 || !al16(Yref) || !al16(W)) return MASQ_ERR_ALIGN;
+  if (T == 0) return MASQ_OK;
+  MASQ_TRY(check_x(X, MASQ_BF16, ld_x, d));
+  const WsLayout L = ws_layout(MASQ_OP_REFERENCE, T, d, d_out, 1, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  uint16_t* wt = reinterpret_cast<uint16_t*>(W8(ws, L.wt));
+  MASQ_CK(launch_transpose_bf16(static_cast<const uint16_t*>(W), d, d_out, wt, S(stream)));
+  GemmArgs g{};
+  g.mode = kModeRef;
+  g.T = T;
+  g.n = d_out;
+  g.d = d;
+  g.xbf = static_cast<const uint16_t*>(X);
+  g.ld_x = ld_x;
+  g.b = wt;
+  g.b_rows = d_out;
+  g.n_mod = 1;
+  g.out = Yref;
+  g.ld_out = ld_ref;
+  MASQ_CK(launch_gemm(g, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                            int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
+                            int32_t wbits, int32_t abits, const float* lambda, const float* Yref, int64_t ld_ref,
+                            double* sums, int64_t* counts, double* loss, void* ws, size_t ws_bytes,
+                            masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  MASQ_TRY(check_bits(wbits));
+  MASQ_TRY(check_bits(abits));
+  if (d_out <= 0 || d_out % 32 != 0) return MASQ_ERR_SHAPE;
+  if (!s || !W || !sums || !counts || !loss) return MASQ_ERR_NULL;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (!al16(W) || !al16(s)) return MASQ_ERR_ALIGN;
+  const WsLayout L = ws_layout(MASQ_OP_LOSS, T, d, d_out, n_mod, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  if (T == 0) {
+    MASQ_CK(cudaMemsetAsync(sums, 0, sizeof(double) * n_mod, st));
+    MASQ_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * n_mod, st));
+    MASQ_CK(cudaMemsetAsync(loss, 0, sizeof(double), st));
+    return MASQ_OK;
+  }
+  MASQ_TRY(check_x(X, xt, ld_x, d));
+  if (!mod_id || !Yref) return MASQ_ERR_NULL;
+  if (ld_ref < d_out || ld_ref % 4 != 0 || !al16(Yref)) return MASQ_ERR_ALIGN;
+  float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
+  float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
+  uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
+  int8_t* qw = reinterpret_cast<int8_t*>(W8(ws, L.qw_all));
+  float* dw = reinterpret_cast<float*>(W8(ws, L.dw_all));
+  uint32_t* amax = reinterpret_cast<uint32_t*>(W8(ws, L.amax));
+  double* partials = reinterpret_cast<double*>(W8(ws, L.partials));
+  const int64_t tiles = ceil_div(T, kTileM) * ceil_div(d_out, kTileN);
+  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
+  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, mask, status_of(ws), st));
+  MASQ_CK(launch_wquant(W, wt, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
+  MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * n_mod * tiles * 4, st));
+  GemmArgs g{};
+  g.mode = kModeLoss;
+  g.T = T;
+  g.n = d_out;
+  g.d = d;
+  g.qx = qx;
+  g.b = qw;
+  g.b_rows = (int64_t)n_mod * d_out;
+  g.dx = dx;
+  g.dw = dw;
+  g.tile_mask = mask;
+  g.ids = mod_id;
+  g.n_mod = n_mod;
+  g.yref = Yref;
+  g.ld_ref = ld_ref;
+  g.partials = partials;
+  MASQ_CK(launch_gemm(g, st));
+  MASQ_CK(launch_loss_reduce(partials, tiles * 4, mod_id, T, n_mod, d_out, lambda, sums, counts, loss, st));
+  return MASQ_OK;
+}
+
+masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const float* lambda, int32_t n_mod,
+                               int64_t d_out, double* loss, masq_stream stream) {
+  if (!sums || !counts || !loss) return MASQ_ERR_NULL;
+  if (n_mod < 1 || n_mod > kMaxMod || d_out <= 0) return MASQ_ERR_SHAPE;
+  MASQ_CK(launch_loss_finalize(sums, counts, lambda, n_mod, d_out, loss, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_check(void* ws, masq_stream stream) {
+  if (!ws) return MASQ_ERR_WORKSPACE;
+  if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return MASQ_ERR_CUDA;
+  uint32_t st = 0;
+  if (cudaMemcpy(&st, ws, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return MASQ_ERR_CUDA;
+  const uint32_t zero = 0;
+  if (cudaMemcpy(ws, &zero, sizeof(zero), cudaMemcpyHostToDevice) != cudaSuccess) return MASQ_ERR_CUDA;
+  if (st & kStBadModality) return MASQ_ERR_BAD_MODALITY;
+  if (st & kStEmptyModality) return MASQ_ERR_EMPTY_MODALITY;
+  return MASQ_OK;
+}
+
+const char* masq_status_string(masq_status s) {
+  switch (s) {
+    case MASQ_OK: return "ok";
+    case MASQ_ERR_NULL: return "a required pointer is NULL";
+    case MASQ_ERR_SHAPE: return "dimension outside the supported limits";
+    case MASQ_ERR_BITS: return "bit-width outside [2, 16]";
+    case MASQ_ERR_ALIGN: return "pointer or leading dimension misaligned (16-byte rows required)";
+    case MASQ_ERR_WORKSPACE: return "workspace missing, misaligned or smaller than masq_workspace_size()";
+    case MASQ_ERR_BAD_MODALITY: return "token tagged with unknown modality (id >= n_mod)";
+    case MASQ_ERR_EMPTY_MODALITY: return "modality with zero calibration tokens";
+    case MASQ_ERR_UNSUPPORTED: return "valid request outside this path (e.g. 16-bit operands)";
+    case MASQ_ERR_CUDA: return "CUDA runtime or driver call failed";
+  }
+  return "unknown status";
+}
+
+const char* masq_version(void) { return "0.1.0 sm_100a"; }
+
+}  // extern "C"

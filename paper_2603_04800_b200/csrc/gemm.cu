@@ -1,0 +1,449 @@
+// gemm.cu — persistent, warp-specialised tcgen05 GEMM for the MASQuant hot path (sm_100a).
+//
+// One kernel template serves four epilogues:
+//   kModeFwd  A6+A7: acc = qx . qw^T (kind::i8, s32 in TMEM); y = acc * dx[t] * dw[j];
+//             tiles that contain non-text tokens get the CMC term
+//             y += [Zhi | Zlo] . [L2^T ; L2^T] (kind::f16, fp32) accumulated on top of y,
+//             which the epilogue writes back into the same TMEM columns first.
+//   kModeAcc  debug tap: raw int32 accumulators.
+//   kModeLoss A8: per modality m present in the tile, acc = qx . Q(S_m W)^T, and
+//             sum |acc*dx*dw_m - Yref| over rows with id == m -> per-(unit, warp) partials.
+//   kModeRef  Yref = X . W (kind::f16 bf16 -> fp32), the loss target.
+//
+// Roles (192 threads, 1 CTA per SM, grid = min(#units, #SMs)):
+//   warp 0 lane 0 : TMA producer  (A [128 x 128B] + B [256 x 128B] per k-block, 4-stage ring)
+//   warp 1 lane 0 : MMA issuer    (4 x tcgen05.mma per k-block into a 256-column TMEM buffer)
+//   warps 2..5    : epilogue      (tcgen05.ld 32x32b -> dequant -> swizzled smem -> TMA store)
+// TMEM holds two 128x256 accumulators (512 columns) so the epilogue of tile i overlaps the
+// main loop of tile i+1.  The CMC k-blocks of tile i are inserted into the k-block stream of
+// tile i+1 (after kCmcDefer main k-blocks), by which time the epilogue has converted tile i's
+// int32 accumulator to f32 in place; no extra TMEM columns and no Y round trip are needed.
+#include <cstdio>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace masq {
+using namespace sm100;
+
+namespace {
+constexpr int BM = kTileM, BN = kTileN, BKB = 128;  // BKB: k-block bytes (128 int8 / 64 bf16)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BKB;
+constexpr int B_BYTES = BN * BKB;
+constexpr int EPI_WARPS = 4;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int STG_BYTES = 32 * 32 * 4;
+constexpr int SMEM_A = 0;
+constexpr int SMEM_B = SMEM_A + STAGES * A_BYTES;
+constexpr int SMEM_STG = SMEM_B + STAGES * B_BYTES;
+constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * 2 * STG_BYTES;
+constexpr int SMEM_USED = SMEM_BAR + 256;
+constexpr int SMEM_ALLOC = SMEM_USED + 1024;
+constexpr int kCmcDefer = 4;
+constexpr int kRasterGroup = 8;
+constexpr uint32_t IDESC_I8 = idesc_i8(BM, BN);
+constexpr uint32_t IDESC_BF16 = idesc_bf16(BM, BN);
+
+struct Params {
+  int mode;
+  int T, n, d;
+  int num_m, num_n, num_kb, n_units, n_tiles;
+  int n_mod;
+  const float* dx;
+  const float* dw;
+  const uint32_t* tile_mask;
+  const uint8_t* ids;
+  int rpad, cmc_kb;
+  const float* yref;
+  long long ld_ref;
+  double* partials;
+};
+
+struct Unit {
+  int tile, mt, nt, m;
+  uint32_t mask;
+};
+
+__device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
+  const bool loss = p.mode == kModeLoss;
+  w.tile = loss ? u / p.n_mod : u;
+  w.m = loss ? u % p.n_mod : 0;
+  // grouped raster: kRasterGroup consecutive n-tiles swept over all m-tiles
+  const int per_group = kRasterGroup * p.num_m;
+  const int g = w.tile / per_group;
+  const int rem = w.tile - g * per_group;
+  const int nt0 = g * kRasterGroup;
+  const int gsz = min(kRasterGroup, p.num_n - nt0);
+  w.mt = rem / gsz;
+  w.nt = nt0 + (rem - w.mt * gsz);
+  w.mask = p.tile_mask ? p.tile_mask[w.mt] : 1u;
+  if (loss && !((w.mask >> w.m) & 1u)) return false;
+  return true;
+}
+__device__ __forceinline__ bool unit_has_cmc(const Params& p, const Unit& w) {
+  return p.mode == kModeFwd && p.rpad > 0 && (w.mask & ~1u) != 0u;
+}
+
+struct Ring {
+  uint32_t stage = 0, phase = 0;
+  __device__ __forceinline__ void advance() {
+    if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+  }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 1)
+masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmZ,
+                 const __grid_constant__ CUtensorMap tmL2, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* smA = smem + SMEM_A;
+  uint8_t* smB = smem + SMEM_B;
+  uint8_t* smS = smem + SMEM_STG;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;     // [2] MMA -> epilogue: accumulator ready
+  uint64_t* tempty = tfull + 2;         // [2] epilogue -> MMA: TMEM buffer drained
+  uint64_t* conv = tempty + 2;          // [2] epilogue -> MMA: y_base written back (CMC)
+  uint64_t* cmcd = conv + 2;            // [2] MMA -> epilogue: CMC accumulated
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cmcd + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (MODE == kModeFwd || MODE == kModeAcc || MODE == kModeRef) tma_prefetch(&tmY);
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI_WARPS);
+      mbar_init(&conv[i], EPI_WARPS);
+      mbar_init(&cmcd[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  constexpr int KELEMS = (MODE == kModeRef) ? 64 : 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      Ring ring;
+      bool pend = false;
+      Unit pu{};
+      auto load_cmc = [&](const Unit& w) {
+        for (int mm = 1; mm < p.n_mod; ++mm) {
+          if (!((w.mask >> mm) & 1u)) continue;
+          for (int kb = 0; kb < p.cmc_kb; ++kb) {
+            mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+            mbar_expect_tx(&full[ring.stage], A_BYTES + B_BYTES);
+            tma_load_2d(smA + ring.stage * A_BYTES, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64,
+                        w.mt * BM);
+            tma_load_2d(smB + ring.stage * B_BYTES, &tmL2, &full[ring.stage], kb * 64,
+                        (mm - 1) * p.n + w.nt * BN);
+            ring.advance();
+          }
+        }
+      };
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        Unit w;
+        if (!decode_unit(p, u, w)) continue;
+        const int brow = (MODE == kModeLoss ? w.m * p.n : 0) + w.nt * BN;
+        const int defer_at = min(kCmcDefer, p.num_kb - 1);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
+          mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+          mbar_expect_tx(&full[ring.stage], A_BYTES + B_BYTES);
+          tma_load_2d(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, w.mt * BM);
+          tma_load_2d(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow);
+          ring.advance();
+        }
+        if (unit_has_cmc(p, w)) { pend = true; pu = w; }
+      }
+      if (pend) load_cmc(pu);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      Ring ring;
+      uint32_t local = 0, cmc_cnt[2] = {0u, 0u};   // conv/cmcd phases count CMC uses per buffer
+      bool pend = false;
+      Unit pu{};
+      uint32_t pbuf = 0, pph = 0;
+      const uint32_t a0 = smem_u32(smA), b0 = smem_u32(smB);
+      auto issue_cmc = [&](const Unit& w, uint32_t buf, uint32_t ph) {
+        mbar_wait(&conv[buf], ph);
+        tc_fence_after();
+        for (int mm = 1; mm < p.n_mod; ++mm) {
+          if (!((w.mask >> mm) & 1u)) continue;
+          for (int kb = 0; kb < p.cmc_kb; ++kb) {
+            mbar_wait(&full[ring.stage], ring.phase);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              mma_bf16(tmem_base + buf * BN, umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32),
+                       umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32), IDESC_BF16, 1u);
+            }
+            mma_commit(&empty[ring.stage]);
+            ring.advance();
+          }
+        }
+        mma_commit(&cmcd[buf]);
+      };
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        Unit w;
+        if (!decode_unit(p, u, w)) continue;
+        const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
+        ++local;
+        mbar_wait(&tempty[buf], ph ^ 1u);
+        tc_fence_after();
+        const uint32_t dtm = tmem_base + buf * BN;
+        const int defer_at = min(kCmcDefer, p.num_kb - 1);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if (pend && kb == defer_at) { issue_cmc(pu, pbuf, pph); pend = false; }
+          mbar_wait(&full[ring.stage], ring.phase);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32);
+            const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
+            if (MODE == kModeRef) mma_bf16(dtm, ad, bd, IDESC_BF16, (kb | k) != 0);
+            else mma_i8(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
+          }
+          mma_commit(&empty[ring.stage]);
+          ring.advance();
+        }
+        mma_commit(&tfull[buf]);
+        if (unit_has_cmc(p, w)) {
+          pend = true;
+          pu = w;
+          pbuf = buf;
+          pph = cmc_cnt[buf] & 1u;
+          ++cmc_cnt[buf];
+        }
+      }
+      if (pend) issue_cmc(pu, pbuf, pph);
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------------------- epilogue warps
+    const uint32_t q = warp & 3u;                       // TMEM lane quarter this warp may access
+    uint8_t* stg0 = smS + q * 2 * STG_BYTES;
+    uint32_t sc = 0, local = 0, cmc_cnt[2] = {0u, 0u};
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      Unit w;
+      if (!decode_unit(p, u, w)) continue;
+      const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
+      ++local;
+      mbar_wait(&tfull[buf], ph);
+      tc_fence_after();
+      const int row0 = w.mt * BM + q * 32;
+      const int row = row0 + (int)lane;
+      const bool rowv = row < p.T;
+      const int col_base = w.nt * BN;
+      const int nchunks = min(BN, p.n - col_base) / 32;
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN;
+      float dxr = 0.f;
+      if (MODE != kModeRef && rowv) dxr = p.dx[row];
+      const float* dwp = p.dw + (MODE == kModeLoss ? (size_t)w.m * p.n : 0) + col_base;
+
+      auto store_chunk = [&](const uint32_t (&v)[32], int c) {
+        uint8_t* sb = stg0 + (sc & 1u) * STG_BYTES;
+        if (sc >= 2) {
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+        }
+        const uint32_t base = smem_u32(sb) + lane * 128u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t dst = base + (((uint32_t)j ^ (lane & 7u)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v[4 * j]), "r"(v[4 * j + 1]),
+                       "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmY, sb, col_base + c * 32, row0);
+          bulk_commit();
+        }
+        ++sc;
+      };
+      auto dequant = [&](uint32_t (&v)[32], int c) {
+        const float4* dw4 = reinterpret_cast<const float4*>(dwp + c * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 s4 = __ldg(dw4 + j);
+          v[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 0], dxr), s4.x));
+          v[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 1], dxr), s4.y));
+          v[4 * j + 2] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 2], dxr), s4.z));
+          v[4 * j + 3] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 3], dxr), s4.w));
+        }
+      };
+
+      if (MODE == kModeFwd && unit_has_cmc(p, w)) {
+        // 1) int32 -> y_base (f32) in place, 2) let the MMA warp accumulate CMC on top, 3) store.
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_wait_ld();
+          dequant(v, c);
+          tmem_st32(taddr + c * 32, v);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[buf]);
+        mbar_wait(&cmcd[buf], cmc_cnt[buf] & 1u);
+        ++cmc_cnt[buf];
+        tc_fence_after();
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_wait_ld();
+          store_chunk(v, c);
+        }
+      } else if (MODE == kModeLoss) {
+        const bool rv = rowv && p.ids[row] == (uint8_t)w.m;
+        double part = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_wait_ld();
+          dequant(v, c);
+          if (rv) {
+            const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)row * p.ld_ref + col_base + c * 32);
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 y = __ldg(r4 + j);
+              acc += fabsf(__uint_as_float(v[4 * j + 0]) - y.x) + fabsf(__uint_as_float(v[4 * j + 1]) - y.y) +
+                     fabsf(__uint_as_float(v[4 * j + 2]) - y.z) + fabsf(__uint_as_float(v[4 * j + 3]) - y.w);
+            }
+            part += (double)acc;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) p.partials[((size_t)w.m * p.n_tiles + w.tile) * EPI_WARPS + q] = part;
+      } else {
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_wait_ld();
+          if (MODE == kModeFwd) dequant(v, c);
+          store_chunk(v, c);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+template <int MODE>
+cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
+                        const CUtensorMap& l2, const Params& p, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(masq_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_ALLOC);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  masq_gemm_kernel<MODE><<<grid, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
+  return cudaGetLastError();
+}
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
+  if (g.T <= 0 || g.n <= 0) return cudaSuccess;
+  CUtensorMap ta, tb, ty, tz, tl2;
+  const bool bf = g.mode == kModeRef;
+  bool ok = true;
+  if (bf) {
+    ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
+    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.b_rows, g.d, g.d, BN, 64, true);
+  } else {
+    ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, BM, 128, true);
+    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BN, 128, true);
+  }
+  if (g.mode != kModeLoss) {
+    ok &= make_tmap_2d(&ty, g.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.T, g.n, g.ld_out, 32, 32, true);
+  } else {
+    ty = ta;
+  }
+  const bool cmc = g.mode == kModeFwd && g.rpad > 0;
+  if (cmc) {
+    const int64_t zc = (int64_t)(g.n_mod - 1) * 2 * g.rpad;
+    ok &= make_tmap_2d(&tz, g.z, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, zc, zc, BM, 64, true);
+    ok &= make_tmap_2d(&tl2, g.l2t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)(g.n_mod - 1) * g.n,
+                       2 * g.rpad, 2 * g.rpad, BN, 64, true);
+  } else {
+    tz = ta;
+    tl2 = tb;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+
+  Params p{};
+  p.mode = g.mode;
+  p.T = (int)g.T;
+  p.n = (int)g.n;
+  p.d = (int)g.d;
+  p.num_m = (int)ceil_div(g.T, BM);
+  p.num_n = (int)ceil_div(g.n, BN);
+  p.num_kb = (int)ceil_div(g.d, bf ? 64 : 128);
+  p.n_tiles = p.num_m * p.num_n;
+  p.n_mod = g.n_mod;
+  p.n_units = g.mode == kModeLoss ? p.n_tiles * g.n_mod : p.n_tiles;
+  p.dx = g.dx;
+  p.dw = g.dw;
+  p.tile_mask = g.tile_mask;
+  p.ids = g.ids;
+  p.rpad = cmc ? g.rpad : 0;
+  p.cmc_kb = cmc ? (2 * g.rpad) / 64 : 0;
+  p.yref = g.yref;
+  p.ld_ref = g.ld_ref;
+  p.partials = g.partials;
+  const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
+  switch (g.mode) {
+    case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, grid, st);
+    case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, grid, st);
+    case kModeLoss: return launch_mode<kModeLoss>(ta, tb, ty, tz, tl2, p, grid, st);
+    case kModeRef: return launch_mode<kModeRef>(ta, tb, ty, tz, tl2, p, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace masq

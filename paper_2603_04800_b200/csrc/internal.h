@@ -1,0 +1,98 @@
+// internal.h — host-side contracts between the C ABI (api.cu) and the kernel translation
+// units (elem.cu, gemm.cu, zgemm.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/masq.h"
+
+namespace masq {
+
+constexpr int kMaxMod = 8;
+constexpr int kTileM = 128;        // GEMM M tile (token rows)
+constexpr int kTileN = 256;        // GEMM N tile (output channels)
+constexpr int kStatusBytes = 256;
+
+// sticky device status bits (stored in ws[0..3])
+constexpr uint32_t kStBadModality = 1u << 0;
+constexpr uint32_t kStEmptyModality = 1u << 1;
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t rpad_of(int64_t r) { return r > 0 ? ceil_div(r, 64) * 64 : 0; }
+
+struct WsLayout {
+  size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0;
+  size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, total = 0;
+};
+WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r);
+
+// ---------------------------------------------------------------- elementwise kernels (elem.cu)
+cudaError_t launch_stats(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                         int n_mod, float* R, int64_t* count, uint32_t* status, cudaStream_t st);
+cudaError_t launch_init(const float* R, const int64_t* count, const void* W, masq_dtype wt, int64_t d, int64_t n,
+                        int n_mod, float* s, float* wmax, uint32_t* status, cudaStream_t st);
+// weight quantization of n_sets factor vectors s[k*d..] -> qw[k*n*d..], dw[k*n..]
+cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_sets, int64_t d, int64_t n,
+                          int wbits, int8_t* qw, float* dw, uint32_t* amax_scratch, cudaStream_t st);
+cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st);
+cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                          int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
+                          uint32_t* status, cudaStream_t st);
+// L1 [(M-1) x d x r] -> L1t [(M-1) x rpad x d];  L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (dup hi/lo)
+cudaError_t launch_pack_lowrank(const uint16_t* L1, const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t d,
+                                int64_t n, int r, int rpad, uint16_t* L1t, uint16_t* L2t, cudaStream_t st);
+// bf16 W [d x n] -> Wt [n x d]
+cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint16_t* Wt, cudaStream_t st);
+cudaError_t launch_loss_reduce(const double* partials, int64_t tiles, const uint8_t* ids, int64_t T, int n_mod,
+                               int64_t n, const float* lambda_host, double* sums, int64_t* counts, double* loss,
+                               cudaStream_t st);
+cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
+                                 int64_t n, double* loss, cudaStream_t st);
+
+// ---------------------------------------------------------------- tensor maps (tmap.cu)
+// 2-D row-major tensor [rows x cols] of elem_bytes elements, row pitch ld elements,
+// box [box_rows x box_cols], 128-byte swizzle when swizzle128 (box_cols*elem_bytes must be 128).
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,
+                  uint64_t cols, uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+
+// ---------------------------------------------------------------- GEMM (gemm.cu)
+enum GemmMode { kModeFwd = 0, kModeAcc = 1, kModeLoss = 2, kModeRef = 3 };
+
+struct GemmArgs {
+  int mode;
+  int64_t T, n, d;                 // rows, output columns, K
+  const int8_t* qx;                // int8 A [T x d]   (kModeFwd/Acc/Loss)
+  const uint16_t* xbf;             // bf16 A [T x ld_x] (kModeRef)
+  int64_t ld_x;
+  const void* b;                   // int8 qw [(n_b) x d] or bf16 Wt [n x d]
+  int64_t b_rows;                  // rows of the B tensor (n, or n_mod*n for the loss)
+  const float* dx;
+  const float* dw;                 // [n] or [n_mod * n] for the loss
+  const uint32_t* tile_mask;       // per 128-row tile
+  const uint8_t* ids;              // loss row masks
+  int n_mod;
+  void* out;                       // Y f32 / acc int32 [T x ld_out]
+  int64_t ld_out;
+  // CMC (kModeFwd, r > 0)
+  int rpad;                        // 0 -> no CMC
+  const uint16_t* z;               // [T x (M-1)*2*rpad] bf16 (hi | lo per modality)
+  const uint16_t* l2t;             // [(M-1)*n x 2*rpad] bf16
+  // loss
+  const float* yref;
+  int64_t ld_ref;
+  double* partials;                // [n_mod][tiles][4]
+};
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
+int num_sms();
+
+// ---------------------------------------------------------------- CMC first factor (zgemm.cu)
+// Z[t, (m-1)*2*rpad + k] = hi(xs_t . L1^m)_k, [.. + rpad + k] = lo(...) for rows with id_t == m,
+// zeros for other rows of tiles that contain modality m.
+cudaError_t launch_zgemm(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                         int n_mod, const float* inv_s, const uint16_t* L1t, int rpad, const uint32_t* tile_mask,
+                         uint16_t* Z, cudaStream_t st);
+
+}  // namespace masq

@@ -1,0 +1,230 @@
+"""Thin PyTorch binding over the C ABI (include/masq.h): argument marshalling only.
+
+Every step of the hot path runs in libmasq.so's sm_100a kernels; torch supplies device
+memory (tensors), the current CUDA stream and nothing else.  Names follow the ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import MasqDebug, lib
+
+MASQ_F32, MASQ_BF16 = 0, 1
+OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE = range(7)
+
+
+class MasqError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib().masq_status_string(status).decode()
+        super().__init__(f"{where}: status {status} ({msg})")
+        self.status = status
+
+
+def _ck(status: int, where: str):
+    if status != 0:
+        raise MasqError(status, where)
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return MASQ_BF16
+    if t.dtype == torch.float32:
+        return MASQ_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or f32)")
+
+
+def _cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    return t
+
+
+class Workspace:
+    """Caller-owned scratch for the ABI (grown on demand; first bytes hold the sticky status)."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.zeros(nbytes + 256, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+    def ptr_size(self, nbytes: int):
+        b = self.get(nbytes)
+        base = b.data_ptr()
+        off = (-base) % 256
+        return ctypes.c_void_p(base + off), b.numel() - off
+
+
+_WS = {}
+
+
+def default_workspace(device=None) -> Workspace:
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    if dev not in _WS:
+        _WS[dev] = Workspace(torch.device("cuda", dev))
+    return _WS[dev]
+
+
+def workspace_size(op: int, T: int, d: int, d_out: int, n_mod: int, r: int = 0) -> int:
+    return int(lib().masq_workspace_size(op, T, d, d_out, n_mod, r))
+
+
+def check(ws: Workspace | None = None, stream=None):
+    """Synchronize and raise if a device-side data error (bad id / empty modality) was flagged."""
+    ws = ws or default_workspace()
+    p, _ = ws.ptr_size(256)
+    _ck(lib().masq_check(p, _stream(stream)), "masq_check")
+
+
+# ----------------------------------------------------------------------------- A1
+def calibrate_stats(X, mod_id, n_mod: int, R=None, count=None, reset: bool = True, ws=None, stream=None):
+    _cuda(X, "X")
+    T, d = X.shape
+    if R is None:
+        R = torch.zeros(n_mod, d, dtype=torch.float32, device=X.device)
+    if count is None:
+        count = torch.zeros(n_mod, dtype=torch.int64, device=X.device)
+    ws = ws or default_workspace(X.device)
+    p, n = ws.ptr_size(workspace_size(OP_STATS, T, d, 0, n_mod))
+    _ck(lib().masq_calibrate_stats(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, n_mod, _p(R), _p(count),
+                                   1 if reset else 0, p, n, _stream(stream)), "masq_calibrate_stats")
+    return R, count
+
+
+# ----------------------------------------------------------------------------- A2
+def init_factors(R, count, W, ws=None, stream=None, return_wmax: bool = False):
+    n_mod, d = R.shape
+    d_out = W.shape[1]
+    s = torch.empty(n_mod, d, dtype=torch.float32, device=R.device)
+    wmax = torch.empty(d, dtype=torch.float32, device=R.device) if return_wmax else None
+    ws = ws or default_workspace(R.device)
+    p, n = ws.ptr_size(workspace_size(OP_INIT, 0, d, d_out, n_mod))
+    _ck(lib().masq_init_factors(_p(R), _p(count), _p(W.contiguous()), _dt(W), d, d_out, n_mod, _p(s), _p(wmax),
+                                p, n, _stream(stream)), "masq_init_factors")
+    return (s, wmax) if return_wmax else s
+
+
+# ----------------------------------------------------------------------------- A3
+def quantize_weight(W, s_vec, wbits: int, ws=None, stream=None):
+    d, d_out = W.shape
+    qw = torch.empty(d_out, d, dtype=torch.int8, device=W.device)
+    dw = torch.empty(d_out, dtype=torch.float32, device=W.device)
+    ws = ws or default_workspace(W.device)
+    p, n = ws.ptr_size(workspace_size(OP_QWEIGHT, 0, d, d_out, 1))
+    _ck(lib().masq_quantize_weight(_p(W.contiguous()), _dt(W), _p(s_vec.contiguous()), d, d_out, wbits, _p(qw),
+                                   _p(dw), p, n, _stream(stream)), "masq_quantize_weight")
+    return qw, dw
+
+
+# ----------------------------------------------------------------------------- A4
+def quantize_activations(X, mod_id, s, abits: int, ws=None, stream=None):
+    T, d = X.shape
+    n_mod = s.shape[0]
+    qx = torch.empty(T, d, dtype=torch.int8, device=X.device)
+    dx = torch.empty(T, dtype=torch.float32, device=X.device)
+    mask = torch.empty((T + 127) // 128, dtype=torch.int32, device=X.device)
+    ws = ws or default_workspace(X.device)
+    p, n = ws.ptr_size(workspace_size(OP_QACT, T, d, 0, n_mod))
+    _ck(lib().masq_quantize_activations(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, n_mod, _p(s.contiguous()),
+                                        abits, _p(qx), _p(dx), _p(mask), p, n, _stream(stream)),
+        "masq_quantize_activations")
+    return qx, dx, mask
+
+
+# ----------------------------------------------------------------------------- A4-A7
+def linear_forward(X, mod_id, s, qw, dw, wbits: int, abits: int, L1=None, L2=None, Y=None,
+                   acc_debug: bool = False, ws=None, stream=None):
+    """Y = Q(X_m S_m^-1) Q(S_t W) [+ X_m S_m^-1 L1^m L2^m for m != text].
+
+    L1: bf16 [n_mod-1, d, r]; L2: bf16 [n_mod-1, r, d_out] (or a column view with a row stride).
+    acc_debug=True returns the raw int32 accumulators instead (CMC skipped).
+    """
+    T, d = X.shape
+    d_out = qw.shape[0]
+    n_mod = s.shape[0]
+    r = 0 if L1 is None else int(L1.shape[-1])
+    ld_l2 = 0 if L2 is None else int(L2.stride(-2))
+    dbg = None
+    if acc_debug:
+        out = torch.empty(T, d_out, dtype=torch.int32, device=X.device)
+        dbg = MasqDebug(out.data_ptr(), out.stride(0))
+        Yp, ldy = None, d_out
+    else:
+        out = torch.empty(T, d_out, dtype=torch.float32, device=X.device) if Y is None else Y
+        Yp, ldy = _p(out), out.stride(0)
+    ws = ws or default_workspace(X.device)
+    p, n = ws.ptr_size(workspace_size(OP_FORWARD, T, d, d_out, n_mod, r if not acc_debug else 0))
+    _ck(lib().masq_linear_forward(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod,
+                                  _p(s.contiguous()), _p(qw), _p(dw), wbits, abits, _p(L1), _p(L2), ld_l2, r,
+                                  Yp, ldy, p, n, ctypes.byref(dbg) if dbg is not None else None,
+                                  _stream(stream)), "masq_linear_forward")
+    return out
+
+
+# ----------------------------------------------------------------------------- A8
+def reference_output(X, W, Yref=None, ws=None, stream=None):
+    T, d = X.shape
+    d_out = W.shape[1]
+    out = torch.empty(T, d_out, dtype=torch.float32, device=X.device) if Yref is None else Yref
+    ws = ws or default_workspace(X.device)
+    p, n = ws.ptr_size(workspace_size(OP_REFERENCE, T, d, d_out, 1))
+    _ck(lib().masq_reference_output(_p(X), X.stride(0), _p(W.contiguous()), T, d, d_out, _p(out), out.stride(0),
+                                    p, n, _stream(stream)), "masq_reference_output")
+    return out
+
+
+def _lambda_arr(lam, n_mod):
+    if lam is None:
+        return None
+    arr = (ctypes.c_float * n_mod)(*[float(v) for v in lam])
+    return arr
+
+
+def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, sums=None, counts=None, loss=None,
+               ws=None, stream=None):
+    """Per-modality sums of |Q(X_m S_m^-1) Q(S_m W) - X_m W|, counts and the weighted MAE loss
+    (PAPER.md:62-70).  Returns device tensors (sums f64 [M], counts i64 [M], loss f64 [1])."""
+    T, d = X.shape
+    d_out = W.shape[1]
+    n_mod = s.shape[0]
+    dev = X.device
+    sums = torch.empty(n_mod, dtype=torch.float64, device=dev) if sums is None else sums
+    counts = torch.empty(n_mod, dtype=torch.int64, device=dev) if counts is None else counts
+    loss = torch.empty(1, dtype=torch.float64, device=dev) if loss is None else loss
+    ws = ws or default_workspace(dev)
+    p, n = ws.ptr_size(workspace_size(OP_LOSS, T, d, d_out, n_mod))
+    lam_arr = _lambda_arr(lam, n_mod)
+    _ck(lib().masq_calib_loss(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod, _p(s.contiguous()),
+                              _p(W.contiguous()), _dt(W), wbits, abits,
+                              ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr is not None else None,
+                              _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), p, n, _stream(stream)),
+        "masq_calib_loss")
+    return sums, counts, loss
+
+
+def loss_finalize(sums, counts, d_out: int, lam=None, loss=None, stream=None):
+    n_mod = sums.shape[0]
+    loss = torch.empty(1, dtype=torch.float64, device=sums.device) if loss is None else loss
+    lam_arr = _lambda_arr(lam, n_mod)
+    _ck(lib().masq_loss_finalize(_p(sums), _p(counts), ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr else None,
+                                 n_mod, d_out, _p(loss), _stream(stream)), "masq_loss_finalize")
+    return loss
+
+
+def version() -> str:
+    return lib().masq_version().decode()

@@ -1,0 +1,86 @@
+"""CPU-side checks of the C ABI boundary: the library loads and exports every symbol that
+include/masq.h declares; the binding mirrors the header; workspace arithmetic; argument
+validation paths that return before any CUDA call."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "masq.h")
+SO = os.path.join(ROOT, "paper_2603_04800_b200", "libmasq.so")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(masq_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def so():
+    if not os.path.exists(SO):
+        import __graft_entry__
+        __graft_entry__.build()
+    return ctypes.CDLL(SO)
+
+
+def test_header_declares_the_five_operations():
+    fns = header_functions()
+    for f in ("masq_calibrate_stats", "masq_init_factors", "masq_quantize_weight", "masq_linear_forward",
+              "masq_calib_loss"):
+        assert f in fns
+
+
+def test_library_exports_every_header_symbol(so):
+    for f in header_functions():
+        assert hasattr(so, f), f
+
+
+def test_binding_mirrors_header():
+    from paper_2603_04800_b200._lib import SIGNATURES
+    assert sorted(SIGNATURES) == header_functions()
+
+
+def test_status_strings_and_version(so):
+    from paper_2603_04800_b200._lib import lib
+    L = lib()
+    assert L.masq_version().decode().endswith("sm_100a")
+    for st in range(10):
+        assert L.masq_status_string(st)
+
+
+def test_workspace_sizes(so):
+    from paper_2603_04800_b200._lib import lib
+    L = lib()
+    T, d, n, M = 16384, 3584, 18944, 2
+    fwd0 = L.masq_workspace_size(4, T, d, n, M, 0)
+    fwd64 = L.masq_workspace_size(4, T, d, n, M, 64)
+    assert fwd0 >= T * d + 4 * T
+    assert fwd64 - fwd0 >= 2 * T * 2 * 64 * (M - 1)   # Z hi/lo
+    loss = L.masq_workspace_size(5, T, d, n, M, 0)
+    assert loss >= M * n * d                          # one Q(S_m W) per modality
+    assert L.masq_workspace_size(0, T, d, 0, M, 0) == 256
+
+
+def test_argument_errors_return_before_launch(so):
+    """Synchronous validation (no device needed): NULL, shape, bits, workspace."""
+    from paper_2603_04800_b200._lib import lib
+    L = lib()
+    ws = ctypes.create_string_buffer(4096)
+    p = ctypes.c_void_p(ctypes.addressof(ws))
+    # n_mod out of range -> SHAPE
+    assert L.masq_calibrate_stats(None, 1, 64, None, 10, 64, 9, p, p, 1, p, 4096, None) == 2
+    # d not multiple of 16 -> SHAPE
+    assert L.masq_calibrate_stats(None, 1, 64, None, 10, 60, 2, p, p, 1, p, 4096, None) == 2
+    # R NULL -> NULL
+    assert L.masq_calibrate_stats(None, 1, 64, None, 10, 64, 2, None, p, 1, p, 4096, None) == 1
+    # wbits 16 -> UNSUPPORTED, wbits 1 -> BITS
+    assert L.masq_quantize_weight(p, 1, p, 64, 128, 16, p, p, p, 4096, None) == 8
+    assert L.masq_quantize_weight(p, 1, p, 64, 128, 1, p, p, p, 4096, None) == 3
+    # r not multiple of 16 -> SHAPE
+    assert L.masq_linear_forward(p, 1, 64, p, 10, 64, 128, 2, p, p, p, 8, 8, p, p, 128, 8, p, 128, p, 4096,
+                                 None, None) == 2
+    # workspace too small -> WORKSPACE
+    assert L.masq_quantize_weight(p, 1, p, 64, 128, 8, p, p, p, 16, None) == 5
