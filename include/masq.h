@@ -21,7 +21,7 @@
  *    561), n_mod = |M| in [1, 8].
  *  - Every array pointer is a DEVICE pointer owned by the caller, except
  *    `lambda` (host).  The library allocates nothing and keeps no global
- *    state; scratch comes from the caller's workspace `ws` (size from
+ *    state (except the opt-in profiler below); scratch comes from the caller's workspace `ws` (size from
  *    masq_workspace_size, 256-byte aligned).  Calls on the same ws must be
  *    stream-ordered; concurrent calls need distinct ws.
  *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
@@ -193,6 +193,17 @@ masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const 
 masq_status masq_check(void* ws, masq_stream stream);
 
 const char* masq_status_string(masq_status s);
+
+/*
+ * Opt-in kernel timing (measurement only; off by default; the one piece of process-global
+ * state).  masq_profile_enable(1) starts recording a cudaEvent pair on the launching stream
+ * around every kernel the library launches (and discards earlier records); it returns the
+ * previous state.  masq_profile_collect() waits for the recorded events and aggregates them
+ * by kernel name: names[i*32 .. i*32+31] (NUL-terminated), total_ms[i], launches[i] for
+ * i < return value (at most max_entries); it clears the records.  Returns -1 on a CUDA error.
+ */
+int32_t masq_profile_enable(int32_t on);
+int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms, int64_t* launches);
 
 /* Library identification: "<version> sm_100a". */
 const char* masq_version(void);

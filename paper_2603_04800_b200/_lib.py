@@ -40,6 +40,8 @@ SIGNATURES = {
                                   c_void_p, c_size_t, c_void_p]),
     "masq_loss_finalize": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]),
     "masq_check": (c_int32, [c_void_p, c_void_p]),
+    "masq_profile_enable": (c_int32, [c_int32]),
+    "masq_profile_collect": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p]),
     "masq_status_string": (ctypes.c_char_p, [c_int32]),
     "masq_version": (ctypes.c_char_p, []),
 }

@@ -148,8 +148,11 @@ cudaError_t stats_dispatch(const XT* X, int64_t ld_x, const uint8_t* ids, int64_
   dim3 grid(gx, strips);
   auto* c = reinterpret_cast<unsigned long long*>(count);
   switch (n_mod) {
-#define MASQ_STATS_CASE(NM) \
-  case NM: stats_kernel<XT, NM><<<grid, 256, 0, st>>>(X, ld_x, ids, T, d, rows, R, c, status); break;
+#define MASQ_STATS_CASE(NM)                                                       \
+  case NM: {                                                                      \
+    ProfScope ps_("stats", st);                                                   \
+    stats_kernel<XT, NM><<<grid, 256, 0, st>>>(X, ld_x, ids, T, d, rows, R, c, status); \
+  } break;
     MASQ_STATS_CASE(1) MASQ_STATS_CASE(2) MASQ_STATS_CASE(3) MASQ_STATS_CASE(4)
     MASQ_STATS_CASE(5) MASQ_STATS_CASE(6) MASQ_STATS_CASE(7) MASQ_STATS_CASE(8)
 #undef MASQ_STATS_CASE
@@ -430,6 +433,7 @@ cudaError_t launch_stats(const void* X, masq_dtype xt, int64_t ld_x, const uint8
 cudaError_t launch_init(const float* R, const int64_t* count, const void* W, masq_dtype wt, int64_t d, int64_t n,
                         int n_mod, float* s, float* wmax, uint32_t* status, cudaStream_t st) {
   const int grid = (int)ceil_div(d, 8);
+  ProfScope ps_("init", st);
   if (wt == MASQ_BF16)
     init_kernel<<<grid, 256, 0, st>>>(R, count, static_cast<const __nv_bfloat16*>(W), d, n, n_mod, s, wmax, status);
   else
@@ -450,17 +454,18 @@ cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_se
   dim3 g1(gx, strips, n_sets), g2((unsigned)ceil_div(n, 128), (unsigned)ceil_div(d, 128), n_sets);
   if (wt == MASQ_BF16) {
     auto* w = static_cast<const __nv_bfloat16*>(W);
-    wcolmax_kernel<<<g1, 256, 0, st>>>(w, s, d, n, rows, amax);
-    wquant_kernel<<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw);
+    { ProfScope ps_("wcolmax", st); wcolmax_kernel<<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
+    { ProfScope ps_("wquant", st); wquant_kernel<<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw); }
   } else {
     auto* w = static_cast<const float*>(W);
-    wcolmax_kernel<<<g1, 256, 0, st>>>(w, s, d, n, rows, amax);
-    wquant_kernel<<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw);
+    { ProfScope ps_("wcolmax", st); wcolmax_kernel<<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
+    { ProfScope ps_("wquant", st); wquant_kernel<<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw); }
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st) {
+  ProfScope ps_("inv", st);
   inv_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(s, count, inv);
   return cudaGetLastError();
 }
@@ -475,6 +480,7 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
   }
   const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
   const unsigned grid = (unsigned)ceil_div(T, 8);
+  ProfScope ps_("aquant", st);
   if (xt == MASQ_BF16)
     aquant_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X), ld_x, ids, T, d, n_mod, inv_s,
                                         (float)qmax, qmin, qmax, qx, dx, mask, status);
@@ -488,6 +494,7 @@ static cudaError_t transpose(const uint16_t* in, int64_t rows, int64_t cols, int
                              uint16_t* out, int64_t ld_out, int64_t out_batch, int64_t dup_off, int batches,
                              cudaStream_t st) {
   dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32), batches), block(32, 8);
+  ProfScope ps_("transpose", st);
   transpose_bf16_kernel<<<grid, block, 0, st>>>(in, rows, cols, ld_in, in_batch, out, ld_out, out_batch, dup_off);
   return cudaGetLastError();
 }
@@ -512,6 +519,7 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
 cudaError_t launch_loss_reduce(const double* partials, int64_t per_mod, const uint8_t* ids, int64_t T, int n_mod,
                                int64_t n, const float* lambda_host, double* sums, int64_t* counts, double* loss,
                                cudaStream_t st) {
+  ProfScope ps_("loss_reduce", st);
   loss_reduce_kernel<<<1, 256, 0, st>>>(partials, per_mod, ids, T, n_mod, n, make_lambda(lambda_host, n_mod), sums,
                                         counts, loss);
   return cudaGetLastError();
@@ -519,6 +527,7 @@ cudaError_t launch_loss_reduce(const double* partials, int64_t per_mod, const ui
 
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st) {
+  ProfScope ps_("loss_finalize", st);
   loss_finalize_kernel<<<1, 1, 0, st>>>(sums, counts, make_lambda(lambda_host, n_mod), n_mod, n, loss);
   return cudaGetLastError();
 }

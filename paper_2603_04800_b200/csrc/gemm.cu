@@ -372,6 +372,8 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  static const char* const kNames[4] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref"};
+  ProfScope ps_(kNames[MODE], st);
   masq_gemm_kernel<MODE><<<grid, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
   return cudaGetLastError();
 }

@@ -29,6 +29,21 @@ struct WsLayout {
 };
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r);
 
+// ---------------------------------------------------------------- opt-in kernel timing (prof.cu)
+// RAII: records a cudaEvent pair around a kernel launch when masq_profile_enable(1) is active.
+class ProfScope {
+ public:
+  ProfScope(const char* name, cudaStream_t st);
+  ~ProfScope();
+  ProfScope(const ProfScope&) = delete;
+  ProfScope& operator=(const ProfScope&) = delete;
+
+ private:
+  const char* name_;
+  cudaStream_t st_;
+  void* a_ = nullptr;
+};
+
 // ---------------------------------------------------------------- elementwise kernels (elem.cu)
 cudaError_t launch_stats(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                          int n_mod, float* R, int64_t* count, uint32_t* status, cudaStream_t st);

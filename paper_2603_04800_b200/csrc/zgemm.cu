@@ -198,6 +198,7 @@ cudaError_t zlaunch(const CUtensorMap& tm, const XT* X, int64_t ld_x, const uint
   uint32_t cols = 32;
   while ((int)cols < rpad) cols <<= 1;
   dim3 grid((unsigned)ceil_div(T, 128), (unsigned)(n_mod - 1));
+  ProfScope ps_("zgemm", st);
   zgemm_kernel<XT><<<grid, ZT, Z_ALLOC, st>>>(tm, X, ld_x, ids, (int)T, (int)d, n_mod, inv_s, rpad, cols, mask, Z);
   return cudaGetLastError();
 }

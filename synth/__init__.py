@@ -50,9 +50,13 @@ def seed_for(config_index: int, layer: int = 0, input_index: int = 0) -> int:
 
 def f32_to_bf16_bits(a: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even f32 -> bf16 bit pattern (finite inputs)."""
-    b = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
-    rounding = ((b >> 16) & 1) + 0x7FFF
-    return ((b + rounding) >> 16).astype(np.uint16)
+    # uint32 arithmetic cannot overflow for finite inputs (|bits| <= 0xFF7FFFFF, + <= 0x8000)
+    b = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    out = (b >> 16) & 1
+    out += 0x7FFF
+    out += b
+    out >>= 16
+    return out.astype(np.uint16)
 
 
 def bf16_bits_to_f32(bits: np.ndarray) -> np.ndarray:
@@ -83,9 +87,13 @@ def activations(ids: np.ndarray, d: int, n_mod: int, seed: int, gamma=None,
     out_idx = rng.choice(d, size=n_out, replace=False)
     chan[:, out_idx] *= 10.0
     g = np.array([gamma.get(m, 1.0) for m in range(n_mod)], dtype=np.float32)
-    scale = (g[:, None] * chan)[ids.astype(np.int64)]          # [T x d]
-    z = rng.standard_normal((ids.size, d), dtype=np.float32)
-    x = (scale * z).astype(np.float32)
+    scale = g[:, None] * chan                                   # [M x d] f32
+    x = rng.standard_normal((ids.size, d), dtype=np.float32)    # z
+    idx = ids.astype(np.int64)
+    for m in range(n_mod):                                      # x = scale[m(t)] * z, in place
+        rows = np.nonzero(idx == m)[0]
+        if rows.size:
+            x[rows] *= scale[m]
     return f32_to_bf16_bits(x) if as_bf16 else x
 
 
