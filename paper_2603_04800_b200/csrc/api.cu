@@ -6,7 +6,7 @@
 
 namespace masq {
 
-WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r) {
+WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x) {
   WsLayout L;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -35,8 +35,9 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.mask = take(sizeof(uint32_t) * tiles_m);
       if (rp > 0 && nnt > 0) {
         L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
-        L.l1t = take(sizeof(uint16_t) * (size_t)nnt * rp * d);
+        L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
         L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
+        if (f32_x) L.xsplit = take(sizeof(uint16_t) * 2 * (size_t)T * d);
       }
       break;
     case MASQ_OP_LOSS:
@@ -199,7 +200,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   if (T == 0) return MASQ_OK;
   MASQ_TRY(check_x(X, xt, ld_x, d));
   if (!mod_id) return MASQ_ERR_NULL;
-  const WsLayout L = ws_layout(MASQ_OP_FORWARD, T, d, d_out, n_mod, cmc ? r : 0);
+  const WsLayout L = ws_layout(MASQ_OP_FORWARD, T, d, d_out, n_mod, cmc ? r : 0, xt == MASQ_F32);
   MASQ_TRY(check_ws(ws, ws_bytes, L));
   cudaStream_t st = S(stream);
   float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
@@ -228,9 +229,16 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
-    MASQ_CK(launch_pack_lowrank(static_cast<const uint16_t*>(L1), static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1,
-                                d, d_out, r, rp, l1t, l2t, st));
-    MASQ_CK(launch_zgemm(X, xt, ld_x, mod_id, T, d, n_mod, inv, l1t, rp, mask, z, st));
+    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), inv, d, r, rp, n_mod - 1, l1t, st));
+    MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
+    if (xt == MASQ_BF16) {
+      MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st));
+    } else {
+      uint16_t* xh = reinterpret_cast<uint16_t*>(W8(ws, L.xsplit));
+      uint16_t* xl = xh + (size_t)T * d;
+      MASQ_CK(launch_split_f32(static_cast<const float*>(X), ld_x, T, d, xh, xl, st));
+      MASQ_CK(launch_zgemm(xh, d, xl, mod_id, T, d, n_mod, l1t, rp, mask, z, st));
+    }
     g.rpad = rp;
     g.z = z;
     g.l2t = l2t;

@@ -499,15 +499,12 @@ static cudaError_t transpose(const uint16_t* in, int64_t rows, int64_t cols, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_lowrank(const uint16_t* L1, const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t d,
-                                int64_t n, int r, int rpad, uint16_t* L1t, uint16_t* L2t, cudaStream_t st) {
-  cudaError_t e;
+cudaError_t launch_pack_l2(const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t n, int r, int rpad, uint16_t* L2t,
+                           cudaStream_t st) {
   if (r < rpad) {
-    if ((e = cudaMemsetAsync(L1t, 0, sizeof(uint16_t) * n_nt * rpad * d, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(L2t, 0, sizeof(uint16_t) * n_nt * n * 2 * rpad, st)) != cudaSuccess) return e;
+    cudaError_t e = cudaMemsetAsync(L2t, 0, sizeof(uint16_t) * n_nt * n * 2 * rpad, st);
+    if (e != cudaSuccess) return e;
   }
-  // L1^m [d x r] -> L1t^m [rpad x d]
-  if ((e = transpose(L1, d, r, r, d * r, L1t, d, (int64_t)rpad * d, -1, n_nt, st)) != cudaSuccess) return e;
   // L2^m [r x n] (ld_l2) -> L2t rows m*n + j, cols [k] and [rpad + k]
   return transpose(L2, r, n, ld_l2, (int64_t)r * ld_l2, L2t, 2 * rpad, n * 2 * rpad, rpad, n_nt, st);
 }

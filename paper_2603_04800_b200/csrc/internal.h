@@ -24,10 +24,11 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rpad_of(int64_t r) { return r > 0 ? ceil_div(r, 64) * 64 : 0; }
 
 struct WsLayout {
-  size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0;
+  size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0, xsplit = 0;
   size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, total = 0;
 };
-WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r);
+// f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
+WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
 
 // ---------------------------------------------------------------- opt-in kernel timing (prof.cu)
 // RAII: records a cudaEvent pair around a kernel launch when masq_profile_enable(1) is active.
@@ -56,9 +57,9 @@ cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t s
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
                           uint32_t* status, cudaStream_t st);
-// L1 [(M-1) x d x r] -> L1t [(M-1) x rpad x d];  L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (dup hi/lo)
-cudaError_t launch_pack_lowrank(const uint16_t* L1, const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t d,
-                                int64_t n, int r, int rpad, uint16_t* L1t, uint16_t* L2t, cudaStream_t st);
+// L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (the same L2^T for the Zhi and Zlo K-blocks)
+cudaError_t launch_pack_l2(const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t n, int r, int rpad, uint16_t* L2t,
+                           cudaStream_t st);
 // bf16 W [d x n] -> Wt [n x d]
 cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint16_t* Wt, cudaStream_t st);
 cudaError_t launch_loss_reduce(const double* partials, int64_t tiles, const uint8_t* ids, int64_t T, int n_mod,
@@ -104,10 +105,16 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
 int num_sms();
 
 // ---------------------------------------------------------------- CMC first factor (zgemm.cu)
-// Z[t, (m-1)*2*rpad + k] = hi(xs_t . L1^m)_k, [.. + rpad + k] = lo(...) for rows with id_t == m,
-// zeros for other rows of tiles that contain modality m.
-cudaError_t launch_zgemm(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
-                         int n_mod, const float* inv_s, const uint16_t* L1t, int rpad, const uint32_t* tile_mask,
-                         uint16_t* Z, cudaStream_t st);
+// L1s planes: [2][(M-1)*rpad][d] bf16, plane 0 = hi, 1 = lo of diag(1/s^m) L1^m (transposed)
+cudaError_t launch_l1_fold(const uint16_t* L1, const float* inv_s, int64_t d, int r, int rpad, int n_nt,
+                           uint16_t* L1s, cudaStream_t st);
+// f32 X -> bf16 hi / lo planes [T x d]
+cudaError_t launch_split_f32(const float* X, int64_t ld_x, int64_t T, int64_t d, uint16_t* hi, uint16_t* lo,
+                             cudaStream_t st);
+// Z[t, (m-1)*2*rpad + k] = hi(x_t . L1'^m)_k, [.. + rpad + k] = lo(...) for rows with id_t == m,
+// zeros for the other rows of tiles that contain modality m.  A0 (and A1 for f32 X) are bf16 planes.
+cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, const uint8_t* ids, int64_t T,
+                         int64_t d, int n_mod, const uint16_t* L1s, int rpad, const uint32_t* tile_mask, uint16_t* Z,
+                         cudaStream_t st);
 
 }  // namespace masq

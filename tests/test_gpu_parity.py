@@ -295,3 +295,20 @@ def test_edge_cases_status():
     R, cnt = m.calibrate_stats(X[:1], tt(c["ids"][:1]), 2)
     Ro, co = O.calibrate_stats(c["X"][:1], c["ids"][:1], 2)
     assert np.array_equal(R.cpu().numpy(), Ro)
+
+
+def test_forward_f32_input_with_cmc():
+    """f32 activations (c1 allows f32 X): the CMC GEMM splits X into bf16 hi/lo planes."""
+    c = case("ragged3")
+    m = M()
+    Xf = O.decode(c["X"]) * np.float32(1.0 + 2.0 ** -12)          # not bf16-representable
+    Xf = Xf.astype(np.float32)
+    R, cnt = O.calibrate_stats(Xf, c["ids"], 3)
+    so = O.init_factors(R, cnt, c["W"])
+    qwo, dwo = O.quantize_weight(c["W"], so[0], 8)
+    Y = m.linear_forward(tt(Xf), tt(c["ids"]), tt(so), tt(qwo), tt(dwo), 8, 8, bf(c["L1"]), bf(c["L2"]))
+    qx, dx, _ = m.quantize_activations(tt(Xf), tt(c["ids"]), tt(so), 8)
+    qxo, dxo = O.quantize_activations(Xf, c["ids"], so, 8)
+    assert np.array_equal(qx.cpu().numpy(), qxo) and np.array_equal(dx.cpu().numpy(), dxo)
+    Yo = O.linear_forward(Xf, c["ids"], so, qwo, dwo, 8, list(c["L1"]), list(c["L2"]))
+    assert max_abs_norm(Y.cpu().numpy(), Yo) <= TOL_Y
