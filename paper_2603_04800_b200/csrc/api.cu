@@ -40,16 +40,19 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
         if (f32_x) L.xsplit = take(sizeof(uint16_t) * 2 * (size_t)T * d);
       }
       break;
-    case MASQ_OP_LOSS:
+    case MASQ_OP_LOSS: {
+      const int64_t Tg = grouped_rows(T, n_mod);              // modality-grouped, tile-padded rows
       L.inv_s = take(sizeof(float) * n_mod * d);
-      L.qx = take((size_t)T * d);
-      L.dx = take(sizeof(float) * T);
-      L.mask = take(sizeof(uint32_t) * tiles_m);
+      L.qx = take((size_t)Tg * d);
+      L.dx = take(sizeof(float) * Tg);
+      L.perm = take(sizeof(int32_t) * Tg);
+      L.tile_mod = take(sizeof(uint32_t) * (Tg / kTileM));
       L.qw_all = take((size_t)n_mod * n * d);
       L.dw_all = take(sizeof(float) * n_mod * n);
       L.amax = take(sizeof(uint32_t) * n_mod * n);
-      L.partials = take(sizeof(double) * n_mod * tiles_m * ceil_div(n, kTileN) * 4);
+      L.partials = take(sizeof(double) * (Tg / kTileM) * ceil_div(n, kTileN) * 16);
       break;
+    }
     case MASQ_OP_REFERENCE:
       L.wt = take(sizeof(uint16_t) * (size_t)n * d);
       break;
@@ -220,7 +223,6 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   g.dx = dx;
   g.dw = dw;
   g.tile_mask = mask;
-  g.ids = mod_id;
   g.n_mod = n_mod;
   g.out = out;
   g.ld_out = ld_out;
@@ -302,19 +304,24 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
   int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
-  uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
+  int32_t* perm = reinterpret_cast<int32_t*>(W8(ws, L.perm));
+  uint32_t* tmod = reinterpret_cast<uint32_t*>(W8(ws, L.tile_mod));
   int8_t* qw = reinterpret_cast<int8_t*>(W8(ws, L.qw_all));
   float* dw = reinterpret_cast<float*>(W8(ws, L.dw_all));
   uint32_t* amax = reinterpret_cast<uint32_t*>(W8(ws, L.amax));
   double* partials = reinterpret_cast<double*>(W8(ws, L.partials));
-  const int64_t tiles = ceil_div(T, kTileM) * ceil_div(d_out, kTileN);
+  const int64_t Tg = grouped_rows(T, n_mod);
+  const int num_n = (int)ceil_div(d_out, kTileN);
+  const int64_t tiles = (Tg / kTileM) * num_n;
+  const int epi = gemm_epilogue_warps();
   MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
-  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, mask, status_of(ws), st));
+  MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, st));
+  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, nullptr, status_of(ws), st, perm, Tg));
   MASQ_CK(launch_wquant(W, wt, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
-  MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * n_mod * tiles * 4, st));
+  MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * tiles * epi, st));
   GemmArgs g{};
   g.mode = kModeLoss;
-  g.T = T;
+  g.T = Tg;
   g.n = d_out;
   g.d = d;
   g.qx = qx;
@@ -322,14 +329,15 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   g.b_rows = (int64_t)n_mod * d_out;
   g.dx = dx;
   g.dw = dw;
-  g.tile_mask = mask;
-  g.ids = mod_id;
+  g.tile_mask = tmod;
+  g.perm = perm;
   g.n_mod = n_mod;
   g.yref = Yref;
   g.ld_ref = ld_ref;
   g.partials = partials;
   MASQ_CK(launch_gemm(g, st));
-  MASQ_CK(launch_loss_reduce(partials, tiles * 4, mod_id, T, n_mod, d_out, lambda, sums, counts, loss, st));
+  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, mod_id, T, n_mod, d_out, lambda, sums, counts, loss,
+                             st));
   return MASQ_OK;
 }
 

@@ -281,13 +281,16 @@ __global__ void __launch_bounds__(256) aquant_kernel(const XT* __restrict__ X, i
                                                      int n_mod, const float* __restrict__ inv_s, float qaf,
                                                      int qmin, int qmax, int8_t* __restrict__ qx,
                                                      float* __restrict__ dx, uint32_t* __restrict__ mask,
-                                                     uint32_t* __restrict__ status) {
+                                                     uint32_t* __restrict__ status, const int32_t* __restrict__ perm,
+                                                     int64_t T_out) {
   constexpr int V = Vec<XT>::N;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);     // output row
   const int lane = threadIdx.x & 31;
-  if (row >= T) return;
-  const int m = __ldg(ids + row);
-  const XT* xr = X + row * ld_x;
+  if (row >= T_out) return;
+  const int64_t src = perm ? (int64_t)__ldg(perm + row) : row;          // input token
+  if (src < 0) return;                                                   // padding row of a modality segment
+  const int m = __ldg(ids + src);
+  const XT* xr = X + src * ld_x;
   int8_t* qr = qx + row * d;
   if (m >= n_mod) {
     if (lane == 0) { atomicOr(status, kStBadModality); dx[row] = 0.f; }
@@ -338,6 +341,63 @@ __global__ void __launch_bounds__(256) aquant_kernel(const XT* __restrict__ X, i
   }
 }
 
+// ------------------------------------------------- modality-grouped row order for the loss GEMM
+// Stable counting sort of the tokens by modality; each modality segment starts on a 128-row
+// tile boundary so every loss tile holds a single modality (uses that modality's Q(S_m W)).
+__global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__ ids, int64_t T, int n_mod,
+                                                     int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
+                                                     int64_t n_tiles) {
+  __shared__ int s_cnt[1024];
+  __shared__ int s_tot[kMaxMod], s_seg[kMaxMod + 1];
+  const int tid = threadIdx.x;
+  const int64_t chunk = (T + 1023) / 1024;
+  const int64_t t0 = tid * chunk, t1 = min(T, t0 + chunk);
+  int cnt[kMaxMod];
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) cnt[m] = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int m = ids[t];
+#pragma unroll
+    for (int mm = 0; mm < kMaxMod; ++mm) cnt[mm] += (m == mm);
+  }
+  int excl[kMaxMod];
+  for (int m = 0; m < n_mod; ++m) {                 // block exclusive scan, one modality at a time
+    s_cnt[tid] = cnt[m];
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int v = tid >= off ? s_cnt[tid - off] : 0;
+      __syncthreads();
+      s_cnt[tid] += v;
+      __syncthreads();
+    }
+    excl[m] = s_cnt[tid] - cnt[m];
+    if (tid == 1023) s_tot[m] = s_cnt[tid];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int acc = 0;
+    for (int m = 0; m < n_mod; ++m) {
+      s_seg[m] = acc;
+      acc += (s_tot[m] + kTileM - 1) / kTileM * kTileM;
+    }
+    s_seg[n_mod] = acc;
+  }
+  __syncthreads();
+  int pos[kMaxMod];
+  for (int m = 0; m < n_mod; ++m) pos[m] = s_seg[m] + excl[m];
+  for (int64_t t = t0; t < t1; ++t) {
+    const int m = ids[t];
+    if (m < n_mod) perm[pos[m]++] = (int32_t)t;
+  }
+  for (int64_t tile = tid; tile < n_tiles; tile += 1024) {
+    const int64_t r = tile * kTileM;
+    uint32_t v = 0xFFFFFFFFu;
+    for (int m = 0; m < n_mod; ++m)
+      if (r >= s_seg[m] && r < s_seg[m + 1] && s_tot[m] > 0) v = (uint32_t)m;
+    tile_mod[tile] = v;
+  }
+}
+
 // =============================================================== packing / transpose
 // out[c * ld_out + r] = in[r * ld_in + c]  (bf16), optional duplicate at out + dup_off
 __global__ void transpose_bf16_kernel(const uint16_t* __restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
@@ -368,7 +428,8 @@ struct Lambda8 {
   float v[kMaxMod];
 };
 
-__global__ void __launch_bounds__(256) loss_reduce_kernel(const double* __restrict__ partials, int64_t per_mod,
+__global__ void __launch_bounds__(256) loss_reduce_kernel(const double* __restrict__ partials, int64_t n_tiles,
+                                                          int num_n, int epi, const uint32_t* __restrict__ tile_mod,
                                                           const uint8_t* __restrict__ ids, int64_t T, int n_mod,
                                                           int64_t n, Lambda8 lam, double* __restrict__ sums,
                                                           int64_t* __restrict__ counts, double* __restrict__ loss) {
@@ -379,7 +440,10 @@ __global__ void __launch_bounds__(256) loss_reduce_kernel(const double* __restri
   for (int m = 0; m < n_mod; ++m) {
     double a = 0.0;
     long long c = 0;
-    for (int64_t i = threadIdx.x; i < per_mod; i += 256) a += partials[(int64_t)m * per_mod + i];
+    for (int64_t lt = threadIdx.x; lt < n_tiles; lt += 256) {     // fixed order -> deterministic
+      if (tile_mod[lt / num_n] != (uint32_t)m) continue;
+      for (int e = 0; e < epi; ++e) a += partials[lt * epi + e];
+    }
     for (int64_t t = threadIdx.x; t < T; t += 256) c += (ids[t] == m);
     red[threadIdx.x] = a;
     cred[threadIdx.x] = c;
@@ -472,21 +536,32 @@ cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t s
 
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
-                          uint32_t* status, cudaStream_t st) {
+                          uint32_t* status, cudaStream_t st, const int32_t* perm, int64_t T_out) {
   if (T <= 0) return cudaSuccess;
+  if (T_out < 0) T_out = T;
   if (mask) {
     cudaError_t e = cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ceil_div(T, kTileM), st);
     if (e != cudaSuccess) return e;
   }
   const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
-  const unsigned grid = (unsigned)ceil_div(T, 8);
+  const unsigned grid = (unsigned)ceil_div(T_out, 8);
   ProfScope ps_("aquant", st);
   if (xt == MASQ_BF16)
     aquant_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X), ld_x, ids, T, d, n_mod, inv_s,
-                                        (float)qmax, qmin, qmax, qx, dx, mask, status);
+                                        (float)qmax, qmin, qmax, qx, dx, mask, status, perm, T_out);
   else
     aquant_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld_x, ids, T, d, n_mod, inv_s, (float)qmax,
-                                        qmin, qmax, qx, dx, mask, status);
+                                        qmin, qmax, qx, dx, mask, status, perm, T_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
+                         cudaStream_t st) {
+  const int64_t Tg = grouped_rows(T, n_mod);
+  cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
+  if (e != cudaSuccess) return e;
+  ProfScope ps_("route", st);
+  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kTileM);
   return cudaGetLastError();
 }
 
@@ -513,12 +588,12 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
   return transpose(W, d, n, n, 0, Wt, d, 0, -1, 1, st);
 }
 
-cudaError_t launch_loss_reduce(const double* partials, int64_t per_mod, const uint8_t* ids, int64_t T, int n_mod,
-                               int64_t n, const float* lambda_host, double* sums, int64_t* counts, double* loss,
-                               cudaStream_t st) {
+cudaError_t launch_loss_reduce(const double* partials, int64_t n_tiles, int num_n, int epi, const uint32_t* tile_mod,
+                               const uint8_t* ids, int64_t T, int n_mod, int64_t n, const float* lambda_host,
+                               double* sums, int64_t* counts, double* loss, cudaStream_t st) {
   ProfScope ps_("loss_reduce", st);
-  loss_reduce_kernel<<<1, 256, 0, st>>>(partials, per_mod, ids, T, n_mod, n, make_lambda(lambda_host, n_mod), sums,
-                                        counts, loss);
+  loss_reduce_kernel<<<1, 256, 0, st>>>(partials, n_tiles, num_n, epi, tile_mod, ids, T, n_mod, n,
+                                        make_lambda(lambda_host, n_mod), sums, counts, loss);
   return cudaGetLastError();
 }
 

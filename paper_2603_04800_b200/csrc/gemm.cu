@@ -6,14 +6,16 @@
 //             y += [Zhi | Zlo] . [L2^T ; L2^T] (kind::f16, fp32) accumulated on top of y,
 //             which the epilogue writes back into the same TMEM columns first.
 //   kModeAcc  debug tap: raw int32 accumulators.
-//   kModeLoss A8: per modality m present in the tile, acc = qx . Q(S_m W)^T, and
-//             sum |acc*dx*dw_m - Yref| over rows with id == m -> per-(unit, warp) partials.
+//   kModeLoss A8: rows arrive grouped by modality (each 128-row tile holds one modality m,
+//             perm maps a grouped row to its token), acc = qx . Q(S_m W)^T and the epilogue
+//             sums |acc*dx*dw_m - Yref[perm[row]]| -> per-(tile, warp) partials.
 //   kModeRef  Yref = X . W (kind::f16 bf16 -> fp32), the loss target.
 //
-// Roles (192 threads, 1 CTA per SM, grid = min(#units, #SMs)):
+// Roles (320 threads, 1 CTA per SM, grid = min(#tiles, #SMs)):
 //   warp 0 lane 0 : TMA producer  (A [128 x 128B] + B [256 x 128B] per k-block, 4-stage ring)
 //   warp 1 lane 0 : MMA issuer    (4 x tcgen05.mma per k-block into a 256-column TMEM buffer)
-//   warps 2..5    : epilogue      (tcgen05.ld 32x32b -> dequant -> swizzled smem -> TMA store)
+//   warps 2..9    : epilogue      (warp w owns TMEM lane quarter w%4 and column half (w-2)/4:
+//                                  tcgen05.ld 32x32b -> dequant -> swizzled smem -> TMA store)
 // TMEM holds two 128x256 accumulators (512 columns) so the epilogue of tile i overlaps the
 // main loop of tile i+1.  The CMC k-blocks of tile i are inserted into the k-block stream of
 // tile i+1 (after kCmcDefer main k-blocks), by which time the epilogue has converted tile i's
@@ -31,33 +33,34 @@ constexpr int BM = kTileM, BN = kTileN, BKB = 128;  // BKB: k-block bytes (128 i
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BKB;
 constexpr int B_BYTES = BN * BKB;
-constexpr int EPI_WARPS = 4;
+constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
-constexpr int STG_BYTES = 32 * 32 * 4;
+constexpr int STG_BYTES = 32 * 32 * 4;              // one 32-row x 32-column f32 staging tile per warp
 constexpr int SMEM_A = 0;
 constexpr int SMEM_B = SMEM_A + STAGES * A_BYTES;
 constexpr int SMEM_STG = SMEM_B + STAGES * B_BYTES;
-constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * 2 * STG_BYTES;
+constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * STG_BYTES;
 constexpr int SMEM_USED = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr int kCmcDefer = 4;
 constexpr int kRasterGroup = 8;
 constexpr uint32_t IDESC_I8 = idesc_i8(BM, BN);
 constexpr uint32_t IDESC_BF16 = idesc_bf16(BM, BN);
+static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 
 struct Params {
   int mode;
   int T, n, d;
-  int num_m, num_n, num_kb, n_units, n_tiles;
+  int num_m, num_n, num_kb, n_tiles;
   int n_mod;
   const float* dx;
   const float* dw;
-  const uint32_t* tile_mask;
-  const uint8_t* ids;
+  const uint32_t* tile_mask;   // fwd: modality bit set per tile; loss: modality index (0xFFFFFFFF = empty)
+  const int32_t* perm;         // loss: grouped row -> token (-1 = padding)
   int rpad, cmc_kb;
   const float* yref;
   long long ld_ref;
-  double* partials;
+  double* partials;            // loss: [n_tiles][EPI_WARPS]
 };
 
 struct Unit {
@@ -66,19 +69,21 @@ struct Unit {
 };
 
 __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
-  const bool loss = p.mode == kModeLoss;
-  w.tile = loss ? u / p.n_mod : u;
-  w.m = loss ? u % p.n_mod : 0;
+  w.tile = u;
   // grouped raster: kRasterGroup consecutive n-tiles swept over all m-tiles
   const int per_group = kRasterGroup * p.num_m;
-  const int g = w.tile / per_group;
-  const int rem = w.tile - g * per_group;
+  const int g = u / per_group;
+  const int rem = u - g * per_group;
   const int nt0 = g * kRasterGroup;
   const int gsz = min(kRasterGroup, p.num_n - nt0);
   w.mt = rem / gsz;
   w.nt = nt0 + (rem - w.mt * gsz);
   w.mask = p.tile_mask ? p.tile_mask[w.mt] : 1u;
-  if (loss && !((w.mask >> w.m) & 1u)) return false;
+  w.m = 0;
+  if (p.mode == kModeLoss) {
+    if (w.mask == 0xFFFFFFFFu) return false;
+    w.m = (int)w.mask;
+  }
   return true;
 }
 __device__ __forceinline__ bool unit_has_cmc(const Params& p, const Unit& w) {
@@ -117,7 +122,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (MODE == kModeFwd || MODE == kModeAcc || MODE == kModeRef) tma_prefetch(&tmY);
+    if (MODE != kModeLoss) tma_prefetch(&tmY);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -155,7 +160,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
       };
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int u = blockIdx.x; u < p.n_tiles; u += gridDim.x) {
         Unit w;
         if (!decode_unit(p, u, w)) continue;
         const int brow = (MODE == kModeLoss ? w.m * p.n : 0) + w.nt * BN;
@@ -201,7 +206,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         mma_commit(&cmcd[buf]);
       };
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int u = blockIdx.x; u < p.n_tiles; u += gridDim.x) {
         Unit w;
         if (!decode_unit(p, u, w)) continue;
         const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
@@ -239,35 +244,54 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   } else {
     // -------------------------------------------------------------- epilogue warps
     const uint32_t q = warp & 3u;                       // TMEM lane quarter this warp may access
-    uint8_t* stg0 = smS + q * 2 * STG_BYTES;
-    uint32_t sc = 0, local = 0, cmc_cnt[2] = {0u, 0u};
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    const uint32_t ew = warp - 2u;                      // 0..7
+    const int c0 = (int)(ew >> 2) * 4;                  // this warp's 4 column chunks: c0 .. c0+3
+    uint8_t* sb = smS + ew * STG_BYTES;
+    const uint32_t sbase = smem_u32(sb) + lane * 128u;
+    uint32_t local = 0, cmc_cnt[2] = {0u, 0u};
+    bool stored = false;
+    for (int u = blockIdx.x; u < p.n_tiles; u += gridDim.x) {
       Unit w;
       if (!decode_unit(p, u, w)) continue;
       const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
       ++local;
+      const int row0 = w.mt * BM + (int)q * 32;
+      const int row = row0 + (int)lane;
+      const int col_base = w.nt * BN;
+      const int nch = max(0, min(4, (p.n - col_base) / 32 - c0));   // valid chunks of this warp
+      // ---- prefetch (overlaps the main loop): row scale, this warp's 128 column scales (lane l
+      //      holds dw[col_base + (c0+c)*32 + l]), and for the loss the source token of the row
+      float dxr = 0.f;
+      if (MODE != kModeRef && row < p.T) dxr = p.dx[row];
+      float dwr[4] = {0.f, 0.f, 0.f, 0.f};
+      if (MODE != kModeRef && MODE != kModeAcc) {
+        const float* dwp = p.dw + (MODE == kModeLoss ? (size_t)w.m * p.n : 0) + col_base + c0 * 32 + lane;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nch) dwr[c] = __ldg(dwp + c * 32);
+      }
+      int src = -1;
+      if (MODE == kModeLoss && row < p.T) src = __ldg(p.perm + row);
+
       mbar_wait(&tfull[buf], ph);
       tc_fence_after();
-      const int row0 = w.mt * BM + q * 32;
-      const int row = row0 + (int)lane;
-      const bool rowv = row < p.T;
-      const int col_base = w.nt * BN;
-      const int nchunks = min(BN, p.n - col_base) / 32;
-      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN;
-      float dxr = 0.f;
-      if (MODE != kModeRef && rowv) dxr = p.dx[row];
-      const float* dwp = p.dw + (MODE == kModeLoss ? (size_t)w.m * p.n : 0) + col_base;
+      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN + c0 * 32;
 
+      auto dequant = [&](uint32_t (&v)[32], int c) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float s = __shfl_sync(0xffffffffu, dwr[c], i);
+          v[i] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[i], dxr), s));
+        }
+      };
       auto store_chunk = [&](const uint32_t (&v)[32], int c) {
-        uint8_t* sb = stg0 + (sc & 1u) * STG_BYTES;
-        if (sc >= 2) {
-          if (lane == 0) bulk_wait_read<1>();
+        if (stored) {                                   // staging tile free again?
+          if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
         }
-        const uint32_t base = smem_u32(sb) + lane * 128u;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint32_t dst = base + (((uint32_t)j ^ (lane & 7u)) << 4);
+          const uint32_t dst = sbase + (((uint32_t)j ^ (lane & 7u)) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v[4 * j]), "r"(v[4 * j + 1]),
                        "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
                        : "memory");
@@ -275,26 +299,17 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tmY, sb, col_base + c * 32, row0);
+          tma_store_2d(&tmY, sb, col_base + (c0 + c) * 32, row0);
           bulk_commit();
         }
-        ++sc;
-      };
-      auto dequant = [&](uint32_t (&v)[32], int c) {
-        const float4* dw4 = reinterpret_cast<const float4*>(dwp + c * 32);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 s4 = __ldg(dw4 + j);
-          v[4 * j + 0] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 0], dxr), s4.x));
-          v[4 * j + 1] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 1], dxr), s4.y));
-          v[4 * j + 2] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 2], dxr), s4.z));
-          v[4 * j + 3] = __float_as_uint(__fmul_rn(__fmul_rn((float)(int)v[4 * j + 3], dxr), s4.w));
-        }
+        stored = true;
       };
 
       if (MODE == kModeFwd && unit_has_cmc(p, w)) {
         // 1) int32 -> y_base (f32) in place, 2) let the MMA warp accumulate CMC on top, 3) store.
-        for (int c = 0; c < nchunks; ++c) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= nch) break;
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
@@ -308,37 +323,47 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         mbar_wait(&cmcd[buf], cmc_cnt[buf] & 1u);
         ++cmc_cnt[buf];
         tc_fence_after();
-        for (int c = 0; c < nchunks; ++c) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= nch) break;
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
           store_chunk(v, c);
         }
       } else if (MODE == kModeLoss) {
-        const bool rv = rowv && p.ids[row] == (uint8_t)w.m;
         double part = 0.0;
-        for (int c = 0; c < nchunks; ++c) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= nch) break;
+          float4 y[8];
+          if (src >= 0) {
+            const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)src * p.ld_ref + col_base +
+                                                               (c0 + c) * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) y[j] = __ldg(r4 + j);
+          }
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
           dequant(v, c);
-          if (rv) {
-            const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)row * p.ld_ref + col_base + c * 32);
+          if (src >= 0) {
             float acc = 0.f;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const float4 y = __ldg(r4 + j);
-              acc += fabsf(__uint_as_float(v[4 * j + 0]) - y.x) + fabsf(__uint_as_float(v[4 * j + 1]) - y.y) +
-                     fabsf(__uint_as_float(v[4 * j + 2]) - y.z) + fabsf(__uint_as_float(v[4 * j + 3]) - y.w);
+              acc += fabsf(__uint_as_float(v[4 * j + 0]) - y[j].x) + fabsf(__uint_as_float(v[4 * j + 1]) - y[j].y) +
+                     fabsf(__uint_as_float(v[4 * j + 2]) - y[j].z) + fabsf(__uint_as_float(v[4 * j + 3]) - y[j].w);
             }
             part += (double)acc;
           }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) p.partials[((size_t)w.m * p.n_tiles + w.tile) * EPI_WARPS + q] = part;
+        if (lane == 0) p.partials[(size_t)(w.mt * p.num_n + w.nt) * EPI_WARPS + ew] = part;
       } else {
-        for (int c = 0; c < nchunks; ++c) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= nch) break;
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
@@ -378,6 +403,8 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   return cudaGetLastError();
 }
 }  // namespace
+
+int gemm_epilogue_warps() { return EPI_WARPS; }
 
 int num_sms() {
   static int n = 0;
@@ -428,17 +455,16 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.num_kb = (int)ceil_div(g.d, bf ? 64 : 128);
   p.n_tiles = p.num_m * p.num_n;
   p.n_mod = g.n_mod;
-  p.n_units = g.mode == kModeLoss ? p.n_tiles * g.n_mod : p.n_tiles;
   p.dx = g.dx;
   p.dw = g.dw;
   p.tile_mask = g.tile_mask;
-  p.ids = g.ids;
+  p.perm = g.perm;
   p.rpad = cmc ? g.rpad : 0;
   p.cmc_kb = cmc ? (2 * g.rpad) / 64 : 0;
   p.yref = g.yref;
   p.ld_ref = g.ld_ref;
   p.partials = g.partials;
-  const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
+  const int grid = (int)std::min<int64_t>(p.n_tiles, num_sms());
   switch (g.mode) {
     case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, grid, st);
     case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, grid, st);

@@ -25,7 +25,7 @@ inline int64_t rpad_of(int64_t r) { return r > 0 ? ceil_div(r, 64) * 64 : 0; }
 
 struct WsLayout {
   size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0, xsplit = 0;
-  size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, total = 0;
+  size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, total = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -54,17 +54,25 @@ cudaError_t launch_init(const float* R, const int64_t* count, const void* W, mas
 cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_sets, int64_t d, int64_t n,
                           int wbits, int8_t* qw, float* dw, uint32_t* amax_scratch, cudaStream_t st);
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st);
+// perm (optional): output row p quantizes input token perm[p] (-1: padding row, left untouched);
+// T_out = number of output rows (T when perm == NULL)
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
-                          uint32_t* status, cudaStream_t st);
+                          uint32_t* status, cudaStream_t st, const int32_t* perm = nullptr, int64_t T_out = -1);
+// rows grouped by modality, each segment padded to a multiple of 128 rows:
+// perm[Tg] (grouped row -> token, -1 padding), tile_mod[Tg/128] (modality of the tile, ~0u empty)
+inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kTileM) * kTileM + (int64_t)n_mod * kTileM; }
+cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
+                         cudaStream_t st);
 // L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (the same L2^T for the Zhi and Zlo K-blocks)
 cudaError_t launch_pack_l2(const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t n, int r, int rpad, uint16_t* L2t,
                            cudaStream_t st);
 // bf16 W [d x n] -> Wt [n x d]
 cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint16_t* Wt, cudaStream_t st);
-cudaError_t launch_loss_reduce(const double* partials, int64_t tiles, const uint8_t* ids, int64_t T, int n_mod,
-                               int64_t n, const float* lambda_host, double* sums, int64_t* counts, double* loss,
-                               cudaStream_t st);
+// sums[m] = fixed-order sum of partials[lt * epi + e] over tiles lt with tile_mod[lt / num_n] == m
+cudaError_t launch_loss_reduce(const double* partials, int64_t n_tiles, int num_n, int epi, const uint32_t* tile_mod,
+                               const uint8_t* ids, int64_t T, int n_mod, int64_t n, const float* lambda_host,
+                               double* sums, int64_t* counts, double* loss, cudaStream_t st);
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st);
 
@@ -87,8 +95,8 @@ struct GemmArgs {
   int64_t b_rows;                  // rows of the B tensor (n, or n_mod*n for the loss)
   const float* dx;
   const float* dw;                 // [n] or [n_mod * n] for the loss
-  const uint32_t* tile_mask;       // per 128-row tile
-  const uint8_t* ids;              // loss row masks
+  const uint32_t* tile_mask;       // per 128-row tile (fwd: modality bit set; loss: modality index)
+  const int32_t* perm;             // loss: grouped row -> token
   int n_mod;
   void* out;                       // Y f32 / acc int32 [T x ld_out]
   int64_t ld_out;
@@ -102,6 +110,7 @@ struct GemmArgs {
   double* partials;                // [n_mod][tiles][4]
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
+int gemm_epilogue_warps();
 int num_sms();
 
 // ---------------------------------------------------------------- CMC first factor (zgemm.cu)
