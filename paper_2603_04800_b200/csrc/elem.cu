@@ -38,60 +38,108 @@ struct Vec<float> {
   }
 };
 
-// round half away from zero, then clamp (reading Q5)
-__device__ __forceinline__ int rha_clamp(float v, int qmin, int qmax) {
-  const float t = truncf(v);
-  const float fr = fabsf(__fsub_rn(v, t));
-  float q = t;
-  if (fr >= 0.5f) q = __fadd_rn(t, copysignf(1.0f, v));
-  int qi = (int)q;
+// code = rha(xs / delta) with the IEEE quotient's rounding: fast path v = xs * (1/delta)
+// (|v - xs/delta| <= 3 ulp(v) < 2.5e-5 for |v| <= 128); only when the fractional part lies
+// within 1/256 of 0.5 -- the one place where that error could flip the rounding -- recompute
+// v with div.rn.  Near integers the rounding is continuous, so no check is needed there.
+__device__ __forceinline__ int quant_code(float xs, float delta, float rcp, int qmin, int qmax) {
+  float v = __fmul_rn(xs, rcp);
+  float t = truncf(v);
+  float fr = fabsf(__fsub_rn(v, t));
+  if (fabsf(__fsub_rn(fr, 0.5f)) < 0.00390625f) {
+    v = __fdiv_rn(xs, delta);
+    t = truncf(v);
+    fr = fabsf(__fsub_rn(v, t));
+  }
+  const float q = fr >= 0.5f ? __fadd_rn(t, copysignf(1.0f, v)) : t;
+  const int qi = (int)q;
   return qi < qmin ? qmin : (qi > qmax ? qmax : qi);
 }
 
-// code = rha(xs / delta): fast path xs * (1/delta); near a half-integer (where the fast
-// quotient could round differently from the IEEE quotient) recompute with div.rn.
-__device__ __forceinline__ int quant_code(float xs, float delta, float rcp, int qmin, int qmax) {
-  float v = __fmul_rn(xs, rcp);
-  const float a = fabsf(v);
-  const float fr = __fsub_rn(a, truncf(a));
-  if (fabsf(fr - 0.5f) <= 1.52587890625e-05f * fmaxf(a, 1.0f)) v = __fdiv_rn(xs, delta);
-  return rha_clamp(v, qmin, qmax);
+__device__ __forceinline__ uint32_t pack4(int q0, int q1, int q2, int q3) {
+  return __byte_perm(__byte_perm(q0, q1, 0x0040), __byte_perm(q2, q3, 0x0040), 0x5410);
 }
 
+// 4 codes sharing one scale, packed little-endian into a word.  Fast path: v = xs * (1/delta),
+// q = rint(v).  If every |v - q| <= 1/2 - 1/256, v is >= 1/256 away from any half-integer, so
+// (a) the IEEE quotient xs/delta (within 2.5e-5 of v for |v| <= 128) rounds to the same q and
+// (b) there is no tie, hence rint == round-half-away.  Otherwise `near` is set and the caller
+// recomputes the quad with quant_code (exact) in a rare, non-unrolled fix-up loop, which keeps
+// the hot loop free of the division code.
+__device__ __forceinline__ uint32_t quant4_fast(float x0, float x1, float x2, float x3, float rcp, int qmin,
+                                                int qmax, bool& near) {
+  const float v0 = __fmul_rn(x0, rcp), v1 = __fmul_rn(x1, rcp), v2 = __fmul_rn(x2, rcp), v3 = __fmul_rn(x3, rcp);
+  const float r0 = rintf(v0), r1 = rintf(v1), r2 = rintf(v2), r3 = rintf(v3);
+  near = fabsf(__fsub_rn(v0, r0)) > 0.49609375f || fabsf(__fsub_rn(v1, r1)) > 0.49609375f ||
+         fabsf(__fsub_rn(v2, r2)) > 0.49609375f || fabsf(__fsub_rn(v3, r3)) > 0.49609375f;
+  return pack4(min(max((int)r0, qmin), qmax), min(max((int)r1, qmin), qmax), min(max((int)r2, qmin), qmax),
+               min(max((int)r3, qmin), qmax));
+}
+__device__ __forceinline__ uint32_t quant4_exact(float x0, float x1, float x2, float x3, float delta, float rcp,
+                                                 int qmin, int qmax) {
+  return pack4(quant_code(x0, delta, rcp, qmin, qmax), quant_code(x1, delta, rcp, qmin, qmax),
+               quant_code(x2, delta, rcp, qmin, qmax), quant_code(x3, delta, rcp, qmin, qmax));
+}
+
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f32(float v) { return v; }
+
 // =============================================================== A1 stats
+// |x| max over packed words: bf16 pairs compare as unsigned 16-bit halves once the sign bits are
+// cleared (non-negative bf16 / f32 order == unsigned bit-pattern order), so the max is exact.
+template <typename XT>
+__device__ __forceinline__ uint32_t absmax_word(uint32_t acc, uint32_t v);
+template <>
+__device__ __forceinline__ uint32_t absmax_word<__nv_bfloat16>(uint32_t acc, uint32_t v) {
+  return __vmaxu2(acc, v & 0x7FFF7FFFu);
+}
+template <>
+__device__ __forceinline__ uint32_t absmax_word<float>(uint32_t acc, uint32_t v) {
+  return max(acc, v & 0x7FFFFFFFu);
+}
+// f32 bit pattern of element e (0..V-1) of a packed 4-word group
+template <typename XT>
+__device__ __forceinline__ uint32_t word_elem_bits(const uint32_t (&w)[4], int e) {
+  if (sizeof(XT) == 2) return (e & 1) ? (w[e >> 1] & 0xFFFF0000u) : (w[e >> 1] << 16);
+  return w[e];
+}
+
+// 128 threads x one 16-byte column group each; a strip of rows per CTA; 4 rows in flight per
+// thread; per-modality packed maxima in 4 registers; CTA combine through smem -> coalesced
+// atomicMax on the u32 bit patterns of R.
 template <typename XT, int NM>
-__global__ void __launch_bounds__(256) stats_kernel(const XT* __restrict__ X, int64_t ld_x,
+__global__ void __launch_bounds__(128) stats_kernel(const XT* __restrict__ X, int64_t ld_x,
                                                     const uint8_t* __restrict__ ids, int64_t T, int64_t d,
                                                     int rows_per_strip, float* __restrict__ R,
                                                     unsigned long long* __restrict__ count,
                                                     uint32_t* __restrict__ status) {
   constexpr int V = Vec<XT>::N;
-  constexpr int U = 8;                      // rows in flight per thread
-  constexpr int CH = 256 * V;               // channels per CTA
-  __shared__ float sm[CH];
+  constexpr int U = 4;
+  constexpr int CH = 128 * V;               // channels per CTA
+  __shared__ uint32_t sm[CH];
   __shared__ uint32_t s_present;
   const int64_t c0 = (int64_t)blockIdx.x * CH + threadIdx.x * V;
   const bool active = c0 < d;
   const int64_t t0 = (int64_t)blockIdx.y * rows_per_strip;
   const int64_t t1 = min(T, t0 + rows_per_strip);
-  float acc[NM][V];
+  uint32_t acc[NM][4];
 #pragma unroll
   for (int m = 0; m < NM; ++m)
 #pragma unroll
-    for (int e = 0; e < V; ++e) acc[m][e] = 0.f;
+    for (int e = 0; e < 4; ++e) acc[m][e] = 0u;
   uint32_t present = 0, bad = 0;
-  unsigned long long cnt[NM];
+  uint32_t cnt[NM];
 #pragma unroll
   for (int m = 0; m < NM; ++m) cnt[m] = 0;
 
   for (int64_t t = t0; t < t1; t += U) {
-    float f[U][V];
+    uint4 v[U];
     int mid[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t tt = t + u;
+      if (active && tt < t1) v[u] = __ldg(reinterpret_cast<const uint4*>(X + tt * ld_x + c0));
       mid[u] = tt < t1 ? (int)__ldg(ids + tt) : -1;
-      if (active && tt < t1) Vec<XT>::load(X + tt * ld_x + c0, f[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -104,8 +152,10 @@ __global__ void __launch_bounds__(256) stats_kernel(const XT* __restrict__ X, in
         if (m == mm) {
           ++cnt[mm];
           if (active) {
-#pragma unroll
-            for (int e = 0; e < V; ++e) acc[mm][e] = fmaxf(acc[mm][e], fabsf(f[u][e]));
+            acc[mm][0] = absmax_word<XT>(acc[mm][0], v[u].x);
+            acc[mm][1] = absmax_word<XT>(acc[mm][1], v[u].y);
+            acc[mm][2] = absmax_word<XT>(acc[mm][2], v[u].z);
+            acc[mm][3] = absmax_word<XT>(acc[mm][3], v[u].w);
           }
         }
       }
@@ -117,7 +167,7 @@ __global__ void __launch_bounds__(256) stats_kernel(const XT* __restrict__ X, in
     if (blockIdx.x == 0) {
 #pragma unroll
       for (int m = 0; m < NM; ++m)
-        if (cnt[m]) atomicAdd(count + m, cnt[m]);
+        if (cnt[m]) atomicAdd(count + m, (unsigned long long)cnt[m]);
     }
   }
   __syncthreads();
@@ -126,12 +176,12 @@ __global__ void __launch_bounds__(256) stats_kernel(const XT* __restrict__ X, in
   for (int mm = 0; mm < NM; ++mm) {
     if (!((pres >> mm) & 1u)) continue;       // CTA-uniform
 #pragma unroll
-    for (int e = 0; e < V; ++e) sm[threadIdx.x * V + e] = acc[mm][e];
+    for (int e = 0; e < V; ++e) sm[threadIdx.x * V + e] = word_elem_bits<XT>(acc[mm], e);
     __syncthreads();
-    for (int c = threadIdx.x; c < CH; c += 256) {
+    for (int c = threadIdx.x; c < CH; c += 128) {
       const int64_t col = (int64_t)blockIdx.x * CH + c;
-      const float v = sm[c];
-      if (col < d && v > 0.f) atomicMax(reinterpret_cast<unsigned int*>(R + (int64_t)mm * d + col), __float_as_uint(v));
+      const uint32_t v = sm[c];
+      if (col < d && v != 0u) atomicMax(reinterpret_cast<unsigned int*>(R + (int64_t)mm * d + col), v);
     }
     __syncthreads();
   }
@@ -140,9 +190,10 @@ __global__ void __launch_bounds__(256) stats_kernel(const XT* __restrict__ X, in
 template <typename XT>
 cudaError_t stats_dispatch(const XT* X, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d, int n_mod, float* R,
                            int64_t* count, uint32_t* status, cudaStream_t st) {
-  constexpr int CH = 256 * Vec<XT>::N;
+  constexpr int CH = 128 * Vec<XT>::N;
   const int gx = (int)ceil_div(d, CH);
-  int strips = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_sms() * 2, gx), ceil_div(T, 64)));
+  // ~12 CTAs of 128 threads per SM in one wave; strips of >= 64 rows bound the atomic traffic
+  int strips = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_sms() * 12, gx), ceil_div(T, 64)));
   const int rows = (int)ceil_div(T, strips);
   strips = (int)ceil_div(T, rows);
   dim3 grid(gx, strips);
@@ -151,7 +202,7 @@ cudaError_t stats_dispatch(const XT* X, int64_t ld_x, const uint8_t* ids, int64_
 #define MASQ_STATS_CASE(NM)                                                       \
   case NM: {                                                                      \
     ProfScope ps_("stats", st);                                                   \
-    stats_kernel<XT, NM><<<grid, 256, 0, st>>>(X, ld_x, ids, T, d, rows, R, c, status); \
+    stats_kernel<XT, NM><<<grid, 128, 0, st>>>(X, ld_x, ids, T, d, rows, R, c, status); \
   } break;
     MASQ_STATS_CASE(1) MASQ_STATS_CASE(2) MASQ_STATS_CASE(3) MASQ_STATS_CASE(4)
     MASQ_STATS_CASE(5) MASQ_STATS_CASE(6) MASQ_STATS_CASE(7) MASQ_STATS_CASE(8)
@@ -192,79 +243,131 @@ __global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ R, 
 }
 
 // =============================================================== A3 weight quantization
-// pass 1: amax[k*n + j] = max_i |s_k[i] * W[i, j]|   (u32 bit patterns of non-negative floats)
-template <typename WT>
+// pass 1: amax[k*n + j] = max_i |s_k[i] * W[i, j]| for all NS factor sets from ONE read of W
+// (u32 bit patterns of non-negative floats -> exact atomicMax)
+template <typename WT, int NS>
 __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, const float* __restrict__ s,
                                                       int64_t d, int64_t n, int rows_per_strip,
                                                       uint32_t* __restrict__ amax) {
   constexpr int V = Vec<WT>::N;
-  const int k = blockIdx.z;
   const int64_t j0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * V;
   if (j0 >= n) return;
   const int64_t i0 = (int64_t)blockIdx.y * rows_per_strip;
   const int64_t i1 = min(d, i0 + rows_per_strip);
-  const float* sk = s + (int64_t)k * d;
-  float m[V];
+  float m[NS][V];
 #pragma unroll
-  for (int e = 0; e < V; ++e) m[e] = 0.f;
-  for (int64_t i = i0; i < i1; ++i) {
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int e = 0; e < V; ++e) m[k][e] = 0.f;
+  int64_t i = i0;
+  for (; i + 4 <= i1; i += 4) {
+    float f[4][V];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Vec<WT>::load(W + (i + u) * n + j0, f[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const float si = __ldg(s + (int64_t)k * d + i + u);
+#pragma unroll
+        for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[u][e])));
+      }
+  }
+  for (; i < i1; ++i) {
     float f[V];
     Vec<WT>::load(W + i * n + j0, f);
-    const float si = __ldg(sk + i);
 #pragma unroll
-    for (int e = 0; e < V; ++e) m[e] = fmaxf(m[e], fabsf(__fmul_rn(si, f[e])));
+    for (int k = 0; k < NS; ++k) {
+      const float si = __ldg(s + (int64_t)k * d + i);
+#pragma unroll
+      for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[e])));
+    }
   }
 #pragma unroll
-  for (int e = 0; e < V; ++e)
-    if (m[e] > 0.f) atomicMax(amax + (int64_t)k * n + j0 + e, __float_as_uint(m[e]));
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int e = 0; e < V; ++e)
+      if (m[k][e] > 0.f) atomicMax(amax + (int64_t)k * n + j0 + e, __float_as_uint(m[k][e]));
 }
 
-// pass 2: codes for a 128 (i) x 128 (j) tile, transposed through smem to K-major qw[j][i]
-template <typename WT>
+// pass 2: one 128 (i) x 64 (j) tile of W read once; for every set k the codes are packed
+// 4 rows per 32-bit word into a smem tile [64 j][128 i] and written K-major (qw[k][j][i]).
+template <typename WT, int NS>
 __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, const float* __restrict__ s,
                                                      int64_t d, int64_t n, float qmaxf, int qmin, int qmax,
                                                      const uint32_t* __restrict__ amax, int8_t* __restrict__ qw,
                                                      float* __restrict__ dw) {
-  constexpr int V = Vec<WT>::N;
-  constexpr int TPR = 128 / V;            // threads per W row segment of 128 columns
-  constexpr int RPI = 256 / TPR;          // rows per iteration
-  __shared__ __align__(16) int8_t tile[128][128 + 16];
-  const int k = blockIdx.z;
-  const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * 128;
-  const int jc = (threadIdx.x % TPR) * V;
-  const int ir = threadIdx.x / TPR;
-  float dwv[V], rcp[V];
+  constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
+  constexpr int CPT = 8;                        // columns per thread
+  constexpr int LPT = CPT / V;                  // loads per row per thread
+  __shared__ __align__(16) uint32_t tile[64][33];   // [j][i/4] packed codes (+1 word pad)
+  const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * 64;
+  const int tx = threadIdx.x & 7;               // column group: j = j0 + 8*tx + e
+  const int ty = threadIdx.x >> 3;              // rows 4*ty .. 4*ty+3 of the tile
+  const int64_t jb = j0 + tx * CPT;
+  const bool colok = jb < n;                    // n % 32 == 0 -> whole 8-column groups
+  float f[4][CPT];
 #pragma unroll
-  for (int e = 0; e < V; ++e) {
-    const int64_t j = j0 + jc + e;
-    dwv[e] = j < n ? fmaxf(__fdiv_rn(__uint_as_float(amax[(int64_t)k * n + j]), qmaxf), kFloor) : 1.f;
-    rcp[e] = __fdiv_rn(1.0f, dwv[e]);
-  }
-  const float* sk = s + (int64_t)k * d;
-  for (int it = 0; it < 128 / RPI; ++it) {
-    const int il = it * RPI + ir;
-    const int64_t i = i0 + il;
-    float f[V];
-    if (i < d && j0 + jc < n) {
-      Vec<WT>::load(W + i * n + j0 + jc, f);
-      const float si = __ldg(sk + i);
+  for (int r = 0; r < 4; ++r) {
+    const int64_t i = i0 + 4 * ty + r;
 #pragma unroll
-      for (int e = 0; e < V; ++e) tile[jc + e][il] = (int8_t)quant_code(__fmul_rn(si, f[e]), dwv[e], rcp[e], qmin, qmax);
+    for (int l = 0; l < LPT; ++l) {
+      float g[V];
+      if (colok && i < d) Vec<WT>::load(W + i * n + jb + l * V, g);
+      else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) g[e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) f[r][l * V + e] = g[e];
     }
   }
-  __syncthreads();
-  // write 128 rows (j) x 128 bytes (i); 8 threads x 16 B per row
-  for (int it = 0; it < 4; ++it) {
-    const int jl = it * 32 + (threadIdx.x >> 3);
-    const int ic = (threadIdx.x & 7) * 16;
-    const int64_t j = j0 + jl, i = i0 + ic;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    float si[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t i = i0 + 4 * ty + r;
+      si[r] = i < d ? __ldg(s + (int64_t)k * d + i) : 0.f;
+    }
+    uint32_t nearmask = 0;
+#pragma unroll
+    for (int e = 0; e < CPT; ++e) {
+      const int64_t j = jb + e;
+      const float dv = colok ? fmaxf(__fdiv_rn(__uint_as_float(__ldg(amax + (int64_t)k * n + j)), qmaxf), kFloor) : 1.f;
+      const float rc = __fdiv_rn(1.0f, dv);
+      bool nr;
+      tile[tx * CPT + e][ty] = quant4_fast(__fmul_rn(si[0], f[0][e]), __fmul_rn(si[1], f[1][e]),
+                                           __fmul_rn(si[2], f[2][e]), __fmul_rn(si[3], f[3][e]), rc, qmin, qmax, nr);
+      nearmask |= (uint32_t)nr << e;
+      if (blockIdx.y == 0 && ty == 0 && colok) dw[(int64_t)k * n + j] = dv;
+    }
+#pragma unroll 1
+    while (nearmask) {                                       // rare exact fix-up of flagged quads
+      const int e = __ffs(nearmask) - 1;
+      nearmask &= nearmask - 1;
+      const int64_t j = jb + e;
+      const float dv = fmaxf(__fdiv_rn(__uint_as_float(__ldg(amax + (int64_t)k * n + j)), qmaxf), kFloor);
+      const float rc = __fdiv_rn(1.0f, dv);
+      float x[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t i = i0 + 4 * ty + r;
+        x[r] = i < d ? __fmul_rn(__ldg(s + (int64_t)k * d + i), to_f32(W[i * n + j])) : 0.f;
+      }
+      tile[tx * CPT + e][ty] = quant4_exact(x[0], x[1], x[2], x[3], dv, rc, qmin, qmax);
+    }
+    __syncthreads();
+    // write 64 rows (j) x 128 bytes (i): 4 threads per row, 32 bytes each
+    const int jr = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int64_t j = j0 + jr, i = i0 + part * 32;
     if (j < n && i < d) {
-      *reinterpret_cast<uint4*>(qw + ((int64_t)k * n + j) * d + i) = *reinterpret_cast<const uint4*>(&tile[jl][ic]);
+      const uint32_t* t = &tile[jr][part * 8];
+      int8_t* dst = qw + ((int64_t)k * n + j) * d + i;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(t[0], t[1], t[2], t[3]);
+      if (i + 16 < d) *reinterpret_cast<uint4*>(dst + 16) = make_uint4(t[4], t[5], t[6], t[7]);
     }
-  }
-  if (blockIdx.y == 0 && threadIdx.x < 128) {
-    const int64_t j = j0 + threadIdx.x;
-    if (j < n) dw[(int64_t)k * n + j] = fmaxf(__fdiv_rn(__uint_as_float(amax[(int64_t)k * n + j]), qmaxf), kFloor);
+    __syncthreads();
   }
 }
 
@@ -272,6 +375,113 @@ __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, c
 __global__ void inv_kernel(const float* __restrict__ s, int64_t count, float* __restrict__ inv) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) inv[i] = __fdiv_rn(1.0f, s[i]);
+}
+
+// Register-resident row kernel: one token row per CTA iteration (grid-stride), G = blockDim/32
+// warps per row, each thread holds CPL 16-byte chunks of the row, so X is read from HBM exactly
+// once; small CTAs (64-1024 threads) keep occupancy high.  The reciprocal factors are read
+// through L1 (consecutive rows share a modality, so the factor row stays resident).
+template <typename XT, int CPL>
+__global__ void __launch_bounds__(1024) aquant_row_kernel(const XT* __restrict__ X, int64_t ld_x,
+                                                          const uint8_t* __restrict__ ids, int64_t d, int n_mod,
+                                                          const float* __restrict__ inv_s, float qaf, int qmin,
+                                                          int qmax, int8_t* __restrict__ qx, float* __restrict__ dx,
+                                                          uint32_t* __restrict__ mask, uint32_t* __restrict__ status,
+                                                          const int32_t* __restrict__ perm, int64_t T_out) {
+  constexpr int V = Vec<XT>::N;
+  __shared__ float s_red[32];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;
+  for (int64_t row = blockIdx.x; row < T_out; row += gridDim.x) {
+    const int64_t src = perm ? (int64_t)__ldg(perm + row) : row;
+    if (src < 0) continue;                                   // CTA-uniform (padding row)
+    uint4 raw[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int64_t c = ((int64_t)k * nthr + tid) * V;
+      if (c < d) raw[k] = __ldg(reinterpret_cast<const uint4*>(X + src * ld_x + c));
+    }
+    const int m = __ldg(ids + src);
+    const bool bad = m >= n_mod;
+    const float* inv = inv_s + (int64_t)(bad ? 0 : m) * d;
+    float amax = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int64_t c = ((int64_t)k * nthr + tid) * V;
+      if (c < d) {
+        const uint32_t w[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+#pragma unroll
+        for (int e = 0; e < V; e += 4) {
+          const float4 iv = __ldg(reinterpret_cast<const float4*>(inv + c + e));
+          amax = fmaxf(amax, fabsf(__fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 0)), iv.x)));
+          amax = fmaxf(amax, fabsf(__fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 1)), iv.y)));
+          amax = fmaxf(amax, fabsf(__fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 2)), iv.z)));
+          amax = fmaxf(amax, fabsf(__fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 3)), iv.w)));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (nw > 1) {
+      if (lane == 0) s_red[warp] = amax;
+      __syncthreads();
+      amax = s_red[0];
+      for (int w = 1; w < nw; ++w) amax = fmaxf(amax, s_red[w]);
+      __syncthreads();
+    }
+    int8_t* qr = qx + row * d;
+    if (bad) {
+      if (tid == 0) { atomicOr(status, kStBadModality); dx[row] = 0.f; }
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int64_t c = ((int64_t)k * nthr + tid) * V;
+        if (c < d) {
+          if (V == 8) *reinterpret_cast<uint2*>(qr + c) = make_uint2(0, 0);
+          else *reinterpret_cast<uint32_t*>(qr + c) = 0u;
+        }
+      }
+      continue;
+    }
+    const float delta = fmaxf(__fdiv_rn(amax, qaf), kFloor);
+    const float rcp = __fdiv_rn(1.0f, delta);
+    uint32_t nearmask = 0;                                   // bit 2k+h: quad h of chunk k needs the exact path
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int64_t c = ((int64_t)k * nthr + tid) * V;
+      if (c < d) {
+        const uint32_t w[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+        uint32_t packed[V / 4];
+#pragma unroll
+        for (int e = 0; e < V; e += 4) {
+          const float4 iv = __ldg(reinterpret_cast<const float4*>(inv + c + e));
+          bool nr;
+          packed[e / 4] = quant4_fast(__fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 0)), iv.x),
+                                      __fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 1)), iv.y),
+                                      __fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 2)), iv.z),
+                                      __fmul_rn(__uint_as_float(word_elem_bits<XT>(w, e + 3)), iv.w), rcp, qmin, qmax,
+                                      nr);
+          nearmask |= (uint32_t)nr << (2 * k + e / 4);
+        }
+        if (V == 8) *reinterpret_cast<uint2*>(qr + c) = make_uint2(packed[0], packed[V / 4 - 1]);
+        else *reinterpret_cast<uint32_t*>(qr + c) = packed[0];
+      }
+    }
+#pragma unroll 1
+    while (nearmask) {                                       // rare exact fix-up (same thread, ordered stores)
+      const int bit = __ffs(nearmask) - 1;
+      nearmask &= nearmask - 1;
+      const int k = bit >> 1, e = (bit & 1) * 4;
+      const int64_t c = ((int64_t)k * nthr + tid) * V + e;
+      float x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __fmul_rn(to_f32(X[src * ld_x + c + u]), __ldg(inv + c + u));
+      *reinterpret_cast<uint32_t*>(qr + c) = quant4_exact(x[0], x[1], x[2], x[3], delta, rcp, qmin, qmax);
+    }
+    if (tid == 0) {
+      dx[row] = delta;
+      if (mask) atomicOr(mask + (row >> 7), 1u << m);
+    }
+  }
 }
 
 // one warp per token row; two passes over the row (absmax, then codes; the 2nd read hits L1/L2)
@@ -505,32 +715,79 @@ cudaError_t launch_init(const float* R, const int64_t* count, const void* W, mas
   return cudaGetLastError();
 }
 
+template <typename WT, int NS>
+static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n, int wbits, int8_t* qw, float* dw,
+                               uint32_t* amax, cudaStream_t st) {
+  const int qmax = (1 << (wbits - 1)) - 1, qmin = -(1 << (wbits - 1));
+  constexpr int V = Vec<WT>::N;
+  const int gx = (int)ceil_div(n, 256 * V);
+  int strips = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_sms() * 6, gx), ceil_div(d, 16)));
+  const int rows = (int)ceil_div(d, strips);
+  strips = (int)ceil_div(d, rows);
+  dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 64), (unsigned)ceil_div(d, 128));
+  { ProfScope ps_("wcolmax", st); wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
+  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS><<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw); }
+  return cudaGetLastError();
+}
+
+template <typename WT>
+static cudaError_t wquant_dispatch(const WT* w, const float* s, int n_sets, int64_t d, int64_t n, int wbits,
+                                   int8_t* qw, float* dw, uint32_t* amax, cudaStream_t st) {
+  // sets in groups of <= 4 (each group reads W once per pass)
+  for (int k0 = 0; k0 < n_sets; k0 += 4) {
+    const int ns = std::min(4, n_sets - k0);
+    const float* sk = s + (int64_t)k0 * d;
+    int8_t* qk = qw + (int64_t)k0 * n * d;
+    float* dk = dw + (int64_t)k0 * n;
+    uint32_t* ak = amax + (int64_t)k0 * n;
+    cudaError_t e;
+    switch (ns) {
+      case 1: e = wquant_sets<WT, 1>(w, sk, d, n, wbits, qk, dk, ak, st); break;
+      case 2: e = wquant_sets<WT, 2>(w, sk, d, n, wbits, qk, dk, ak, st); break;
+      case 3: e = wquant_sets<WT, 3>(w, sk, d, n, wbits, qk, dk, ak, st); break;
+      default: e = wquant_sets<WT, 4>(w, sk, d, n, wbits, qk, dk, ak, st); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_sets, int64_t d, int64_t n, int wbits,
                           int8_t* qw, float* dw, uint32_t* amax, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(uint32_t) * n_sets * n, st);
   if (e != cudaSuccess) return e;
-  const int qmax = (1 << (wbits - 1)) - 1, qmin = -(1 << (wbits - 1));
-  const int V = wt == MASQ_BF16 ? 8 : 4;
-  const int gx = (int)ceil_div(n, 256 * V);
-  int strips = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_sms() * 4, gx * n_sets), ceil_div(d, 32)));
-  const int rows = (int)ceil_div(d, strips);
-  strips = (int)ceil_div(d, rows);
-  dim3 g1(gx, strips, n_sets), g2((unsigned)ceil_div(n, 128), (unsigned)ceil_div(d, 128), n_sets);
-  if (wt == MASQ_BF16) {
-    auto* w = static_cast<const __nv_bfloat16*>(W);
-    { ProfScope ps_("wcolmax", st); wcolmax_kernel<<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
-    { ProfScope ps_("wquant", st); wquant_kernel<<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw); }
-  } else {
-    auto* w = static_cast<const float*>(W);
-    { ProfScope ps_("wcolmax", st); wcolmax_kernel<<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
-    { ProfScope ps_("wquant", st); wquant_kernel<<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw); }
-  }
-  return cudaGetLastError();
+  if (wt == MASQ_BF16)
+    return wquant_dispatch(static_cast<const __nv_bfloat16*>(W), s, n_sets, d, n, wbits, qw, dw, amax, st);
+  return wquant_dispatch(static_cast<const float*>(W), s, n_sets, d, n, wbits, qw, dw, amax, st);
 }
 
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st) {
   ProfScope ps_("inv", st);
   inv_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(s, count, inv);
+  return cudaGetLastError();
+}
+
+// cudaErrorNotSupported -> use the streaming two-pass kernel
+template <typename XT>
+static cudaError_t aquant_reg_dispatch(const XT* X, int64_t ld_x, const uint8_t* ids, int64_t d, int n_mod,
+                                       const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx, float* dx,
+                                       uint32_t* mask, uint32_t* status, const int32_t* perm, int64_t T_out,
+                                       cudaStream_t st) {
+  constexpr int V = Vec<XT>::N;
+  const int64_t ch = ceil_div(d, V);                      // 16-byte chunks per row
+  if (ch > 1024 * 8) return cudaErrorNotSupported;
+  const int64_t warps = std::max<int64_t>(1, ceil_div(ch, 32 * 8));   // <= 8 chunks per thread
+  const int nthr = (int)(32 * warps);
+  const int64_t cpl = ceil_div(ch, nthr);
+  const int per_sm = std::max(1, 2048 / nthr);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(T_out, (int64_t)num_sms() * per_sm));
+  ProfScope ps_("aquant", st);
+#define AQ(C) aquant_row_kernel<XT, C><<<grid, nthr, 0, st>>>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out)
+  if (cpl <= 1) AQ(1);
+  else if (cpl <= 2) AQ(2);
+  else if (cpl <= 4) AQ(4);
+  else AQ(8);
+#undef AQ
   return cudaGetLastError();
 }
 
@@ -544,6 +801,12 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
     if (e != cudaSuccess) return e;
   }
   const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
+  cudaError_t er;
+  if (xt == MASQ_BF16) er = aquant_reg_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s,
+                                                (float)qmax, qmin, qmax, qx, dx, mask, status, perm, T_out, st);
+  else er = aquant_reg_dispatch(static_cast<const float*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax, qmin, qmax,
+                                qx, dx, mask, status, perm, T_out, st);
+  if (er != cudaErrorNotSupported) return er;
   const unsigned grid = (unsigned)ceil_div(T_out, 8);
   ProfScope ps_("aquant", st);
   if (xt == MASQ_BF16)
