@@ -61,17 +61,20 @@ __device__ __forceinline__ uint32_t pack4(int q0, int q1, int q2, int q3) {
 }
 
 // 4 codes sharing one scale, packed little-endian into a word.  Fast path: v = xs * (1/delta),
-// q = rint(v).  If every |v - q| <= 1/2 - 1/256, v is >= 1/256 away from any half-integer, so
-// (a) the IEEE quotient xs/delta (within 2.5e-5 of v for |v| <= 128) rounds to the same q and
-// (b) there is no tie, hence rint == round-half-away.  Otherwise `near` is set and the caller
+// q = rint(v).  rcp = fl(1/delta) and v = fl(xs * rcp) each carry <= 2^-24 relative error, so
+// |v - xs/delta| <= 2^-23 |v| <= 2^-16 for |v| <= 128, and the IEEE quotient fl(xs/delta) is
+// within 2^-17 of xs/delta: |v - fl(xs/delta)| < 2^-15.  If every |v - q| <= 1/2 - 2^-12, v is
+// >= 2^-12 away from any half-integer, so (a) fl(xs/delta) rounds to the same q and (b) there is
+// no tie, hence rint == round-half-away.  Otherwise `near` is set and the caller
 // recomputes the quad with quant_code (exact) in a rare, non-unrolled fix-up loop, which keeps
 // the hot loop free of the division code.
 __device__ __forceinline__ uint32_t quant4_fast(float x0, float x1, float x2, float x3, float rcp, int qmin,
                                                 int qmax, bool& near) {
   const float v0 = __fmul_rn(x0, rcp), v1 = __fmul_rn(x1, rcp), v2 = __fmul_rn(x2, rcp), v3 = __fmul_rn(x3, rcp);
   const float r0 = rintf(v0), r1 = rintf(v1), r2 = rintf(v2), r3 = rintf(v3);
-  near = fabsf(__fsub_rn(v0, r0)) > 0.49609375f || fabsf(__fsub_rn(v1, r1)) > 0.49609375f ||
-         fabsf(__fsub_rn(v2, r2)) > 0.49609375f || fabsf(__fsub_rn(v3, r3)) > 0.49609375f;
+  constexpr float kLim = 0.5f - 0.000244140625f;      // 1/2 - 2^-12
+  near = fabsf(__fsub_rn(v0, r0)) > kLim || fabsf(__fsub_rn(v1, r1)) > kLim || fabsf(__fsub_rn(v2, r2)) > kLim ||
+         fabsf(__fsub_rn(v3, r3)) > kLim;
   return pack4(min(max((int)r0, qmin), qmax), min(max((int)r1, qmin), qmax), min(max((int)r2, qmin), qmax),
                min(max((int)r3, qmin), qmax));
 }
@@ -783,10 +786,16 @@ static cudaError_t aquant_reg_dispatch(const XT* X, int64_t ld_x, const uint8_t*
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(T_out, (int64_t)num_sms() * per_sm));
   ProfScope ps_("aquant", st);
 #define AQ(C) aquant_row_kernel<XT, C><<<grid, nthr, 0, st>>>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out)
-  if (cpl <= 1) AQ(1);
-  else if (cpl <= 2) AQ(2);
-  else if (cpl <= 4) AQ(4);
-  else AQ(8);
+  switch (cpl) {
+    case 1: AQ(1); break;
+    case 2: AQ(2); break;
+    case 3: AQ(3); break;
+    case 4: AQ(4); break;
+    case 5: AQ(5); break;
+    case 6: AQ(6); break;
+    case 7: AQ(7); break;
+    default: AQ(8); break;
+  }
 #undef AQ
   return cudaGetLastError();
 }
