@@ -249,6 +249,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2603_04800_b200 as M
+    from paper_2603_04800_b200 import parallel as P
     from paper_2603_04800_b200._lib import lib
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -294,9 +295,7 @@ def main():
         for li, e in enumerate(L):
             X = e["X"] if X_override is None else X_override[li]
             M.calibrate_stats(X, idt, N_MOD, R=Rv[li], count=Cbuf[li], reset=True, ws=ws)
-        if world > 1:                                   # one batched exchange per step (max is order-free)
-            dist.all_reduce(Rbuf, op=dist.ReduceOp.MAX)
-            dist.all_reduce(Cbuf, op=dist.ReduceOp.SUM)
+        P.reduce_stats([Rbuf], Cbuf)                    # one batched exchange per step (max is order-free)
         for li, e in enumerate(L):
             X = e["X"] if X_override is None else X_override[li]
             s = M.init_factors(Rv[li], Cbuf[li], e["W"], ws=ws)
@@ -306,8 +305,7 @@ def main():
             M.calib_loss(X, idt, s, e["W"], WBITS, ABITS, e["Yref"], sums=Sbuf[li], counts=Nbuf[li],
                          loss=losses[li:li + 1], ws=ws)
         if world > 1:
-            dist.all_reduce(Sbuf, op=dist.ReduceOp.SUM)
-            dist.all_reduce(Nbuf, op=dist.ReduceOp.SUM)
+            P.reduce_loss(Sbuf, Nbuf)
             for li, e in enumerate(L):
                 M.loss_finalize(Sbuf[li], Nbuf[li], e["n"], loss=losses[li:li + 1])
 
@@ -316,11 +314,7 @@ def main():
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return P.max_over_ranks(x, device=dev)
 
     # ------------------------------------------------------------------ warm-up
     for _ in range(max(args.warmup, 0)):
