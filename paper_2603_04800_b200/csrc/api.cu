@@ -46,11 +46,11 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.qx = take((size_t)Tg * d);
       L.dx = take(sizeof(float) * Tg);
       L.perm = take(sizeof(int32_t) * Tg);
-      L.tile_mod = take(sizeof(uint32_t) * (Tg / kTileM));
+      L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
       L.qw_all = take((size_t)n_mod * n * d);
       L.dw_all = take(sizeof(float) * n_mod * n);
       L.amax = take(sizeof(uint32_t) * n_mod * n);
-      L.partials = take(sizeof(double) * (Tg / kTileM) * ceil_div(n, kTileN) * 16);
+      L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
       break;
     }
     case MASQ_OP_REFERENCE:
@@ -312,7 +312,7 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   double* partials = reinterpret_cast<double*>(W8(ws, L.partials));
   const int64_t Tg = grouped_rows(T, n_mod);
   const int num_n = (int)ceil_div(d_out, kTileN);
-  const int64_t tiles = (Tg / kTileM) * num_n;
+  const int64_t tiles = (Tg / kUnitM) * num_n;
   const int epi = gemm_epilogue_warps();
   MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
   MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, st));

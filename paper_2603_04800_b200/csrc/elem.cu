@@ -555,8 +555,8 @@ __global__ void __launch_bounds__(256) aquant_kernel(const XT* __restrict__ X, i
 }
 
 // ------------------------------------------------- modality-grouped row order for the loss GEMM
-// Stable counting sort of the tokens by modality; each modality segment starts on a 128-row
-// tile boundary so every loss tile holds a single modality (uses that modality's Q(S_m W)).
+// Stable counting sort of the tokens by modality; each modality segment starts on a 256-row
+// unit boundary so every loss unit (one CTA pair) holds a single modality (uses its Q(S_m W)).
 __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__ ids, int64_t T, int n_mod,
                                                      int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
                                                      int64_t n_tiles) {
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
     int acc = 0;
     for (int m = 0; m < n_mod; ++m) {
       s_seg[m] = acc;
-      acc += (s_tot[m] + kTileM - 1) / kTileM * kTileM;
+      acc += (s_tot[m] + kUnitM - 1) / kUnitM * kUnitM;
     }
     s_seg[n_mod] = acc;
   }
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
     if (m < n_mod) perm[pos[m]++] = (int32_t)t;
   }
   for (int64_t tile = tid; tile < n_tiles; tile += 1024) {
-    const int64_t r = tile * kTileM;
+    const int64_t r = tile * kUnitM;
     uint32_t v = 0xFFFFFFFFu;
     for (int m = 0; m < n_mod; ++m)
       if (r >= s_seg[m] && r < s_seg[m + 1] && s_tot[m] > 0) v = (uint32_t)m;
@@ -833,7 +833,7 @@ cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm
   cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
   if (e != cudaSuccess) return e;
   ProfScope ps_("route", st);
-  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kTileM);
+  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM);
   return cudaGetLastError();
 }
 

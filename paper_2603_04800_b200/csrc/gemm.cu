@@ -1,24 +1,32 @@
-// gemm.cu — persistent, warp-specialised tcgen05 GEMM for the MASQuant hot path (sm_100a).
+// gemm.cu — persistent, warp-specialised, CTA-pair (cta_group::2) tcgen05 GEMM for the MASQuant
+// hot path (sm_100a).
 //
 // One kernel template serves four epilogues:
 //   kModeFwd  A6+A7: acc = qx . qw^T (kind::i8, s32 in TMEM); y = acc * dx[t] * dw[j];
-//             tiles that contain non-text tokens get the CMC term
+//             units that contain non-text tokens get the CMC term
 //             y += [Zhi | Zlo] . [L2^T ; L2^T] (kind::f16, fp32) accumulated on top of y,
 //             which the epilogue writes back into the same TMEM columns first.
 //   kModeAcc  debug tap: raw int32 accumulators.
-//   kModeLoss A8: rows arrive grouped by modality (each 128-row tile holds one modality m,
+//   kModeLoss A8: rows arrive grouped by modality (each 256-row unit holds one modality m,
 //             perm maps a grouped row to its token), acc = qx . Q(S_m W)^T and the epilogue
-//             sums |acc*dx*dw_m - Yref[perm[row]]| -> per-(tile, warp) partials.
+//             sums |acc*dx*dw_m - Yref[perm[row]]| -> per-(unit, CTA, warp) partials.
 //   kModeRef  Yref = X . W (kind::f16 bf16 -> fp32), the loss target.
 //
-// Roles (320 threads, 1 CTA per SM, grid = min(#tiles, #SMs)):
-//   warp 0 lane 0 : TMA producer  (A [128 x 128B] + B [256 x 128B] per k-block, 4-stage ring)
-//   warp 1 lane 0 : MMA issuer    (4 x tcgen05.mma per k-block into a 256-column TMEM buffer)
+// A cluster of two CTAs (one per SM of a TPC) computes a 256 x 256 output unit with
+// tcgen05.mma.cta_group::2 (M = 256, N = 256): CTA r loads rows [128r, 128r+128) of the A tile
+// and rows [128r, 128r+128) of the B tile (2-SM TMA, bytes counted on the leader's barrier), so
+// each SM streams 32 KB per k-block instead of 48 KB for a 1-CTA 128 x 256 tile.  The leader
+// (rank 0) issues the MMAs and multicasts its commits to both CTAs; each CTA's TMEM holds its
+// 128 rows x 256 columns.
+//
+// Roles per CTA (320 threads, 1 CTA per SM, grid = 2 x min(#units, #SMs / 2)):
+//   warp 0 lane 0 : TMA producer  (both CTAs; 6-stage ring of 16 KB A + 16 KB B)
+//   warp 1        : TMEM allocation (both CTAs); lane 0 of the leader issues the MMAs
 //   warps 2..9    : epilogue      (warp w owns TMEM lane quarter w%4 and column half (w-2)/4:
 //                                  tcgen05.ld 32x32b -> dequant -> swizzled smem -> TMA store)
-// TMEM holds two 128x256 accumulators (512 columns) so the epilogue of tile i overlaps the
-// main loop of tile i+1.  The CMC k-blocks of tile i are inserted into the k-block stream of
-// tile i+1 (after kCmcDefer main k-blocks), by which time the epilogue has converted tile i's
+// TMEM holds two 256-column accumulators (512 columns) so the epilogue of unit i overlaps the
+// main loop of unit i+1.  The CMC k-blocks of unit i are inserted into the k-block stream of
+// unit i+1 (after kCmcDefer main k-blocks), by which time both epilogues have converted unit i's
 // int32 accumulator to f32 in place; no extra TMEM columns and no Y round trip are needed.
 #include <cstdio>
 
@@ -29,13 +37,17 @@ namespace masq {
 using namespace sm100;
 
 namespace {
-constexpr int BM = kTileM, BN = kTileN, BKB = 128;  // BKB: k-block bytes (128 int8 / 64 bf16)
-constexpr int STAGES = 4;
+constexpr int BM = 128;                              // rows per CTA
+constexpr int UM = 2 * BM;                           // rows per cluster unit
+constexpr int BN = kTileN;                           // columns per unit (MMA N)
+constexpr int BNH = BN / 2;                          // B rows held by each CTA
+constexpr int BKB = 128;                             // k-block bytes (128 int8 / 64 bf16)
+constexpr int STAGES = 6;
 constexpr int A_BYTES = BM * BKB;
-constexpr int B_BYTES = BN * BKB;
+constexpr int B_BYTES = BNH * BKB;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
-constexpr int STG_BYTES = 32 * 32 * 4;              // one 32-row x 32-column f32 staging tile per warp
+constexpr int STG_BYTES = 32 * 32 * 4;               // one 32-row x 32-column f32 staging tile per warp
 constexpr int SMEM_A = 0;
 constexpr int SMEM_B = SMEM_A + STAGES * A_BYTES;
 constexpr int SMEM_STG = SMEM_B + STAGES * B_BYTES;
@@ -44,33 +56,34 @@ constexpr int SMEM_USED = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr int kCmcDefer = 4;
 constexpr int kRasterGroup = 8;
-constexpr uint32_t IDESC_I8 = idesc_i8(BM, BN);
-constexpr uint32_t IDESC_BF16 = idesc_bf16(BM, BN);
+constexpr uint32_t IDESC_I8 = idesc_i8(UM, BN);
+constexpr uint32_t IDESC_BF16 = idesc_bf16(UM, BN);
+constexpr uint16_t kBoth = 0x3;
 static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 
 struct Params {
   int mode;
   int T, n, d;
-  int num_m, num_n, num_kb, n_tiles;
+  int num_m, num_n, num_kb, n_units;  // num_m = 256-row units
+  int n_tiles128;                     // forward: entries of the 128-row modality mask
   int n_mod;
   const float* dx;
   const float* dw;
-  const uint32_t* tile_mask;   // fwd: modality bit set per tile; loss: modality index (0xFFFFFFFF = empty)
+  const uint32_t* tile_mask;   // fwd: modality bit set per 128-row tile; loss: modality per 256-row unit
   const int32_t* perm;         // loss: grouped row -> token (-1 = padding)
   int rpad, cmc_kb;
   const float* yref;
   long long ld_ref;
-  double* partials;            // loss: [n_tiles][EPI_WARPS]
+  double* partials;            // loss: [n_units][2][EPI_WARPS]
 };
 
 struct Unit {
-  int tile, mt, nt, m;
+  int mt, nt, m;
   uint32_t mask;
 };
 
 __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
-  w.tile = u;
-  // grouped raster: kRasterGroup consecutive n-tiles swept over all m-tiles
+  // grouped raster: kRasterGroup consecutive n-tiles swept over all m-units
   const int per_group = kRasterGroup * p.num_m;
   const int g = u / per_group;
   const int rem = u - g * per_group;
@@ -78,11 +91,16 @@ __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
   const int gsz = min(kRasterGroup, p.num_n - nt0);
   w.mt = rem / gsz;
   w.nt = nt0 + (rem - w.mt * gsz);
-  w.mask = p.tile_mask ? p.tile_mask[w.mt] : 1u;
   w.m = 0;
   if (p.mode == kModeLoss) {
+    w.mask = p.tile_mask[w.mt];
     if (w.mask == 0xFFFFFFFFu) return false;
     w.m = (int)w.mask;
+  } else if (p.tile_mask) {
+    const int t0 = 2 * w.mt;
+    w.mask = p.tile_mask[t0] | (t0 + 1 < p.n_tiles128 ? p.tile_mask[t0 + 1] : 0u);
+  } else {
+    w.mask = 1u;
   }
   return true;
 }
@@ -98,7 +116,7 @@ struct Ring {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmZ,
                  const __grid_constant__ CUtensorMap tmL2, const Params p) {
@@ -108,16 +126,19 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint8_t* smA = smem + SMEM_A;
   uint8_t* smB = smem + SMEM_B;
   uint8_t* smS = smem + SMEM_STG;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;     // [2] MMA -> epilogue: accumulator ready
-  uint64_t* tempty = tfull + 2;         // [2] epilogue -> MMA: TMEM buffer drained
-  uint64_t* conv = tempty + 2;          // [2] epilogue -> MMA: y_base written back (CMC)
-  uint64_t* cmcd = conv + 2;            // [2] MMA -> epilogue: CMC accumulated
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);  // leader's is used
+  uint64_t* empty = full + STAGES;      // both: multicast MMA commit frees the stage
+  uint64_t* tfull = empty + STAGES;     // [2] both: accumulator ready
+  uint64_t* tempty = tfull + 2;         // [2] leader's: both epilogues drained the buffer
+  uint64_t* conv = tempty + 2;          // [2] leader's: both epilogues wrote y_base back (CMC)
+  uint64_t* cmcd = conv + 2;            // [2] both: CMC accumulated
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cmcd + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -126,15 +147,15 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_WARPS);
-      mbar_init(&conv[i], EPI_WARPS);
+      mbar_init(&tempty[i], 2 * EPI_WARPS);
+      mbar_init(&conv[i], 2 * EPI_WARPS);
       mbar_init(&cmcd[i], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();                       // barriers of both CTAs initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -142,35 +163,38 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
+      // ------------------------------------------------------------ TMA producer (both CTAs)
       Ring ring;
       bool pend = false;
       Unit pu{};
+      auto stage_arm = [&]() {
+        mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+        if (leader) mbar_expect_tx(&full[ring.stage], 2 * (A_BYTES + B_BYTES));
+      };
       auto load_cmc = [&](const Unit& w) {
         for (int mm = 1; mm < p.n_mod; ++mm) {
           if (!((w.mask >> mm) & 1u)) continue;
           for (int kb = 0; kb < p.cmc_kb; ++kb) {
-            mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
-            mbar_expect_tx(&full[ring.stage], A_BYTES + B_BYTES);
-            tma_load_2d(smA + ring.stage * A_BYTES, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64,
-                        w.mt * BM);
-            tma_load_2d(smB + ring.stage * B_BYTES, &tmL2, &full[ring.stage], kb * 64,
-                        (mm - 1) * p.n + w.nt * BN);
+            stage_arm();
+            tma_load_2d_2sm(smA + ring.stage * A_BYTES, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64,
+                            w.mt * UM + (int)rank * BM);
+            tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmL2, &full[ring.stage], kb * 64,
+                            (mm - 1) * p.n + w.nt * BN + (int)rank * BNH);
             ring.advance();
           }
         }
       };
-      for (int u = blockIdx.x; u < p.n_tiles; u += gridDim.x) {
+      for (int u = cid; u < p.n_units; u += ncl) {
         Unit w;
         if (!decode_unit(p, u, w)) continue;
-        const int brow = (MODE == kModeLoss ? w.m * p.n : 0) + w.nt * BN;
+        const int brow = (MODE == kModeLoss ? w.m * p.n : 0) + w.nt * BN + (int)rank * BNH;
+        const int arow = w.mt * UM + (int)rank * BM;
         const int defer_at = min(kCmcDefer, p.num_kb - 1);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
-          mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
-          mbar_expect_tx(&full[ring.stage], A_BYTES + B_BYTES);
-          tma_load_2d(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, w.mt * BM);
-          tma_load_2d(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow);
+          stage_arm();
+          tma_load_2d_2sm(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, arow);
+          tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow);
           ring.advance();
         }
         if (unit_has_cmc(p, w)) { pend = true; pu = w; }
@@ -179,8 +203,8 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    if (leader && lane == 0) {
+      // ------------------------------------------------------------ MMA issuer (leader CTA)
       Ring ring;
       uint32_t local = 0, cmc_cnt[2] = {0u, 0u};   // conv/cmcd phases count CMC uses per buffer
       bool pend = false;
@@ -197,16 +221,16 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              mma_bf16(tmem_base + buf * BN, umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32),
-                       umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32), IDESC_BF16, 1u);
+              mma_bf16_2sm(tmem_base + buf * BN, umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32),
+                           umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32), IDESC_BF16, 1u);
             }
-            mma_commit(&empty[ring.stage]);
+            mma_commit_2sm(&empty[ring.stage], kBoth);
             ring.advance();
           }
         }
-        mma_commit(&cmcd[buf]);
+        mma_commit_2sm(&cmcd[buf], kBoth);
       };
-      for (int u = blockIdx.x; u < p.n_tiles; u += gridDim.x) {
+      for (int u = cid; u < p.n_units; u += ncl) {
         Unit w;
         if (!decode_unit(p, u, w)) continue;
         const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
@@ -223,13 +247,13 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32);
             const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
-            if (MODE == kModeRef) mma_bf16(dtm, ad, bd, IDESC_BF16, (kb | k) != 0);
-            else mma_i8(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
+            if (MODE == kModeRef) mma_bf16_2sm(dtm, ad, bd, IDESC_BF16, (kb | k) != 0);
+            else mma_i8_2sm(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
           }
-          mma_commit(&empty[ring.stage]);
+          mma_commit_2sm(&empty[ring.stage], kBoth);
           ring.advance();
         }
-        mma_commit(&tfull[buf]);
+        mma_commit_2sm(&tfull[buf], kBoth);
         if (unit_has_cmc(p, w)) {
           pend = true;
           pu = w;
@@ -242,7 +266,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     __syncwarp();
   } else {
-    // -------------------------------------------------------------- epilogue warps
+    // -------------------------------------------------------------- epilogue warps (both CTAs)
     const uint32_t q = warp & 3u;                       // TMEM lane quarter this warp may access
     const uint32_t ew = warp - 2u;                      // 0..7
     const int c0 = (int)(ew >> 2) * 4;                  // this warp's 4 column chunks: c0 .. c0+3
@@ -250,12 +274,12 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t sbase = smem_u32(sb) + lane * 128u;
     uint32_t local = 0, cmc_cnt[2] = {0u, 0u};
     bool stored = false;
-    for (int u = blockIdx.x; u < p.n_tiles; u += gridDim.x) {
+    for (int u = cid; u < p.n_units; u += ncl) {
       Unit w;
       if (!decode_unit(p, u, w)) continue;
       const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
       ++local;
-      const int row0 = w.mt * BM + (int)q * 32;
+      const int row0 = w.mt * UM + (int)rank * BM + (int)q * 32;
       const int row = row0 + (int)lane;
       const int col_base = w.nt * BN;
       const int nch = max(0, min(4, (p.n - col_base) / 32 - c0));   // valid chunks of this warp
@@ -306,7 +330,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       };
 
       if (MODE == kModeFwd && unit_has_cmc(p, w)) {
-        // 1) int32 -> y_base (f32) in place, 2) let the MMA warp accumulate CMC on top, 3) store.
+        // 1) int32 -> y_base (f32) in place, 2) let the MMA accumulate CMC on top, 3) store.
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (c >= nch) break;
@@ -319,7 +343,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[buf]);
+        if (lane == 0) mbar_arrive_cluster(&conv[buf], 0);
         mbar_wait(&cmcd[buf], cmc_cnt[buf] & 1u);
         ++cmc_cnt[buf];
         tc_fence_after();
@@ -359,7 +383,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) p.partials[(size_t)(w.mt * p.num_n + w.nt) * EPI_WARPS + ew] = part;
+        if (lane == 0) p.partials[((size_t)(w.mt * p.num_n + w.nt) * 2 + rank) * EPI_WARPS + ew] = part;
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -373,23 +397,23 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();                       // both CTAs done with TMEM and with each other's barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc_2sm(tmem_base, 512);
   }
 }
 
 template <int MODE>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
-                        const CUtensorMap& l2, const Params& p, int grid, cudaStream_t st) {
+                        const CUtensorMap& l2, const Params& p, int clusters, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(masq_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -399,12 +423,12 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   }
   static const char* const kNames[4] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref"};
   ProfScope ps_(kNames[MODE], st);
-  masq_gemm_kernel<MODE><<<grid, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
+  masq_gemm_kernel<MODE><<<2 * clusters, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
   return cudaGetLastError();
 }
 }  // namespace
 
-int gemm_epilogue_warps() { return EPI_WARPS; }
+int gemm_epilogue_warps() { return 2 * EPI_WARPS; }   // partial slots per unit (2 CTAs x 8 warps)
 
 int num_sms() {
   static int n = 0;
@@ -423,10 +447,10 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   bool ok = true;
   if (bf) {
     ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
-    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.b_rows, g.d, g.d, BN, 64, true);
+    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.b_rows, g.d, g.d, BNH, 64, true);
   } else {
     ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, BM, 128, true);
-    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BN, 128, true);
+    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BNH, 128, true);
   }
   if (g.mode != kModeLoss) {
     ok &= make_tmap_2d(&ty, g.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.T, g.n, g.ld_out, 32, 32, true);
@@ -438,7 +462,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     const int64_t zc = (int64_t)(g.n_mod - 1) * 2 * g.rpad;
     ok &= make_tmap_2d(&tz, g.z, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, zc, zc, BM, 64, true);
     ok &= make_tmap_2d(&tl2, g.l2t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)(g.n_mod - 1) * g.n,
-                       2 * g.rpad, 2 * g.rpad, BN, 64, true);
+                       2 * g.rpad, 2 * g.rpad, BNH, 64, true);
   } else {
     tz = ta;
     tl2 = tb;
@@ -450,10 +474,11 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.T = (int)g.T;
   p.n = (int)g.n;
   p.d = (int)g.d;
-  p.num_m = (int)ceil_div(g.T, BM);
+  p.num_m = (int)ceil_div(g.T, UM);
   p.num_n = (int)ceil_div(g.n, BN);
   p.num_kb = (int)ceil_div(g.d, bf ? 64 : 128);
-  p.n_tiles = p.num_m * p.num_n;
+  p.n_units = p.num_m * p.num_n;
+  p.n_tiles128 = (int)ceil_div(g.T, kTileM);
   p.n_mod = g.n_mod;
   p.dx = g.dx;
   p.dw = g.dw;
@@ -464,12 +489,12 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.yref = g.yref;
   p.ld_ref = g.ld_ref;
   p.partials = g.partials;
-  const int grid = (int)std::min<int64_t>(p.n_tiles, num_sms());
+  const int clusters = (int)std::min<int64_t>(p.n_units, num_sms() / 2);
   switch (g.mode) {
-    case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, grid, st);
-    case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, grid, st);
-    case kModeLoss: return launch_mode<kModeLoss>(ta, tb, ty, tz, tl2, p, grid, st);
-    case kModeRef: return launch_mode<kModeRef>(ta, tb, ty, tz, tl2, p, grid, st);
+    case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, clusters, st);
+    case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, clusters, st);
+    case kModeLoss: return launch_mode<kModeLoss>(ta, tb, ty, tz, tl2, p, clusters, st);
+    case kModeRef: return launch_mode<kModeRef>(ta, tb, ty, tz, tl2, p, clusters, st);
     default: return cudaErrorInvalidValue;
   }
 }

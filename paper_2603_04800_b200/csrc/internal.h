@@ -13,6 +13,7 @@ namespace masq {
 constexpr int kMaxMod = 8;
 constexpr int kTileM = 128;        // GEMM M tile (token rows)
 constexpr int kTileN = 256;        // GEMM N tile (output channels)
+constexpr int kUnitM = 256;        // GEMM M unit of a CTA pair (cta_group::2); loss segments align to it
 constexpr int kStatusBytes = 256;
 
 // sticky device status bits (stored in ws[0..3])
@@ -59,9 +60,9 @@ cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t s
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
                           uint32_t* status, cudaStream_t st, const int32_t* perm = nullptr, int64_t T_out = -1);
-// rows grouped by modality, each segment padded to a multiple of 128 rows:
-// perm[Tg] (grouped row -> token, -1 padding), tile_mod[Tg/128] (modality of the tile, ~0u empty)
-inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kTileM) * kTileM + (int64_t)n_mod * kTileM; }
+// rows grouped by modality, each segment padded to a multiple of kUnitM (256) rows:
+// perm[Tg] (grouped row -> token, -1 padding), tile_mod[Tg/256] (modality of the unit, ~0u empty)
+inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kUnitM) * kUnitM + (int64_t)n_mod * kUnitM; }
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
                          cudaStream_t st);
 // L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (the same L2^T for the Zhi and Zlo K-blocks)

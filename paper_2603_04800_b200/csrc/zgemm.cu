@@ -40,7 +40,10 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   const int mt = blockIdx.x;
   const int m0 = 1 + blockIdx.y * per;
   const int m1 = min(m0 + per, n_mod);           // exclusive
-  const uint32_t tmask = tile_mask[mt];
+  // the forward GEMM works on 256-row units (tile pairs): write every modality block present in
+  // either tile of the pair, so the CMC K-blocks of the unit read zeros (never stale data)
+  const int n_tiles = (T + 127) / 128;
+  const uint32_t tmask = tile_mask[mt] | ((mt ^ 1) < n_tiles ? tile_mask[mt ^ 1] : 0u);
   uint32_t want = 0;
   for (int mm = m0; mm < m1; ++mm) want |= 1u << mm;
   if (!(tmask & want)) return;                   // CTA-uniform: no modality of this pass here
