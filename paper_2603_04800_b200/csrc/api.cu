@@ -54,7 +54,6 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       break;
     }
     case MASQ_OP_REFERENCE:
-      L.wt = take(sizeof(uint16_t) * (size_t)n * d);
       break;
     default:
       break;
@@ -259,8 +258,6 @@ masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, in
   MASQ_TRY(check_x(X, MASQ_BF16, ld_x, d));
   const WsLayout L = ws_layout(MASQ_OP_REFERENCE, T, d, d_out, 1, 0);
   MASQ_TRY(check_ws(ws, ws_bytes, L));
-  uint16_t* wt = reinterpret_cast<uint16_t*>(W8(ws, L.wt));
-  MASQ_CK(launch_transpose_bf16(static_cast<const uint16_t*>(W), d, d_out, wt, S(stream)));
   GemmArgs g{};
   g.mode = kModeRef;
   g.T = T;
@@ -268,8 +265,8 @@ masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, in
   g.d = d;
   g.xbf = static_cast<const uint16_t*>(X);
   g.ld_x = ld_x;
-  g.b = wt;
-  g.b_rows = d_out;
+  g.b = W;                                              // read as stored (MN-major B operand)
+  g.b_rows = d;
   g.n_mod = 1;
   g.out = Yref;
   g.ld_out = ld_ref;

@@ -58,6 +58,7 @@ constexpr int kCmcDefer = 4;
 constexpr int kRasterGroup = 8;
 constexpr uint32_t IDESC_I8 = idesc_i8(UM, BN);
 constexpr uint32_t IDESC_BF16 = idesc_bf16(UM, BN);
+constexpr uint32_t IDESC_BF16_BMN = idesc_bf16(UM, BN) | (1u << 16);   // B MN-major (X.W reads W as stored)
 constexpr uint16_t kBoth = 0x3;
 static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 
@@ -194,7 +195,14 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
           stage_arm();
           tma_load_2d_2sm(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, arow);
-          tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow);
+          if (MODE == kModeRef) {
+            // W [d x n] as stored: two 64(n) x 64(k) boxes -> MN-major B tile [n-half][k][64 n]
+            tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], brow, kb * KELEMS);
+            tma_load_2d_2sm(smB + ring.stage * B_BYTES + B_BYTES / 2, &tmB, &full[ring.stage], brow + 64,
+                            kb * KELEMS);
+          } else {
+            tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow);
+          }
           ring.advance();
         }
         if (unit_has_cmc(p, w)) { pend = true; pu = w; }
@@ -246,9 +254,13 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32);
-            const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
-            if (MODE == kModeRef) mma_bf16_2sm(dtm, ad, bd, IDESC_BF16, (kb | k) != 0);
-            else mma_i8_2sm(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
+            if (MODE == kModeRef) {
+              const uint64_t bd = umma_desc_sw128_mn(b0 + ring.stage * B_BYTES + k * 2048, B_BYTES / 2);
+              mma_bf16_2sm(dtm, ad, bd, IDESC_BF16_BMN, (kb | k) != 0);
+            } else {
+              const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
+              mma_i8_2sm(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
+            }
           }
           mma_commit_2sm(&empty[ring.stage], kBoth);
           ring.advance();
@@ -447,7 +459,8 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   bool ok = true;
   if (bf) {
     ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
-    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.b_rows, g.d, g.d, BNH, 64, true);
+    // B = W [d x n] row-major (MN-major for the MMA): box 64 (n) x 64 (k)
+    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.d, g.n, g.n, 64, 64, true);
   } else {
     ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, BM, 128, true);
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BNH, 128, true);

@@ -158,6 +158,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   desc |= static_cast<uint64_t>(2u) << 61;            // SWIZZLE_128B
   return desc;
 }
+// MN-major operand tile (bf16), SWIZZLE_128B: 64-element (128-byte) MN rows, one row per K index,
+// K groups of 8 rows 1024 B apart (SBO), consecutive 64-element MN blocks lbo_bytes apart (LBO).
+// Advancing K by 16 elements = 16 rows = +2048 bytes on the start address.
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t desc = 0;
+  desc |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  desc |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  desc |= static_cast<uint64_t>(1024u >> 4) << 32;
+  desc |= static_cast<uint64_t>(1u) << 46;
+  desc |= static_cast<uint64_t>(2u) << 61;
+  return desc;
+}
 // Instruction descriptors (32-bit): c_format [4,6), a_format [7,10), b_format [10,13),
 // a_major [15], b_major [16] (0 = K-major), N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
