@@ -47,6 +47,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.dx = take(sizeof(float) * Tg);
       L.perm = take(sizeof(int32_t) * Tg);
       L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
+      L.cnt = take(sizeof(int64_t) * n_mod);
       L.qw_all = take((size_t)n_mod * n * d);
       L.dw_all = take(sizeof(float) * n_mod * n);
       L.amax = take(sizeof(uint32_t) * n_mod * n);
@@ -312,7 +313,8 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   const int64_t tiles = (Tg / kUnitM) * num_n;
   const int epi = gemm_epilogue_warps();
   MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
-  MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, st));
+  int64_t* cnt = reinterpret_cast<int64_t*>(W8(ws, L.cnt));
+  MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, cnt, st));
   MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, nullptr, status_of(ws), st, perm, Tg));
   MASQ_CK(launch_wquant(W, wt, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
   MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * tiles * epi, st));
@@ -333,8 +335,7 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   g.ld_ref = ld_ref;
   g.partials = partials;
   MASQ_CK(launch_gemm(g, st));
-  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, mod_id, T, n_mod, d_out, lambda, sums, counts, loss,
-                             st));
+  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st));
   return MASQ_OK;
 }
 

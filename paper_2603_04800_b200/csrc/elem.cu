@@ -559,10 +559,10 @@ __global__ void __launch_bounds__(256) aquant_kernel(const XT* __restrict__ X, i
 // unit boundary so every loss unit (one CTA pair) holds a single modality (uses its Q(S_m W)).
 __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__ ids, int64_t T, int n_mod,
                                                      int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
-                                                     int64_t n_tiles) {
-  __shared__ int s_cnt[1024];
+                                                     int64_t n_tiles, int64_t* __restrict__ counts) {
+  __shared__ int s_warp[kMaxMod][32];
   __shared__ int s_tot[kMaxMod], s_seg[kMaxMod + 1];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t chunk = (T + 1023) / 1024;
   const int64_t t0 = tid * chunk, t1 = min(T, t0 + chunk);
   int cnt[kMaxMod];
@@ -573,34 +573,53 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
 #pragma unroll
     for (int mm = 0; mm < kMaxMod; ++mm) cnt[mm] += (m == mm);
   }
+  // exclusive prefix of cnt[m] over threads: warp shuffle scan + scan of the 32 warp totals
   int excl[kMaxMod];
-  for (int m = 0; m < n_mod; ++m) {                 // block exclusive scan, one modality at a time
-    s_cnt[tid] = cnt[m];
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-      const int v = tid >= off ? s_cnt[tid - off] : 0;
-      __syncthreads();
-      s_cnt[tid] += v;
-      __syncthreads();
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) {
+    int v = cnt[m];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
     }
-    excl[m] = s_cnt[tid] - cnt[m];
-    if (tid == 1023) s_tot[m] = s_cnt[tid];
-    __syncthreads();
+    excl[m] = v - cnt[m];
+    if (lane == 31) s_warp[m][warp] = v;
   }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int m = 0; m < kMaxMod; ++m) {
+      const int w = s_warp[m][lane];
+      int v = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      s_warp[m][lane] = v - w;                       // exclusive over warps
+      if (lane == 31) s_tot[m] = v;
+    }
+  }
+  __syncthreads();
   if (tid == 0) {
     int acc = 0;
     for (int m = 0; m < n_mod; ++m) {
       s_seg[m] = acc;
       acc += (s_tot[m] + kUnitM - 1) / kUnitM * kUnitM;
+      if (counts) counts[m] = s_tot[m];
     }
     s_seg[n_mod] = acc;
   }
   __syncthreads();
   int pos[kMaxMod];
-  for (int m = 0; m < n_mod; ++m) pos[m] = s_seg[m] + excl[m];
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) pos[m] = (m < n_mod ? s_seg[m] : 0) + s_warp[m][warp] + excl[m];
   for (int64_t t = t0; t < t1; ++t) {
     const int m = ids[t];
-    if (m < n_mod) perm[pos[m]++] = (int32_t)t;
+#pragma unroll
+    for (int mm = 0; mm < kMaxMod; ++mm)
+      if (m == mm && mm < n_mod) perm[pos[mm]++] = (int32_t)t;
   }
   for (int64_t tile = tid; tile < n_tiles; tile += 1024) {
     const int64_t r = tile * kUnitM;
@@ -641,42 +660,39 @@ struct Lambda8 {
   float v[kMaxMod];
 };
 
-__global__ void __launch_bounds__(256) loss_reduce_kernel(const double* __restrict__ partials, int64_t n_tiles,
-                                                          int num_n, int epi, const uint32_t* __restrict__ tile_mod,
-                                                          const uint8_t* __restrict__ ids, int64_t T, int n_mod,
-                                                          int64_t n, Lambda8 lam, double* __restrict__ sums,
-                                                          int64_t* __restrict__ counts, double* __restrict__ loss) {
-  __shared__ double red[256];
-  __shared__ long long cred[256];
-  __shared__ double s_sum[kMaxMod];
-  __shared__ long long s_cnt[kMaxMod];
-  for (int m = 0; m < n_mod; ++m) {
+__global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restrict__ partials, int64_t n_units,
+                                                           int num_n, int epi, const uint32_t* __restrict__ tile_mod,
+                                                           const int64_t* __restrict__ counts_in, int n_mod,
+                                                           int64_t n, Lambda8 lam, double* __restrict__ sums,
+                                                           int64_t* __restrict__ counts, double* __restrict__ loss) {
+  __shared__ double red[kMaxMod][512];
+  double acc[kMaxMod];
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) acc[m] = 0.0;
+  for (int64_t u = threadIdx.x; u < n_units; u += 512) {         // fixed assignment -> deterministic
+    const uint32_t m = tile_mod[u / num_n];
+    if (m >= (uint32_t)n_mod) continue;
     double a = 0.0;
-    long long c = 0;
-    for (int64_t lt = threadIdx.x; lt < n_tiles; lt += 256) {     // fixed order -> deterministic
-      if (tile_mod[lt / num_n] != (uint32_t)m) continue;
-      for (int e = 0; e < epi; ++e) a += partials[lt * epi + e];
-    }
-    for (int64_t t = threadIdx.x; t < T; t += 256) c += (ids[t] == m);
-    red[threadIdx.x] = a;
-    cred[threadIdx.x] = c;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-      if (threadIdx.x < o) {
-        red[threadIdx.x] += red[threadIdx.x + o];
-        cred[threadIdx.x] += cred[threadIdx.x + o];
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) { s_sum[m] = red[0]; s_cnt[m] = cred[0]; }
+    for (int e = 0; e < epi; ++e) a += partials[u * epi + e];
+#pragma unroll
+    for (int mm = 0; mm < kMaxMod; ++mm)
+      if (mm == (int)m) acc[mm] += a;
+  }
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) red[m][threadIdx.x] = acc[m];
+  __syncthreads();
+  for (int o = 256; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int m = 0; m < n_mod; ++m) red[m][threadIdx.x] += red[m][threadIdx.x + o];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     double L = 0.0;
     for (int m = 0; m < n_mod; ++m) {
-      sums[m] = s_sum[m];
-      counts[m] = s_cnt[m];
-      if (s_cnt[m] > 0) L += (double)lam.v[m] * s_sum[m] / ((double)s_cnt[m] * (double)n);
+      const int64_t c = counts_in[m];
+      sums[m] = red[m][0];
+      counts[m] = c;
+      if (c > 0) L += (double)lam.v[m] * red[m][0] / ((double)c * (double)n);
     }
     loss[0] = L;
   }
@@ -828,12 +844,12 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
 }
 
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
-                         cudaStream_t st) {
+                         int64_t* counts, cudaStream_t st) {
   const int64_t Tg = grouped_rows(T, n_mod);
   cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
   if (e != cudaSuccess) return e;
   ProfScope ps_("route", st);
-  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM);
+  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM, counts);
   return cudaGetLastError();
 }
 
@@ -860,12 +876,12 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
   return transpose(W, d, n, n, 0, Wt, d, 0, -1, 1, st);
 }
 
-cudaError_t launch_loss_reduce(const double* partials, int64_t n_tiles, int num_n, int epi, const uint32_t* tile_mod,
-                               const uint8_t* ids, int64_t T, int n_mod, int64_t n, const float* lambda_host,
+cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
+                               const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
                                double* sums, int64_t* counts, double* loss, cudaStream_t st) {
   ProfScope ps_("loss_reduce", st);
-  loss_reduce_kernel<<<1, 256, 0, st>>>(partials, n_tiles, num_n, epi, tile_mod, ids, T, n_mod, n,
-                                        make_lambda(lambda_host, n_mod), sums, counts, loss);
+  loss_reduce_kernel<<<1, 512, 0, st>>>(partials, n_units, num_n, epi, tile_mod, counts_in, n_mod, n,
+                                         make_lambda(lambda_host, n_mod), sums, counts, loss);
   return cudaGetLastError();
 }
 

@@ -26,7 +26,7 @@ inline int64_t rpad_of(int64_t r) { return r > 0 ? ceil_div(r, 64) * 64 : 0; }
 
 struct WsLayout {
   size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0, xsplit = 0;
-  size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, total = 0;
+  size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, cnt = 0, total = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -63,16 +63,18 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
 // rows grouped by modality, each segment padded to a multiple of kUnitM (256) rows:
 // perm[Tg] (grouped row -> token, -1 padding), tile_mod[Tg/256] (modality of the unit, ~0u empty)
 inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kUnitM) * kUnitM + (int64_t)n_mod * kUnitM; }
+// counts (optional): per-modality token counts [n_mod] (int64)
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
-                         cudaStream_t st);
+                         int64_t* counts, cudaStream_t st);
 // L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (the same L2^T for the Zhi and Zlo K-blocks)
 cudaError_t launch_pack_l2(const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t n, int r, int rpad, uint16_t* L2t,
                            cudaStream_t st);
 // bf16 W [d x n] -> Wt [n x d]
 cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint16_t* Wt, cudaStream_t st);
-// sums[m] = fixed-order sum of partials[lt * epi + e] over tiles lt with tile_mod[lt / num_n] == m
-cudaError_t launch_loss_reduce(const double* partials, int64_t n_tiles, int num_n, int epi, const uint32_t* tile_mod,
-                               const uint8_t* ids, int64_t T, int n_mod, int64_t n, const float* lambda_host,
+// sums[m] = fixed-order sum of partials[u * epi + e] over units u with tile_mod[u / num_n] == m;
+// counts_in: per-modality token counts from launch_route
+cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
+                               const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
                                double* sums, int64_t* counts, double* loss, cudaStream_t st);
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st);
