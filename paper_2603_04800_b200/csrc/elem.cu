@@ -253,39 +253,52 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
                                                       int64_t d, int64_t n, int rows_per_strip,
                                                       uint32_t* __restrict__ amax) {
   constexpr int V = Vec<WT>::N;
-  const int64_t j0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * V;
-  if (j0 >= n) return;
+  constexpr int U = 8;
+  __shared__ float ss[NS][256];                       // factors of the current 256-row sub-strip
   const int64_t i0 = (int64_t)blockIdx.y * rows_per_strip;
   const int64_t i1 = min(d, i0 + rows_per_strip);
+  const int64_t j0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * V;
+  const bool active = j0 < n;
   float m[NS][V];
 #pragma unroll
   for (int k = 0; k < NS; ++k)
 #pragma unroll
     for (int e = 0; e < V; ++e) m[k][e] = 0.f;
-  int64_t i = i0;
-  for (; i + 4 <= i1; i += 4) {
-    float f[4][V];
+  for (int64_t sb = i0; sb < i1; sb += 256) {
+    const int nr = (int)min((int64_t)256, i1 - sb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < NS * nr; t += 256) {
+      const int k = t / nr, r = t - k * nr;
+      ss[k][r] = __ldg(s + (int64_t)k * d + sb + r);
+    }
+    __syncthreads();
+    if (!active) continue;
+    int r = 0;
+    for (; r + U <= nr; r += U) {
+      float f[U][V];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) Vec<WT>::load(W + (i + u) * n + j0, f[u]);
+      for (int u = 0; u < U; ++u) Vec<WT>::load(W + (sb + r + u) * n + j0, f[u]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const float si = ss[k][r + u];
+#pragma unroll
+          for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[u][e])));
+        }
+    }
+    for (; r < nr; ++r) {
+      float f[V];
+      Vec<WT>::load(W + (sb + r) * n + j0, f);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const float si = __ldg(s + (int64_t)k * d + i + u);
+        const float si = ss[k][r];
 #pragma unroll
-        for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[u][e])));
+        for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[e])));
       }
-  }
-  for (; i < i1; ++i) {
-    float f[V];
-    Vec<WT>::load(W + i * n + j0, f);
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      const float si = __ldg(s + (int64_t)k * d + i);
-#pragma unroll
-      for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[e])));
     }
   }
+  if (!active) return;
 #pragma unroll
   for (int k = 0; k < NS; ++k)
 #pragma unroll
@@ -293,13 +306,23 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
       if (m[k][e] > 0.f) atomicMax(amax + (int64_t)k * n + j0 + e, __float_as_uint(m[k][e]));
 }
 
+// dw[j] = max(amax[j] / q_max, 1e-12f) (the output scales); amax[j] is overwritten in place with
+// the f32 reciprocal 1/dw[j] used by the fast quantizer path
+__global__ void wscale_kernel(uint32_t* __restrict__ amax, float* __restrict__ dw, int64_t count, float qmaxf) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  const float dv = fmaxf(__fdiv_rn(__uint_as_float(amax[j]), qmaxf), kFloor);
+  dw[j] = dv;
+  amax[j] = __float_as_uint(__fdiv_rn(1.0f, dv));
+}
+
 // pass 2: one 128 (i) x 64 (j) tile of W read once; for every set k the codes are packed
 // 4 rows per 32-bit word into a smem tile [64 j][128 i] and written K-major (qw[k][j][i]).
 template <typename WT, int NS>
 __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, const float* __restrict__ s,
-                                                     int64_t d, int64_t n, float qmaxf, int qmin, int qmax,
-                                                     const uint32_t* __restrict__ amax, int8_t* __restrict__ qw,
-                                                     float* __restrict__ dw) {
+                                                     int64_t d, int64_t n, int qmin, int qmax,
+                                                     const float* __restrict__ rcp, int8_t* __restrict__ qw,
+                                                     const float* __restrict__ dw) {
   constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
   constexpr int CPT = 8;                        // columns per thread
   constexpr int LPT = CPT / V;                  // loads per row per thread
@@ -333,25 +356,31 @@ __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, c
       const int64_t i = i0 + 4 * ty + r;
       si[r] = i < d ? __ldg(s + (int64_t)k * d + i) : 0.f;
     }
+    float rcv[CPT];
+    if (colok) {
+      const float4* r4 = reinterpret_cast<const float4*>(rcp + (int64_t)k * n + jb);
+      const float4 a = __ldg(r4), b = __ldg(r4 + 1);
+      rcv[0] = a.x; rcv[1] = a.y; rcv[2] = a.z; rcv[3] = a.w; rcv[4] = b.x; rcv[5] = b.y; rcv[6] = b.z; rcv[7] = b.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) rcv[e] = 1.f;
+    }
     uint32_t nearmask = 0;
 #pragma unroll
     for (int e = 0; e < CPT; ++e) {
-      const int64_t j = jb + e;
-      const float dv = colok ? fmaxf(__fdiv_rn(__uint_as_float(__ldg(amax + (int64_t)k * n + j)), qmaxf), kFloor) : 1.f;
-      const float rc = __fdiv_rn(1.0f, dv);
+      const float rc = rcv[e];
       bool nr;
       tile[tx * CPT + e][ty] = quant4_fast(__fmul_rn(si[0], f[0][e]), __fmul_rn(si[1], f[1][e]),
                                            __fmul_rn(si[2], f[2][e]), __fmul_rn(si[3], f[3][e]), rc, qmin, qmax, nr);
       nearmask |= (uint32_t)nr << e;
-      if (blockIdx.y == 0 && ty == 0 && colok) dw[(int64_t)k * n + j] = dv;
     }
 #pragma unroll 1
     while (nearmask) {                                       // rare exact fix-up of flagged quads
       const int e = __ffs(nearmask) - 1;
       nearmask &= nearmask - 1;
       const int64_t j = jb + e;
-      const float dv = fmaxf(__fdiv_rn(__uint_as_float(__ldg(amax + (int64_t)k * n + j)), qmaxf), kFloor);
-      const float rc = __fdiv_rn(1.0f, dv);
+      const float dv = __ldg(dw + (int64_t)k * n + j);
+      const float rc = __ldg(rcp + (int64_t)k * n + j);
       float x[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -740,12 +769,15 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   const int qmax = (1 << (wbits - 1)) - 1, qmin = -(1 << (wbits - 1));
   constexpr int V = Vec<WT>::N;
   const int gx = (int)ceil_div(n, 256 * V);
-  int strips = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(num_sms() * 6, gx), ceil_div(d, 16)));
+  // ~4 CTAs per SM, but at most 128 strips (bounds the atomicMax traffic on tall weights)
+  int strips = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(ceil_div(num_sms() * 4, gx), 128),
+                                                           ceil_div(d, 16)));
   const int rows = (int)ceil_div(d, strips);
   strips = (int)ceil_div(d, rows);
   dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 64), (unsigned)ceil_div(d, 128));
   { ProfScope ps_("wcolmax", st); wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
-  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS><<<g2, 256, 0, st>>>(w, s, d, n, (float)qmax, qmin, qmax, amax, qw, dw); }
+  { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, NS * n, (float)qmax); }
+  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, reinterpret_cast<const float*>(amax), qw, dw); }
   return cudaGetLastError();
 }
 

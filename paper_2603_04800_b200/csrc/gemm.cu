@@ -75,7 +75,7 @@ struct Params {
   int rpad, cmc_kb;
   const float* yref;
   long long ld_ref;
-  double* partials;            // loss: [n_units][2][EPI_WARPS]
+  double* partials;            // loss: [n_units][2] (one per CTA of the pair)
 };
 
 struct Unit {
@@ -134,6 +134,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t* conv = tempty + 2;          // [2] leader's: both epilogues wrote y_base back (CMC)
   uint64_t* cmcd = conv + 2;            // [2] both: CMC accumulated
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cmcd + 2);
+  double* red = reinterpret_cast<double*>(tmem_slot + 2);   // [EPI_WARPS] loss partials of one unit
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -395,7 +396,16 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) p.partials[((size_t)(w.mt * p.num_n + w.nt) * 2 + rank) * EPI_WARPS + ew] = part;
+        // combine the 8 epilogue warps in a fixed order -> one partial per (unit, CTA)
+        if (lane == 0) red[ew] = part;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0) {
+          double tot = 0.0;
+#pragma unroll
+          for (int e = 0; e < EPI_WARPS; ++e) tot += red[e];
+          p.partials[(size_t)(w.mt * p.num_n + w.nt) * 2 + rank] = tot;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -440,7 +450,7 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
 }
 }  // namespace
 
-int gemm_epilogue_warps() { return 2 * EPI_WARPS; }   // partial slots per unit (2 CTAs x 8 warps)
+int gemm_epilogue_warps() { return 2; }   // loss partial slots per unit (one per CTA of the pair)
 
 int num_sms() {
   static int n = 0;
