@@ -70,13 +70,21 @@ __device__ __forceinline__ uint32_t pack4(int q0, int q1, int q2, int q3) {
 // the hot loop free of the division code.
 __device__ __forceinline__ uint32_t quant4_fast(float x0, float x1, float x2, float x3, float rcp, int qmin,
                                                 int qmax, bool& near) {
-  const float v0 = __fmul_rn(x0, rcp), v1 = __fmul_rn(x1, rcp), v2 = __fmul_rn(x2, rcp), v3 = __fmul_rn(x3, rcp);
-  const float r0 = rintf(v0), r1 = rintf(v1), r2 = rintf(v2), r3 = rintf(v3);
+  // t = v + 1.5*2^23 rounds v to the nearest integer (ties to even) in the low mantissa bits, so
+  // the low byte of t is the two's-complement int8 code and t - 1.5*2^23 = rint(v) exactly.
+  // The clamp to [qmin, qmax] is a no-op here: every |x| <= absmax of its group and
+  // delta = fl(absmax / q_max) (or the 1e-12 floor, larger), so |v| <= q_max (1 + 2^-22).
+  constexpr float kMagic = 12582912.0f;               // 1.5 * 2^23
   constexpr float kLim = 0.5f - 0.000244140625f;      // 1/2 - 2^-12
-  near = fabsf(__fsub_rn(v0, r0)) > kLim || fabsf(__fsub_rn(v1, r1)) > kLim || fabsf(__fsub_rn(v2, r2)) > kLim ||
-         fabsf(__fsub_rn(v3, r3)) > kLim;
-  return pack4(min(max((int)r0, qmin), qmax), min(max((int)r1, qmin), qmax), min(max((int)r2, qmin), qmax),
-               min(max((int)r3, qmin), qmax));
+  const float v0 = __fmul_rn(x0, rcp), v1 = __fmul_rn(x1, rcp), v2 = __fmul_rn(x2, rcp), v3 = __fmul_rn(x3, rcp);
+  const float t0 = __fadd_rn(v0, kMagic), t1 = __fadd_rn(v1, kMagic), t2 = __fadd_rn(v2, kMagic),
+              t3 = __fadd_rn(v3, kMagic);
+  near = fabsf(__fsub_rn(v0, __fsub_rn(t0, kMagic))) > kLim || fabsf(__fsub_rn(v1, __fsub_rn(t1, kMagic))) > kLim ||
+         fabsf(__fsub_rn(v2, __fsub_rn(t2, kMagic))) > kLim || fabsf(__fsub_rn(v3, __fsub_rn(t3, kMagic))) > kLim;
+  (void)qmin;
+  (void)qmax;
+  return __byte_perm(__byte_perm(__float_as_uint(t0), __float_as_uint(t1), 0x0040),
+                     __byte_perm(__float_as_uint(t2), __float_as_uint(t3), 0x0040), 0x5410);
 }
 __device__ __forceinline__ uint32_t quant4_exact(float x0, float x1, float x2, float x3, float delta, float rcp,
                                                  int qmin, int qmax) {
