@@ -29,6 +29,7 @@
 // unit i+1 (after kCmcDefer main k-blocks), by which time both epilogues have converted unit i's
 // int32 accumulator to f32 in place; no extra TMEM columns and no Y round trip are needed.
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -55,7 +56,7 @@ constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * STG_BYTES;
 constexpr int SMEM_USED = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr int kCmcDefer = 4;
-constexpr int kRasterGroup = 8;
+constexpr int kRasterGroupDefault = 16;
 constexpr uint32_t IDESC_I8 = idesc_i8(UM, BN);
 constexpr uint32_t IDESC_BF16 = idesc_bf16(UM, BN);
 constexpr uint32_t IDESC_BF16_BMN = idesc_bf16(UM, BN) | (1u << 16);   // B MN-major (X.W reads W as stored)
@@ -67,6 +68,7 @@ struct Params {
   int T, n, d;
   int num_m, num_n, num_kb, n_units;  // num_m = 256-row units
   int n_tiles128;                     // forward: entries of the 128-row modality mask
+  int group;                          // raster: n-tiles per group swept over all m-units
   int n_mod;
   const float* dx;
   const float* dw;
@@ -84,12 +86,12 @@ struct Unit {
 };
 
 __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
-  // grouped raster: kRasterGroup consecutive n-tiles swept over all m-units
-  const int per_group = kRasterGroup * p.num_m;
+  // grouped raster: p.group consecutive n-tiles swept over all m-units
+  const int per_group = p.group * p.num_m;
   const int g = u / per_group;
   const int rem = u - g * per_group;
-  const int nt0 = g * kRasterGroup;
-  const int gsz = min(kRasterGroup, p.num_n - nt0);
+  const int nt0 = g * p.group;
+  const int gsz = min(p.group, p.num_n - nt0);
   w.mt = rem / gsz;
   w.nt = nt0 + (rem - w.mt * gsz);
   w.m = 0;
@@ -502,6 +504,14 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.num_kb = (int)ceil_div(g.d, bf ? 64 : 128);
   p.n_units = p.num_m * p.num_n;
   p.n_tiles128 = (int)ceil_div(g.T, kTileM);
+  {
+    static int env_group = -1;
+    if (env_group < 0) {
+      const char* e = getenv("MASQ_RASTER_GROUP");         // tuning knob (measurement only)
+      env_group = e ? atoi(e) : 0;
+    }
+    p.group = env_group > 0 ? env_group : kRasterGroupDefault;
+  }
   p.n_mod = g.n_mod;
   p.dx = g.dx;
   p.dw = g.dw;
