@@ -312,3 +312,28 @@ def test_forward_f32_input_with_cmc():
     assert np.array_equal(qx.cpu().numpy(), qxo) and np.array_equal(dx.cpu().numpy(), dxo)
     Yo = O.linear_forward(Xf, c["ids"], so, qwo, dwo, 8, list(c["L1"]), list(c["L2"]))
     assert max_abs_norm(Y.cpu().numpy(), Yo) <= TOL_Y
+
+
+def test_forward_max_tokens_sampled():
+    """c5's largest point: 262144 tokens (256 samples of the c3 layout) through the forward,
+    d = 3584 -> 3584, W4A8, CMC r = 64; sampled rows against the oracle, acc bit-exact."""
+    T = 262144
+    cfg = synth.CONFIGS["c3"]
+    ids = synth.modality_ids(cfg["pattern"], T=T)
+    X = synth.activations(ids, 3584, 2, synth.seed_for(4, 0, 0))
+    W = synth.weight(3584, 3584, synth.seed_for(4, 0, 1))
+    L1, L2 = synth.lowrank(3584, 3584, 64, 2, synth.seed_for(4, 0, 2))
+    m = M()
+    Ro, co = O.calibrate_stats(X, ids, 2)
+    so = O.init_factors(Ro, co, W)
+    qwo, dwo = O.quantize_weight(W, so[0], 4)
+    Xg = bf(X)
+    Y = m.linear_forward(Xg, tt(ids), tt(so), tt(qwo), tt(dwo), 4, 8, bf(L1), bf(L2))
+    acc = m.linear_forward(Xg, tt(ids), tt(so), tt(qwo), tt(dwo), 4, 8, acc_debug=True)
+    m.check()
+    rows = np.concatenate([np.arange(0, 256), np.arange(T - 256, T),
+                           np.random.Generator(np.random.PCG64(7)).choice(T, 512, replace=False)])
+    Yo = O.linear_forward(X, ids, so, qwo, dwo, 8, [L1[0]], [L2[0]], rows=rows)
+    assert max_abs_norm(Y.cpu().numpy()[rows], Yo) <= TOL_Y
+    qxo, _ = O.quantize_activations(O.decode(X)[rows], ids[rows], so, 8)
+    assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), O.int_gemm(qxo, qwo))
