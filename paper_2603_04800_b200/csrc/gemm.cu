@@ -311,6 +311,13 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       int src = -1;
       if (MODE == kModeLoss && row < p.T) src = __ldg(p.perm + row);
+      // loss: issue the first chunk's Yref loads now, under the main loop of this unit
+      float4 ycur[8];
+      if (MODE == kModeLoss && src >= 0 && nch > 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)src * p.ld_ref + col_base + c0 * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ycur[j] = __ldg(r4 + j);
+      }
 
       mbar_wait(&tfull[buf], ph);
       tc_fence_after();
@@ -375,26 +382,30 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (c >= nch) break;
-          float4 y[8];
-          if (src >= 0) {
-            const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)src * p.ld_ref + col_base +
-                                                               (c0 + c) * 32);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) y[j] = __ldg(r4 + j);
-          }
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
+          float4 ynext[8];
+          if (src >= 0 && c + 1 < nch) {                 // prefetch the next chunk's Yref row segment
+            const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)src * p.ld_ref + col_base +
+                                                               (c0 + c + 1) * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ynext[j] = __ldg(r4 + j);
+          }
           tmem_wait_ld();
           dequant(v, c);
           if (src >= 0) {
             float acc = 0.f;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              acc += fabsf(__uint_as_float(v[4 * j + 0]) - y[j].x) + fabsf(__uint_as_float(v[4 * j + 1]) - y[j].y) +
-                     fabsf(__uint_as_float(v[4 * j + 2]) - y[j].z) + fabsf(__uint_as_float(v[4 * j + 3]) - y[j].w);
+              acc += fabsf(__uint_as_float(v[4 * j + 0]) - ycur[j].x) +
+                     fabsf(__uint_as_float(v[4 * j + 1]) - ycur[j].y) +
+                     fabsf(__uint_as_float(v[4 * j + 2]) - ycur[j].z) +
+                     fabsf(__uint_as_float(v[4 * j + 3]) - ycur[j].w);
             }
             part += (double)acc;
           }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ycur[j] = ynext[j];
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
