@@ -168,6 +168,10 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer (both CTAs)
+      // A streams through (evict-first); B is re-read by every m-unit of the raster group (evict-last)
+      // (int8 modes: default policy measured as fast or faster)
+      const uint64_t pol_a = MODE == kModeRef ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_b = MODE == kModeRef ? policy_evict_last() : policy_evict_normal();
       Ring ring;
       bool pend = false;
       Unit pu{};
@@ -197,14 +201,14 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
           stage_arm();
-          tma_load_2d_2sm(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, arow);
+          tma_load_2d_2sm_hint(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, arow, pol_a);
           if (MODE == kModeRef) {
             // W [d x n] as stored: two 64(n) x 64(k) boxes -> MN-major B tile [n-half][k][64 n]
-            tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], brow, kb * KELEMS);
-            tma_load_2d_2sm(smB + ring.stage * B_BYTES + B_BYTES / 2, &tmB, &full[ring.stage], brow + 64,
-                            kb * KELEMS);
+            tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], brow, kb * KELEMS, pol_b);
+            tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES + B_BYTES / 2, &tmB, &full[ring.stage], brow + 64,
+                                 kb * KELEMS, pol_b);
           } else {
-            tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow);
+            tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow, pol_b);
           }
           ring.advance();
         }
@@ -289,6 +293,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t sbase = smem_u32(sb) + lane * 128u;
     uint32_t local = 0, cmc_cnt[2] = {0u, 0u};
     bool stored = false;
+    const uint64_t pol_y = policy_evict_first();          // Y is written once, never re-read here
     for (int u = cid; u < p.n_units; u += ncl) {
       Unit w;
       if (!decode_unit(p, u, w)) continue;
@@ -345,7 +350,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tmY, sb, col_base + (c0 + c) * 32, row0);
+          tma_store_2d_hint(&tmY, sb, col_base + (c0 + c) * 32, row0, pol_y);
           bulk_commit();
         }
         stored = true;
