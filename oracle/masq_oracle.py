@@ -247,3 +247,53 @@ def loss_finalize(sums, counts, lam, n: int) -> float:
         if counts[m] > 0:
             loss += float(lam[m]) * float(sums[m]) / (float(counts[m]) * n)
     return loss
+
+
+# --------------------------------------------------------------------------- N1 (next row)
+def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None):
+    """N1 — gradient of L = sum_m lambda_m MAE_m (O8) w.r.t. theta^m = ln s^m (SPEC.md:307-316:
+    log-space parameters, rounding treated as identity — the straight-through contract; reading
+    Q24: the dynamic scales Delta are held constant, i.e. stop-gradient on the scales).
+
+    With A = X_m S_m^-1 (xs), B = S_m W (ws), Ahat = Q(A), Bhat = Q(B), E = Ahat Bhat - X_m W and
+    G = lambda_m / (N_m n) sign(E):  dL/dA = G Bhat^T, dL/dB = Ahat^T G, dA/dtheta_i = -A[:, i],
+    dB/dtheta_i = B[i, :], hence
+        grad_i = sum_j (Ahat^T G)_ij B_ij - sum_j (X_m^T G)_ij inv_i Bhat_ij     (xs = X inv)
+    Returns (loss f64, grad f64 [M x d]).
+    """
+    s = np.asarray(s, F32)
+    n_mod = s.shape[0]
+    Xf = decode(X)
+    Wf = decode(W)
+    ids = _check_ids(ids, n_mod)
+    lam = np.ones(n_mod) if lam is None else np.asarray(lam, F64)
+    n = Wf.shape[1]
+    xs_all = smooth_activations(Xf, ids, s)
+    grad = np.zeros((n_mod, Wf.shape[0]), F64)
+    loss = 0.0
+    for m in range(n_mod):
+        sel = np.nonzero(ids == m)[0]
+        if not sel.size:
+            continue
+        xs = xs_all[sel]
+        qx, dx = quantize_rows(xs, abits)
+        Ahat = dequantize_rows(qx, dx)                                   # [T_m x d]
+        qw, dw = quantize_weight(W, s[m], wbits)
+        Bhat = dequantize_rows(qw, dw).T                                 # [d x n]
+        Bs = np.multiply(s[m][:, None], Wf, dtype=F32).astype(F64)       # S_m W as quantized (f32)
+        E = Ahat @ Bhat - np.asarray(Xf[sel], F64) @ np.asarray(Wf, F64)
+        scale = float(lam[m]) / (sel.size * n)
+        loss += scale * np.abs(E).sum()
+        G = scale * np.sign(E)
+        grad[m] = ((Ahat.T @ G) * Bs).sum(axis=1) - ((np.asarray(xs, F64).T @ G) * Bhat).sum(axis=1)
+    return loss, grad
+
+
+def adam_step(theta, grad, m1, m2, step: int, lr: float, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8):
+    """Adam in log space (SPEC.md:334 adaptive-moment choice), f64: returns (theta, m1, m2);
+    s = exp(theta).  step counts from 1."""
+    m1 = b1 * np.asarray(m1, F64) + (1 - b1) * grad
+    m2 = b2 * np.asarray(m2, F64) + (1 - b2) * grad * grad
+    mh = m1 / (1 - b1 ** step)
+    vh = m2 / (1 - b2 ** step)
+    return np.asarray(theta, F64) - lr * mh / (np.sqrt(vh) + eps), m1, m2

@@ -352,3 +352,65 @@ def test_hand_worked_example():
     assert np.allclose(sums, e["loss_sums"], rtol=0, atol=2e-5)
     assert counts.tolist() == e["loss_counts"]
     assert np.isclose(loss, e["loss"], rtol=0, atol=2e-5)
+
+
+# ----------------------------------------------------------------------------- N1 gradient
+def _autograd_ste_loss_grad(X, ids, s, W, wbits, abits):
+    """Independent implementation of the straight-through graph with torch.autograd (f64):
+    Q(u) = u + (Delta * round_half_away(u / Delta) - u).detach(), Delta detached."""
+    import torch
+    Xt = torch.from_numpy(O.decode(X).astype(np.float64))
+    Wt = torch.from_numpy(O.decode(W).astype(np.float64))
+    theta = torch.tensor(np.log(s.astype(np.float64)), requires_grad=True)
+
+    def q_rows(u, bits):
+        qmax = 2 ** (bits - 1) - 1
+        delta = (u.detach().abs().amax(dim=1, keepdim=True) / qmax).clamp_min(1e-12)
+        v = u.detach() / delta
+        r = torch.trunc(v) + torch.sign(v) * (torch.abs(v - torch.trunc(v)) >= 0.5)
+        return u + (delta * r.clamp(-qmax - 1, qmax) - u).detach()
+
+    loss = 0.0
+    n = Wt.shape[1]
+    for m in range(s.shape[0]):
+        sel = torch.from_numpy(np.nonzero(ids == m)[0])
+        A = Xt[sel] * torch.exp(-theta[m])[None, :]
+        B = torch.exp(theta[m])[:, None] * Wt
+        Ah = q_rows(A, abits)
+        Bh = q_rows(B.T, wbits).T                                   # per output channel
+        E = Ah @ Bh - Xt[sel] @ Wt
+        loss = loss + E.abs().sum() / (sel.numel() * n)
+    loss.backward()
+    return float(loss), theta.grad.numpy()
+
+
+def test_loss_grad_matches_autograd_ste():
+    """N1 pin: the closed-form straight-through gradient equals torch.autograd on the STE graph
+    (up to the f32 smoothing / quantization of the oracle; codes are identical on these inputs)."""
+    c = synth.config_inputs("c2", T=1024, d=32, n=48)
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 3)
+    s = O.init_factors(R, cnt, c["W"])
+    loss, grad = O.calib_loss_grad(c["X"], c["ids"], s, c["W"], 4, 8)
+    _, _, loss_o8 = O.calib_loss(c["X"], c["ids"], s, c["W"], 4, 8)
+    assert np.isclose(loss, loss_o8, rtol=1e-12)
+    la, ga = _autograd_ste_loss_grad(c["X"], c["ids"], s, c["W"], 4, 8)
+    assert np.isclose(la, loss, rtol=1e-5)
+    assert np.abs(grad - ga).max() <= 1e-4 * np.abs(ga).max()
+
+
+def test_loss_grad_descent_direction_and_adam():
+    """A small step against the gradient does not increase the (piecewise) loss; Adam's first
+    step moves every coordinate by ~lr against the gradient sign (closed form at step 1)."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    loss0, grad = O.calib_loss_grad(c["X"], c["ids"], s, c["W"], 4, 8)
+    theta = np.log(s.astype(np.float64))
+    th1, m1, m2 = O.adam_step(theta, grad, np.zeros_like(theta), np.zeros_like(theta), 1, 1e-3)
+    nz = grad != 0
+    step = (th1 - theta)[nz]
+    assert np.all(np.sign(step) == -np.sign(grad[nz])) and np.all(np.abs(step) <= 1e-3 * (1 + 1e-12))
+    assert np.all(np.abs(step) >= 1e-3 * (1 - 1e-8 / np.abs(grad[nz])) * (1 - 1e-9))
+    assert np.all(th1[~nz] == theta[~nz])
+    _, _, loss1 = O.calib_loss(c["X"], c["ids"], np.exp(th1).astype(np.float32), c["W"], 4, 8)
+    assert loss1 <= loss0 * (1 + 1e-3)
