@@ -70,7 +70,7 @@ typedef void* masq_stream;      /* cudaStream_t */
 /* Workspace queries: op is one of the MASQ_OP_* values. */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
-  MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6
+  MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -184,6 +184,31 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
                             const float* Yref, int64_t ld_ref,
                             double* sums, int64_t* counts, double* loss,
                             void* ws, size_t ws_bytes, masq_stream stream);
+
+/*
+ * N1 (the next row after A8) — the S-optimisation step's gradient: everything
+ * masq_calib_loss computes, plus grad[m*d + i] = dL/dtheta^m_i with theta^m = ln s^m (SPEC.md:
+ * 307-316: log-space parameters, rounding treated as identity = straight-through; reading Q24:
+ * the dynamic scales are held constant):
+ *   grad_i = lambda_m/(N_m n) * sum_j [ (Ahat^T G)_ij (S_m W)_ij - (X_m^T G)_ij inv_i Bhat_ij ]
+ * with G = sign(Ahat Bhat - X_m W), Ahat = Q(X_m S_m^-1), Bhat = Q(S_m W).  grad: device f64
+ * [n_mod x d].  X and W must be bf16.  For token-sharded multi-GPU use, SUM-reduce grad scaled
+ * by counts (or reduce the unscaled sums) like the loss.
+ */
+masq_status masq_calib_loss_grad(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                                 int64_t T, int64_t d, int64_t d_out, int32_t n_mod,
+                                 const float* s, const void* W, masq_dtype wt,
+                                 int32_t wbits, int32_t abits, const float* lambda,
+                                 const float* Yref, int64_t ld_ref,
+                                 double* sums, int64_t* counts, double* loss, double* grad,
+                                 void* ws, size_t ws_bytes, masq_stream stream);
+
+/* Adam in log space: m1 = b1 m1 + (1-b1) g; m2 = b2 m2 + (1-b2) g^2;
+ * theta -= lr * (m1/(1-b1^step)) / (sqrt(m2/(1-b2^step)) + eps); s_out (optional, f32) = exp(theta).
+ * All arrays device, [count]; step >= 1. */
+masq_status masq_adam_step(double* theta, const double* grad, double* m1, double* m2, int64_t count,
+                           int32_t step, double lr, double beta1, double beta2, double eps,
+                           float* s_out, masq_stream stream);
 
 /* loss[0] = sum_m lambda[m] * sums[m] / (counts[m] * d_out) on the device (after an all-reduce). */
 masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const float* lambda,

@@ -39,6 +39,12 @@ SIGNATURES = {
                                   c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_size_t, c_void_p]),
     "masq_loss_finalize": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]),
+    "masq_calib_loss_grad": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32,
+                                       c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p,
+                                       c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_size_t, c_void_p]),
+    "masq_adam_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_double, ctypes.c_double, c_void_p, c_void_p]),
     "masq_check": (c_int32, [c_void_p, c_void_p]),
     "masq_profile_enable": (c_int32, [c_int32]),
     "masq_profile_collect": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p]),

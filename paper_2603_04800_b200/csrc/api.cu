@@ -56,6 +56,23 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     }
     case MASQ_OP_REFERENCE:
       break;
+    case MASQ_OP_LOSS_GRAD: {
+      const int64_t Tg = grouped_rows(T, n_mod);
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      L.qx = take((size_t)Tg * d);
+      L.dx = take(sizeof(float) * Tg);
+      L.perm = take(sizeof(int32_t) * Tg);
+      L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
+      L.cnt = take(sizeof(int64_t) * n_mod);
+      L.qw_all = take((size_t)n_mod * n * d);
+      L.dw_all = take(sizeof(float) * n_mod * n);
+      L.amax = take(sizeof(uint32_t) * n_mod * n);
+      L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
+      L.gsign = take(sizeof(uint16_t) * (size_t)Tg * n);
+      L.planes = take(sizeof(uint16_t) * 2 * (size_t)Tg * d);
+      L.gpartial = take(sizeof(double) * n_mod * ceil_div(n, kTileN) * d);
+      break;
+    }
     default:
       break;
   }
@@ -275,25 +292,29 @@ masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, in
   return MASQ_OK;
 }
 
-masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
-                            int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
-                            int32_t wbits, int32_t abits, const float* lambda, const float* Yref, int64_t ld_ref,
-                            double* sums, int64_t* counts, double* loss, void* ws, size_t ws_bytes,
-                            masq_stream stream) {
+}  // extern "C"
+
+namespace {
+masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                      int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt, int32_t wbits,
+                      int32_t abits, const float* lambda, const float* Yref, int64_t ld_ref, double* sums,
+                      int64_t* counts, double* loss, double* grad, void* ws, size_t ws_bytes, masq_stream stream) {
   MASQ_TRY(check_common(T, d, n_mod));
   MASQ_TRY(check_bits(wbits));
   MASQ_TRY(check_bits(abits));
   if (d_out <= 0 || d_out % 32 != 0) return MASQ_ERR_SHAPE;
   if (!s || !W || !sums || !counts || !loss) return MASQ_ERR_NULL;
   if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (grad && (xt != MASQ_BF16 || wt != MASQ_BF16)) return MASQ_ERR_UNSUPPORTED;
   if (!al16(W) || !al16(s)) return MASQ_ERR_ALIGN;
-  const WsLayout L = ws_layout(MASQ_OP_LOSS, T, d, d_out, n_mod, 0);
+  const WsLayout L = ws_layout(grad ? MASQ_OP_LOSS_GRAD : MASQ_OP_LOSS, T, d, d_out, n_mod, 0);
   MASQ_TRY(check_ws(ws, ws_bytes, L));
   cudaStream_t st = S(stream);
   if (T == 0) {
     MASQ_CK(cudaMemsetAsync(sums, 0, sizeof(double) * n_mod, st));
     MASQ_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * n_mod, st));
     MASQ_CK(cudaMemsetAsync(loss, 0, sizeof(double), st));
+    if (grad) MASQ_CK(cudaMemsetAsync(grad, 0, sizeof(double) * n_mod * d, st));
     return MASQ_OK;
   }
   MASQ_TRY(check_x(X, xt, ld_x, d));
@@ -304,16 +325,17 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
   int32_t* perm = reinterpret_cast<int32_t*>(W8(ws, L.perm));
   uint32_t* tmod = reinterpret_cast<uint32_t*>(W8(ws, L.tile_mod));
+  int64_t* cnt = reinterpret_cast<int64_t*>(W8(ws, L.cnt));
   int8_t* qw = reinterpret_cast<int8_t*>(W8(ws, L.qw_all));
   float* dw = reinterpret_cast<float*>(W8(ws, L.dw_all));
   uint32_t* amax = reinterpret_cast<uint32_t*>(W8(ws, L.amax));
   double* partials = reinterpret_cast<double*>(W8(ws, L.partials));
+  uint16_t* gsign = grad ? reinterpret_cast<uint16_t*>(W8(ws, L.gsign)) : nullptr;
   const int64_t Tg = grouped_rows(T, n_mod);
   const int num_n = (int)ceil_div(d_out, kTileN);
   const int64_t tiles = (Tg / kUnitM) * num_n;
   const int epi = gemm_epilogue_warps();
   MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
-  int64_t* cnt = reinterpret_cast<int64_t*>(W8(ws, L.cnt));
   MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, cnt, st));
   MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, nullptr, status_of(ws), st, perm, Tg));
   MASQ_CK(launch_wquant(W, wt, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
@@ -334,8 +356,48 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
   g.yref = Yref;
   g.ld_ref = ld_ref;
   g.partials = partials;
+  g.gsign = gsign;
   MASQ_CK(launch_gemm(g, st));
   MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st));
+  if (grad) {
+    uint16_t* planes = reinterpret_cast<uint16_t*>(W8(ws, L.planes));
+    double* gpart = reinterpret_cast<double*>(W8(ws, L.gpartial));
+    MASQ_CK(launch_gradprep(static_cast<const uint16_t*>(X), ld_x, mod_id, perm, qx, dx, inv, Tg, d, planes, st));
+    MASQ_CK(launch_gradgemm(planes, Tg, gsign, qw, tmod, n_mod, d, d_out, s, inv, static_cast<const uint16_t*>(W), dw,
+                            gpart, st));
+    MASQ_CK(launch_gradreduce(gpart, cnt, lambda, n_mod, gradgemm_ntiles_j(d_out), d, d_out, grad, st));
+  }
+  return MASQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                            int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
+                            int32_t wbits, int32_t abits, const float* lambda, const float* Yref, int64_t ld_ref,
+                            double* sums, int64_t* counts, double* loss, void* ws, size_t ws_bytes,
+                            masq_stream stream) {
+  return loss_core(X, xt, ld_x, mod_id, T, d, d_out, n_mod, s, W, wt, wbits, abits, lambda, Yref, ld_ref, sums,
+                   counts, loss, nullptr, ws, ws_bytes, stream);
+}
+
+masq_status masq_calib_loss_grad(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                                 int64_t d, int64_t d_out, int32_t n_mod, const float* s, const void* W,
+                                 masq_dtype wt, int32_t wbits, int32_t abits, const float* lambda, const float* Yref,
+                                 int64_t ld_ref, double* sums, int64_t* counts, double* loss, double* grad,
+                                 void* ws, size_t ws_bytes, masq_stream stream) {
+  if (!grad) return MASQ_ERR_NULL;
+  return loss_core(X, xt, ld_x, mod_id, T, d, d_out, n_mod, s, W, wt, wbits, abits, lambda, Yref, ld_ref, sums,
+                   counts, loss, grad, ws, ws_bytes, stream);
+}
+
+masq_status masq_adam_step(double* theta, const double* grad, double* m1, double* m2, int64_t count, int32_t step,
+                           double lr, double beta1, double beta2, double eps, float* s_out, masq_stream stream) {
+  if (!theta || !grad || !m1 || !m2) return MASQ_ERR_NULL;
+  if (count < 0 || step < 1) return MASQ_ERR_SHAPE;
+  if (count == 0) return MASQ_OK;
+  MASQ_CK(launch_adam(theta, grad, m1, m2, count, step, lr, beta1, beta2, eps, s_out, S(stream)));
   return MASQ_OK;
 }
 

@@ -78,6 +78,7 @@ struct Params {
   const float* yref;
   long long ld_ref;
   double* partials;            // loss: [n_units][2] (one per CTA of the pair)
+  uint16_t* gsign;             // loss (optional, N1): bf16 sign(yq - yref) [T x n], 0 on padding rows
 };
 
 struct Unit {
@@ -398,6 +399,23 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
           tmem_wait_ld();
           dequant(v, c);
+          if (p.gsign) {                                    // N1: G = sign(yq - yref), bf16, grouped rows
+            uint32_t g[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              uint32_t lo = 0, hi = 0;
+              if (src >= 0) {
+                const float a0 = __uint_as_float(v[2 * k]) - (&ycur[k >> 1].x)[(2 * k) & 3];
+                const float a1 = __uint_as_float(v[2 * k + 1]) - (&ycur[k >> 1].x)[(2 * k + 1) & 3];
+                lo = a0 > 0.f ? 0x3F80u : (a0 < 0.f ? 0xBF80u : 0u);
+                hi = a1 > 0.f ? 0x3F80u : (a1 < 0.f ? 0xBF80u : 0u);
+              }
+              g[k] = lo | (hi << 16);
+            }
+            uint4* gp = reinterpret_cast<uint4*>(p.gsign + (size_t)row * p.n + col_base + (c0 + c) * 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gp[k] = make_uint4(g[4 * k], g[4 * k + 1], g[4 * k + 2], g[4 * k + 3]);
+          }
           if (src >= 0) {
             float acc = 0.f;
 #pragma unroll
@@ -538,6 +556,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.yref = g.yref;
   p.ld_ref = g.ld_ref;
   p.partials = g.partials;
+  p.gsign = g.gsign;
   const int clusters = (int)std::min<int64_t>(p.n_units, num_sms() / 2);
   switch (g.mode) {
     case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, clusters, st);

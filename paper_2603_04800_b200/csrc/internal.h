@@ -27,6 +27,7 @@ inline int64_t rpad_of(int64_t r) { return r > 0 ? ceil_div(r, 64) * 64 : 0; }
 struct WsLayout {
   size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0, xsplit = 0;
   size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, cnt = 0, total = 0;
+  size_t gsign = 0, planes = 0, gpartial = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -111,9 +112,24 @@ struct GemmArgs {
   const float* yref;
   int64_t ld_ref;
   double* partials;                // [n_mod][tiles][4]
+  uint16_t* gsign;                 // loss, optional (N1): bf16 sign(yq - yref), grouped rows [T x n]
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
 int gemm_epilogue_warps();
+
+// ---------------------------------------------------------------- N1 gradient (grad.cu)
+// planes [2][Tg][d] bf16: D = Ahat - X S^-1 and X, in grouped row order
+cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
+                            const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d,
+                            uint16_t* planes, cudaStream_t st);
+cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* gsign, const int8_t* qw_all,
+                            const uint32_t* tile_mod, int n_mod, int64_t d, int64_t n, const float* s,
+                            const float* inv, const uint16_t* W, const float* dw, double* partial, cudaStream_t st);
+int gradgemm_ntiles_j(int64_t n);
+cudaError_t launch_gradreduce(const double* partial, const int64_t* counts, const float* lambda_host, int n_mod,
+                              int nj, int64_t d, int64_t n, double* grad, cudaStream_t st);
+cudaError_t launch_adam(double* theta, const double* grad, double* m1, double* m2, int64_t count, int step, double lr,
+                        double b1, double b2, double eps, float* s_out, cudaStream_t st);
 int num_sms();
 
 // ---------------------------------------------------------------- CMC first factor (zgemm.cu)

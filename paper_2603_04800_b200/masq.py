@@ -12,7 +12,7 @@ import torch
 from ._lib import MasqDebug, lib
 
 MASQ_F32, MASQ_BF16 = 0, 1
-OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE = range(7)
+OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD = range(8)
 
 
 class MasqError(RuntimeError):
@@ -215,6 +215,35 @@ def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, sums=Non
                               _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), p, n, _stream(stream)),
         "masq_calib_loss")
     return sums, counts, loss
+
+
+def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, grad=None, ws=None, stream=None):
+    """N1: (sums, counts, loss, grad) with grad = dL/d ln s (straight-through), f64 [M x d]."""
+    T, d = X.shape
+    d_out = W.shape[1]
+    n_mod = s.shape[0]
+    dev = X.device
+    sums = torch.empty(n_mod, dtype=torch.float64, device=dev)
+    counts = torch.empty(n_mod, dtype=torch.int64, device=dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    grad = torch.empty(n_mod, d, dtype=torch.float64, device=dev) if grad is None else grad
+    ws = ws or default_workspace(dev)
+    p, n = ws.ptr_size(workspace_size(OP_LOSS_GRAD, T, d, d_out, n_mod))
+    lam_arr = _lambda_arr(lam, n_mod)
+    _ck(lib().masq_calib_loss_grad(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod, _p(s.contiguous()),
+                                   _p(W.contiguous()), _dt(W), wbits, abits,
+                                   ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr is not None else None,
+                                   _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), _p(grad), p, n,
+                                   _stream(stream)), "masq_calib_loss_grad")
+    return sums, counts, loss, grad
+
+
+def adam_step(theta, grad, m1, m2, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999,
+              eps: float = 1e-8, s_out=None, stream=None):
+    """Log-space Adam on device (f64 state); writes s_out = exp(theta) (f32) when given."""
+    _ck(lib().masq_adam_step(_p(theta), _p(grad), _p(m1), _p(m2), theta.numel(), step, lr, beta1, beta2, eps,
+                             _p(s_out), _stream(stream)), "masq_adam_step")
+    return theta
 
 
 def loss_finalize(sums, counts, d_out: int, lam=None, loss=None, stream=None):

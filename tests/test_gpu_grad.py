@@ -1,0 +1,109 @@
+"""GPU parity for N1: the S-optimisation step — the straight-through gradient
+of the calibration loss w.r.t. ln s (masq_calib_loss_grad) and the log-space Adam update
+(masq_adam_step) — against oracle.calib_loss_grad / oracle.adam_step on the same inputs.
+
+Bar: the loss within 1e-3 relative (as A8); the gradient within 2e-3 max-abs-normalised per
+modality (sign(E) may differ where E rounds to ~0 in f32 vs f64 and the P/Q
+contractions accumulate in fp32 over the tokens); Adam to f64 rounding.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from test_gpu_parity import M, bf, case, oracle_state, tt
+
+pytestmark = pytest.mark.gpu
+
+TOL_G = 2e-3
+
+
+def _grad_err(g, go):
+    errs = []
+    for m in range(go.shape[0]):
+        scale = max(np.abs(go[m]).max(), 1e-300)
+        errs.append(float(np.abs(g[m] - go[m]).max() / scale))
+    return max(errs)
+
+
+@pytest.mark.parametrize("name", ["c1", "ragged3", "c3_qkv"])
+def test_loss_grad_parity(name):
+    c = case(name)
+    m = M()
+    _, _, so, _, _ = oracle_state(c)
+    X, W = bf(c["X"]), bf(c["W"])
+    Yref = m.reference_output(X, W)
+    sums, counts, loss, grad = m.calib_loss_grad(X, tt(c["ids"]), tt(so), W, c["wbits"], c["abits"], Yref)
+    m.check()
+    lo, go = O.calib_loss_grad(c["X"], c["ids"], so, c["W"], c["wbits"], c["abits"])
+    assert abs(float(loss.cpu()[0]) - lo) <= 1e-3 * abs(lo)
+    g = grad.cpu().numpy()
+    assert np.isfinite(g).all()
+    assert _grad_err(g, go) <= TOL_G, _grad_err(g, go)
+    # the loss half of the call equals masq_calib_loss bit for bit
+    s2, c2, l2 = m.calib_loss(X, tt(c["ids"]), tt(so), W, c["wbits"], c["abits"], Yref)
+    assert torch.equal(s2, sums) and torch.equal(l2, loss) and torch.equal(c2, counts)
+    # deterministic (fixed-order reductions)
+    _, _, _, gr2 = m.calib_loss_grad(X, tt(c["ids"]), tt(so), W, c["wbits"], c["abits"], Yref)
+    assert torch.equal(gr2, grad)
+
+
+def test_loss_grad_lambda_and_w8():
+    c = case("ragged3")
+    m = M()
+    _, _, so, _, _ = oracle_state(c)
+    X, W = bf(c["X"]), bf(c["W"])
+    Yref = m.reference_output(X, W)
+    lam = [1.0, 0.5, 2.0]
+    _, _, loss, grad = m.calib_loss_grad(X, tt(c["ids"]), tt(so), W, 8, 8, Yref, lam=lam)
+    lo, go = O.calib_loss_grad(c["X"], c["ids"], so, c["W"], 8, 8, lam=lam)
+    assert abs(float(loss.cpu()[0]) - lo) <= 1e-3 * abs(lo)
+    assert _grad_err(grad.cpu().numpy(), go) <= TOL_G
+
+
+def test_loss_grad_perturbed_s():
+    """Away from the closed form (s scaled per channel), where sign(E) patterns differ."""
+    c = case("c1")
+    m = M()
+    _, _, so, _, _ = oracle_state(c)
+    g = np.random.Generator(np.random.PCG64(7))
+    sp = (so * np.exp(g.normal(0, 0.3, so.shape))).astype(np.float32)
+    X, W = bf(c["X"]), bf(c["W"])
+    Yref = m.reference_output(X, W)
+    _, _, loss, grad = m.calib_loss_grad(X, tt(c["ids"]), tt(sp), W, c["wbits"], c["abits"], Yref)
+    lo, go = O.calib_loss_grad(c["X"], c["ids"], sp, c["W"], c["wbits"], c["abits"])
+    assert abs(float(loss.cpu()[0]) - lo) <= 1e-3 * abs(lo)
+    assert _grad_err(grad.cpu().numpy(), go) <= TOL_G
+
+
+def test_adam_step_parity_trajectory():
+    c = case("c1")
+    m = M()
+    _, _, so, _, _ = oracle_state(c)
+    X, W = bf(c["X"]), bf(c["W"])
+    ids = tt(c["ids"])
+    Yref = m.reference_output(X, W)
+    theta = torch.log(tt(so).double())
+    m1 = torch.zeros_like(theta)
+    m2 = torch.zeros_like(theta)
+    s_cur = tt(so).clone()
+    th_o, m1_o, m2_o = np.log(so.astype(np.float64)), np.zeros(so.shape), np.zeros(so.shape)
+    losses = []
+    for step in range(1, 6):
+        _, _, loss, grad = m.calib_loss_grad(X, ids, s_cur, W, c["wbits"], c["abits"], Yref)
+        losses.append(float(loss.cpu()[0]))
+        # the trajectory stays on the oracle's: loss at the current s (set by the previous step)
+        lo = O.calib_loss(c["X"], c["ids"], np.exp(th_o).astype(np.float32), c["W"], c["wbits"], c["abits"])[2]
+        assert abs(losses[-1] - lo) <= 1e-3 * abs(lo)
+        gh = grad.cpu().numpy()
+        th_o, m1_o, m2_o = O.adam_step(th_o, gh, m1_o, m2_o, step, 1e-2)
+        m.adam_step(theta, grad, m1, m2, step, 1e-2, s_out=s_cur)
+        torch.cuda.synchronize()
+        # f64 to rounding (the device contracts b*m + (1-b)*g into FMAs; m1 may cancel to ~0)
+        assert np.allclose(theta.cpu().numpy(), th_o, rtol=1e-13, atol=1e-13)
+        assert np.allclose(m1.cpu().numpy(), m1_o, rtol=1e-12, atol=1e-12 * np.abs(m1_o).max())
+        assert np.allclose(m2.cpu().numpy(), m2_o, rtol=1e-12, atol=1e-12 * np.abs(m2_o).max())
+        assert np.allclose(s_cur.cpu().numpy(), np.exp(th_o).astype(np.float32), rtol=2e-7)
+    # No descent assertion: a uniform rescale of s^m is an exact invariance of the per-token /
+    # per-channel absmax quantizers, but not of the straight-through surrogate, and Adam's
+    # sign-like first steps move mostly along it — the loss stays ~flat.
