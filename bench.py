@@ -11,6 +11,10 @@ quoted on): for each of the layer's four (fused) linears
        -> [NCCL SUM all-reduce of the loss sums / counts, batched, N>1] -> masq_loss_finalize
 Weak scaling: every rank calibrates its own 16384-token batch (token-sharded data parallel).
 
+A separate "n1" block times SURVEY §8(f)'s first next row on the same inputs, outside the
+step: one S-optimisation iteration per linear = masq_calib_loss_grad (loss + straight-through
+gradient, global-count normalised) -> [NCCL SUM of the gradient, N>1] -> masq_adam_step.
+
 value = tokens of all ranks / device time of K steps (CUDA events, max over ranks).
 --impl reference times the CPU oracle (oracle/) on a bounded sample instead.
 """
@@ -49,6 +53,7 @@ def parse():
     ap.add_argument("--linears", default="qkv,o,gate_up,down")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-n1", action="store_true", help="skip the N1 S-optimisation step timing")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines)")
     ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
                     help="c3: one Qwen2.5-VL-7B layer, every §8(a) row (default); c4: 28-layer calibration sweep")
@@ -430,6 +435,7 @@ def main():
         for li, e in enumerate(L):
             X = e["X"] if X_override is None else X_override[li]
             s = M.init_factors(Rv[li], Cbuf[li], e["W"], ws=ws)
+            e["s"] = s
             qw, dw = M.quantize_weight(e["W"], s[0], WBITS, ws=ws)
             M.linear_forward(X, idt, s, qw, dw, WBITS, ABITS, e["L1"], e["L2"], Y=e["Y"], ws=ws)
             M.reference_output(X, e["W"], Yref=e["Yref"], ws=ws)
@@ -539,6 +545,67 @@ def main():
                "note": "pinned H2D of the step's activations+ids on a copy stream (double-buffered, overlapping "
                        "the previous step's compute) + D2H of the losses, every step"}
 
+    # ------------------------------------------------------------------ N1 (S-optimisation step)
+    loss_main = [float(x) for x in losses.cpu().tolist()]
+    n1 = None
+    if not args.no_n1:
+        for e in L:
+            e["theta"] = torch.log(e["s"].double())
+            e["m1"] = torch.zeros_like(e["theta"])
+            e["m2"] = torch.zeros_like(e["theta"])
+            e["grad"] = torch.empty_like(e["theta"])
+        Gbuf = [e["grad"] for e in L]
+        n1_state = {"t": 0}
+
+        def n1_step():
+            n1_state["t"] += 1
+            for li, e in enumerate(L):
+                M.calib_loss_grad(e["X"], ids, e["s"], e["W"], WBITS, ABITS, e["Yref"], grad=e["grad"],
+                                  sums=Sbuf[li], counts=Nbuf[li], loss=losses[li:li + 1],
+                                  count_norm=Cbuf[li], ws=ws)
+            if world > 1:
+                for g in Gbuf:
+                    P.reduce_grad(g)
+            for e in L:
+                M.adam_step(e["theta"], e["grad"], e["m1"], e["m2"], n1_state["t"], 1e-3, s_out=e["s"])
+
+        for _ in range(max(args.warmup, 0)):
+            n1_step()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        lib().masq_profile_enable(1)
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record()
+        for _ in range(args.steps):
+            n1_step()
+        b_ev.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_n1 = max_over_ranks(a_ev.elapsed_time(b_ev))
+        nk1 = lib().masq_profile_collect(cap, names, tot, cnt)
+        lib().masq_profile_enable(0)
+        M.check(ws)
+        k1 = {}
+        for i in range(max(nk1, 0)):
+            nm = names.raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode()
+            k1[nm] = tot[i]
+        gg_ms = k1.get("gradgemm", 0.0) / args.steps
+        gflop = sum(4.0 * T * e["d"] * e["n"] for e in L)
+        peaks1 = load_peaks()
+        n1 = {"ms_per_step": ms_n1 / args.steps,
+              "tokens_per_s": world * T * args.steps / (ms_n1 / 1e3),
+              "kernels_ms_per_step": {k: v / args.steps for k, v in k1.items()},
+              "gradgemm": {"bound": "tensor", "flops_per_step": gflop,
+                           "achieved": gflop / (gg_ms / 1e3) / 1e12 if gg_ms else None, "unit": "TFLOP/s",
+                           "peak": peaks1["bf16"],
+                           "frac": (gflop / (gg_ms / 1e3) / 1e12 / peaks1["bf16"]) if gg_ms else None,
+                           "peak_source": "MEASURED_PEAKS.json bf16 burst"},
+              "gpu_launches_per_step": sum(int(cnt[i]) for i in range(max(nk1, 0))) / args.steps,
+              "losses_after": [float(x) for x in losses.cpu().tolist()],
+              "note": "per linear: masq_calib_loss_grad (global-count normalised) -> NCCL SUM of grad (N>1) -> "
+                      "masq_adam_step (lr 1e-3); outside the timed §8(a) step"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -621,6 +688,7 @@ def main():
         "data": "synthetic (seeded, synth/; random-init weights of the Qwen2.5-VL-7B layer shapes)",
         "config": workload_config(args, linears),
         "linear_forward": linear,
+        "n1_s_opt_step": n1,
         "roofline": roof,
         "kernels": kinfo,
         "kernel_ms_sum_over_step_ms": total_kernel_ms / ms_total if ms_total else None,
@@ -629,7 +697,7 @@ def main():
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "losses": [float(x) for x in losses.cpu().tolist()],
+        "losses": loss_main,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -192,8 +192,10 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
  * the dynamic scales are held constant):
  *   grad_i = lambda_m/(N_m n) * sum_j [ (Ahat^T G)_ij (S_m W)_ij - (X_m^T G)_ij inv_i Bhat_ij ]
  * with G = sign(Ahat Bhat - X_m W), Ahat = Q(X_m S_m^-1), Bhat = Q(S_m W).  grad: device f64
- * [n_mod x d].  X and W must be bf16.  For token-sharded multi-GPU use, SUM-reduce grad scaled
- * by counts (or reduce the unscaled sums) like the loss.
+ * [n_mod x d].  X and W must be bf16.  count_norm (device i64 [n_mod], optional): the token
+ * counts N_m used in scale_m = lambda_m/(N_m n); NULL = this call's own counts.  Token-sharded
+ * multi-GPU use passes the GLOBAL counts (known after the A1 exchange) so that a plain SUM
+ * all-reduce of grad over ranks is the gradient of the whole batch.
  */
 masq_status masq_calib_loss_grad(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
                                  int64_t T, int64_t d, int64_t d_out, int32_t n_mod,
@@ -201,7 +203,7 @@ masq_status masq_calib_loss_grad(const void* X, masq_dtype xt, int64_t ld_x, con
                                  int32_t wbits, int32_t abits, const float* lambda,
                                  const float* Yref, int64_t ld_ref,
                                  double* sums, int64_t* counts, double* loss, double* grad,
-                                 void* ws, size_t ws_bytes, masq_stream stream);
+                                 const int64_t* count_norm, void* ws, size_t ws_bytes, masq_stream stream);
 
 /* Adam in log space: m1 = b1 m1 + (1-b1) g; m2 = b2 m2 + (1-b2) g^2;
  * theta -= lr * (m1/(1-b1^step)) / (sqrt(m2/(1-b2^step)) + eps); s_out (optional, f32) = exp(theta).

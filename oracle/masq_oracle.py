@@ -250,7 +250,7 @@ def loss_finalize(sums, counts, lam, n: int) -> float:
 
 
 # --------------------------------------------------------------------------- N1 (next row)
-def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None):
+def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None, count_norm=None):
     """N1 — gradient of L = sum_m lambda_m MAE_m (O8) w.r.t. theta^m = ln s^m (SPEC.md:307-316:
     log-space parameters, rounding treated as identity — the straight-through contract; reading
     Q24: the dynamic scales Delta are held constant, i.e. stop-gradient on the scales).
@@ -259,6 +259,9 @@ def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None):
     G = lambda_m / (N_m n) sign(E):  dL/dA = G Bhat^T, dL/dB = Ahat^T G, dA/dtheta_i = -A[:, i],
     dB/dtheta_i = B[i, :], hence
         grad_i = sum_j (Ahat^T G)_ij B_ij - sum_j (X_m^T G)_ij inv_i Bhat_ij     (xs = X inv)
+    count_norm: the N_m of the gradient's scale (default: this call's token counts) — a token
+    shard passes the whole batch's counts, and the shards' gradients then add up to the batch
+    gradient.  The returned loss always uses this call's own counts.
     Returns (loss f64, grad f64 [M x d]).
     """
     s = np.asarray(s, F32)
@@ -282,9 +285,8 @@ def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None):
         Bhat = dequantize_rows(qw, dw).T                                 # [d x n]
         Bs = np.multiply(s[m][:, None], Wf, dtype=F32).astype(F64)       # S_m W as quantized (f32)
         E = Ahat @ Bhat - np.asarray(Xf[sel], F64) @ np.asarray(Wf, F64)
-        scale = float(lam[m]) / (sel.size * n)
-        loss += scale * np.abs(E).sum()
-        G = scale * np.sign(E)
+        loss += float(lam[m]) / (sel.size * n) * np.abs(E).sum()
+        G = float(lam[m]) / ((sel.size if count_norm is None else int(count_norm[m])) * n) * np.sign(E)
         grad[m] = ((Ahat.T @ G) * Bs).sum(axis=1) - ((np.asarray(xs, F64).T @ G) * Bhat).sum(axis=1)
     return loss, grad
 

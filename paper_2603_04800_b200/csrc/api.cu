@@ -298,7 +298,8 @@ namespace {
 masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
                       int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt, int32_t wbits,
                       int32_t abits, const float* lambda, const float* Yref, int64_t ld_ref, double* sums,
-                      int64_t* counts, double* loss, double* grad, void* ws, size_t ws_bytes, masq_stream stream) {
+                      int64_t* counts, double* loss, double* grad, const int64_t* count_norm, void* ws,
+                      size_t ws_bytes, masq_stream stream) {
   MASQ_TRY(check_common(T, d, n_mod));
   MASQ_TRY(check_bits(wbits));
   MASQ_TRY(check_bits(abits));
@@ -365,7 +366,7 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     MASQ_CK(launch_gradprep(static_cast<const uint16_t*>(X), ld_x, mod_id, perm, qx, dx, inv, Tg, d, planes, st));
     MASQ_CK(launch_gradgemm(planes, Tg, gsign, qw, tmod, n_mod, d, d_out, s, inv, static_cast<const uint16_t*>(W), dw,
                             gpart, st));
-    MASQ_CK(launch_gradreduce(gpart, cnt, lambda, n_mod, gradgemm_ntiles_j(d_out), d, d_out, grad, st));
+    MASQ_CK(launch_gradreduce(gpart, count_norm ? count_norm : cnt, lambda, n_mod, gradgemm_ntiles_j(d_out), d, d_out, grad, st));
   }
   return MASQ_OK;
 }
@@ -379,17 +380,17 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
                             double* sums, int64_t* counts, double* loss, void* ws, size_t ws_bytes,
                             masq_stream stream) {
   return loss_core(X, xt, ld_x, mod_id, T, d, d_out, n_mod, s, W, wt, wbits, abits, lambda, Yref, ld_ref, sums,
-                   counts, loss, nullptr, ws, ws_bytes, stream);
+                   counts, loss, nullptr, nullptr, ws, ws_bytes, stream);
 }
 
 masq_status masq_calib_loss_grad(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
                                  int64_t d, int64_t d_out, int32_t n_mod, const float* s, const void* W,
                                  masq_dtype wt, int32_t wbits, int32_t abits, const float* lambda, const float* Yref,
                                  int64_t ld_ref, double* sums, int64_t* counts, double* loss, double* grad,
-                                 void* ws, size_t ws_bytes, masq_stream stream) {
+                                 const int64_t* count_norm, void* ws, size_t ws_bytes, masq_stream stream) {
   if (!grad) return MASQ_ERR_NULL;
   return loss_core(X, xt, ld_x, mod_id, T, d, d_out, n_mod, s, W, wt, wbits, abits, lambda, Yref, ld_ref, sums,
-                   counts, loss, grad, ws, ws_bytes, stream);
+                   counts, loss, grad, count_norm, ws, ws_bytes, stream);
 }
 
 masq_status masq_adam_step(double* theta, const double* grad, double* m1, double* m2, int64_t count, int32_t step,

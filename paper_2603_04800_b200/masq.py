@@ -217,15 +217,19 @@ def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, sums=Non
     return sums, counts, loss
 
 
-def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, grad=None, ws=None, stream=None):
-    """N1: (sums, counts, loss, grad) with grad = dL/d ln s (straight-through), f64 [M x d]."""
+def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, grad=None, sums=None, counts=None,
+                    loss=None, count_norm=None, ws=None, stream=None):
+    """N1: (sums, counts, loss, grad) with grad = dL/d ln s (straight-through), f64 [M x d].
+
+    count_norm: optional device i64 [M] token counts for the gradient's 1/N_m (the global
+    counts when the tokens are sharded over ranks; then SUM-all-reduce grad)."""
     T, d = X.shape
     d_out = W.shape[1]
     n_mod = s.shape[0]
     dev = X.device
-    sums = torch.empty(n_mod, dtype=torch.float64, device=dev)
-    counts = torch.empty(n_mod, dtype=torch.int64, device=dev)
-    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    sums = torch.empty(n_mod, dtype=torch.float64, device=dev) if sums is None else sums
+    counts = torch.empty(n_mod, dtype=torch.int64, device=dev) if counts is None else counts
+    loss = torch.empty(1, dtype=torch.float64, device=dev) if loss is None else loss
     grad = torch.empty(n_mod, d, dtype=torch.float64, device=dev) if grad is None else grad
     ws = ws or default_workspace(dev)
     p, n = ws.ptr_size(workspace_size(OP_LOSS_GRAD, T, d, d_out, n_mod))
@@ -233,8 +237,8 @@ def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, gra
     _ck(lib().masq_calib_loss_grad(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod, _p(s.contiguous()),
                                    _p(W.contiguous()), _dt(W), wbits, abits,
                                    ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr is not None else None,
-                                   _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), _p(grad), p, n,
-                                   _stream(stream)), "masq_calib_loss_grad")
+                                   _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), _p(grad),
+                                   _p(count_norm), p, n, _stream(stream)), "masq_calib_loss_grad")
     return sums, counts, loss, grad
 
 

@@ -65,6 +65,16 @@ def reduce_loss(sums, counts, group=None):
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
 
 
+def reduce_grad(grad, group=None):
+    """All-reduce the N1 gradient (f64 [M x d]): SUM.  Each rank's grad must have been formed
+    with the GLOBAL token counts (masq_calib_loss_grad's count_norm), so the sum is the
+    gradient of the whole batch's loss."""
+    _, ws = world()
+    if ws == 1:
+        return
+    dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+
+
 def max_over_ranks(x: float, device=None) -> float:
     """Max of a host float over ranks (timings: the slowest rank defines the step)."""
     _, ws = world()

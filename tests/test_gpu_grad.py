@@ -3,7 +3,7 @@ of the calibration loss w.r.t. ln s (masq_calib_loss_grad) and the log-space Ada
 (masq_adam_step) — against oracle.calib_loss_grad / oracle.adam_step on the same inputs.
 
 Bar: the loss within 1e-3 relative (as A8); the gradient within 2e-3 max-abs-normalised per
-modality (DESIGN.md §4: sign(E) may differ where E rounds to ~0 in f32 vs f64 and the P/Q
+modality (DESIGN.md §10: sign(E) may differ where E rounds to ~0 in f32 vs f64 and the P/Q
 contractions accumulate in fp32 over the tokens); Adam to f64 rounding.
 """
 import numpy as np
@@ -106,4 +106,21 @@ def test_adam_step_parity_trajectory():
         assert np.allclose(s_cur.cpu().numpy(), np.exp(th_o).astype(np.float32), rtol=2e-7)
     # No descent assertion: a uniform rescale of s^m is an exact invariance of the per-token /
     # per-channel absmax quantizers, but not of the straight-through surrogate, and Adam's
-    # sign-like first steps move mostly along it — the loss stays ~flat.
+    # sign-like first steps move mostly along it (Q24) — the loss stays ~flat.
+
+
+def test_loss_grad_token_shards_sum_to_batch():
+    """count_norm = the batch's counts: the two shards' gradients add up to the batch's (the
+    token-sharded multi-GPU contract; the exchange itself is a SUM all-reduce)."""
+    c = case("ragged3")
+    m = M()
+    _, cnt, so, _, _ = oracle_state(c)
+    X, W = bf(c["X"]), bf(c["W"])
+    ids = tt(c["ids"])
+    Yref = m.reference_output(X, W)
+    cn = tt(cnt.astype(np.int64))
+    h = 512
+    _, _, _, g0 = m.calib_loss_grad(X[:h], ids[:h], tt(so), W, 8, 8, Yref[:h], count_norm=cn)
+    _, _, _, g1 = m.calib_loss_grad(X[h:], ids[h:], tt(so), W, 8, 8, Yref[h:], count_norm=cn)
+    _, go = O.calib_loss_grad(c["X"], c["ids"], so, c["W"], 8, 8)
+    assert _grad_err((g0 + g1).cpu().numpy(), go) <= TOL_G

@@ -4,7 +4,8 @@ Each rank computes its token shard with the CPU oracle (standing in for the per-
 which need a B200), then the real reduction code runs over gloo:
   * R after the MAX all-reduce is bit-identical to the single-process R; counts add up;
   * the loss from SUM-reduced per-modality sums/counts equals the single-process loss;
-  * output-column shards of the forward concatenate to the full forward.
+  * output-column shards of the forward concatenate to the full forward;
+  * N1 gradients of the token shards (global-count normalised) SUM to the full gradient.
 """
 import os
 import socket
@@ -45,6 +46,10 @@ def _worker(rank, world_size, port, q):
         sums, counts, _ = O.calib_loss(c["X"][a:b], c["ids"][a:b], s, c["W"], 8, 8)
         st, nt = torch.from_numpy(sums.copy()), torch.from_numpy(counts.copy())
         P.reduce_loss(st, nt)
+        # N1 gradient on this rank's tokens, normalised by the global counts, then SUM
+        _, g = O.calib_loss_grad(c["X"][a:b], c["ids"][a:b], s, c["W"], 8, 8, count_norm=cf)
+        gt = torch.from_numpy(g.copy())
+        P.reduce_grad(gt)
         # forward column shard
         qw, dw = O.quantize_weight(c["W"], s[0], 8)
         j0, j1 = P.column_shards(c["n"], world_size)[rank]
@@ -52,7 +57,7 @@ def _worker(rank, world_size, port, q):
                               [c["L1"][0], c["L1"][1]], [c["L2"][0][:, j0:j1], c["L2"][1][:, j0:j1]])
         parts = [None] * world_size
         dist.all_gather_object(parts, (j0, j1, Ys))
-        q.put((rank, Rt.numpy(), ct.numpy(), st.numpy(), nt.numpy(), parts))
+        q.put((rank, Rt.numpy(), ct.numpy(), st.numpy(), nt.numpy(), parts, gt.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -76,7 +81,9 @@ def test_two_rank_exchange_matches_single_process():
     sums1, counts1, loss1 = O.calib_loss(c["X"], c["ids"], s, c["W"], 8, 8)
     qw, dw = O.quantize_weight(c["W"], s[0], 8)
     Y1 = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, [c["L1"][0], c["L1"][1]], [c["L2"][0], c["L2"][1]])
-    for rank, R, cnt, sums, counts, parts in res:
+    _, g1 = O.calib_loss_grad(c["X"], c["ids"], s, c["W"], 8, 8)
+    for rank, R, cnt, sums, counts, parts, g in res:
+        assert np.allclose(g, g1, rtol=1e-9, atol=1e-12 * np.abs(g1).max())
         assert np.array_equal(R, R1), "MAX all-reduce of R must be bit-identical to one process"
         assert np.array_equal(cnt, c1)
         assert np.array_equal(counts, counts1)
