@@ -250,15 +250,28 @@ def loss_finalize(sums, counts, lam, n: int) -> float:
 
 
 # --------------------------------------------------------------------------- N1 (next row)
+def _first_argmax_abs(A, axis: int):
+    """Index of the first maximum of |A| along axis (np.argmax returns the first occurrence)."""
+    return np.argmax(np.abs(A), axis=axis)
+
+
 def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None, count_norm=None):
     """N1 — gradient of L = sum_m lambda_m MAE_m (O8) w.r.t. theta^m = ln s^m (SPEC.md:307-316:
-    log-space parameters, rounding treated as identity — the straight-through contract; reading
-    Q24: the dynamic scales Delta are held constant, i.e. stop-gradient on the scales).
+    log-space parameters; "gradient of the rounding operator treated as identity inside the
+    clamp range and zero outside" — reading Q24: ONLY round() is straight-through; the dynamic
+    scales Delta = max|.|/q_max stay functions of their inputs, so they are differentiated
+    through their (first) arg-max element; the clamp is never active for absmax scales, and a
+    floored Delta (1e-12f) has zero derivative).
 
-    With A = X_m S_m^-1 (xs), B = S_m W (ws), Ahat = Q(A), Bhat = Q(B), E = Ahat Bhat - X_m W and
-    G = lambda_m / (N_m n) sign(E):  dL/dA = G Bhat^T, dL/dB = Ahat^T G, dA/dtheta_i = -A[:, i],
-    dB/dtheta_i = B[i, :], hence
-        grad_i = sum_j (Ahat^T G)_ij B_ij - sum_j (X_m^T G)_ij inv_i Bhat_ij     (xs = X inv)
+    Per modality, with A = X_m S_m^-1 (xs), B = S_m W, Ahat = Q(A) = A + D, Bhat = Q(B),
+    E = Ahat Bhat - X_m W and G = lambda_m / (N_m n) sign(E):
+      Ahat_ti = Delta_t code_ti  with  d Ahat = dA + (code - A/Delta) dDelta_t  (round: identity)
+      dA_ti/dtheta_l = -A_ti [i = l];  dDelta_t/dtheta_l = -Delta_t [l = k_t],  k_t = argmax_i |A_ti|
+      dB_ij/dtheta_l =  B_ij [i = l];  dDelta_j/dtheta_l =  Delta_j [l = k_j],  k_j = argmax_i |B_ij|
+    hence
+      grad_l = sum_j (Ahat^T G)_lj B_lj - sum_j (A^T G)_lj Bhat_lj
+             + sum_{j: k_j = l} beta_j - sum_{t: k_t = l} alpha_t,
+      beta_j  = sum_i (Ahat^T G)_ij (Bhat - B)_ij,   alpha_t = sum_i (G Bhat^T)_ti (Ahat - A)_ti.
     count_norm: the N_m of the gradient's scale (default: this call's token counts) — a token
     shard passes the whole batch's counts, and the shards' gradients then add up to the batch
     gradient.  The returned loss always uses this call's own counts.
@@ -271,6 +284,7 @@ def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None, count_norm=N
     ids = _check_ids(ids, n_mod)
     lam = np.ones(n_mod) if lam is None else np.asarray(lam, F64)
     n = Wf.shape[1]
+    qa, qw_max = F32(2 ** (abits - 1) - 1), F32(2 ** (wbits - 1) - 1)
     xs_all = smooth_activations(Xf, ids, s)
     grad = np.zeros((n_mod, Wf.shape[0]), F64)
     loss = 0.0
@@ -283,12 +297,57 @@ def calib_loss_grad(X, ids, s, W, wbits: int, abits: int, lam=None, count_norm=N
         Ahat = dequantize_rows(qx, dx)                                   # [T_m x d]
         qw, dw = quantize_weight(W, s[m], wbits)
         Bhat = dequantize_rows(qw, dw).T                                 # [d x n]
-        Bs = np.multiply(s[m][:, None], Wf, dtype=F32).astype(F64)       # S_m W as quantized (f32)
+        Bs32 = np.multiply(s[m][:, None], Wf, dtype=F32)                 # S_m W as quantized (f32)
+        Bs, A = Bs32.astype(F64), np.asarray(xs, F64)
         E = Ahat @ Bhat - np.asarray(Xf[sel], F64) @ np.asarray(Wf, F64)
         loss += float(lam[m]) / (sel.size * n) * np.abs(E).sum()
         G = float(lam[m]) / ((sel.size if count_norm is None else int(count_norm[m])) * n) * np.sign(E)
-        grad[m] = ((Ahat.T @ G) * Bs).sum(axis=1) - ((np.asarray(xs, F64).T @ G) * Bhat).sum(axis=1)
+        GB = Ahat.T @ G                                                  # dL/dBhat  [d x n]
+        g = (GB * Bs).sum(axis=1) - ((A.T @ G) * Bhat).sum(axis=1)
+        # scale terms: weight columns (Delta_j not floored) and token rows (Delta_t not floored)
+        beta = (GB * (Bhat - Bs)).sum(axis=0)                            # [n]
+        live_j = np.divide(np.abs(Bs32).max(axis=0), qw_max, dtype=F32) >= FLOOR
+        np.add.at(g, _first_argmax_abs(Bs32, 0)[live_j], beta[live_j])
+        alpha = ((G @ Bhat.T) * (Ahat - A)).sum(axis=1)                  # [T_m]
+        live_t = np.divide(np.abs(xs).max(axis=1), qa, dtype=F32) >= FLOOR
+        np.add.at(g, _first_argmax_abs(xs, 1)[live_t], -alpha[live_t])
+        grad[m] = g
     return loss, grad
+
+
+def optimize_factors(X, ids, s0, W, wbits: int, abits: int, epochs: int = 2, batch_tokens: int = 1024,
+                     lr: float = 1e-2, lam=None, max_rejections: int = 10):
+    """N1 driver — SPEC.md:307-316 optimize_factors, step by step: theta = ln s0; per epoch one
+    pass over the calibration batches (contiguous slices of batch_tokens tokens), each an Adam
+    step (step 1e-2) on that batch's straight-through gradient; a non-finite loss
+    or gradient rejects the step and halves the step size, 10 consecutive rejections end the
+    run; after each epoch the objective over the whole set is evaluated and the best-so-far
+    iterate kept (so the result never has a higher objective than s0).
+    Returns (s_best f32 [M x d], best objective, [objective after each epoch]).
+    """
+    s0 = np.asarray(s0, F32)
+    T = np.asarray(ids).shape[0]
+    objective = lambda s: calib_loss(X, ids, s, W, wbits, abits, lam=lam)[2]
+    best, s_best = objective(s0), s0.copy()
+    theta, m1, m2 = np.log(s0.astype(F64)), np.zeros(s0.shape), np.zeros(s0.shape)
+    s, t, rejections, history = s0.copy(), 0, 0, []
+    for _ in range(epochs):
+        for a in range(0, T, batch_tokens):
+            b = min(T, a + batch_tokens)
+            loss, g = calib_loss_grad(X[a:b], ids[a:b], s, W, wbits, abits, lam=lam)
+            if not (np.isfinite(loss) and np.all(np.isfinite(g))):
+                lr, rejections = lr * 0.5, rejections + 1
+                if rejections >= max_rejections:
+                    return s_best, best, history
+                continue
+            rejections, t = 0, t + 1
+            theta, m1, m2 = adam_step(theta, g, m1, m2, t, lr)
+            s = np.exp(theta).astype(F32)
+        L = objective(s)
+        history.append(L)
+        if np.isfinite(L) and L < best:
+            best, s_best = L, s.copy()
+    return s_best, best, history
 
 
 def adam_step(theta, grad, m1, m2, step: int, lr: float, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8):

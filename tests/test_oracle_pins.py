@@ -357,7 +357,9 @@ def test_hand_worked_example():
 # ----------------------------------------------------------------------------- N1 gradient
 def _autograd_ste_loss_grad(X, ids, s, W, wbits, abits):
     """Independent implementation of the straight-through graph with torch.autograd (f64):
-    Q(u) = u + (Delta * round_half_away(u / Delta) - u).detach(), Delta detached."""
+    Delta = max(amax|u| / q_max, 1e-12) differentiable (through the arg-max element);
+    Q(u) = Delta * (v + (round_half_away(v) - v).detach()), v = u / Delta — only round() is
+    straight-through (reading Q24)."""
     import torch
     Xt = torch.from_numpy(O.decode(X).astype(np.float64))
     Wt = torch.from_numpy(O.decode(W).astype(np.float64))
@@ -365,10 +367,11 @@ def _autograd_ste_loss_grad(X, ids, s, W, wbits, abits):
 
     def q_rows(u, bits):
         qmax = 2 ** (bits - 1) - 1
-        delta = (u.detach().abs().amax(dim=1, keepdim=True) / qmax).clamp_min(1e-12)
-        v = u.detach() / delta
-        r = torch.trunc(v) + torch.sign(v) * (torch.abs(v - torch.trunc(v)) >= 0.5)
-        return u + (delta * r.clamp(-qmax - 1, qmax) - u).detach()
+        delta = (u.abs().amax(dim=1, keepdim=True) / qmax).clamp_min(1e-12)
+        v = u / delta
+        vd = v.detach()
+        r = torch.trunc(vd) + torch.sign(vd) * (torch.abs(vd - torch.trunc(vd)) >= 0.5)
+        return delta * (v + (r.clamp(-qmax - 1, qmax) - vd))
 
     loss = 0.0
     n = Wt.shape[1]
@@ -381,12 +384,13 @@ def _autograd_ste_loss_grad(X, ids, s, W, wbits, abits):
         E = Ah @ Bh - Xt[sel] @ Wt
         loss = loss + E.abs().sum() / (sel.numel() * n)
     loss.backward()
-    return float(loss), theta.grad.numpy()
+    return float(loss.detach()), theta.grad.numpy()
 
 
 def test_loss_grad_matches_autograd_ste():
-    """N1 pin: the closed-form straight-through gradient equals torch.autograd on the STE graph
-    (up to the f32 smoothing / quantization of the oracle; codes are identical on these inputs)."""
+    """N1 pin: the closed-form straight-through gradient (incl. the arg-max scale terms) equals
+    torch.autograd on the STE graph (up to the f32 smoothing / quantization of the oracle;
+    codes are identical on these inputs, and no |.|-maximum is tied)."""
     c = synth.config_inputs("c2", T=1024, d=32, n=48)
     R, cnt = O.calibrate_stats(c["X"], c["ids"], 3)
     s = O.init_factors(R, cnt, c["W"])
@@ -396,6 +400,19 @@ def test_loss_grad_matches_autograd_ste():
     la, ga = _autograd_ste_loss_grad(c["X"], c["ids"], s, c["W"], 4, 8)
     assert np.isclose(la, loss, rtol=1e-5)
     assert np.abs(grad - ga).max() <= 1e-4 * np.abs(ga).max()
+
+
+def test_loss_grad_uniform_rescale_is_a_null_direction():
+    """s^m -> c s^m leaves every code and the loss unchanged (absmax scales rescale with it), and
+    the straight-through gradient with the scale terms sees that: sum_i grad_i = 0 per modality
+    (up to rounding), while dropping the scale terms (Delta held constant) would not."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    loss, grad = O.calib_loss_grad(c["X"], c["ids"], s, c["W"], 4, 8)
+    _, _, l2 = O.calib_loss(c["X"], c["ids"], s * np.float32(2.0), c["W"], 4, 8)
+    assert abs(l2 - loss) <= 1e-12 * loss                         # exact invariance (power of 2)
+    assert np.all(np.abs(grad.sum(axis=1)) <= 1e-9 * np.abs(grad).sum(axis=1))
 
 
 def test_loss_grad_descent_direction_and_adam():
@@ -414,3 +431,39 @@ def test_loss_grad_descent_direction_and_adam():
     assert np.all(th1[~nz] == theta[~nz])
     _, _, loss1 = O.calib_loss(c["X"], c["ids"], np.exp(th1).astype(np.float32), c["W"], 4, 8)
     assert loss1 <= loss0 * (1 + 1e-3)
+
+
+def test_optimize_factors_contract():
+    """SPEC.md:307-316 optimize_factors: epochs = 0 returns the init unchanged; the result is
+    the best-so-far iterate (objective never above the init's, and equal to the objective
+    recomputed at the returned factors); positivity is preserved."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s0 = O.init_factors(R, cnt, c["W"])
+    L0 = O.calib_loss(c["X"], c["ids"], s0, c["W"], 4, 8)[2]
+    s, best, hist = O.optimize_factors(c["X"], c["ids"], s0, c["W"], 4, 8, epochs=0)
+    assert np.array_equal(s, s0) and best == L0 and hist == []
+    s, best, hist = O.optimize_factors(c["X"], c["ids"], s0, c["W"], 4, 8, epochs=2, batch_tokens=64, lr=3e-2)
+    assert len(hist) == 2 and best <= L0 and np.all(s > 0)
+    assert best == O.calib_loss(c["X"], c["ids"], s, c["W"], 4, 8)[2]
+    assert best == min([L0] + hist)
+
+
+def test_optimize_factors_beats_unified_smoothing():
+    """SPEC.md:315 example: a two-modality layer with a 30x range gap, W4A8, 2 epochs — the
+    weighted loss ends strictly below the unified-smoothing closed form (one s from the range
+    over all tokens, PAPER.md:19-23 / 36-39) on the same data."""
+    g = np.random.Generator(np.random.PCG64(11))
+    T, d, n = 512, 64, 96
+    ids = np.repeat(np.array([0, 1, 0, 1], np.uint8), T // 4)
+    ch = np.exp(g.normal(0, 0.5, d))
+    X = g.normal(0, 1, (T, d)) * ch * np.where(ids == 1, 30.0, 1.0)[:, None]
+    X = synth.f32_to_bf16_bits(X.astype(np.float32))
+    W = synth.f32_to_bf16_bits((g.normal(0, 1, (d, n)) / np.sqrt(d)).astype(np.float32))
+    R, cnt = O.calibrate_stats(X, ids, 2)
+    Ru = np.repeat(R.max(axis=0, keepdims=True), 2, axis=0)
+    su = O.init_factors(Ru, cnt, W)                      # unified: the same s for both modalities
+    Lu = O.calib_loss(X, ids, su, W, 4, 8)[2]
+    s0 = O.init_factors(R, cnt, W)
+    s, best, _ = O.optimize_factors(X, ids, s0, W, 4, 8, epochs=2, batch_tokens=128)
+    assert best < Lu
