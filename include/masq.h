@@ -212,6 +212,17 @@ masq_status masq_adam_step(double* theta, const double* grad, double* m1, double
                            int32_t step, double lr, double beta1, double beta2, double eps,
                            float* s_out, masq_stream stream);
 
+/* Adam state from factors: theta = ln s (f64 of the f32 s), m1 = m2 = 0.  Device arrays [count]. */
+masq_status masq_adam_init(const float* s, double* theta, double* m1, double* m2, int64_t count,
+                           masq_stream stream);
+
+/* Best-so-far iterate ("the returned factors are the best-so-far iterate"): if
+ * loss[0] is finite and < best_loss[0] (or best_loss[0] is NaN), copy s -> s_best ([count] f32)
+ * and set best_loss[0] = loss[0].  improved (optional, device i32) receives 1 / 0.  All device
+ * pointers; stream-ordered, no host sync. */
+masq_status masq_keep_best(const double* loss, double* best_loss, const float* s, float* s_best,
+                           int64_t count, int32_t* improved, masq_stream stream);
+
 /* loss[0] = sum_m lambda[m] * sums[m] / (counts[m] * d_out) on the device (after an all-reduce). */
 masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const float* lambda,
                                int32_t n_mod, int64_t d_out, double* loss, masq_stream stream);

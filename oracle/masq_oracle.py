@@ -322,7 +322,9 @@ def optimize_factors(X, ids, s0, W, wbits: int, abits: int, epochs: int = 2, bat
     step (step 1e-2) on that batch's straight-through gradient; a non-finite loss
     or gradient rejects the step and halves the step size, 10 consecutive rejections end the
     run; after each epoch the objective over the whole set is evaluated and the best-so-far
-    iterate kept (so the result never has a higher objective than s0).
+    iterate kept (so the result never has a higher objective than s0).  Batch slices are views
+    of the calibration set in token order (reading Q25: a batch is batch_tokens consecutive
+    tokens; the default 1024 is one synthetic sample).
     Returns (s_best f32 [M x d], best objective, [objective after each epoch]).
     """
     s0 = np.asarray(s0, F32)
@@ -335,7 +337,7 @@ def optimize_factors(X, ids, s0, W, wbits: int, abits: int, epochs: int = 2, bat
         for a in range(0, T, batch_tokens):
             b = min(T, a + batch_tokens)
             loss, g = calib_loss_grad(X[a:b], ids[a:b], s, W, wbits, abits, lam=lam)
-            if not (np.isfinite(loss) and np.all(np.isfinite(g))):
+            if not np.isfinite(loss):                 # non-finite loss -> reject
                 lr, rejections = lr * 0.5, rejections + 1
                 if rejections >= max_rejections:
                     return s_best, best, history

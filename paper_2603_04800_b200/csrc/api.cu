@@ -23,7 +23,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     case MASQ_OP_INIT:
       break;
     case MASQ_OP_QWEIGHT:
-      L.amax = take(sizeof(uint32_t) * n);
+      L.amax = take(2 * sizeof(uint32_t) * n);
       break;
     case MASQ_OP_QACT:
       L.inv_s = take(sizeof(float) * n_mod * d);
@@ -50,7 +50,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.cnt = take(sizeof(int64_t) * n_mod);
       L.qw_all = take((size_t)n_mod * n * d);
       L.dw_all = take(sizeof(float) * n_mod * n);
-      L.amax = take(sizeof(uint32_t) * n_mod * n);
+      L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
       L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
       break;
     }
@@ -66,11 +66,19 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.cnt = take(sizeof(int64_t) * n_mod);
       L.qw_all = take((size_t)n_mod * n * d);
       L.dw_all = take(sizeof(float) * n_mod * n);
-      L.amax = take(sizeof(uint32_t) * n_mod * n);
+      L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
       L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
       L.gsign = take(sizeof(uint16_t) * (size_t)Tg * n);
       L.planes = take(sizeof(uint16_t) * 2 * (size_t)Tg * d);
-      L.gpartial = take(sizeof(double) * n_mod * ceil_div(n, kTileN) * d);
+      L.gpartial = take(sizeof(double) * n_mod * gradgemm_ntiles_j(n) * d);
+      L.codes16 = take(sizeof(uint16_t) * (size_t)n_mod * n * d);
+      L.apart = take(sizeof(float) * (size_t)Tg * 2 * ceil_div(n, kTileN));
+      L.bpart = take(sizeof(float) * (size_t)n_mod * 4 * gradgemm_ntiles_i(d) * n);
+      L.kj = take(sizeof(int32_t) * (size_t)n_mod * n);
+      const int64_t nkeys = (int64_t)n_mod * n + Tg;
+      L.keys = take(sizeof(int32_t) * nkeys);
+      L.vals = take(sizeof(double) * nkeys);
+      L.bucket = take(sizeof(double) * (size_t)bucket_chunks(nkeys) * n_mod * d);
       break;
     }
     default:
@@ -363,10 +371,42 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
   if (grad) {
     uint16_t* planes = reinterpret_cast<uint16_t*>(W8(ws, L.planes));
     double* gpart = reinterpret_cast<double*>(W8(ws, L.gpartial));
-    MASQ_CK(launch_gradprep(static_cast<const uint16_t*>(X), ld_x, mod_id, perm, qx, dx, inv, Tg, d, planes, st));
+    uint16_t* codes16 = reinterpret_cast<uint16_t*>(W8(ws, L.codes16));
+    float* apart = reinterpret_cast<float*>(W8(ws, L.apart));
+    float* bpart = reinterpret_cast<float*>(W8(ws, L.bpart));
+    int32_t* kj = reinterpret_cast<int32_t*>(W8(ws, L.kj));
+    int32_t* keys = reinterpret_cast<int32_t*>(W8(ws, L.keys));
+    double* vals = reinterpret_cast<double*>(W8(ws, L.vals));
+    double* bucket = reinterpret_cast<double*>(W8(ws, L.bucket));
+    const int64_t nj = (int64_t)n_mod * d_out, nkeys = nj + Tg;
+    int32_t* ktkey = keys + nj;
+    const uint32_t* colmax = amax;                     // first half of the scratch: column maxima
+    MASQ_CK(launch_gradprep(static_cast<const uint16_t*>(X), ld_x, mod_id, perm, qx, dx, inv, Tg, d, abits, planes,
+                            ktkey, st));
+    MASQ_CK(launch_codes16(qw, (int64_t)n_mod * d_out * d, codes16, st));
+    MASQ_CK(cudaMemsetAsync(kj, 0x7F, sizeof(int32_t) * nj, st));
     MASQ_CK(launch_gradgemm(planes, Tg, gsign, qw, tmod, n_mod, d, d_out, s, inv, static_cast<const uint16_t*>(W), dw,
-                            gpart, st));
-    MASQ_CK(launch_gradreduce(gpart, count_norm ? count_norm : cnt, lambda, n_mod, gradgemm_ntiles_j(d_out), d, d_out, grad, st));
+                            colmax, gpart, bpart, kj, st));
+    GemmArgs ga{};
+    ga.mode = kModeAlpha;
+    ga.T = Tg;
+    ga.n = d_out;
+    ga.d = d;
+    ga.xbf = planes;                                   // plane 0 = D
+    ga.ld_x = d;
+    ga.b = codes16;
+    ga.b_rows = (int64_t)n_mod * d_out;
+    ga.dw = dw;
+    ga.tile_mask = tmod;
+    ga.n_mod = n_mod;
+    ga.gsign = gsign;
+    ga.apart = apart;
+    MASQ_CK(launch_gemm(ga, st));
+    MASQ_CK(launch_gradkeys(bpart, 4 * gradgemm_ntiles_i(d), kj, colmax, wbits, apart, 2 * num_n, ktkey, n_mod, d,
+                            d_out, Tg, keys, vals, st));
+    MASQ_CK(launch_bucket(keys, vals, nkeys, (int64_t)n_mod * d, bucket, st));
+    MASQ_CK(launch_gradreduce(gpart, bucket, bucket_chunks(nkeys), count_norm ? count_norm : cnt, lambda, n_mod,
+                              gradgemm_ntiles_j(d_out), d, d_out, grad, st));
   }
   return MASQ_OK;
 }
@@ -399,6 +439,23 @@ masq_status masq_adam_step(double* theta, const double* grad, double* m1, double
   if (count < 0 || step < 1) return MASQ_ERR_SHAPE;
   if (count == 0) return MASQ_OK;
   MASQ_CK(launch_adam(theta, grad, m1, m2, count, step, lr, beta1, beta2, eps, s_out, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_adam_init(const float* s, double* theta, double* m1, double* m2, int64_t count,
+                           masq_stream stream) {
+  if (!s || !theta || !m1 || !m2) return MASQ_ERR_NULL;
+  if (count < 0) return MASQ_ERR_SHAPE;
+  if (count == 0) return MASQ_OK;
+  MASQ_CK(launch_adam_init(s, theta, m1, m2, count, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_keep_best(const double* loss, double* best_loss, const float* s, float* s_best, int64_t count,
+                           int32_t* improved, masq_stream stream) {
+  if (!loss || !best_loss || !s || !s_best) return MASQ_ERR_NULL;
+  if (count < 0) return MASQ_ERR_SHAPE;
+  MASQ_CK(launch_keep_best(loss, best_loss, s, s_best, count, improved, S(stream)));
   return MASQ_OK;
 }
 

@@ -314,14 +314,15 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
       if (m[k][e] > 0.f) atomicMax(amax + (int64_t)k * n + j0 + e, __float_as_uint(m[k][e]));
 }
 
-// dw[j] = max(amax[j] / q_max, 1e-12f) (the output scales); amax[j] is overwritten in place with
-// the f32 reciprocal 1/dw[j] used by the fast quantizer path
-__global__ void wscale_kernel(uint32_t* __restrict__ amax, float* __restrict__ dw, int64_t count, float qmaxf) {
+// dw[j] = max(amax[j] / q_max, 1e-12f) (the output scales) and rcp[j] = the f32 reciprocal
+// 1/dw[j] used by the fast quantizer path; amax (the column maxima) is kept for N1's arg-max
+__global__ void wscale_kernel(const uint32_t* __restrict__ amax, float* __restrict__ dw, float* __restrict__ rcp,
+                              int64_t count, float qmaxf) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= count) return;
   const float dv = fmaxf(__fdiv_rn(__uint_as_float(amax[j]), qmaxf), kFloor);
   dw[j] = dv;
-  amax[j] = __float_as_uint(__fdiv_rn(1.0f, dv));
+  rcp[j] = __fdiv_rn(1.0f, dv);
 }
 
 // pass 2: one 128 (i) x 64 (j) tile of W read once; for every set k the codes are packed
@@ -773,7 +774,7 @@ cudaError_t launch_init(const float* R, const int64_t* count, const void* W, mas
 
 template <typename WT, int NS>
 static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n, int wbits, int8_t* qw, float* dw,
-                               uint32_t* amax, cudaStream_t st) {
+                               uint32_t* amax, float* rcp, cudaStream_t st) {
   const int qmax = (1 << (wbits - 1)) - 1, qmin = -(1 << (wbits - 1));
   constexpr int V = Vec<WT>::N;
   const int gx = (int)ceil_div(n, 256 * V);
@@ -784,8 +785,8 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   strips = (int)ceil_div(d, rows);
   dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 64), (unsigned)ceil_div(d, 128));
   { ProfScope ps_("wcolmax", st); wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
-  { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, NS * n, (float)qmax); }
-  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, reinterpret_cast<const float*>(amax), qw, dw); }
+  { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, rcp, NS * n, (float)qmax); }
+  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, rcp, qw, dw); }
   return cudaGetLastError();
 }
 
@@ -799,12 +800,13 @@ static cudaError_t wquant_dispatch(const WT* w, const float* s, int n_sets, int6
     int8_t* qk = qw + (int64_t)k0 * n * d;
     float* dk = dw + (int64_t)k0 * n;
     uint32_t* ak = amax + (int64_t)k0 * n;
+    float* rk = reinterpret_cast<float*>(amax + (int64_t)n_sets * n) + (int64_t)k0 * n;
     cudaError_t e;
     switch (ns) {
-      case 1: e = wquant_sets<WT, 1>(w, sk, d, n, wbits, qk, dk, ak, st); break;
-      case 2: e = wquant_sets<WT, 2>(w, sk, d, n, wbits, qk, dk, ak, st); break;
-      case 3: e = wquant_sets<WT, 3>(w, sk, d, n, wbits, qk, dk, ak, st); break;
-      default: e = wquant_sets<WT, 4>(w, sk, d, n, wbits, qk, dk, ak, st); break;
+      case 1: e = wquant_sets<WT, 1>(w, sk, d, n, wbits, qk, dk, ak, rk, st); break;
+      case 2: e = wquant_sets<WT, 2>(w, sk, d, n, wbits, qk, dk, ak, rk, st); break;
+      case 3: e = wquant_sets<WT, 3>(w, sk, d, n, wbits, qk, dk, ak, rk, st); break;
+      default: e = wquant_sets<WT, 4>(w, sk, d, n, wbits, qk, dk, ak, rk, st); break;
     }
     if (e != cudaSuccess) return e;
   }

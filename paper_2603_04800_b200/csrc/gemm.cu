@@ -11,6 +11,9 @@
 //             perm maps a grouped row to its token), acc = qx . Q(S_m W)^T and the epilogue
 //             sums |acc*dx*dw_m - Yref[perm[row]]| -> per-(unit, CTA, warp) partials.
 //   kModeRef  Yref = X . W (kind::f16 bf16 -> fp32), the loss target.
+//   kModeAlpha N1 scale term: rows grouped as for the loss, acc = D . codes(Q(S_m W))^T
+//             (kind::f16, both K-major; D = Ahat - X S^-1 as bf16), and the epilogue reduces
+//             sum_j sign(E)_tj * dw_m[j] * acc_tj per row into per-(row, CTA column half) partials.
 //
 // A cluster of two CTAs (one per SM of a TPC) computes a 256 x 256 output unit with
 // tcgen05.mma.cta_group::2 (M = 256, N = 256): CTA r loads rows [128r, 128r+128) of the A tile
@@ -79,6 +82,7 @@ struct Params {
   long long ld_ref;
   double* partials;            // loss: [n_units][2] (one per CTA of the pair)
   uint16_t* gsign;             // loss (optional, N1): bf16 sign(yq - yref) [T x n], 0 on padding rows
+  float* apart;                // alpha: [T][2 * num_n] per-row partials
 };
 
 struct Unit {
@@ -96,7 +100,7 @@ __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
   w.mt = rem / gsz;
   w.nt = nt0 + (rem - w.mt * gsz);
   w.m = 0;
-  if (p.mode == kModeLoss) {
+  if (p.mode == kModeLoss || p.mode == kModeAlpha) {
     w.mask = p.tile_mask[w.mt];
     if (w.mask == 0xFFFFFFFFu) return false;
     w.m = (int)w.mask;
@@ -148,7 +152,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (MODE != kModeLoss) tma_prefetch(&tmY);
+    if (MODE != kModeLoss && MODE != kModeAlpha) tma_prefetch(&tmY);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -164,7 +168,8 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  constexpr int KELEMS = (MODE == kModeRef) ? 64 : 128;
+  constexpr int KELEMS = (MODE == kModeRef || MODE == kModeAlpha) ? 64 : 128;
+  constexpr bool kGrouped = MODE == kModeLoss || MODE == kModeAlpha;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -196,7 +201,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int u = cid; u < p.n_units; u += ncl) {
         Unit w;
         if (!decode_unit(p, u, w)) continue;
-        const int brow = (MODE == kModeLoss ? w.m * p.n : 0) + w.nt * BN + (int)rank * BNH;
+        const int brow = (kGrouped ? w.m * p.n : 0) + w.nt * BN + (int)rank * BNH;
         const int arow = w.mt * UM + (int)rank * BM;
         const int defer_at = min(kCmcDefer, p.num_kb - 1);
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -265,6 +270,9 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             if (MODE == kModeRef) {
               const uint64_t bd = umma_desc_sw128_mn(b0 + ring.stage * B_BYTES + k * 2048, B_BYTES / 2);
               mma_bf16_2sm(dtm, ad, bd, IDESC_BF16_BMN, (kb | k) != 0);
+            } else if (MODE == kModeAlpha) {
+              const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
+              mma_bf16_2sm(dtm, ad, bd, IDESC_BF16, (kb | k) != 0);
             } else {
               const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
               mma_i8_2sm(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
@@ -307,10 +315,10 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       // ---- prefetch (overlaps the main loop): row scale, this warp's 128 column scales (lane l
       //      holds dw[col_base + (c0+c)*32 + l]), and for the loss the source token of the row
       float dxr = 0.f;
-      if (MODE != kModeRef && row < p.T) dxr = p.dx[row];
+      if (MODE != kModeRef && MODE != kModeAlpha && row < p.T) dxr = p.dx[row];
       float dwr[4] = {0.f, 0.f, 0.f, 0.f};
       if (MODE != kModeRef && MODE != kModeAcc) {
-        const float* dwp = p.dw + (MODE == kModeLoss ? (size_t)w.m * p.n : 0) + col_base + c0 * 32 + lane;
+        const float* dwp = p.dw + (kGrouped ? (size_t)w.m * p.n : 0) + col_base + c0 * 32 + lane;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           if (c < nch) dwr[c] = __ldg(dwp + c * 32);
@@ -442,6 +450,27 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           p.partials[(size_t)(w.mt * p.num_n + w.nt) * 2 + rank] = tot;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+      } else if (MODE == kModeAlpha) {
+        float part = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= nch) break;
+          uint32_t v[32];
+          tmem_ld32(taddr + c * 32, v);
+          const uint4* gp = reinterpret_cast<const uint4*>(p.gsign + (size_t)row * p.n + col_base + (c0 + c) * 32);
+          uint4 g4[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) g4[k] = __ldg(gp + k);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint32_t gw = (&g4[i >> 3].x)[(i >> 1) & 3];
+            const float g = __uint_as_float((i & 1) ? (gw & 0xFFFF0000u) : (gw << 16));   // +-1 or 0
+            const float dws = __shfl_sync(0xffffffffu, dwr[c], i);
+            part = fmaf(g * dws, __uint_as_float(v[i]), part);
+          }
+        }
+        if (row < p.T) p.apart[(size_t)row * (2 * p.num_n) + 2 * w.nt + (ew >> 2)] = part;
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -479,7 +508,7 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  static const char* const kNames[4] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref"};
+  static const char* const kNames[5] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha"};
   ProfScope ps_(kNames[MODE], st);
   masq_gemm_kernel<MODE><<<2 * clusters, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
   return cudaGetLastError();
@@ -501,9 +530,12 @@ int num_sms() {
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   if (g.T <= 0 || g.n <= 0) return cudaSuccess;
   CUtensorMap ta, tb, ty, tz, tl2;
-  const bool bf = g.mode == kModeRef;
+  const bool bf = g.mode == kModeRef || g.mode == kModeAlpha;
   bool ok = true;
-  if (bf) {
+  if (g.mode == kModeAlpha) {
+    ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
+    ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.b_rows, g.d, g.d, BNH, 64, true);
+  } else if (bf) {
     ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
     // B = W [d x n] row-major (MN-major for the MMA): box 64 (n) x 64 (k)
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.d, g.n, g.n, 64, 64, true);
@@ -511,7 +543,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, BM, 128, true);
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BNH, 128, true);
   }
-  if (g.mode != kModeLoss) {
+  if (g.mode != kModeLoss && g.mode != kModeAlpha) {
     ok &= make_tmap_2d(&ty, g.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.T, g.n, g.ld_out, 32, 32, true);
   } else {
     ty = ta;
@@ -557,12 +589,14 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.ld_ref = g.ld_ref;
   p.partials = g.partials;
   p.gsign = g.gsign;
+  p.apart = g.apart;
   const int clusters = (int)std::min<int64_t>(p.n_units, num_sms() / 2);
   switch (g.mode) {
     case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, clusters, st);
     case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, clusters, st);
     case kModeLoss: return launch_mode<kModeLoss>(ta, tb, ty, tz, tl2, p, clusters, st);
     case kModeRef: return launch_mode<kModeRef>(ta, tb, ty, tz, tl2, p, clusters, st);
+    case kModeAlpha: return launch_mode<kModeAlpha>(ta, tb, ty, tz, tl2, p, clusters, st);
     default: return cudaErrorInvalidValue;
   }
 }

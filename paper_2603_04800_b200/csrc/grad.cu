@@ -9,6 +9,12 @@
 //   grad_i = scale_m * sum_j [ (D^T G)_ij B_ij + inv_i (X^T G)_ij (B - Bhat)_ij ],  D = Ahat - A,
 // whose two terms are the activation and weight quantisation residuals taken directly — no
 // cancellation between two large near-equal products, so one bf16 plane of D suffices.
+// The scales are differentiated too (reading Q24: only round() is straight-through):
+//   + sum_{j: k_j = l} beta_j - sum_{t: k_t = l} alpha_t,
+//   beta_j = sum_i (Ahat^T G)_ij (Bhat - B)_ij   (this kernel's epilogue, per 32-row group),
+//   alpha_t = sum_j G_tj (D Bhat)_tj              (gemm.cu kModeAlpha, D . codes^T),
+// k_j / k_t the first arg-max rows / channels of |B| / |A|, summed into grad by a fixed-order
+// bucket pass (deterministic).
 // Q' = D^T G and P = X^T G are tcgen05 kind::f16 GEMMs with the token axis as K: A operand
 // planes [D | X] (bf16, MN-major: i contiguous), B operand G (MN-major: j contiguous), two fp32
 // TMEM accumulators (Q' in columns 0..255, P in 256..511).  The epilogue reads W and the tile
@@ -44,8 +50,26 @@ struct GParams {
   const float* inv;              // [M][d]
   const uint16_t* W;             // [d][n] bf16
   const float* dw;               // [M][n]
+  const uint32_t* colmax;        // [M][n] f32 bits of max_i |s_i w_ij|
   double* partial;               // [M][nj][d]
+  float* bpart;                  // [M][4 * ni][n]
+  int32_t* kj;                   // [M][n]
 };
+
+// 32 values per lane -> lane l returns the sum over the warp of v[l] (transpose-reduce, 31 shuffles)
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[32], uint32_t lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & (uint32_t)off) != 0u;
+#pragma unroll
+    for (int k = 0; k < off; ++k) {
+      const float send = upper ? v[k] : v[k + off];
+      const float keep = upper ? v[k + off] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
 
 __device__ __forceinline__ void seg_of(const GParams& p, int m, int& k0, int& nkb) {
   int first = -1, cnt = 0;
@@ -168,15 +192,23 @@ gradgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int il = (int)(q * 32u + lane);
       const int i = it * GM + il;
       double* out = p.partial + ((size_t)m * p.nj + jt) * p.d;
-      if (nkb == 0) {
+      if (nkb == 0) {                      // no tokens of modality m: zero contributions
         if (i < p.d) out[i] = 0.0;
+        float* bz = p.bpart + ((size_t)m * 4 * p.ni + 4 * it + q) * p.n + jt * GN;
+        const int nz = min(8, (p.n - jt * GN) / 32);
+        for (int c = 0; c < nz; ++c) bz[c * 32 + lane] = 0.f;
         continue;
       }
       const int j0 = jt * GN;
       const int nch = min(8, (p.n - j0) / 32);
       float dwr[8];
+      uint32_t cmr[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) dwr[c] = c < nch ? __ldg(p.dw + (size_t)m * p.n + j0 + c * 32 + lane) : 0.f;
+      for (int c = 0; c < 8; ++c) {
+        dwr[c] = c < nch ? __ldg(p.dw + (size_t)m * p.n + j0 + c * 32 + lane) : 0.f;
+        cmr[c] = c < nch ? __ldg(p.colmax + (size_t)m * p.n + j0 + c * 32 + lane) : 0xFFFFFFFFu;
+      }
+      float* bout = p.bpart + ((size_t)m * 4 * p.ni + 4 * it + q) * p.n + j0;
       const bool iv = i < p.d;
       const float si = iv ? __ldg(p.s + (size_t)m * p.d + i) : 0.f;
       const float invi = iv ? __ldg(p.inv + (size_t)m * p.d + i) : 0.f;
@@ -202,17 +234,24 @@ gradgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           for (int k = 0; k < 4; ++k) w4[k] = make_uint4(0, 0, 0, 0);
         }
         tmem_wait_ld();
+        float bj[32];
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const uint32_t wv = (&w4[jj >> 3].x)[(jj >> 1) & 3];
           const float w = __uint_as_float((jj & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
           const float dwj = __shfl_sync(0xffffffffu, dwr[c], jj);
+          const uint32_t cmj = __shfl_sync(0xffffffffu, cmr[c], jj);
           const int qv = (int)(int8_t)qws[(c * 32 + jj) * GM + il];
           const float bs = __fmul_rn(si, w);                       // (S_m W)_ij as quantized
           const float bh = __fmul_rn(dwj, (float)qv);              // Bhat_ij
-          acc = fmaf(__uint_as_float(vq[jj]), bs, acc);
-          acc = fmaf(__uint_as_float(vp[jj]) * invi, __fsub_rn(bs, bh), acc);
+          const float q = __uint_as_float(vq[jj]), pv = __uint_as_float(vp[jj]);
+          const float dbw = __fsub_rn(bs, bh);                     // B - Bhat
+          acc = fmaf(q, bs, acc);
+          acc = fmaf(pv * invi, dbw, acc);
+          bj[jj] = -fmaf(pv, invi, q) * dbw;                       // (Ahat^T G)_ij (Bhat - B)_ij
+          if (iv && (__float_as_uint(bs) & 0x7FFFFFFFu) == cmj) atomicMin(p.kj + (size_t)m * p.n + j0 + c * 32 + jj, i);
         }
+        bout[c * 32 + lane] = warp_transpose_sum(bj, lane);
       }
       if (iv) out[i] = (double)acc;
       tc_fence_before();
@@ -236,13 +275,17 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
                                                        const uint8_t* __restrict__ mod_id,
                                                        const int32_t* __restrict__ perm, const int8_t* __restrict__ qx,
                                                        const float* __restrict__ dx, const float* __restrict__ inv,
-                                                       int64_t Tg, int64_t d, uint16_t* __restrict__ planes) {
+                                                       int64_t Tg, int64_t d, float qa, uint16_t* __restrict__ planes,
+                                                       int32_t* __restrict__ ktkey) {
   const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= Tg) return;
   const int32_t src = __ldg(perm + p);
   const float dxv = src >= 0 ? __ldg(dx + p) : 0.f;
-  const float* invm = inv + (src >= 0 ? (int64_t)__ldg(mod_id + src) * d : 0);
+  const int mrow = src >= 0 ? (int)__ldg(mod_id + src) : 0;
+  const float* invm = inv + (int64_t)mrow * d;
+  uint32_t best = 0;                          // |xs| bits of the lane's first maximum
+  int bidx = 0x7FFFFFFF;
   uint16_t* pd = planes + p * d;
   uint16_t* px = planes + (Tg + p) * d;
   for (int64_t c = (int64_t)lane * 8; c < d; c += 256) {
@@ -267,6 +310,8 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
           const float ah = __fmul_rn(dxv, (float)qv);
           const float xs = __fmul_rn(x, iv[idx]);
           h[k] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(ah, xs)));
+          const uint32_t ab = __float_as_uint(xs) & 0x7FFFFFFFu;
+          if (ab > best) { best = ab; bidx = (int)(c + idx); }
         }
         o[e] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
       }
@@ -275,21 +320,103 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
     *reinterpret_cast<uint4*>(pd + c) = dv;
     *reinterpret_cast<uint4*>(px + c) = xv;
   }
+  // first arg-max over the row: larger |xs| wins, ties -> smaller index
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint32_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+  }
+  if (lane == 0) {
+    // the scale derivative exists only when Delta_t = max/q_a is not floored (and the row is real)
+    const bool live = src >= 0 && __fdiv_rn(__uint_as_float(best), qa) >= 1e-12f;
+    ktkey[p] = live ? mrow * (int)d + bidx : -1;
+  }
+}
+
+__global__ void codes16_kernel(const int8_t* __restrict__ q, int64_t count, uint16_t* __restrict__ out) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i >= count) return;
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(q + i));
+  const uint32_t w[2] = {v.x, v.y};
+  uint32_t o[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int a = (int)(int8_t)((w[e >> 1] >> (16 * (e & 1))) & 0xFF);
+    const int b = (int)(int8_t)((w[e >> 1] >> (16 * (e & 1) + 8)) & 0xFF);
+    o[e] = (uint32_t)__bfloat16_as_ushort(__int2bfloat16_rn(a)) |
+           ((uint32_t)__bfloat16_as_ushort(__int2bfloat16_rn(b)) << 16);
+  }
+  *reinterpret_cast<uint4*>(out + i) = make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// keys / values of the scale terms (fixed-order partial sums)
+__global__ void gradkeys_kernel(const float* __restrict__ bpart, int nb, const int32_t* __restrict__ kj,
+                                const uint32_t* __restrict__ colmax, float qw, const float* __restrict__ apart, int na,
+                                const int32_t* __restrict__ ktkey, int n_mod, int64_t d, int64_t n, int64_t Tg,
+                                int32_t* __restrict__ keys, double* __restrict__ vals) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nj = (int64_t)n_mod * n;
+  if (idx < nj) {
+    const int64_t m = idx / n, j = idx - m * n;
+    double b = 0.0;
+    for (int r = 0; r < nb; ++r) b += (double)bpart[((int64_t)m * nb + r) * n + j];
+    const int32_t k = kj[idx];
+    const bool live = k >= 0 && k < d && __fdiv_rn(__uint_as_float(colmax[idx]), qw) >= 1e-12f;
+    keys[idx] = live ? (int32_t)(m * d + k) : -1;
+    vals[idx] = b;
+  } else if (idx < nj + Tg) {
+    const int64_t t = idx - nj;
+    double a = 0.0;
+    for (int r = 0; r < na; ++r) a += (double)apart[t * na + r];
+    keys[idx] = ktkey[t];
+    vals[idx] = -a;
+  }
+}
+
+constexpr int kBucketChunk = 2048;
+
+// bucket[c][l] = sum_{k in chunk c, keys[k] == l} vals[k]   (fixed order within the chunk)
+__global__ void __launch_bounds__(256) bucket_kernel(const int32_t* __restrict__ keys, const double* __restrict__ vals,
+                                                     int64_t nkeys, int64_t nl, double* __restrict__ bucket) {
+  __shared__ int32_t sk[kBucketChunk];
+  __shared__ double sv[kBucketChunk];
+  const int64_t k0 = (int64_t)blockIdx.y * kBucketChunk;
+  const int nk = (int)(nkeys - k0 < kBucketChunk ? nkeys - k0 : kBucketChunk);
+  const int64_t lbase = (int64_t)blockIdx.x * 256;
+  int cnt = 0;
+  for (int k = threadIdx.x; k < nk; k += 256) {
+    const int32_t key = keys[k0 + k];
+    sk[k] = key;
+    sv[k] = vals[k0 + k];
+    cnt += (key >= lbase && key < lbase + 256) ? 1 : 0;
+  }
+  cnt = __syncthreads_or(cnt);
+  const int64_t l = lbase + threadIdx.x;
+  if (l >= nl) return;
+  double a = 0.0;
+  if (cnt)
+    for (int k = 0; k < nk; ++k)
+      if (sk[k] == (int32_t)l) a += sv[k];
+  bucket[(int64_t)blockIdx.y * nl + l] = a;
 }
 
 struct Lam8 {
   float v[kMaxMod];
 };
 
-// grad[m][i] = lambda_m / (counts_m * n) * sum_jt partial[m][jt][i]   (fixed order)
-__global__ void gradreduce_kernel(const double* __restrict__ partial, const int64_t* __restrict__ counts, Lam8 lam,
-                                  int n_mod, int nj, int64_t d, int64_t n, double* __restrict__ grad) {
+// grad[m][i] = lambda_m / (counts_m * n) * (sum_jt partial[m][jt][i] + sum_c bucket[c][m*d + i])
+// (fixed order)
+__global__ void gradreduce_kernel(const double* __restrict__ partial, const double* __restrict__ bucket, int nchunks,
+                                  const int64_t* __restrict__ counts, Lam8 lam, int n_mod, int nj, int64_t d,
+                                  int64_t n, double* __restrict__ grad) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_mod * d) return;
   const int m = (int)(idx / d);
   const int64_t i = idx - (int64_t)m * d;
   double a = 0.0;
   for (int jt = 0; jt < nj; ++jt) a += partial[((int64_t)m * nj + jt) * d + i];
+  for (int c = 0; c < nchunks; ++c) a += bucket[(int64_t)c * n_mod * d + idx];
   const int64_t c = counts[m];
   grad[idx] = c > 0 ? (double)lam.v[m] * a / ((double)c * (double)n) : 0.0;
 }
@@ -310,20 +437,85 @@ __global__ void adam_kernel(double* __restrict__ theta, const double* __restrict
   theta[i] = t;
   if (s_out) s_out[i] = (float)exp(t);
 }
+__global__ void adam_init_kernel(const float* __restrict__ s, double* __restrict__ theta, double* __restrict__ m1,
+                                 double* __restrict__ m2, int64_t count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  theta[i] = log((double)s[i]);
+  m1[i] = 0.0;
+  m2[i] = 0.0;
+}
+
+// best-so-far: if loss < best (or best is NaN), s_best = s and best = loss.  One CTA, so the
+// decision is read by every thread before thread 0 overwrites best.
+__global__ void __launch_bounds__(1024) keep_best_kernel(const double* __restrict__ loss, double* __restrict__ best,
+                                                         const float* __restrict__ s, float* __restrict__ s_best,
+                                                         int64_t count, int32_t* __restrict__ improved) {
+  const double l = *loss, b = *best;
+  const bool take = isfinite(l) && (l < b || isnan(b));
+  if (take)
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s_best[i] = s[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (take) *best = l;
+    if (improved) *improved = take ? 1 : 0;
+  }
+}
 }  // namespace
 
+cudaError_t launch_adam_init(const float* s, double* theta, double* m1, double* m2, int64_t count, cudaStream_t st) {
+  ProfScope ps_("adam_init", st);
+  adam_init_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(s, theta, m1, m2, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keep_best(const double* loss, double* best, const float* s, float* s_best, int64_t count,
+                             int32_t* improved, cudaStream_t st) {
+  ProfScope ps_("keep_best", st);
+  keep_best_kernel<<<1, 1024, 0, st>>>(loss, best, s, s_best, count, improved);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
-                            const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d,
-                            uint16_t* planes, cudaStream_t st) {
+                            const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d, int abits,
+                            uint16_t* planes, int32_t* ktkey, cudaStream_t st) {
   ProfScope ps_("gradprep", st);
-  gradprep_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(X, ld_x, mod_id, perm, qx, dx, inv, Tg, d, planes);
+  gradprep_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(X, ld_x, mod_id, perm, qx, dx, inv, Tg, d,
+                                                             (float)((1 << (abits - 1)) - 1), planes, ktkey);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_codes16(const int8_t* q, int64_t count, uint16_t* out, cudaStream_t st) {
+  ProfScope ps_("codes16", st);
+  codes16_kernel<<<(unsigned)ceil_div(count, 8 * 256), 256, 0, st>>>(q, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gradkeys(const float* bpart, int nb, const int32_t* kj, const uint32_t* colmax, int wbits,
+                            const float* apart, int na, const int32_t* ktkey, int n_mod, int64_t d, int64_t n,
+                            int64_t Tg, int32_t* keys, double* vals, cudaStream_t st) {
+  ProfScope ps_("gradkeys", st);
+  const int64_t count = (int64_t)n_mod * n + Tg;
+  gradkeys_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(bpart, nb, kj, colmax,
+                                                                  (float)((1 << (wbits - 1)) - 1), apart, na, ktkey,
+                                                                  n_mod, d, n, Tg, keys, vals);
+  return cudaGetLastError();
+}
+
+int bucket_chunks(int64_t nkeys) { return (int)ceil_div(nkeys, kBucketChunk); }
+
+cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys, int64_t nl, double* bucket,
+                          cudaStream_t st) {
+  ProfScope ps_("bucket", st);
+  dim3 grid((unsigned)ceil_div(nl, 256), (unsigned)bucket_chunks(nkeys));
+  bucket_kernel<<<grid, 256, 0, st>>>(keys, vals, nkeys, nl, bucket);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* gsign, const int8_t* qw_all,
                             const uint32_t* tile_mod, int n_mod, int64_t d, int64_t n, const float* s,
-                            const float* inv, const uint16_t* W, const float* dw, double* partial,
-                            cudaStream_t st) {
+                            const float* inv, const uint16_t* W, const float* dw, const uint32_t* colmax,
+                            double* partial, float* bpart, int32_t* kj, cudaStream_t st) {
   CUtensorMap ta, tb, tq;
   bool ok = make_tmap_2d(&ta, planes, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)NPL * Tg, d, d, 64, 64, true);
   ok &= make_tmap_2d(&tb, gsign, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Tg, n, n, 64, 64, true);
@@ -349,7 +541,10 @@ cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* 
   p.inv = inv;
   p.W = W;
   p.dw = dw;
+  p.colmax = colmax;
   p.partial = partial;
+  p.bpart = bpart;
+  p.kj = kj;
   const int grid = std::min(p.n_units, num_sms());
   ProfScope ps_("gradgemm", st);
   gradgemm_kernel<<<grid, GT, G_ALLOC, st>>>(ta, tb, tq, p);
@@ -357,14 +552,17 @@ cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* 
 }
 
 int gradgemm_ntiles_j(int64_t n) { return (int)ceil_div(n, GN); }
+int gradgemm_ntiles_i(int64_t d) { return (int)ceil_div(d, GM); }
 
-cudaError_t launch_gradreduce(const double* partial, const int64_t* counts, const float* lambda_host, int n_mod,
-                              int nj, int64_t d, int64_t n, double* grad, cudaStream_t st) {
+cudaError_t launch_gradreduce(const double* partial, const double* bucket, int nchunks, const int64_t* counts,
+                              const float* lambda_host, int n_mod, int nj, int64_t d, int64_t n, double* grad,
+                              cudaStream_t st) {
   Lam8 l;
   for (int m = 0; m < kMaxMod; ++m) l.v[m] = (lambda_host && m < n_mod) ? lambda_host[m] : 1.0f;
   const int64_t count = (int64_t)n_mod * d;
   ProfScope ps_("gradreduce", st);
-  gradreduce_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(partial, counts, l, n_mod, nj, d, n, grad);
+  gradreduce_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(partial, bucket, nchunks, counts, l, n_mod, nj, d,
+                                                                    n, grad);
   return cudaGetLastError();
 }
 

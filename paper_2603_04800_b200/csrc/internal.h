@@ -28,6 +28,8 @@ struct WsLayout {
   size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0, xsplit = 0;
   size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, cnt = 0, total = 0;
   size_t gsign = 0, planes = 0, gpartial = 0;
+  // N1 scale terms
+  size_t codes16 = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -55,6 +57,8 @@ cudaError_t launch_init(const float* R, const int64_t* count, const void* W, mas
 // weight quantization of n_sets factor vectors s[k*d..] -> qw[k*n*d..], dw[k*n..]
 cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_sets, int64_t d, int64_t n,
                           int wbits, int8_t* qw, float* dw, uint32_t* amax_scratch, cudaStream_t st);
+// amax_scratch: [2 x n_sets x n] u32 — the column maxima max_i |s_i w_ij| (f32 bits, kept after
+// the call), then the f32 reciprocals of the scales used by the quantizer
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st);
 // perm (optional): output row p quantizes input token perm[p] (-1: padding row, left untouched);
 // T_out = number of output rows (T when perm == NULL)
@@ -87,13 +91,13 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, in
                   uint64_t cols, uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
 
 // ---------------------------------------------------------------- GEMM (gemm.cu)
-enum GemmMode { kModeFwd = 0, kModeAcc = 1, kModeLoss = 2, kModeRef = 3 };
+enum GemmMode { kModeFwd = 0, kModeAcc = 1, kModeLoss = 2, kModeRef = 3, kModeAlpha = 4 };
 
 struct GemmArgs {
   int mode;
   int64_t T, n, d;                 // rows, output columns, K
   const int8_t* qx;                // int8 A [T x d]   (kModeFwd/Acc/Loss)
-  const uint16_t* xbf;             // bf16 A [T x ld_x] (kModeRef)
+  const uint16_t* xbf;             // bf16 A [T x ld_x] (kModeRef; kModeAlpha: the D plane)
   int64_t ld_x;
   const void* b;                   // int8 qw [(n_b) x d] or bf16 Wt [n x d]
   int64_t b_rows;                  // rows of the B tensor (n, or n_mod*n for the loss)
@@ -113,21 +117,44 @@ struct GemmArgs {
   int64_t ld_ref;
   double* partials;                // [n_mod][tiles][4]
   uint16_t* gsign;                 // loss, optional (N1): bf16 sign(yq - yref), grouped rows [T x n]
+  // kModeAlpha (N1): acc = D . codes_m^T (bf16 codes of Q(S_m W), K-major [n_mod*n x d]);
+  // apart[row][2*nt + half] = sum_j gsign[row][j] * dw_m[j] * acc[row][j] over the CTA's columns
+  float* apart;
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
 int gemm_epilogue_warps();
 
 // ---------------------------------------------------------------- N1 gradient (grad.cu)
 // planes [2][Tg][d] bf16: D = Ahat - X S^-1 and X, in grouped row order
+// ktkey[Tg]: m*d + (first arg-max_i |xs_ti|) of every grouped row (-1: padding / floored scale)
 cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
-                            const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d,
-                            uint16_t* planes, cudaStream_t st);
+                            const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d, int abits,
+                            uint16_t* planes, int32_t* ktkey, cudaStream_t st);
+// int8 codes [rows x d] -> bf16 [rows x d] (exact)
+cudaError_t launch_codes16(const int8_t* q, int64_t count, uint16_t* out, cudaStream_t st);
+// partial[m][jt][i] (sum_j of the direct terms), bpart[m][4*it + q][j] (beta_j over 32 rows i),
+// kj[m][j] = min i with |f32(s_i w_ij)| == colmax[m][j] (atomicMin; preset to INT_MAX)
 cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* gsign, const int8_t* qw_all,
                             const uint32_t* tile_mod, int n_mod, int64_t d, int64_t n, const float* s,
-                            const float* inv, const uint16_t* W, const float* dw, double* partial, cudaStream_t st);
+                            const float* inv, const uint16_t* W, const float* dw, const uint32_t* colmax,
+                            double* partial, float* bpart, int32_t* kj, cudaStream_t st);
 int gradgemm_ntiles_j(int64_t n);
-cudaError_t launch_gradreduce(const double* partial, const int64_t* counts, const float* lambda_host, int n_mod,
-                              int nj, int64_t d, int64_t n, double* grad, cudaStream_t st);
+int gradgemm_ntiles_i(int64_t d);
+// keys/vals [n_mod*n + Tg]: (m*d + k_j, +beta_j) for every weight column, (ktkey[t], -alpha_t) for
+// every grouped row; alpha_t = sum of apart[t][0..na), beta = sum of bpart over the 4*ni row groups
+cudaError_t launch_gradkeys(const float* bpart, int nb, const int32_t* kj, const uint32_t* colmax, int wbits,
+                            const float* apart, int na, const int32_t* ktkey, int n_mod, int64_t d, int64_t n,
+                            int64_t Tg, int32_t* keys, double* vals, cudaStream_t st);
+int bucket_chunks(int64_t nkeys);
+// bucket[c][l] = sum over keys of chunk c equal to l of vals (fixed order), l in [0, n_mod*d)
+cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys, int64_t nl, double* bucket,
+                          cudaStream_t st);
+cudaError_t launch_gradreduce(const double* partial, const double* bucket, int nchunks, const int64_t* counts,
+                              const float* lambda_host, int n_mod, int nj, int64_t d, int64_t n, double* grad,
+                              cudaStream_t st);
+cudaError_t launch_adam_init(const float* s, double* theta, double* m1, double* m2, int64_t count, cudaStream_t st);
+cudaError_t launch_keep_best(const double* loss, double* best, const float* s, float* s_best, int64_t count,
+                             int32_t* improved, cudaStream_t st);
 cudaError_t launch_adam(double* theta, const double* grad, double* m1, double* m2, int64_t count, int step, double lr,
                         double b1, double b2, double eps, float* s_out, cudaStream_t st);
 int num_sms();

@@ -250,6 +250,22 @@ def adam_step(theta, grad, m1, m2, step: int, lr: float, beta1: float = 0.9, bet
     return theta
 
 
+def adam_init(s, theta=None, m1=None, m2=None, stream=None):
+    """(theta, m1, m2) = (ln s, 0, 0) as f64 device tensors shaped like s."""
+    theta = torch.empty(s.shape, dtype=torch.float64, device=s.device) if theta is None else theta
+    m1 = torch.empty_like(theta) if m1 is None else m1
+    m2 = torch.empty_like(theta) if m2 is None else m2
+    _ck(lib().masq_adam_init(_p(s.contiguous()), _p(theta), _p(m1), _p(m2), s.numel(), _stream(stream)),
+        "masq_adam_init")
+    return theta, m1, m2
+
+
+def keep_best(loss, best_loss, s, s_best, improved=None, stream=None):
+    """Best-so-far on the device: s_best <- s and best_loss <- loss when loss < best_loss."""
+    _ck(lib().masq_keep_best(_p(loss), _p(best_loss), _p(s), _p(s_best), s.numel(), _p(improved),
+                             _stream(stream)), "masq_keep_best")
+
+
 def loss_finalize(sums, counts, d_out: int, lam=None, loss=None, stream=None):
     n_mod = sums.shape[0]
     loss = torch.empty(1, dtype=torch.float64, device=sums.device) if loss is None else loss
