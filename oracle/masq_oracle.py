@@ -360,3 +360,74 @@ def adam_step(theta, grad, m1, m2, step: int, lr: float, b1: float = 0.9, b2: fl
     mh = m1 / (1 - b1 ** step)
     vh = m2 / (1 - b2 ** step)
     return np.asarray(theta, F64) - lr * mh / (np.sqrt(vh) + eps), m1, m2
+
+
+# --------------------------------------------------------------------------- N4 baselines
+def smooth_factors(num, den, beta: float) -> np.ndarray:
+    """N4 — the beta-parameterised closed forms the paper compares against (PAPER.md:19-23
+    SmoothQuant s_i = R_i^beta / wmax_i^(1-beta); PAPER.md:24-28 AWQ s_i = mean_i^beta with
+    den = None; PAPER.md:36-39 unified factors = num taken over all modalities).  num, den are
+    floored at 1e-12 (Q7); evaluated in f64 and rounded once to f32 (reading Q26).
+    num: [.. x d]; den: [d] or None.  Returns f32 like num."""
+    n = np.maximum(np.asarray(num, F32), FLOOR).astype(F64)
+    r = n ** F64(beta)
+    if den is not None:
+        dd = np.maximum(np.asarray(den, F32), FLOOR).astype(F64)
+        r = r / dd ** (F64(1.0) - F64(beta))
+    return r.astype(F32)
+
+
+def unified_stats(R) -> np.ndarray:
+    """max_m R^m_i — the range a single unified factor is computed from."""
+    return np.asarray(R, F32).max(axis=0)
+
+
+def meanabs_stats(X, ids, n_mod: int):
+    """AWQ's activation statistic per modality: sum_t |x^m_t,i| (f64, exact
+    summation order irrelevant at f64 for the tested sizes) and token counts."""
+    Xf = np.abs(decode(X).astype(F64))
+    ids = _check_ids(ids, n_mod)
+    S = np.zeros((n_mod, Xf.shape[1]), F64)
+    cnt = np.zeros(n_mod, np.int64)
+    for m in range(n_mod):
+        sel = ids == m
+        S[m] = Xf[sel].sum(axis=0)
+        cnt[m] = int(sel.sum())
+    return S, cnt
+
+
+def range_ratio(R, dominant: int, other: int) -> np.ndarray:
+    """alpha^{m,m'}_i = R^m_i / R^{m'}_i, R^{m'} floored at 1e-12 (PAPER.md:83 Theorem 1;
+    SPEC.md:317-320), f32 division."""
+    R = np.asarray(R, F32)
+    return np.divide(R[dominant], np.maximum(R[other], FLOOR), dtype=F32)
+
+
+def dominance_stats(R):
+    """Per modality, the number of channels whose max_m R^m_i it attains (PAPER.md:410,
+    fig:modality_dominance): ties go to the first such modality and are also
+    counted in a separate bucket.  Returns int64 [M + 1] (last entry = tied channels)."""
+    R = np.asarray(R, F32)
+    M, d = R.shape
+    out = np.zeros(M + 1, np.int64)
+    for i in range(d):
+        col = R[:, i]
+        top = col.max()
+        winners = [m for m in range(M) if col[m] == top]
+        out[winners[0]] += 1
+        if len(winners) > 1:
+            out[M] += 1
+    return out
+
+
+def awq_grid_search(X, ids, W, wbits: int, abits: int, betas, n_mod: int, lam=None):
+    """AWQ-style search: unified s(beta) = (mean_t |x_t,i|)^beta over all
+    tokens, beta* = argmin_beta of the loss (O8) — each point scored by calib_loss with the same
+    s for every modality.  Returns (beta*, [loss(beta)])."""
+    S, cnt = meanabs_stats(X, ids, n_mod)
+    mean = (S.sum(axis=0) / cnt.sum()).astype(F32)
+    losses = []
+    for b in betas:
+        s = smooth_factors(mean, None, b)
+        losses.append(calib_loss(X, ids, np.repeat(s[None, :], n_mod, axis=0), W, wbits, abits, lam=lam)[2])
+    return float(betas[int(np.argmin(losses))]), losses

@@ -467,3 +467,59 @@ def test_optimize_factors_beats_unified_smoothing():
     s0 = O.init_factors(R, cnt, W)
     s, best, _ = O.optimize_factors(X, ids, s0, W, 4, 8, epochs=2, batch_tokens=128)
     assert best < Lu
+
+
+# ----------------------------------------------------------------------------- N4 baselines
+def test_smooth_factors_closed_forms():
+    """beta = 1 returns R exactly; beta = 0 returns 1/wmax (correctly rounded); beta = 0.5
+    agrees with the A2 init sequence sqrt(R / wmax) within 1 ulp; log s = beta log(R wmax) -
+    log wmax is increasing in beta exactly where R wmax > 1."""
+    g = np.random.Generator(np.random.PCG64(5))
+    R = np.exp(g.normal(0, 2, (2, 300))).astype(np.float32)
+    wm = np.exp(g.normal(-2, 1, 300)).astype(np.float32)
+    assert np.array_equal(O.smooth_factors(R, wm, 1.0), R)
+    assert np.array_equal(O.smooth_factors(R, wm, 0.0)[0], (1.0 / wm.astype(np.float64)).astype(np.float32))
+    s5 = O.smooth_factors(R, wm, 0.5)
+    ref = np.sqrt(np.divide(R, wm[None, :], dtype=np.float32), dtype=np.float32)
+    assert np.all(np.abs(s5.view(np.int32) - ref.view(np.int32)) <= 1)
+    assert np.array_equal(O.smooth_factors(R, None, 1.0), R)
+    hi = R.astype(np.float64) * wm[None, :] > 1.0
+    assert np.all(O.smooth_factors(R, wm, 0.7)[hi] >= O.smooth_factors(R, wm, 0.6)[hi])
+    assert np.all(O.smooth_factors(R, wm, 0.7)[~hi] <= O.smooth_factors(R, wm, 0.6)[~hi])
+
+
+def test_range_ratio_and_dominance_spec_examples():
+    """SPEC.md:317-326 / 484-490 examples, plus a loop oracle on random profiles."""
+    g = np.random.Generator(np.random.PCG64(6))
+    R = np.exp(g.normal(0, 1, (3, 64))).astype(np.float32)
+    assert np.array_equal(O.range_ratio(R[[0, 0]], 0, 1), np.ones(64, np.float32))     # identical
+    R10 = np.stack([R[0] * np.float32(10), R[0]])
+    assert np.allclose(O.range_ratio(R10, 0, 1), 10.0, rtol=1e-6)                       # 10x everywhere
+    dom = O.dominance_stats(R10)
+    assert dom.tolist() == [64, 0, 0]                                                   # fraction 1.0
+    half = np.stack([np.where(np.arange(64) < 32, 2.0, 1.0), np.where(np.arange(64) < 32, 1.0, 2.0)])
+    assert O.dominance_stats(half.astype(np.float32)).tolist() == [32, 32, 0]           # 0.5 / 0.5
+    tie = np.ones((2, 8), np.float32)
+    assert O.dominance_stats(tie).tolist() == [8, 0, 8]                                 # ties: first + tied
+    d = O.dominance_stats(R)
+    assert d[:3].sum() == 64 and all(d[m] == int(np.sum(np.argmax(R, axis=0) == m)) for m in range(3))
+    zero = np.zeros((2, 4), np.float32)
+    assert np.all(O.range_ratio(zero, 0, 1) == 0.0)                                     # floored denominator
+
+
+def test_meanabs_and_awq_grid():
+    """Mean-abs statistic against a brute-force loop; the AWQ grid's beta = 0 point is s = 1
+    (no smoothing) and its loss equals calib_loss with unit factors."""
+    c = synth.config_inputs("c1")
+    S, cnt = O.meanabs_stats(c["X"], c["ids"], 2)
+    Xf = O.decode(c["X"]).astype(np.float64)
+    for m in range(2):
+        acc = np.zeros(Xf.shape[1])
+        for t in range(Xf.shape[0]):
+            if c["ids"][t] == m:
+                acc += np.abs(Xf[t])
+        assert np.allclose(S[m], acc, rtol=1e-12) and cnt[m] == int((c["ids"] == m).sum())
+    betas = [0.0, 0.25, 0.5]
+    b, losses = O.awq_grid_search(c["X"], c["ids"], c["W"], 4, 8, betas, 2)
+    l1 = O.calib_loss(c["X"], c["ids"], np.ones((2, Xf.shape[1]), np.float32), c["W"], 4, 8)[2]
+    assert losses[0] == l1 and b == betas[int(np.argmin(losses))]
