@@ -70,7 +70,8 @@ typedef void* masq_stream;      /* cudaStream_t */
 /* Workspace queries: op is one of the MASQ_OP_* values. */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
-  MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7
+  MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,
+  MASQ_OP_MEANABS = 8
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -222,6 +223,37 @@ masq_status masq_adam_init(const float* s, double* theta, double* m1, double* m2
  * pointers; stream-ordered, no host sync. */
 masq_status masq_keep_best(const double* loss, double* best_loss, const float* s, float* s_best,
                            int64_t count, int32_t* improved, masq_stream stream);
+
+/* ---------------------------------------------------------------- N4: baseline factor methods
+ * — the closed forms the paper compares MASQuant against, on the same data. */
+
+/* s[r*d + i] = max(num[r*d+i], 1e-12)^beta / max(den[i], 1e-12)^(1-beta), evaluated in f64 and
+ * rounded once to f32 (reading Q26).  SmoothQuant: num = R^m (or the unified
+ * max_m R^m), den = max_j |w_ji| (masq_init_factors' wmax_out).  AWQ
+ * (PAPER.md:24-28): num = mean_t |x_t,i|, den = NULL (treated as 1).  beta in [0, 1] (f64;
+ * anything else -> MASQ_ERR_SHAPE).
+ * All device arrays: num / s [rows x d], den [d]. */
+masq_status masq_smooth_factors(const float* num, int64_t rows, int64_t d, const float* den, double beta,
+                                float* s, masq_stream stream);
+
+/* AWQ's activation statistic: sumabs[m*d + i] (+)= sum over tokens of modality m
+ * of |x_t,i| (f64; f32 partials over 64-token slabs, fixed-order f64 reduction, so the result is
+ * deterministic), count[m] (+)= tokens of m; optional f32 outputs mean[m*d+i] = sumabs/count and
+ * mean_unified[i] = sum_m sumabs / sum_m count (the unified statistic over all tokens).
+ * reset != 0 zeroes sumabs / count first; otherwise the call accumulates (multi-batch).
+ * A bad id sets MASQ_ERR_BAD_MODALITY in the sticky status (the token is skipped). */
+masq_status masq_calibrate_meanabs(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                                   int64_t T, int64_t d, int32_t n_mod, double* sumabs, int64_t* count,
+                                   float* mean, float* mean_unified, int32_t reset,
+                                   void* ws, size_t ws_bytes, masq_stream stream);
+
+/* Channel statistics across modalities from R [n_mod x d] (each output optional):
+ * alpha[i] = R[dominant][i] / max(R[other][i], 1e-12) (f32 division; Theorem 1 range
+ * ratio); r_unified[i] = max_m R[m][i]; dom_counts[m] = number of
+ * channels whose maximum modality m attains (ties go to the first such m) and
+ * dom_counts[n_mod] = number of tied channels. */
+masq_status masq_range_stats(const float* R, int32_t n_mod, int64_t d, int32_t dominant, int32_t other,
+                             float* alpha, float* r_unified, int64_t* dom_counts, masq_stream stream);
 
 /* loss[0] = sum_m lambda[m] * sums[m] / (counts[m] * d_out) on the device (after an all-reduce). */
 masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const float* lambda,

@@ -22,6 +22,9 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     case MASQ_OP_STATS:
     case MASQ_OP_INIT:
       break;
+    case MASQ_OP_MEANABS:
+      L.partials = take(sizeof(float) * (size_t)meanabs_slabs(T) * n_mod * d);
+      break;
     case MASQ_OP_QWEIGHT:
       L.amax = take(2 * sizeof(uint32_t) * n);
       break;
@@ -456,6 +459,47 @@ masq_status masq_keep_best(const double* loss, double* best_loss, const float* s
   if (!loss || !best_loss || !s || !s_best) return MASQ_ERR_NULL;
   if (count < 0) return MASQ_ERR_SHAPE;
   MASQ_CK(launch_keep_best(loss, best_loss, s, s_best, count, improved, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_smooth_factors(const float* num, int64_t rows, int64_t d, const float* den, double beta, float* s,
+                                masq_stream stream) {
+  if (!num || !s) return MASQ_ERR_NULL;
+  if (rows < 0 || d < 0 || !(beta >= 0.0 && beta <= 1.0)) return MASQ_ERR_SHAPE;
+  if (rows == 0 || d == 0) return MASQ_OK;
+  MASQ_CK(launch_smooth_factors(num, rows, d, den, beta, s, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_calibrate_meanabs(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                                   int64_t d, int32_t n_mod, double* sumabs, int64_t* count, float* mean,
+                                   float* mean_unified, int32_t reset, void* ws, size_t ws_bytes,
+                                   masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  if (!sumabs || !count) return MASQ_ERR_NULL;
+  if (T > 0) {
+    MASQ_TRY(check_x(X, xt, ld_x, d));
+    if (!mod_id) return MASQ_ERR_NULL;
+  }
+  const WsLayout L = ws_layout(MASQ_OP_MEANABS, T, d, 0, n_mod, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  if (reset) {
+    MASQ_CK(cudaMemsetAsync(sumabs, 0, sizeof(double) * n_mod * d, st));
+    MASQ_CK(cudaMemsetAsync(count, 0, sizeof(int64_t) * n_mod, st));
+  }
+  if (T == 0) return MASQ_OK;
+  MASQ_CK(launch_meanabs(X, xt, ld_x, mod_id, T, d, n_mod, sumabs, count, mean, mean_unified,
+                         reinterpret_cast<float*>(W8(ws, L.partials)), status_of(ws), st));
+  return MASQ_OK;
+}
+
+masq_status masq_range_stats(const float* R, int32_t n_mod, int64_t d, int32_t dominant, int32_t other,
+                             float* alpha, float* r_unified, int64_t* dom_counts, masq_stream stream) {
+  MASQ_TRY(check_common(0, d, n_mod));
+  if (!R) return MASQ_ERR_NULL;
+  if (alpha && (dominant < 0 || dominant >= n_mod || other < 0 || other >= n_mod)) return MASQ_ERR_SHAPE;
+  MASQ_CK(launch_range_stats(R, n_mod, d, dominant, other, alpha, r_unified, dom_counts, S(stream)));
   return MASQ_OK;
 }
 

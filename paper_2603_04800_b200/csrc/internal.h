@@ -159,6 +159,16 @@ cudaError_t launch_adam(double* theta, const double* grad, double* m1, double* m
                         double b1, double b2, double eps, float* s_out, cudaStream_t st);
 int num_sms();
 
+// ---------------------------------------------------------------- N4 baselines (baseline.cu)
+int meanabs_slabs(int64_t T);
+cudaError_t launch_smooth_factors(const float* num, int64_t rows, int64_t d, const float* den, double beta, float* s,
+                                  cudaStream_t st);
+cudaError_t launch_meanabs(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                           int n_mod, double* S, int64_t* cnt, float* mean, float* uni, float* part,
+                           uint32_t* status, cudaStream_t st);
+cudaError_t launch_range_stats(const float* R, int n_mod, int64_t d, int dominant, int other, float* alpha,
+                               float* runi, int64_t* dom, cudaStream_t st);
+
 // ---------------------------------------------------------------- CMC first factor (zgemm.cu)
 // L1s planes: [2][(M-1)*rpad][d] bf16, plane 0 = hi, 1 = lo of diag(1/s^m) L1^m (transposed)
 cudaError_t launch_l1_fold(const uint16_t* L1, const float* inv_s, int64_t d, int r, int rpad, int n_nt,

@@ -12,7 +12,7 @@ import torch
 from ._lib import MasqDebug, lib
 
 MASQ_F32, MASQ_BF16 = 0, 1
-OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD = range(8)
+OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS = range(9)
 
 
 class MasqError(RuntimeError):
@@ -264,6 +264,45 @@ def keep_best(loss, best_loss, s, s_best, improved=None, stream=None):
     """Best-so-far on the device: s_best <- s and best_loss <- loss when loss < best_loss."""
     _ck(lib().masq_keep_best(_p(loss), _p(best_loss), _p(s), _p(s_best), s.numel(), _p(improved),
                              _stream(stream)), "masq_keep_best")
+
+
+# ----------------------------------------------------------------------------- N4
+def smooth_factors(num, beta: float, den=None, s=None, stream=None):
+    """s = num^beta / den^(1-beta) (f64 pow, one f32 rounding); den None = AWQ form."""
+    num = num.contiguous()
+    d = num.shape[-1]
+    rows = num.numel() // d if d else 0
+    s = torch.empty_like(num) if s is None else s
+    _ck(lib().masq_smooth_factors(_p(num), rows, d, _p(den.contiguous()) if den is not None else None, float(beta),
+                                  _p(s), _stream(stream)), "masq_smooth_factors")
+    return s
+
+
+def calibrate_meanabs(X, mod_id, n_mod: int, sumabs=None, count=None, reset: bool = True, ws=None, stream=None):
+    """(sumabs f64 [M x d], count i64 [M], mean f32 [M x d], mean_unified f32 [d])."""
+    T, d = X.shape
+    dev = X.device
+    sumabs = torch.zeros(n_mod, d, dtype=torch.float64, device=dev) if sumabs is None else sumabs
+    count = torch.zeros(n_mod, dtype=torch.int64, device=dev) if count is None else count
+    mean = torch.empty(n_mod, d, dtype=torch.float32, device=dev)
+    uni = torch.empty(d, dtype=torch.float32, device=dev)
+    ws = ws or default_workspace(dev)
+    p, n = ws.ptr_size(workspace_size(OP_MEANABS, T, d, 0, n_mod))
+    _ck(lib().masq_calibrate_meanabs(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, n_mod, _p(sumabs), _p(count),
+                                     _p(mean), _p(uni), 1 if reset else 0, p, n, _stream(stream)),
+        "masq_calibrate_meanabs")
+    return sumabs, count, mean, uni
+
+
+def range_stats(R, dominant: int = 0, other: int = 1, stream=None):
+    """(alpha f32 [d] or None, r_unified f32 [d], dom_counts i64 [M + 1])."""
+    n_mod, d = R.shape
+    alpha = torch.empty(d, dtype=torch.float32, device=R.device) if n_mod > 1 else None
+    runi = torch.empty(d, dtype=torch.float32, device=R.device)
+    dom = torch.empty(n_mod + 1, dtype=torch.int64, device=R.device)
+    _ck(lib().masq_range_stats(_p(R.contiguous()), n_mod, d, dominant, other, _p(alpha), _p(runi), _p(dom),
+                               _stream(stream)), "masq_range_stats")
+    return alpha, runi, dom
 
 
 def loss_finalize(sums, counts, d_out: int, lam=None, loss=None, stream=None):
