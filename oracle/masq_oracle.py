@@ -431,3 +431,78 @@ def awq_grid_search(X, ids, W, wbits: int, abits: int, betas, n_mod: int, lam=No
         s = smooth_factors(mean, None, b)
         losses.append(calib_loss(X, ids, np.repeat(s[None, :], n_mod, axis=0), W, wbits, abits, lam=lam)[2])
     return float(betas[int(np.argmin(losses))]), losses
+
+
+# --------------------------------------------------------------------------- N2 CMC factors
+def weight_residual(W, s_m, qw_t, dw_t) -> np.ndarray:
+    """Delta W = S_m W - Q(S_t W), f64 of the exact values:
+    s_m (f32) x w (bf16) is exact in f64, Q(S_t W) = dw_j * code_ji (qw_t is K-major [n x d])."""
+    Wf = decode(W).astype(F64)
+    return np.asarray(s_m, F32).astype(F64)[:, None] * Wf - dequantize_rows(qw_t, dw_t).T
+
+
+def whitening_transform(A, eps_rel: float = 1e-8):
+    """SVD(A^T A) = P Lambda P^T, T = (P Lambda^1/2)^T, with Lambda + eps I
+    before the square roots, eps = eps_rel * lambda_max (reading Q27).
+    A = X_m S_m^-1 (f64 of the f32 smoothed activations).  Returns (T, T^-1, lambda)."""
+    A = np.asarray(A, F64)
+    lam, P = np.linalg.eigh(A.T @ A)
+    lam = np.maximum(lam, 0.0)
+    lam_r = lam + eps_rel * lam.max()
+    T = (P * np.sqrt(lam_r)[None, :]).T
+    T_inv = P / np.sqrt(lam_r)[None, :]
+    return T, T_inv, lam
+
+
+def cmc_factors(A, dW, r: int, eps_rel: float = 1e-8):
+    """PAPER.md:143-149 (eq:l1l2): SVD(T dW) = U Sigma V^T ~ U_r Sigma_r V_r^T,
+    L1 = T^-1 U_r [d x r], L2 = Sigma_r V_r^T [r x n]; r = 0 -> empty factors."""
+    T, T_inv, _ = whitening_transform(A, eps_rel)
+    d, n = dW.shape
+    if r == 0:
+        return np.zeros((d, 0)), np.zeros((0, n))
+    U, sig, Vt = np.linalg.svd(T @ dW, full_matrices=False)
+    return T_inv @ U[:, :r], sig[:r, None] * Vt[:r]
+
+
+def reconstruction_loss(A, dW, L1, L2) -> float:
+    """Theorem 2 objective ||A (dW - L1 L2)||_F^2 in f64."""
+    A = np.asarray(A, F64)
+    return float(np.sum((A @ (dW - L1 @ L2)) ** 2))
+
+
+def naive_svd_factors(dW, r: int):
+    """Plain truncated SVD of dW without whitening ("directly applying SVD fails")."""
+    U, sig, Vt = np.linalg.svd(dW, full_matrices=False)
+    return U[:, :r] * sig[None, :r], Vt[:r]
+
+
+def effective_rank(M) -> float:
+    """exp(-sum p_i ln p_i), p_i = sigma_i / sum sigma (fig:effective_rank)."""
+    sig = np.linalg.svd(np.asarray(M, F64), compute_uv=False)
+    p = sig / sig.sum()
+    p = p[p > 0]
+    return float(np.exp(-(p * np.log(p)).sum()))
+
+
+def cmc_layer_factors(X, ids, s, W, wbits: int, r: int, eps_rel: float = 1e-8):
+    """N2 end to end for one linear: for every non-text modality m present, A_m = X_m S_m^-1
+    (f32 as the path computes it), dW_m = S_m W - Q(S_t W) with the text-smoothed base weight
+    (PAPER.md:128-131), and (L1^m, L2^m) = cmc_factors(A_m, dW_m, r).
+    Returns lists over m = 1..M-1 (None for an absent modality) and the residual losses."""
+    s = np.asarray(s, F32)
+    n_mod = s.shape[0]
+    ids = _check_ids(ids, n_mod)
+    xs = smooth_activations(decode(X), ids, s)
+    qw_t, dw_t = quantize_weight(W, s[0], wbits)
+    L1s, L2s, losses = [], [], []
+    for m in range(1, n_mod):
+        sel = ids == m
+        if not sel.any():
+            L1s.append(None), L2s.append(None), losses.append(None)
+            continue
+        A = xs[sel].astype(F64)
+        dW = weight_residual(W, s[m], qw_t, dw_t)
+        L1, L2 = cmc_factors(A, dW, r, eps_rel)
+        L1s.append(L1), L2s.append(L2), losses.append(reconstruction_loss(A, dW, L1, L2))
+    return L1s, L2s, losses

@@ -523,3 +523,99 @@ def test_meanabs_and_awq_grid():
     b, losses = O.awq_grid_search(c["X"], c["ids"], c["W"], 4, 8, betas, 2)
     l1 = O.calib_loss(c["X"], c["ids"], np.ones((2, Xf.shape[1]), np.float32), c["W"], 4, 8)[2]
     assert losses[0] == l1 and b == betas[int(np.argmin(losses))]
+
+
+# ----------------------------------------------------------------------------- N2 CMC factors
+def _aniso(g, T, d, cond=1e3):
+    """Activations with an anisotropic covariance (condition number ~cond^2)."""
+    Q, _ = np.linalg.qr(g.normal(size=(d, d)))
+    return g.normal(size=(T, d)) @ (np.logspace(0, np.log10(cond), d)[:, None] * Q.T)
+
+
+def test_weight_residual_spec_examples():
+    """s_m == s_t with a lossless Q -> 0; s_m = 2 s_t -> diag(s_t) W; a random
+    case equals direct recomputation."""
+    g = np.random.Generator(np.random.PCG64(31))
+    d, n = 16, 32
+    codes = g.integers(-7, 8, (d, n))
+    codes[0] = 7                                               # every column's max |code| = 7
+    W = synth.f32_to_bf16_bits((codes * np.float32(0.125)).astype(np.float32))   # exact grid values
+    st = np.ones(d, np.float32)
+    qw, dw = O.quantize_weight(W, st, 4)
+    assert np.array_equal(O.weight_residual(W, st, qw, dw), np.zeros((d, n)))
+    assert np.array_equal(O.weight_residual(W, 2 * st, qw, dw), O.decode(W).astype(np.float64))
+    s = np.exp(g.normal(0, 0.5, d)).astype(np.float32)
+    Wr = synth.f32_to_bf16_bits(g.normal(0, 1, (d, n)).astype(np.float32))
+    qw, dw = O.quantize_weight(Wr, st * np.float32(1.5), 4)
+    ref = np.array([[float(s[i]) * float(O.decode(Wr)[i, j]) - float(dw[j]) * int(qw[j, i]) for j in range(n)]
+                    for i in range(d)])
+    assert np.array_equal(O.weight_residual(Wr, s, qw, dw), ref)
+
+
+def test_whitening_transform():
+    """SPEC.md:385-388: Gram = I -> T orthogonal; scaled orthonormal rows -> whitened Gram = I;
+    random full rank (eps = 0): ||(A T^-1)^T (A T^-1) - I||_max <= 1e-8; T T^-1 = I."""
+    g = np.random.Generator(np.random.PCG64(32))
+    Q, _ = np.linalg.qr(g.normal(size=(40, 12)))
+    T, Ti, _ = O.whitening_transform(Q, 0.0)
+    assert np.abs(T.T @ T - np.eye(12)).max() <= 1e-10
+    T, Ti, _ = O.whitening_transform(3.0 * Q, 0.0)
+    assert np.abs((3 * Q @ Ti).T @ (3 * Q @ Ti) - np.eye(12)).max() <= 1e-8
+    A = _aniso(g, 200, 24)
+    T, Ti, _ = O.whitening_transform(A, 0.0)
+    assert np.abs((A @ Ti).T @ (A @ Ti) - np.eye(24)).max() <= 1e-8
+    assert np.abs(T @ Ti - np.eye(24)).max() <= 1e-8
+
+
+def test_cmc_factors_theorem2():
+    """Theorem 2 (PAPER.md:147-165; SPEC.md:389-417): loss(L1 L2) = tail energy sum_{i>r}
+    sigma_i^2 of SVD(A dW) (eps = 0); <= the naive SVD's loss and every perturbed / random rank-r
+    candidate; full rank recovers dW; dW = 0 -> 0; monotone in r; and an independent whitening
+    route (Cholesky factor instead of the eigendecomposition) gives the same L1 L2."""
+    g = np.random.Generator(np.random.PCG64(33))
+    T_, d, n, r = 300, 20, 28, 4
+    A = _aniso(g, T_, d)
+    dW = g.normal(size=(d, n))
+    L1, L2 = O.cmc_factors(A, dW, r, 0.0)
+    loss = O.reconstruction_loss(A, dW, L1, L2)
+    tail = np.sum(np.linalg.svd(A @ dW, compute_uv=False)[r:] ** 2)
+    assert abs(loss - tail) <= 1e-8 * tail
+    n1, n2 = O.naive_svd_factors(dW, r)
+    assert loss <= O.reconstruction_loss(A, dW, n1, n2)
+    for k in range(200):
+        e1, e2 = g.normal(size=L1.shape), g.normal(size=L2.shape)
+        sc = 1e-3 if k < 100 else 1.0
+        c1 = L1 + sc * e1 * np.abs(L1).max() if k < 100 else e1
+        c2 = L2 + sc * e2 * np.abs(L2).max() if k < 100 else e2
+        assert loss <= O.reconstruction_loss(A, dW, c1, c2)
+    F1, F2 = O.cmc_factors(A, dW, d, 0.0)
+    assert np.abs(F1 @ F2 - dW).max() <= 1e-8 * np.abs(dW).max()
+    Z1, Z2 = O.cmc_factors(A, np.zeros((d, n)), r, 0.0)
+    assert np.abs(Z1 @ Z2).max() == 0.0
+    losses = [O.reconstruction_loss(A, dW, *O.cmc_factors(A, dW, k, 0.0)) for k in range(0, d + 1, 4)]
+    assert all(a >= b * (1 - 1e-12) for a, b in zip(losses, losses[1:]))
+    Lc = np.linalg.cholesky(A.T @ A)                   # A^T A = Lc Lc^T -> T' = Lc^T
+    U, sig, Vt = np.linalg.svd(Lc.T @ dW, full_matrices=False)
+    Lstar = np.linalg.solve(Lc.T, U[:, :r]) @ (sig[:r, None] * Vt[:r])
+    assert np.abs(Lstar - L1 @ L2).max() <= 1e-8 * np.abs(Lstar).max()
+
+
+def test_cmc_isotropic_and_effective_rank():
+    """isotropic activations -> whitened and naive losses agree; fig:effective_rank
+    (SPEC.md:418): on anisotropic activations T dW has a lower effective rank than dW in >= 9 of
+    10 seeded trials (dW = a residual with correlated structure)."""
+    g = np.random.Generator(np.random.PCG64(34))
+    Q, _ = np.linalg.qr(g.normal(size=(64, 16)))
+    A = 2.0 * Q
+    dW = g.normal(size=(16, 20))
+    a = O.reconstruction_loss(A, dW, *O.cmc_factors(A, dW, 3, 0.0))
+    b = O.reconstruction_loss(A, dW, *O.naive_svd_factors(dW, 3))
+    assert abs(a - b) <= 1e-6 * b
+    wins = 0
+    for t in range(10):
+        gg = np.random.Generator(np.random.PCG64(100 + t))
+        A = _aniso(gg, 200, 24, cond=1e2)
+        dW = gg.normal(size=(24, 32))
+        T, _, _ = O.whitening_transform(A, 0.0)
+        wins += O.effective_rank(T @ dW) <= O.effective_rank(dW)
+    assert wins >= 9
