@@ -71,7 +71,7 @@ typedef void* masq_stream;      /* cudaStream_t */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
   MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,
-  MASQ_OP_MEANABS = 8
+  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -223,6 +223,28 @@ masq_status masq_adam_init(const float* s, double* theta, double* m1, double* m2
  * pointers; stream-ordered, no host sync. */
 masq_status masq_keep_best(const double* loss, double* best_loss, const float* s, float* s_best,
                            int64_t count, int32_t* improved, masq_stream stream);
+
+/* ---------------------------------------------------------------- N2: CMC factor construction
+ * (PAPER.md:126-160 eq:l1l2, Theorem 2).
+ * For every non-text modality m = 1..n_mod-1, with A_m = X_m S_m^-1 (f32 smoothing as the path
+ * computes it) and dW_m = S_m W - Q(S_t W) (qw_text [d_out x d] int8 / dw_text [d_out] f32 are
+ * the text-smoothed base weight from masq_quantize_weight(s[0])):
+ *   eig(A_m^T A_m) = P Lambda P^T, T = (P (Lambda + eps_rel*lambda_max)^1/2)^T   (reading Q27)
+ *   SVD(T dW_m) ~ U_r Sigma_r V_r^T,  L1^m = T^-1 U_r [d x r],  L2^m = Sigma_r V_r^T [r x d_out]
+ * in f64 (cuBLAS GEMM/SYRK and the cuSOLVER symmetric eigensolver, loaded on first use; no
+ * linear-algebra libraries -> MASQ_ERR_UNSUPPORTED).  Outputs in the layout masq_linear_forward
+ * consumes: L1 [(n_mod-1) x d x r], L2 [(n_mod-1) x r x d_out], dtype lt (MASQ_F32 / MASQ_BF16),
+ * columns of L1 / rows of L2 in descending singular-value order.  resid (optional, device f64
+ * [n_mod-1]) = ||A_m (dW_m - L1 L2)||_F^2 (Theorem 2's objective).  A modality with no tokens
+ * gets zero factors.  1 <= r <= min(d, d_out).  One-off calibration work: O(d^3) eigensolves
+ * and O(d^2 (T + d_out)) f64 GEMMs per modality; the workspace holds f64 [T x d], 2 x [d x d]
+ * and 2 x [d x d_out] buffers. */
+masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                             int64_t T, int64_t d, int64_t d_out, int32_t n_mod,
+                             const float* s, const void* W, masq_dtype wt,
+                             const int8_t* qw_text, const float* dw_text, int32_t r, double eps_rel,
+                             void* L1, void* L2, masq_dtype lt, double* resid,
+                             void* ws, size_t ws_bytes, masq_stream stream);
 
 /* ---------------------------------------------------------------- N4: baseline factor methods
  * — the closed forms the paper compares MASQuant against, on the same data. */

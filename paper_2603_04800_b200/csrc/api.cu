@@ -22,6 +22,26 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     case MASQ_OP_STATS:
     case MASQ_OP_INIT:
       break;
+    case MASQ_OP_CMC: {
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      L.a64 = take(sizeof(double) * (size_t)T * d);
+      L.g = take(sizeof(double) * (size_t)d * d);
+      L.c = take(sizeof(double) * (size_t)d * d);
+      L.lam = take(sizeof(double) * d);
+      L.sig2 = take(sizeof(double) * d);
+      L.sq = take(sizeof(double) * d);
+      L.isq = take(sizeof(double) * d);
+      L.dw64 = take(sizeof(double) * (size_t)d * n);
+      L.m64 = take(sizeof(double) * (size_t)d * n);
+      L.l1t64 = take(sizeof(double) * (size_t)d * r);
+      L.urs = take(sizeof(double) * (size_t)d * r);
+      L.l2t64 = take(sizeof(double) * (size_t)r * n);
+      L.lwork = cmc_syevd_lwork(d);
+      L.work = take(sizeof(double) * (L.lwork + 1));
+      L.info = take(sizeof(int) * 2);
+      L.dot = take(sizeof(double) * cmc_dot_blocks());
+      break;
+    }
     case MASQ_OP_MEANABS:
       L.partials = take(sizeof(float) * (size_t)meanabs_slabs(T) * n_mod * d);
       break;
@@ -459,6 +479,70 @@ masq_status masq_keep_best(const double* loss, double* best_loss, const float* s
   if (!loss || !best_loss || !s || !s_best) return MASQ_ERR_NULL;
   if (count < 0) return MASQ_ERR_SHAPE;
   MASQ_CK(launch_keep_best(loss, best_loss, s, s_best, count, improved, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                             int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
+                             const int8_t* qw_text, const float* dw_text, int32_t r, double eps_rel, void* L1,
+                             void* L2, masq_dtype lt, double* resid, void* ws, size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  if (n_mod < 2) return MASQ_ERR_SHAPE;
+  if (d_out <= 0 || r < 1 || r > d || r > d_out || !(eps_rel >= 0.0)) return MASQ_ERR_SHAPE;
+  if (d > 2147483647 / 8 || d_out > 2147483647 / 8 || T > 2147483647) return MASQ_ERR_SHAPE;
+  if (!s || !W || !qw_text || !dw_text || !L1 || !L2) return MASQ_ERR_NULL;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (lt != MASQ_BF16 && lt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (T > 0) {
+    MASQ_TRY(check_x(X, xt, ld_x, d));
+    if (!mod_id) return MASQ_ERR_NULL;
+  }
+  if (!cmc_linalg_available()) return MASQ_ERR_UNSUPPORTED;
+  const WsLayout L = ws_layout(MASQ_OP_CMC, T, d, d_out, n_mod, r);
+  if (L.lwork == 0) return MASQ_ERR_UNSUPPORTED;
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  CmcArgs a{};
+  a.X = X;
+  a.xt = xt;
+  a.ld_x = ld_x;
+  a.ids = mod_id;
+  a.T = T;
+  a.d = d;
+  a.n = d_out;
+  a.n_mod = n_mod;
+  a.r = r;
+  a.inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  a.s = s;
+  a.W = W;
+  a.wt = wt;
+  a.qw_t = qw_text;
+  a.dw_t = dw_text;
+  a.eps_rel = eps_rel;
+  a.L1 = L1;
+  a.L2 = L2;
+  a.lt = lt;
+  a.resid = resid;
+  a.A64 = reinterpret_cast<double*>(W8(ws, L.a64));
+  a.G = reinterpret_cast<double*>(W8(ws, L.g));
+  a.C = reinterpret_cast<double*>(W8(ws, L.c));
+  a.lam = reinterpret_cast<double*>(W8(ws, L.lam));
+  a.sig2 = reinterpret_cast<double*>(W8(ws, L.sig2));
+  a.sq = reinterpret_cast<double*>(W8(ws, L.sq));
+  a.isq = reinterpret_cast<double*>(W8(ws, L.isq));
+  a.dW = reinterpret_cast<double*>(W8(ws, L.dw64));
+  a.Mb = reinterpret_cast<double*>(W8(ws, L.m64));
+  a.L1t = reinterpret_cast<double*>(W8(ws, L.l1t64));
+  a.Urs = reinterpret_cast<double*>(W8(ws, L.urs));
+  a.L2t = reinterpret_cast<double*>(W8(ws, L.l2t64));
+  a.work = reinterpret_cast<double*>(W8(ws, L.work));
+  a.info = reinterpret_cast<int*>(W8(ws, L.info));
+  a.dot = reinterpret_cast<double*>(W8(ws, L.dot));
+  a.lwork = L.lwork;
+  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, const_cast<float*>(a.inv), st));
+  const cudaError_t e = launch_cmc_factors(a, st);
+  if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
+  MASQ_CK(e);
   return MASQ_OK;
 }
 

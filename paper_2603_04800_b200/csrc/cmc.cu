@@ -1,0 +1,305 @@
+// cmc.cu — N2: construction of the CMC factors L1^m, L2^m on the GPU
+// (eq:l1l2).
+//
+// For every non-text modality m, in f64 throughout the decomposition:
+//   A_m = X_m S_m^-1 (the f32 smoothed activations the path computes, other tokens zeroed)
+//   G = A_m^T A_m (cuBLAS Dsyrk)             -> eig G = P Lambda P^T (cuSOLVER Dsyevd)
+//   Lambda' = max(Lambda, 0) + eps_rel * lambda_max (reading Q27)
+//   dW = S_m W - Q(S_t W) (exact in f64, this file's kernel, from the text codes and scales)
+//   M = T dW = diag(sqrt Lambda') P^T dW      (Dgemm + row scaling)
+//   C = M M^T (Dsyrk) -> eig: the top-r eigenvectors are the left singular vectors U_r of M and
+//   the eigenvalues its squared singular values (only the leading r are needed)
+//   L2 = U_r^T M = Sigma_r V_r^T,  L1 = T^-1 U_r = P diag(1/sqrt Lambda') U_r
+//   resid (optional) = ||A_m (dW - L1 L2)||_F^2 = <E, G E>, E = dW - L1 L2 (Dsymm + reduction).
+// cuBLAS / cuSOLVER are plain library linear algebra here (GEMM, SYRK, symmetric eigensolver);
+// they are loaded with dlopen on first use so that libmasq.so itself has no link dependency on
+// them (a box without them fails this call with MASQ_ERR_UNSUPPORTED, nothing else).
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <cuda_bf16.h>
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include "internal.h"
+
+namespace masq {
+namespace {
+
+struct LinAlg {
+  bool tried = false, ok = false;
+  decltype(&cublasCreate_v2) create = nullptr;
+  decltype(&cublasSetStream_v2) set_stream = nullptr;
+  decltype(&cublasDgemm_v2) dgemm = nullptr;
+  decltype(&cublasDsyrk_v2) dsyrk = nullptr;
+  decltype(&cublasDsymm_v2) dsymm = nullptr;
+  decltype(&cusolverDnCreate) sv_create = nullptr;
+  decltype(&cusolverDnSetStream) sv_set_stream = nullptr;
+  decltype(&cusolverDnDsyevd_bufferSize) syevd_size = nullptr;
+  decltype(&cusolverDnDsyevd) syevd = nullptr;
+  cublasHandle_t hb[64] = {};
+  cusolverDnHandle_t hs[64] = {};
+};
+
+std::mutex g_la_mu;
+LinAlg g_la;
+
+void* open_first(const char* const* names) {
+  for (int i = 0; names[i]; ++i)
+    if (void* h = dlopen(names[i], RTLD_NOW | RTLD_GLOBAL)) return h;
+  return nullptr;
+}
+
+// returns the loaded table with this device's handles bound to st, or nullptr
+LinAlg* linalg(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_la_mu);
+  LinAlg& L = g_la;
+  if (!L.tried) {
+    L.tried = true;
+    static const char* const kBlas[] = {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12",
+                                        nullptr};
+    static const char* const kSolver[] = {"libcusolver.so.11", "libcusolver.so",
+                                          "/usr/local/cuda/lib64/libcusolver.so.11", nullptr};
+    void* hb = open_first(kBlas);
+    void* hs = open_first(kSolver);
+    if (hb && hs) {
+      L.create = reinterpret_cast<decltype(L.create)>(dlsym(hb, "cublasCreate_v2"));
+      L.set_stream = reinterpret_cast<decltype(L.set_stream)>(dlsym(hb, "cublasSetStream_v2"));
+      L.dgemm = reinterpret_cast<decltype(L.dgemm)>(dlsym(hb, "cublasDgemm_v2"));
+      L.dsyrk = reinterpret_cast<decltype(L.dsyrk)>(dlsym(hb, "cublasDsyrk_v2"));
+      L.dsymm = reinterpret_cast<decltype(L.dsymm)>(dlsym(hb, "cublasDsymm_v2"));
+      L.sv_create = reinterpret_cast<decltype(L.sv_create)>(dlsym(hs, "cusolverDnCreate"));
+      L.sv_set_stream = reinterpret_cast<decltype(L.sv_set_stream)>(dlsym(hs, "cusolverDnSetStream"));
+      L.syevd_size = reinterpret_cast<decltype(L.syevd_size)>(dlsym(hs, "cusolverDnDsyevd_bufferSize"));
+      L.syevd = reinterpret_cast<decltype(L.syevd)>(dlsym(hs, "cusolverDnDsyevd"));
+      L.ok = L.create && L.set_stream && L.dgemm && L.dsyrk && L.dsymm && L.sv_create && L.sv_set_stream &&
+             L.syevd_size && L.syevd;
+    }
+  }
+  if (!L.ok) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!L.hb[dev] && L.create(&L.hb[dev]) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  if (!L.hs[dev] && L.sv_create(&L.hs[dev]) != CUSOLVER_STATUS_SUCCESS) return nullptr;
+  if (L.set_stream(L.hb[dev], st) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  if (L.sv_set_stream(L.hs[dev], st) != CUSOLVER_STATUS_SUCCESS) return nullptr;
+  return &L;
+}
+
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// A64 [T x d] row-major (= column-major d x T): xs of modality m, zeros elsewhere
+template <typename XT>
+__global__ void xs64_kernel(const XT* __restrict__ X, int64_t ld_x, const uint8_t* __restrict__ ids, int64_t T,
+                            int64_t d, int m, const float* __restrict__ inv, double* __restrict__ A) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * d) return;
+  const int64_t t = idx / d, i = idx - t * d;
+  double v = 0.0;
+  if (ids[t] == m) {
+    const float x = (float)X[t * ld_x + i];
+    v = (double)__fmul_rn(x, inv[(int64_t)m * d + i]);
+  }
+  A[idx] = v;
+}
+
+// dW column-major [d x n]: dW(i, j) = s_i w_ij - dw_j code_ji   (32 x 32 tiles, W transposed via smem)
+template <typename WT>
+__global__ void dw64_kernel(const WT* __restrict__ W, const float* __restrict__ s, const int8_t* __restrict__ qw,
+                            const float* __restrict__ dw, int64_t d, int64_t n, double* __restrict__ out) {
+  __shared__ float tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {                 // load W[i0 + r][j0 + tx]
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < d && j < n) ? (float)W[i * n + j] : 0.f;
+  }
+  __syncthreads();
+  for (int c = threadIdx.y; c < 32; c += 8) {                 // write column j0 + c, rows i0 + tx
+    const int64_t i = i0 + threadIdx.x, j = j0 + c;
+    if (i < d && j < n)
+      out[j * d + i] = (double)s[i] * (double)tile[threadIdx.x][c] - (double)dw[j] * (double)qw[j * d + i];
+  }
+}
+
+// sq[k] = sqrt(Lambda'_k), isq[k] = 1/sq[k] (0 when Lambda' is 0: an all-zero A)
+__global__ void whiten_kernel(const double* __restrict__ lam, int64_t d, double eps_rel, double* __restrict__ sq,
+                              double* __restrict__ isq) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d) return;
+  const double lmax = fmax(lam[d - 1], 0.0);
+  const double l = fmax(lam[k], 0.0) + eps_rel * lmax;
+  const double q = sqrt(l);
+  sq[k] = q;
+  isq[k] = q > 0.0 ? 1.0 / q : 0.0;
+}
+
+// column-major [rows x cols]: row k scaled by f[k]
+__global__ void scale_rows_kernel(const double* in, int64_t rows, int64_t cols, const double* __restrict__ f,
+                                  double* out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  out[idx] = in[idx] * f[idx % rows];
+}
+
+template <typename OT>
+__device__ __forceinline__ OT cvt_out(double v);
+template <>
+__device__ __forceinline__ float cvt_out<float>(double v) { return (float)v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(double v) { return __float2bfloat16_rn((float)v); }
+
+// L1 out [d x r] row-major from L1t column-major [d x r] (column k = ascending eigen order, so
+// output column c takes k = r - 1 - c: descending singular values); L2 out [r x n] row-major
+// from L2t column-major [r x n] with the same row reversal.
+template <typename OT>
+__global__ void out_factors_kernel(const double* __restrict__ L1t, const double* __restrict__ L2t, int64_t d,
+                                   int64_t n, int r, OT* __restrict__ L1, OT* __restrict__ L2) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = d * r, n2 = (int64_t)r * n;
+  if (idx < n1) {
+    const int64_t i = idx / r;
+    const int c = (int)(idx - i * r);
+    L1[idx] = cvt_out<OT>(L1t[(int64_t)(r - 1 - c) * d + i]);
+  } else if (idx < n1 + n2) {
+    const int64_t e = idx - n1;
+    const int c = (int)(e / n);
+    const int64_t j = e - (int64_t)c * n;
+    L2[e] = cvt_out<OT>(L2t[j * r + (r - 1 - c)]);
+  }
+}
+
+// sum_k a_k b_k, two stages, fixed order (deterministic)
+__global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t count,
+                                   double* __restrict__ part) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * 256 + threadIdx.x; k < count; k += (int64_t)gridDim.x * 256)
+    acc += a[k] * b[k];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void dot_final_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0.0;
+    for (int k = 0; k < nb; ++k) a += part[k];
+    *out = a;
+  }
+}
+constexpr int kDotBlocks = 592;
+
+}  // namespace
+
+bool cmc_linalg_available() { return linalg(0) != nullptr; }
+
+size_t cmc_syevd_lwork(int64_t d) {
+  LinAlg* L = linalg(0);
+  if (!L || d <= 0) return 0;
+  int lw = 0;
+  if (L->syevd_size(L->hs[cur_dev()], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d,
+                    nullptr, &lw) != CUSOLVER_STATUS_SUCCESS)
+    return 0;
+  return (size_t)lw;
+}
+
+cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st) {
+  LinAlg* L = linalg(st);
+  if (!L) return cudaErrorNotSupported;
+  const int dev = cur_dev();
+  cublasHandle_t hb = L->hb[dev];
+  cusolverDnHandle_t hs = L->hs[dev];
+  const int64_t T = a.T, d = a.d, n = a.n;
+  const int r = a.r;
+  const int di = (int)d, ni = (int)n, Ti = (int)T;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+#define CK_B(x) do { if ((x) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
+#define CK_S(x) do { if ((x) != CUSOLVER_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
+  for (int m = 1; m < a.n_mod; ++m) {
+    // A_m and its Gram matrix
+    {
+      ProfScope ps_("cmc_xs64", st);
+      const unsigned g = (unsigned)ceil_div(T * d, 256);
+      if (a.xt == MASQ_BF16)
+        xs64_kernel<<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.X), a.ld_x, a.ids, T, d, m, a.inv, a.A64);
+      else
+        xs64_kernel<<<g, 256, 0, st>>>(static_cast<const float*>(a.X), a.ld_x, a.ids, T, d, m, a.inv, a.A64);
+    }
+    {
+      ProfScope ps_("cmc_gram", st);
+      CK_B(L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, Ti, &one, a.A64, di, &zero, a.G, di));
+    }
+    {
+      ProfScope ps_("cmc_eig_gram", st);
+      CK_S(L->syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, di, a.G, di, a.lam, a.work, (int)a.lwork,
+                    a.info));
+    }
+    whiten_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(a.lam, d, a.eps_rel, a.sq, a.isq);
+    // dW and M = diag(sqrt Lambda') P^T dW
+    {
+      ProfScope ps_("cmc_dw", st);
+      dim3 grid((unsigned)ceil_div(d, 32), (unsigned)ceil_div(n, 32)), block(32, 8);
+      const float* sm = a.s + (int64_t)m * d;
+      if (a.wt == MASQ_BF16)
+        dw64_kernel<<<grid, block, 0, st>>>(static_cast<const __nv_bfloat16*>(a.W), sm, a.qw_t, a.dw_t, d, n, a.dW);
+      else
+        dw64_kernel<<<grid, block, 0, st>>>(static_cast<const float*>(a.W), sm, a.qw_t, a.dw_t, d, n, a.dW);
+    }
+    {
+      ProfScope ps_("cmc_whiten_gemm", st);
+      CK_B(L->dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, di, ni, di, &one, a.G, di, a.dW, di, &zero, a.Mb, di));
+    }
+    scale_rows_kernel<<<(unsigned)ceil_div(d * n, 256), 256, 0, st>>>(a.Mb, d, n, a.sq, a.Mb);
+    // top-r left singular vectors of M from eig(M M^T)
+    {
+      ProfScope ps_("cmc_mmt", st);
+      CK_B(L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, ni, &one, a.Mb, di, &zero, a.C, di));
+    }
+    {
+      ProfScope ps_("cmc_eig_mmt", st);
+      CK_S(L->syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, di, a.C, di, a.sig2, a.work, (int)a.lwork,
+                    a.info + 1));
+    }
+    const double* Ur = a.C + (int64_t)(d - r) * d;            // columns d-r .. d-1 (ascending)
+    {
+      ProfScope ps_("cmc_factors_gemm", st);
+      CK_B(L->dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, r, ni, di, &one, Ur, di, a.Mb, di, &zero, a.L2t, r));
+      scale_rows_kernel<<<(unsigned)ceil_div(d * r, 256), 256, 0, st>>>(Ur, d, r, a.isq, a.Urs);
+      CK_B(L->dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, di, r, di, &one, a.G, di, a.Urs, di, &zero, a.L1t, di));
+    }
+    {
+      const int64_t cnt = d * r + (int64_t)r * n;
+      const unsigned g = (unsigned)ceil_div(cnt, 256);
+      if (a.lt == MASQ_BF16)
+        out_factors_kernel<<<g, 256, 0, st>>>(a.L1t, a.L2t, d, n, r,
+                                              static_cast<__nv_bfloat16*>(a.L1) + (int64_t)(m - 1) * d * r,
+                                              static_cast<__nv_bfloat16*>(a.L2) + (int64_t)(m - 1) * r * n);
+      else
+        out_factors_kernel<<<g, 256, 0, st>>>(a.L1t, a.L2t, d, n, r, static_cast<float*>(a.L1) + (int64_t)(m - 1) * d * r,
+                                              static_cast<float*>(a.L2) + (int64_t)(m - 1) * r * n);
+    }
+    if (a.resid) {
+      // E = dW - L1t L2t (in place), G again (the eigensolver overwrote it), F = G E, <E, F>
+      ProfScope ps_("cmc_resid", st);
+      CK_B(L->dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, di, ni, r, &mone, a.L1t, di, a.L2t, r, &one, a.dW, di));
+      CK_B(L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, Ti, &one, a.A64, di, &zero, a.C, di));
+      CK_B(L->dsymm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, di, ni, &one, a.C, di, a.dW, di, &zero, a.Mb, di));
+      dot_partial_kernel<<<kDotBlocks, 256, 0, st>>>(a.dW, a.Mb, d * n, a.dot);
+      dot_final_kernel<<<1, 32, 0, st>>>(a.dot, kDotBlocks, a.resid + (m - 1));
+    }
+  }
+#undef CK_B
+#undef CK_S
+  return cudaGetLastError();
+}
+
+int cmc_dot_blocks() { return kDotBlocks; }
+
+}  // namespace masq

@@ -30,6 +30,10 @@ struct WsLayout {
   size_t gsign = 0, planes = 0, gpartial = 0;
   // N1 scale terms
   size_t codes16 = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0;
+  // N2 CMC factors (f64)
+  size_t a64 = 0, g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
+         work = 0, info = 0, dot = 0;
+  size_t lwork = 0;   // doubles
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -158,6 +162,34 @@ cudaError_t launch_keep_best(const double* loss, double* best, const float* s, f
 cudaError_t launch_adam(double* theta, const double* grad, double* m1, double* m2, int64_t count, int step, double lr,
                         double b1, double b2, double eps, float* s_out, cudaStream_t st);
 int num_sms();
+
+// ---------------------------------------------------------------- N2 CMC factors (cmc.cu)
+struct CmcArgs {
+  const void* X;
+  masq_dtype xt;
+  int64_t ld_x;
+  const uint8_t* ids;
+  int64_t T, d, n;
+  int n_mod, r;
+  const float* inv;              // [M][d] f32 reciprocals of s
+  const float* s;                // [M][d]
+  const void* W;
+  masq_dtype wt;
+  const int8_t* qw_t;            // text codes [n x d]
+  const float* dw_t;             // text scales [n]
+  double eps_rel;
+  void* L1;                      // [(M-1) x d x r]
+  void* L2;                      // [(M-1) x r x n]
+  masq_dtype lt;
+  double* resid;                 // optional [(M-1)]
+  double *A64, *G, *C, *lam, *sig2, *sq, *isq, *dW, *Mb, *L1t, *Urs, *L2t, *work, *dot;
+  int* info;
+  size_t lwork;
+};
+bool cmc_linalg_available();
+size_t cmc_syevd_lwork(int64_t d);
+int cmc_dot_blocks();
+cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- N4 baselines (baseline.cu)
 int meanabs_slabs(int64_t T);

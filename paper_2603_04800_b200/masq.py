@@ -12,7 +12,8 @@ import torch
 from ._lib import MasqDebug, lib
 
 MASQ_F32, MASQ_BF16 = 0, 1
-OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS = range(9)
+(OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS,
+ OP_CMC) = range(10)
 
 
 class MasqError(RuntimeError):
@@ -264,6 +265,26 @@ def keep_best(loss, best_loss, s, s_best, improved=None, stream=None):
     """Best-so-far on the device: s_best <- s and best_loss <- loss when loss < best_loss."""
     _ck(lib().masq_keep_best(_p(loss), _p(best_loss), _p(s), _p(s_best), s.numel(), _p(improved),
                              _stream(stream)), "masq_keep_best")
+
+
+# ----------------------------------------------------------------------------- N2
+def cmc_factors(X, mod_id, s, W, qw_text, dw_text, r: int, eps_rel: float = 1e-8, dtype=torch.bfloat16,
+                with_resid: bool = True, ws=None, stream=None):
+    """(L1 [M-1, d, r], L2 [M-1, r, n], resid f64 [M-1] or None): whitened truncated-SVD CMC
+    factors for every non-text modality."""
+    T, d = X.shape
+    n = W.shape[1]
+    n_mod = s.shape[0]
+    dev = X.device
+    L1 = torch.empty(n_mod - 1, d, r, dtype=dtype, device=dev)
+    L2 = torch.empty(n_mod - 1, r, n, dtype=dtype, device=dev)
+    resid = torch.empty(n_mod - 1, dtype=torch.float64, device=dev) if with_resid else None
+    ws = ws or default_workspace(dev)
+    p, nb = ws.ptr_size(workspace_size(OP_CMC, T, d, n, n_mod, r))
+    _ck(lib().masq_cmc_factors(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, n, n_mod, _p(s.contiguous()),
+                               _p(W.contiguous()), _dt(W), _p(qw_text), _p(dw_text), r, float(eps_rel), _p(L1), _p(L2),
+                               _dt(L1), _p(resid), p, nb, _stream(stream)), "masq_cmc_factors")
+    return L1, L2, resid
 
 
 # ----------------------------------------------------------------------------- N4
