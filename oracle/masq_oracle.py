@@ -506,3 +506,51 @@ def cmc_layer_factors(X, ids, s, W, wbits: int, r: int, eps_rel: float = 1e-8):
         L1, L2 = cmc_factors(A, dW, r, eps_rel)
         L1s.append(L1), L2s.append(L2), losses.append(reconstruction_loss(A, dW, L1, L2))
     return L1s, L2s, losses
+
+
+# --------------------------------------------------------------------------- N3 int4 groups
+def quantize_weight_grouped(W, s, wbits: int, group: int):
+    """N3 — Q(S W) with sub-channel groups: per output channel j and group g of `group`
+    consecutive input channels, Delta_jg = max(div(max_{i in g} |ws_ij|, q_max), 1e-12f) and
+    codes = clamp(rha(div(ws, Delta_jg))) — the O3 quantizer at group
+    granularity (reading Q28: SURVEY §8(f) N3's g = 128).  d % group == 0.
+    Returns (codes int8 [n x d] K-major, Delta f32 [n x d/group])."""
+    Wf = decode(W)
+    s = np.asarray(s, F32)
+    d, n = Wf.shape
+    if d % group:
+        raise ValueError("d must be a multiple of the group size")
+    ws = np.multiply(s[:, None], Wf, dtype=F32).T                 # [n x d]
+    codes, delta = quantize_rows(np.ascontiguousarray(ws.reshape(n * (d // group), group)), wbits)
+    return codes.reshape(n, d), delta.reshape(n, d // group)
+
+
+def pack_int4(codes) -> np.ndarray:
+    """Two's-complement nibbles, two per byte along K: byte k holds code 2k in the low nibble and
+    code 2k+1 in the high nibble (reading Q28).  codes in [-8, 7], [n x d] -> uint8 [n x d/2]."""
+    c = np.asarray(codes, np.int16) & 0xF
+    return (c[:, 0::2] | (c[:, 1::2] << 4)).astype(np.uint8)
+
+
+def unpack_int4(packed) -> np.ndarray:
+    """Inverse of pack_int4 (sign-extends every nibble)."""
+    p = np.asarray(packed, np.uint8).astype(np.int16)
+    lo, hi = p & 0xF, p >> 4
+    lo = np.where(lo >= 8, lo - 16, lo)
+    hi = np.where(hi >= 8, hi - 16, hi)
+    out = np.empty((p.shape[0], 2 * p.shape[1]), np.int8)
+    out[:, 0::2], out[:, 1::2] = lo, hi
+    return out
+
+
+def linear_decode(X, s_t, codes, delta, abits: int, group: int) -> np.ndarray:
+    """N3 decode-shaped forward for text tokens (the base modality; decoding is
+    CMC-free): Y = Q(X S_t^-1) . Q_g(S_t W) with per-token activation scales and per-(channel,
+    group) weight scales, f64 of the dequantized values.  Returns f64 [T x n]."""
+    Xf = decode(X)
+    inv = np.divide(F32(1.0), np.asarray(s_t, F32), dtype=F32)
+    xs = np.multiply(Xf, inv[None, :], dtype=F32)
+    qx, dx = quantize_rows(xs, abits)
+    n, d = codes.shape
+    What = (np.asarray(codes, F64).reshape(n, d // group, group) * np.asarray(delta, F64)[:, :, None]).reshape(n, d)
+    return dequantize_rows(qx, dx) @ What.T

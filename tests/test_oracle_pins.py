@@ -619,3 +619,53 @@ def test_cmc_isotropic_and_effective_rank():
         T, _, _ = O.whitening_transform(A, 0.0)
         wins += O.effective_rank(T @ dW) <= O.effective_rank(dW)
     assert wins >= 9
+
+
+# ----------------------------------------------------------------------------- N3 int4 groups
+def test_grouped_weight_quantizer_pins():
+    """group = d reduces to the per-output-channel O3 quantizer bit for bit; every code is the
+    nearest grid point of its group's scale (ties away); pack/unpack round trip with the
+    documented nibble order."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    d = c["d"]
+    q1, d1 = O.quantize_weight_grouped(c["W"], s[0], 4, d)
+    q0, d0 = O.quantize_weight(c["W"], s[0], 4)
+    assert np.array_equal(q1, q0) and np.array_equal(d1[:, 0], d0)
+    q, dl = O.quantize_weight_grouped(c["W"], s[0], 4, 16)
+    ws = np.multiply(s[0][:, None], O.decode(c["W"]), dtype=np.float32).T.astype(np.float64)
+    grid = np.arange(-8, 8, dtype=np.float64)
+    scale = np.repeat(dl.astype(np.float64), 16, axis=1)
+    v = ws / scale
+    best = grid[np.argmin(np.abs(v[..., None] - grid) - 1e-9 * np.abs(grid), axis=-1)]   # ties -> away
+    assert np.array_equal(q.astype(np.float64), best)
+    packed = O.pack_int4(q)
+    assert packed.shape == (q.shape[0], d // 2)
+    assert np.array_equal(O.unpack_int4(packed), q)
+    assert O.pack_int4(np.array([[1, -1, -8, 7]], np.int8)).tolist() == [[0xF1, 0x78]]
+
+
+def test_linear_decode_brute_force():
+    """Y = Q(X S^-1) Q_g(S W) against a per-element loop over groups with integer partial sums
+    (the decode kernel's arithmetic order) on a tiny case."""
+    c = synth.config_inputs("c1")
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    c = dict(c, X=c["X"][:8])
+    g = 16
+    q, dl = O.quantize_weight_grouped(c["W"], s[0], 4, g)
+    Y = O.linear_decode(c["X"], s[0], q, dl, 8, g)
+    inv = np.divide(np.float32(1), s[0], dtype=np.float32)
+    qa, da = O.quantize_rows(np.multiply(O.decode(c["X"]), inv, dtype=np.float32), 8)
+    T, d = qa.shape
+    n = q.shape[0]
+    ref = np.zeros((T, n))
+    for t in range(T):
+        for j in range(n):
+            acc = 0.0
+            for gg in range(d // g):
+                sl = slice(gg * g, (gg + 1) * g)
+                acc += float(dl[j, gg]) * int(np.dot(qa[t, sl].astype(np.int64), q[j, sl].astype(np.int64)))
+            ref[t, j] = float(da[t]) * acc
+    assert np.allclose(Y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
