@@ -71,7 +71,7 @@ typedef void* masq_stream;      /* cudaStream_t */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
   MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,
-  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9
+  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9, MASQ_OP_DECODE = 10
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -245,6 +245,28 @@ masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const u
                              const int8_t* qw_text, const float* dw_text, int32_t r, double eps_rel,
                              void* L1, void* L2, masq_dtype lt, double* resid,
                              void* ws, size_t ws_bytes, masq_stream stream);
+
+/* ---------------------------------------------------------------- N3: packed int4 + decode
+ * (SURVEY §8(f)).  W4 with sub-channel groups of 128 input channels (reading Q28): per output
+ * channel j and group g, Delta_jg = max(max_{i in g} |f32(s_i w_ij)| / 7, 1e-12) and codes
+ * rha(ws / Delta_jg) in [-8, 7] (the A3 quantizer at group granularity).  packed: d_out*d/2
+ * bytes in the decode kernel's register order (nibbles hold code + 8; tile (jt, g) = 512
+ * bytes for output channels 8jt..8jt+7 and inputs 128g..128g+127; see csrc/decode.cu);
+ * scales f32 tile-major [d_out/8][d/128][8] (Delta of channel 8jt+c, group g at (jt*(d/128)+g)*8+c).
+ * d % 128 == 0, d_out % 8 == 0, group == 128. */
+masq_status masq_quantize_weight_int4(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t d_out,
+                                      int32_t group, uint8_t* packed, float* scales, masq_stream stream);
+/* codes int8 [d_out x d] (K-major) from the packed format (inspection / tests). */
+masq_status masq_unpack_int4(const uint8_t* packed, int64_t d, int64_t d_out, int32_t group, int8_t* codes,
+                             masq_stream stream);
+/* Decode-shaped W4A8 forward for 1 <= T <= 16 text tokens (text is the base
+ * modality, so decoding carries no CMC): Y[t, j] = Q(x_t S_t^-1) . Q_g(S_t W)_:j, per-token int8
+ * activations (abits), per-(channel, group) weight scales; f32 Y [T x ld_y].  Weight-bandwidth
+ * bound: streams d_out*d/2 bytes of codes + 4*d_out*d/128 bytes of scales once. */
+masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64_t T, int64_t d, int64_t d_out,
+                               const float* s_t, const uint8_t* packed, const float* scales, int32_t group,
+                               int32_t abits, float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
+                               masq_stream stream);
 
 /* ---------------------------------------------------------------- N4: baseline factor methods
  * — the closed forms the paper compares MASQuant against, on the same data. */

@@ -42,6 +42,13 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.dot = take(sizeof(double) * cmc_dot_blocks());
       break;
     }
+    case MASQ_OP_DECODE:
+      L.inv_s = take(sizeof(float) * d);
+      L.ids0 = take((size_t)T);
+      L.qx = take((size_t)T * d);
+      L.dx = take(sizeof(float) * T);
+      L.dpart = take(sizeof(float) * (size_t)decode_kchunks(d) * (n / 8) * 128);
+      break;
     case MASQ_OP_MEANABS:
       L.partials = take(sizeof(float) * (size_t)meanabs_slabs(T) * n_mod * d);
       break;
@@ -543,6 +550,53 @@ masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const u
   const cudaError_t e = launch_cmc_factors(a, st);
   if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
   MASQ_CK(e);
+  return MASQ_OK;
+}
+
+masq_status masq_quantize_weight_int4(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t d_out,
+                                      int32_t group, uint8_t* packed, float* scales, masq_stream stream) {
+  if (!W || !s || !packed || !scales) return MASQ_ERR_NULL;
+  if (group != 128) return MASQ_ERR_UNSUPPORTED;
+  if (d <= 0 || d % 128 != 0 || d_out <= 0 || d_out % 8 != 0) return MASQ_ERR_SHAPE;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (!al16(packed)) return MASQ_ERR_ALIGN;
+  MASQ_CK(launch_wq4(W, wt, s, d, d_out, packed, scales, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_unpack_int4(const uint8_t* packed, int64_t d, int64_t d_out, int32_t group, int8_t* codes,
+                             masq_stream stream) {
+  if (!packed || !codes) return MASQ_ERR_NULL;
+  if (group != 128) return MASQ_ERR_UNSUPPORTED;
+  if (d <= 0 || d % 128 != 0 || d_out <= 0 || d_out % 8 != 0) return MASQ_ERR_SHAPE;
+  MASQ_CK(launch_unpack4(packed, d, d_out, codes, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64_t T, int64_t d, int64_t d_out,
+                               const float* s_t, const uint8_t* packed, const float* scales, int32_t group,
+                               int32_t abits, float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
+                               masq_stream stream) {
+  if (T < 0 || T > decode_max_tokens()) return MASQ_ERR_SHAPE;
+  if (group != 128) return MASQ_ERR_UNSUPPORTED;
+  if (d <= 0 || d % 128 != 0 || d_out <= 0 || d_out % 8 != 0) return MASQ_ERR_SHAPE;
+  MASQ_TRY(check_bits(abits));
+  if (!s_t || !packed || !scales || !Y) return MASQ_ERR_NULL;
+  if (ld_y < d_out || !al16(packed)) return MASQ_ERR_ALIGN;
+  const WsLayout L = ws_layout(MASQ_OP_DECODE, T, d, d_out, 1, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  if (T == 0) return MASQ_OK;
+  MASQ_TRY(check_x(X, xt, ld_x, d));
+  cudaStream_t st = S(stream);
+  float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  uint8_t* ids0 = reinterpret_cast<uint8_t*>(W8(ws, L.ids0));
+  int8_t* qa = reinterpret_cast<int8_t*>(W8(ws, L.qx));
+  float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
+  MASQ_CK(cudaMemsetAsync(ids0, 0, (size_t)T, st));
+  MASQ_CK(launch_inv(s_t, d, inv, st));
+  MASQ_CK(launch_aquant(X, xt, ld_x, ids0, T, d, 1, inv, abits, qa, dx, nullptr, status_of(ws), st, nullptr, T));
+  MASQ_CK(launch_decode(qa, dx, (int)T, d, d_out, packed, scales, reinterpret_cast<float*>(W8(ws, L.dpart)), Y,
+                        ld_y, st));
   return MASQ_OK;
 }
 

@@ -34,6 +34,8 @@ struct WsLayout {
   size_t a64 = 0, g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
          work = 0, info = 0, dot = 0;
   size_t lwork = 0;   // doubles
+  // N3 decode
+  size_t ids0 = 0, dpart = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -190,6 +192,15 @@ bool cmc_linalg_available();
 size_t cmc_syevd_lwork(int64_t d);
 int cmc_dot_blocks();
 cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- N3 int4 decode (decode.cu)
+int decode_kchunks(int64_t d);
+int decode_max_tokens();
+cudaError_t launch_wq4(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t n, uint8_t* packed,
+                       float* scales, cudaStream_t st);
+cudaError_t launch_unpack4(const uint8_t* packed, int64_t d, int64_t n, int8_t* codes, cudaStream_t st);
+cudaError_t launch_decode(const int8_t* qa, const float* dx, int T, int64_t d, int64_t n, const uint8_t* packed,
+                          const float* scales, float* part, float* Y, int64_t ldy, cudaStream_t st);
 
 // ---------------------------------------------------------------- N4 baselines (baseline.cu)
 int meanabs_slabs(int64_t T);

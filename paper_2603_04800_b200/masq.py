@@ -13,7 +13,7 @@ from ._lib import MasqDebug, lib
 
 MASQ_F32, MASQ_BF16 = 0, 1
 (OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS,
- OP_CMC) = range(10)
+ OP_CMC, OP_DECODE) = range(11)
 
 
 class MasqError(RuntimeError):
@@ -285,6 +285,35 @@ def cmc_factors(X, mod_id, s, W, qw_text, dw_text, r: int, eps_rel: float = 1e-8
                                _p(W.contiguous()), _dt(W), _p(qw_text), _p(dw_text), r, float(eps_rel), _p(L1), _p(L2),
                                _dt(L1), _p(resid), p, nb, _stream(stream)), "masq_cmc_factors")
     return L1, L2, resid
+
+
+# ----------------------------------------------------------------------------- N3
+def quantize_weight_int4(W, s_vec, group: int = 128, stream=None):
+    """(packed uint8 [n*d/2] in the decode kernel's order, scales f32 [n/8, d/group, 8])."""
+    d, n = W.shape
+    packed = torch.empty(n * d // 2, dtype=torch.uint8, device=W.device)
+    scales = torch.empty(n // 8, d // group, 8, dtype=torch.float32, device=W.device)
+    _ck(lib().masq_quantize_weight_int4(_p(W.contiguous()), _dt(W), _p(s_vec.contiguous()), d, n, group, _p(packed),
+                                        _p(scales), _stream(stream)), "masq_quantize_weight_int4")
+    return packed, scales
+
+
+def unpack_int4(packed, d: int, n: int, group: int = 128, stream=None):
+    codes = torch.empty(n, d, dtype=torch.int8, device=packed.device)
+    _ck(lib().masq_unpack_int4(_p(packed), d, n, group, _p(codes), _stream(stream)), "masq_unpack_int4")
+    return codes
+
+
+def linear_decode(X, s_t, packed, scales, abits: int = 8, group: int = 128, Y=None, ws=None, stream=None):
+    """Decode-shaped W4A8 forward of 1..16 text tokens: f32 [T x n]."""
+    T, d = X.shape
+    n = scales.shape[0] * 8
+    Y = torch.empty(T, n, dtype=torch.float32, device=X.device) if Y is None else Y
+    ws = ws or default_workspace(X.device)
+    p, nb = ws.ptr_size(workspace_size(OP_DECODE, T, d, n, 1))
+    _ck(lib().masq_linear_decode(_p(X), _dt(X), X.stride(0), T, d, n, _p(s_t.contiguous()), _p(packed), _p(scales),
+                                 group, abits, _p(Y), Y.stride(0), p, nb, _stream(stream)), "masq_linear_decode")
+    return Y
 
 
 # ----------------------------------------------------------------------------- N4

@@ -4,7 +4,7 @@ counts, and the AWQ beta grid scored by the calibration loss — against the ora
 
 Bar: integer and comparison outputs (counts, alpha, unified range, dominance) bit-exact; the
 f64-pow factors within 1 ulp of f32; the mean-abs sums within 1e-5 relative (f32 partials over
-64-token slabs, DESIGN.md §12); grid losses within 1e-3.
+64-token slabs, DESIGN.md §13); grid losses within 1e-3.
 """
 import numpy as np
 import pytest
