@@ -15,7 +15,7 @@ SO = os.path.join(ROOT, "paper_2603_04800_b200", "libmasq.so")
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(masq_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(masq_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
