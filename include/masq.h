@@ -71,7 +71,7 @@ typedef void* masq_stream;      /* cudaStream_t */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
   MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,
-  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9, MASQ_OP_DECODE = 10
+  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9, MASQ_OP_DECODE = 10, MASQ_OP_LAYER = 11
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -298,6 +298,25 @@ masq_status masq_calibrate_meanabs(const void* X, masq_dtype xt, int64_t ld_x, c
  * dom_counts[n_mod] = number of tied channels. */
 masq_status masq_range_stats(const float* R, int32_t n_mod, int64_t d, int32_t dominant, int32_t other,
                              float* alpha, float* r_unified, int64_t* dom_counts, masq_stream stream);
+
+/*
+ * One calibration pass of a linear layer in one call (A3 for every modality, A4-A7, A8): the
+ * results of masq_quantize_weight(s[0]) + masq_linear_forward + masq_reference_output +
+ * masq_calib_loss, bit-identical to those calls, with the shared work done once: every
+ * modality's weight codes come from one read of W (set 0 = the forward's Q(S_t W)), and the
+ * activations are quantized once in token order for the forward and gathered into the
+ * modality-grouped order for the loss (A4's codes are row-wise, so the gathered rows are the
+ * codes the loss call would compute).  X and W bf16.  Outputs: Y [T x ld_y] and Yref
+ * [T x ld_ref] f32; optional qw_text [d_out x d] int8 / dw_text [d_out] f32 (the text-smoothed
+ * base weight for serving); sums / counts / loss as masq_calib_loss.  CMC as masq_linear_forward
+ * (L1 / L2 bf16, r = 0 disables).
+ */
+masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                             int64_t d_out, int32_t n_mod, const float* s, const void* W,
+                             int32_t wbits, int32_t abits, const void* L1, const void* L2, int64_t ld_l2,
+                             int32_t r, const float* lambda, float* Y, int64_t ld_y, float* Yref,
+                             int64_t ld_ref, int8_t* qw_text, float* dw_text, double* sums,
+                             int64_t* counts, double* loss, void* ws, size_t ws_bytes, masq_stream stream);
 
 /* loss[0] = sum_m lambda[m] * sums[m] / (counts[m] * d_out) on the device (after an all-reduce). */
 masq_status masq_loss_finalize(const double* sums, const int64_t* counts, const float* lambda,

@@ -56,6 +56,10 @@ SIGNATURES = {
                                          c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
     "masq_range_stats": (c_int32, [c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                    c_void_p]),
+    "masq_calib_layer": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p,
+                                   c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int64, c_int32, c_void_p,
+                                   c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_size_t, c_void_p]),
     "masq_adam_init": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "masq_keep_best": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "masq_adam_step": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, ctypes.c_double,

@@ -42,6 +42,28 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.dot = take(sizeof(double) * cmc_dot_blocks());
       break;
     }
+    case MASQ_OP_LAYER: {
+      const int64_t Tg = grouped_rows(T, n_mod);
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      L.qx_tok = take((size_t)T * d);
+      L.dx_tok = take(sizeof(float) * T);
+      L.mask = take(sizeof(uint32_t) * tiles_m);
+      L.qx = take((size_t)Tg * d);
+      L.dx = take(sizeof(float) * Tg);
+      L.perm = take(sizeof(int32_t) * Tg);
+      L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
+      L.cnt = take(sizeof(int64_t) * n_mod);
+      L.qw_all = take((size_t)n_mod * n * d);
+      L.dw_all = take(sizeof(float) * n_mod * n);
+      L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
+      L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
+      if (rp > 0 && nnt > 0) {
+        L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
+        L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
+        L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
+      }
+      break;
+    }
     case MASQ_OP_DECODE:
       L.inv_s = take(sizeof(float) * d);
       L.ids0 = take((size_t)T);
@@ -301,6 +323,127 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
     g.l2t = l2t;
   }
   MASQ_CK(launch_gemm(g, st));
+  return MASQ_OK;
+}
+
+masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d, int64_t d_out,
+                             int32_t n_mod, const float* s, const void* W, int32_t wbits, int32_t abits, const void* L1,
+                             const void* L2, int64_t ld_l2, int32_t r, const float* lambda, float* Y, int64_t ld_y,
+                             float* Yref, int64_t ld_ref, int8_t* qw_text, float* dw_text, double* sums,
+                             int64_t* counts, double* loss, void* ws, size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  MASQ_TRY(check_bits(wbits));
+  MASQ_TRY(check_bits(abits));
+  if (d_out <= 0 || d_out % 32 != 0 || d_out >= (1LL << 31)) return MASQ_ERR_SHAPE;
+  if (r < 0 || r > 256 || r % 16 != 0) return MASQ_ERR_SHAPE;
+  if (!s || !W || !Y || !Yref || !sums || !counts || !loss) return MASQ_ERR_NULL;
+  const bool cmc = r > 0 && n_mod > 1;
+  if (cmc) {
+    if (!L1 || !L2) return MASQ_ERR_NULL;
+    if (ld_l2 < d_out || !al16(L1) || !al16(L2) || (ld_l2 % 8) != 0) return MASQ_ERR_ALIGN;
+  }
+  if (ld_y < d_out || ld_y % 4 != 0 || !al16(Y)) return MASQ_ERR_ALIGN;
+  if (ld_ref < d_out || ld_ref % 4 != 0 || !al16(Yref)) return MASQ_ERR_ALIGN;
+  if (!al16(W) || !al16(s)) return MASQ_ERR_ALIGN;
+  if ((qw_text && !al16(qw_text)) || (dw_text && !al16(dw_text))) return MASQ_ERR_ALIGN;
+  const WsLayout L = ws_layout(MASQ_OP_LAYER, T, d, d_out, n_mod, cmc ? r : 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  if (T == 0) {
+    MASQ_CK(cudaMemsetAsync(sums, 0, sizeof(double) * n_mod, st));
+    MASQ_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * n_mod, st));
+    MASQ_CK(cudaMemsetAsync(loss, 0, sizeof(double), st));
+    return MASQ_OK;
+  }
+  MASQ_TRY(check_x(X, MASQ_BF16, ld_x, d));
+  if (!mod_id) return MASQ_ERR_NULL;
+  float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  int8_t* qt = reinterpret_cast<int8_t*>(W8(ws, L.qx_tok));
+  float* dt = reinterpret_cast<float*>(W8(ws, L.dx_tok));
+  uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
+  int8_t* qg = reinterpret_cast<int8_t*>(W8(ws, L.qx));
+  float* dg = reinterpret_cast<float*>(W8(ws, L.dx));
+  int32_t* perm = reinterpret_cast<int32_t*>(W8(ws, L.perm));
+  uint32_t* tmod = reinterpret_cast<uint32_t*>(W8(ws, L.tile_mod));
+  int64_t* cnt = reinterpret_cast<int64_t*>(W8(ws, L.cnt));
+  int8_t* qw = reinterpret_cast<int8_t*>(W8(ws, L.qw_all));
+  float* dw = reinterpret_cast<float*>(W8(ws, L.dw_all));
+  uint32_t* amax = reinterpret_cast<uint32_t*>(W8(ws, L.amax));
+  double* partials = reinterpret_cast<double*>(W8(ws, L.partials));
+  const int64_t Tg = grouped_rows(T, n_mod);
+  const int num_n = (int)ceil_div(d_out, kTileN);
+  const int64_t tiles = (Tg / kUnitM) * num_n;
+  const int epi = gemm_epilogue_warps();
+  // shared front half: factors, routing, every modality's weight codes (set 0 = the forward's
+  // Q(S_t W)), the token-order activation codes (forward) and their grouped copy (loss)
+  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
+  MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, cnt, st));
+  MASQ_CK(launch_wquant(W, MASQ_BF16, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
+  MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask, status_of(ws), st));
+  MASQ_CK(launch_gather_rows(qt, dt, perm, Tg, d, qg, dg, st));
+  // A4-A7 forward
+  GemmArgs g{};
+  g.mode = kModeFwd;
+  g.T = T;
+  g.n = d_out;
+  g.d = d;
+  g.qx = qt;
+  g.b = qw;
+  g.b_rows = d_out;
+  g.dx = dt;
+  g.dw = dw;
+  g.tile_mask = mask;
+  g.n_mod = n_mod;
+  g.out = Y;
+  g.ld_out = ld_y;
+  if (cmc) {
+    const int rp = (int)rpad_of(r);
+    uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
+    uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
+    uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
+    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), inv, d, r, rp, n_mod - 1, l1t, st));
+    MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
+    MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st));
+    g.rpad = rp;
+    g.z = z;
+    g.l2t = l2t;
+  }
+  MASQ_CK(launch_gemm(g, st));
+  // A8 target and loss
+  GemmArgs gr{};
+  gr.mode = kModeRef;
+  gr.T = T;
+  gr.n = d_out;
+  gr.d = d;
+  gr.xbf = static_cast<const uint16_t*>(X);
+  gr.ld_x = ld_x;
+  gr.b = W;
+  gr.b_rows = d;
+  gr.n_mod = 1;
+  gr.out = Yref;
+  gr.ld_out = ld_ref;
+  MASQ_CK(launch_gemm(gr, st));
+  MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * tiles * epi, st));
+  GemmArgs gl{};
+  gl.mode = kModeLoss;
+  gl.T = Tg;
+  gl.n = d_out;
+  gl.d = d;
+  gl.qx = qg;
+  gl.b = qw;
+  gl.b_rows = (int64_t)n_mod * d_out;
+  gl.dx = dg;
+  gl.dw = dw;
+  gl.tile_mask = tmod;
+  gl.perm = perm;
+  gl.n_mod = n_mod;
+  gl.yref = Yref;
+  gl.ld_ref = ld_ref;
+  gl.partials = partials;
+  MASQ_CK(launch_gemm(gl, st));
+  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st));
+  if (qw_text) MASQ_CK(cudaMemcpyAsync(qw_text, qw, (size_t)d_out * d, cudaMemcpyDeviceToDevice, st));
+  if (dw_text) MASQ_CK(cudaMemcpyAsync(dw_text, dw, sizeof(float) * d_out, cudaMemcpyDeviceToDevice, st));
   return MASQ_OK;
 }
 

@@ -885,6 +885,27 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
   return cudaGetLastError();
 }
 
+// grouped copy of token-order codes: row p of qg = row perm[p] of qt (zeros and dx 0 for padding)
+__global__ void __launch_bounds__(256) gather_rows_kernel(const int8_t* __restrict__ qt, const float* __restrict__ dt,
+                                                          const int32_t* __restrict__ perm, int64_t Tg, int64_t d,
+                                                          int8_t* __restrict__ qg, float* __restrict__ dg) {
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= Tg) return;
+  const int32_t src = __ldg(perm + p);
+  const uint4* in = reinterpret_cast<const uint4*>(qt + (int64_t)(src < 0 ? 0 : src) * d);
+  uint4* out = reinterpret_cast<uint4*>(qg + p * d);
+  for (int64_t c = lane; c < d / 16; c += 32) out[c] = src >= 0 ? __ldg(in + c) : make_uint4(0, 0, 0, 0);
+  if (lane == 0) dg[p] = src >= 0 ? __ldg(dt + src) : 0.f;
+}
+
+cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t* perm, int64_t Tg, int64_t d, int8_t* qg,
+                               float* dg, cudaStream_t st) {
+  ProfScope ps_("gather_rows", st);
+  gather_rows_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(qt, dt, perm, Tg, d, qg, dg);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
                          int64_t* counts, cudaStream_t st) {
   const int64_t Tg = grouped_rows(T, n_mod);

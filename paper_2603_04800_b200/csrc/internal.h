@@ -36,6 +36,8 @@ struct WsLayout {
   size_t lwork = 0;   // doubles
   // N3 decode
   size_t ids0 = 0, dpart = 0;
+  // fused layer call: token-order codes next to the grouped ones
+  size_t qx_tok = 0, dx_tok = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -66,6 +68,9 @@ cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_se
 // amax_scratch: [2 x n_sets x n] u32 — the column maxima max_i |s_i w_ij| (f32 bits, kept after
 // the call), then the f32 reciprocals of the scales used by the quantizer
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st);
+// qg[p] = qt[perm[p]] (rows of d bytes, d % 16 == 0), dg[p] = dt[perm[p]]; zeros for perm < 0
+cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t* perm, int64_t Tg, int64_t d, int8_t* qg,
+                               float* dg, cudaStream_t st);
 // perm (optional): output row p quantizes input token perm[p] (-1: padding row, left untouched);
 // T_out = number of output rows (T when perm == NULL)
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,

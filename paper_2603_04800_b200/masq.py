@@ -13,7 +13,7 @@ from ._lib import MasqDebug, lib
 
 MASQ_F32, MASQ_BF16 = 0, 1
 (OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS,
- OP_CMC, OP_DECODE) = range(11)
+ OP_CMC, OP_DECODE, OP_LAYER) = range(12)
 
 
 class MasqError(RuntimeError):
@@ -216,6 +216,32 @@ def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, sums=Non
                               _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), p, n, _stream(stream)),
         "masq_calib_loss")
     return sums, counts, loss
+
+
+def calib_layer(X, mod_id, s, W, wbits: int, abits: int, L1=None, L2=None, lam=None, Y=None, Yref=None,
+                qw_text=None, dw_text=None, sums=None, counts=None, loss=None, ws=None, stream=None):
+    """One fused calibration pass of a linear: (Y, Yref, sums, counts, loss); bit-identical to
+    quantize_weight(s[0]) + linear_forward + reference_output + calib_loss."""
+    T, d = X.shape
+    n = W.shape[1]
+    n_mod = s.shape[0]
+    dev = X.device
+    r = 0 if L1 is None else int(L1.shape[-1])
+    ld_l2 = 0 if L2 is None else int(L2.stride(-2))
+    Y = torch.empty(T, n, dtype=torch.float32, device=dev) if Y is None else Y
+    Yref = torch.empty(T, n, dtype=torch.float32, device=dev) if Yref is None else Yref
+    sums = torch.empty(n_mod, dtype=torch.float64, device=dev) if sums is None else sums
+    counts = torch.empty(n_mod, dtype=torch.int64, device=dev) if counts is None else counts
+    loss = torch.empty(1, dtype=torch.float64, device=dev) if loss is None else loss
+    ws = ws or default_workspace(dev)
+    p, nb = ws.ptr_size(workspace_size(OP_LAYER, T, d, n, n_mod, r))
+    lam_arr = _lambda_arr(lam, n_mod)
+    _ck(lib().masq_calib_layer(_p(X), X.stride(0), _p(mod_id), T, d, n, n_mod, _p(s.contiguous()), _p(W.contiguous()),
+                               wbits, abits, _p(L1), _p(L2), ld_l2, r,
+                               ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr is not None else None,
+                               _p(Y), Y.stride(0), _p(Yref), Yref.stride(0), _p(qw_text), _p(dw_text), _p(sums),
+                               _p(counts), _p(loss), p, nb, _stream(stream)), "masq_calib_layer")
+    return Y, Yref, sums, counts, loss
 
 
 def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, grad=None, sums=None, counts=None,
