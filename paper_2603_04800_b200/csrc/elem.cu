@@ -325,22 +325,23 @@ __global__ void wscale_kernel(const uint32_t* __restrict__ amax, float* __restri
   rcp[j] = __fdiv_rn(1.0f, dv);
 }
 
-// pass 2: one 128 (i) x 64 (j) tile of W read once; for every set k the codes are packed
-// 4 rows per 32-bit word into a smem tile [64 j][128 i] and written K-major (qw[k][j][i]).
-template <typename WT, int NS>
+// pass 2: one 128 (i) x JT (j) tile of W read once (JT = 8 * CPT: 256-byte bf16 row segments
+// for CPT = 16, which keeps the DRAM access pattern page-friendly); for every set k the codes
+// are packed 4 rows per 32-bit word into a smem tile [JT j][128 i] and written K-major.
+template <typename WT, int NS, int CPT>
 __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, const float* __restrict__ s,
                                                      int64_t d, int64_t n, int qmin, int qmax,
                                                      const float* __restrict__ rcp, int8_t* __restrict__ qw,
                                                      const float* __restrict__ dw) {
   constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
-  constexpr int CPT = 8;                        // columns per thread
   constexpr int LPT = CPT / V;                  // loads per row per thread
-  __shared__ __align__(16) uint32_t tile[64][33];   // [j][i/4] packed codes (+1 word pad)
-  const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * 64;
+  constexpr int JT = 8 * CPT;                   // tile columns
+  __shared__ __align__(16) uint32_t tile[JT][33];   // [j][i/4] packed codes (+1 word pad)
+  const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * JT;
   const int tx = threadIdx.x & 7;               // column group: j = j0 + 8*tx + e
   const int ty = threadIdx.x >> 3;              // rows 4*ty .. 4*ty+3 of the tile
   const int64_t jb = j0 + tx * CPT;
-  const bool colok = jb < n;                    // n % 32 == 0 -> whole 8-column groups
+  const bool colok = jb < n;                    // n % 32 == 0 -> whole CPT-column groups
   float f[4][CPT];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -368,8 +369,11 @@ __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, c
     float rcv[CPT];
     if (colok) {
       const float4* r4 = reinterpret_cast<const float4*>(rcp + (int64_t)k * n + jb);
-      const float4 a = __ldg(r4), b = __ldg(r4 + 1);
-      rcv[0] = a.x; rcv[1] = a.y; rcv[2] = a.z; rcv[3] = a.w; rcv[4] = b.x; rcv[5] = b.y; rcv[6] = b.z; rcv[7] = b.w;
+#pragma unroll
+      for (int q = 0; q < CPT / 4; ++q) {
+        const float4 a = __ldg(r4 + q);
+        rcv[4 * q] = a.x; rcv[4 * q + 1] = a.y; rcv[4 * q + 2] = a.z; rcv[4 * q + 3] = a.w;
+      }
     } else {
 #pragma unroll
       for (int e = 0; e < CPT; ++e) rcv[e] = 1.f;
@@ -399,14 +403,15 @@ __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, c
       tile[tx * CPT + e][ty] = quant4_exact(x[0], x[1], x[2], x[3], dv, rc, qmin, qmax);
     }
     __syncthreads();
-    // write 64 rows (j) x 128 bytes (i): 4 threads per row, 32 bytes each
-    const int jr = threadIdx.x >> 2, part = threadIdx.x & 3;
-    const int64_t j = j0 + jr, i = i0 + part * 32;
-    if (j < n && i < d) {
-      const uint32_t* t = &tile[jr][part * 8];
-      int8_t* dst = qw + ((int64_t)k * n + j) * d + i;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(t[0], t[1], t[2], t[3]);
-      if (i + 16 < d) *reinterpret_cast<uint4*>(dst + 16) = make_uint4(t[4], t[5], t[6], t[7]);
+    // write JT rows (j) x 128 bytes (i): 8 threads per row, 16 bytes each
+#pragma unroll
+    for (int q = 0; q < JT / 32; ++q) {
+      const int jr = q * 32 + (threadIdx.x >> 3), part = threadIdx.x & 7;
+      const int64_t j = j0 + jr, i = i0 + part * 16;
+      if (j < n && i < d) {
+        const uint32_t* t = &tile[jr][part * 4];
+        *reinterpret_cast<uint4*>(qw + ((int64_t)k * n + j) * d + i) = make_uint4(t[0], t[1], t[2], t[3]);
+      }
     }
     __syncthreads();
   }
@@ -783,10 +788,11 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
                                                            ceil_div(d, 16)));
   const int rows = (int)ceil_div(d, strips);
   strips = (int)ceil_div(d, rows);
-  dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 64), (unsigned)ceil_div(d, 128));
+  constexpr int CPT = NS == 1 ? 8 : 16;            // measured: 16 columns per thread pays off for >= 2 sets
+  dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 8 * CPT), (unsigned)ceil_div(d, 128));
   { ProfScope ps_("wcolmax", st); wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
   { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, rcp, NS * n, (float)qmax); }
-  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, rcp, qw, dw); }
+  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS, CPT><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, rcp, qw, dw); }
   return cudaGetLastError();
 }
 

@@ -51,9 +51,17 @@ def main():
         t = prof(lambda: M.quantize_activations(X, ids, s, 8))
         r["aquant_ms"] = t["aquant"]
         r["aquant_gbs"] = (3 * T * d + 4 * T) / t["aquant"] / 1e6
+        wkeys = ("wq_strip", "wcolmax", "wscale", "wquant")
         t = prof(lambda: M.quantize_weight(W, s[0], 4))
         r["wq1"] = t
-        r["wq1_gbs"] = (2 * d * n * 2 + d * n) / (t["wcolmax"] + t["wquant"]) / 1e6
+        wt = sum(t.get(k, 0.0) for k in wkeys)
+        r["wq1_ms"] = wt
+        r["wq1_gbs_1read"] = (2 * d * n + d * n) / wt / 1e6          # algorithmic: W once + codes
+        Yref = M.reference_output(X[:2048], W)
+        t2 = prof(lambda: M.calib_loss(X[:2048], ids[:2048], s, W, 4, 8, Yref))
+        wt2 = sum(t2.get(k, 0.0) for k in wkeys)
+        r["wq2_ms"] = wt2
+        r["wq2_gbs_1read"] = (2 * d * n + 2 * d * n) / wt2 / 1e6
         t = prof(lambda: M.init_factors(R, cnt, W))
         r["init_ms"] = t["init"]
         r["init_gbs"] = 2 * d * n / t["init"] / 1e6

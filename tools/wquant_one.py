@@ -1,0 +1,21 @@
+"""Run the loss-side weight quantization (2 factor sets) at the c3 gate_up shape (ncu target)."""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+import paper_2603_04800_b200 as M  # noqa: E402
+
+d, n, T = int(os.environ.get("D", 3584)), int(os.environ.get("N", 37888)), 2048
+dev = torch.device("cuda", 0)
+ids = torch.from_numpy(synth.modality_ids(synth.CONFIGS["c3"]["pattern"], T=T)).to(dev)
+X = (torch.randn(T, d, device=dev) * 3).to(torch.bfloat16)
+W = (torch.randn(d, n, device=dev) / d ** 0.5).to(torch.bfloat16)
+s = torch.rand(2, d, device=dev) + 0.5
+for _ in range(3):
+    out = M.calib_layer(X, ids, s, W, 4, 8)
+torch.cuda.synchronize()
+print("ok")
