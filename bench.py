@@ -156,8 +156,8 @@ def oracle_sample_step(ids_s, lin_s, r):
 
 
 def oracle_sample(T, r, seed_rank=0):
-    """Sample = the qkv linear (3584 -> 4608) of the c3 layer on 32 text + 32 image tokens (and a
-    64 + 64 variant to split per-token from per-step weight-side cost)."""
+    """Sample = the qkv linear (3584 -> 4608) of the c3 layer on k text + k image tokens (two sizes
+    split the per-token from the per-step weight-side cost)."""
     cfg = synth.CONFIGS[CFG]
     name, d, n = layer_linears(["qkv"])[0]
     ids_full = synth.modality_ids(cfg["pattern"], T=T)
@@ -182,30 +182,34 @@ def oracle_threads():
         return os.cpu_count() or 1
 
 
-def time_oracle(T, r, linears, repeats=1):
-    """Returns (tokens/s extrapolated to the full layer at T tokens, seconds of one sample step, desc)."""
+def time_oracle(T, r, linears, repeats=3, k_small=128, k_large=512):
+    """Returns (tokens/s extrapolated to the full layer at T tokens, seconds of CPU work, desc).
+    ~10-15 s of oracle work: `repeats` steps at 2*k_small and at 2*k_large tokens."""
     sample = oracle_sample(T, r)
-    ids32, s32 = sample(32)
-    ids64, s64 = sample(64)
-    oracle_sample_step(ids32, s32, r)                     # warm caches / BLAS threads
+    ids_a, s_a = sample(k_small)
+    ids_b, s_b = sample(k_large)
+    t0 = time.perf_counter()
+    oracle_sample_step(ids_a, s_a, r)                     # warm caches / BLAS threads
     t = time.perf_counter()
     for _ in range(repeats):
-        oracle_sample_step(ids32, s32, r)
-    t64 = (time.perf_counter() - t) / repeats
+        oracle_sample_step(ids_a, s_a, r)
+    ta = (time.perf_counter() - t) / repeats
     t = time.perf_counter()
     for _ in range(repeats):
-        oracle_sample_step(ids64, s64, r)
-    t128 = (time.perf_counter() - t) / repeats
-    per_tok = max(t128 - t64, 1e-9) / 64.0
-    fixed = max(t64 - 64 * per_tok, 0.0)
+        oracle_sample_step(ids_b, s_b, r)
+    tb = (time.perf_counter() - t) / repeats
+    total = time.perf_counter() - t0
+    na, nb = 2 * k_small, 2 * k_large
+    per_tok = max(tb - ta, 1e-9) / (nb - na)
+    fixed = max(ta - na * per_tok, 0.0)
     dn_qkv = 3584 * 4608
     scale = sum(d * n for _, d, n in linears) / dn_qkv
     layer_time = scale * (fixed + T * per_tok)
     desc = (f"oracle step (stats, init, wquant, forward+CMC, loss incl. X W) on the qkv linear "
-            f"3584->4608 with 64 and 128 tokens (half text, half image): {t64:.2f} s / {t128:.2f} s; "
-            f"extrapolated to the {len(linears)}-linear layer at {T} tokens by sum(d*n) "
-            f"(x{scale:.1f}): {layer_time:.1f} s")
-    return T / layer_time, t64 + t128, desc
+            f"3584->4608 with {na} and {nb} tokens (half text, half image), {repeats} repeats each: "
+            f"{ta:.2f} s / {tb:.2f} s per step; extrapolated to the {len(linears)}-linear layer at {T} tokens "
+            f"by sum(d*n) (x{scale:.1f}): {layer_time:.1f} s")
+    return T / layer_time, total, desc
 
 
 def run_reference(args):
