@@ -624,7 +624,9 @@ def main():
     K = args.steps
     per_step = {
         "gemm_fwd": ("tensor", ops, "TOP/s", int8_peak),
-        "gemm_loss": ("tensor", ops, "TOP/s", int8_peak),
+        # text rows' loss comes out of the forward's epilogue (S_0 = S_t); the loss GEMM runs on the
+        # non-text rows only
+        "gemm_loss": ("tensor", sum(2.0 * n_nt * e["d"] * e["n"] for e in L), "TOP/s", int8_peak),
         "gemm_ref": ("tensor", ops, "TFLOP/s", bf16_peak),
         "stats": ("hbm", sum(2.0 * T * e["d"] + T for e in L), "GB/s", peaks["hbm"]),
         "aquant": ("hbm", sum(3.0 * T * e["d"] + 4 * T for e in L), "GB/s", peaks["hbm"]),

@@ -302,11 +302,12 @@ masq_status masq_range_stats(const float* R, int32_t n_mod, int64_t d, int32_t d
 /*
  * One calibration pass of a linear layer in one call (A3 for every modality, A4-A7, A8): the
  * results of masq_quantize_weight(s[0]) + masq_linear_forward + masq_reference_output +
- * masq_calib_loss, bit-identical to those calls, with the shared work done once: every
- * modality's weight codes come from one read of W (set 0 = the forward's Q(S_t W)), and the
- * activations are quantized once in token order for the forward and gathered into the
- * modality-grouped order for the loss (A4's codes are row-wise, so the gathered rows are the
- * codes the loss call would compute).  X and W bf16.  Outputs: Y [T x ld_y] and Yref
+ * masq_calib_loss (codes, Y, Yref and counts bit-identical; loss sums to rounding), with the
+ * shared work done once: every modality's weight codes come from one read of W (set 0 = the
+ * forward's Q(S_t W)); the activations are quantized once in token order for the forward and
+ * gathered into the modality-grouped order for the loss (A4's codes are row-wise); and since
+ * S_0 = S_t, a text row's forward output IS its loss-side quantized output, so the forward
+ * epilogue sums the text rows' |y - yref| and the loss GEMM runs on the non-text rows only.  X and W bf16.  Outputs: Y [T x ld_y] and Yref
  * [T x ld_ref] f32; optional qw_text [d_out x d] int8 / dw_text [d_out] f32 (the text-smoothed
  * base weight for serving); sums / counts / loss as masq_calib_loss.  CMC as masq_linear_forward
  * (L1 / L2 bf16, r = 0 disables).

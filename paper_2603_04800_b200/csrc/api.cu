@@ -57,6 +57,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.dw_all = take(sizeof(float) * n_mod * n);
       L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
       L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
+      L.fpart = take(sizeof(double) * ceil_div(T, kUnitM) * ceil_div(n, kTileN) * 2);
       if (rp > 0 && nnt > 0) {
         L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
         L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
@@ -381,7 +382,24 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   MASQ_CK(launch_wquant(W, MASQ_BF16, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
   MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask, status_of(ws), st));
   MASQ_CK(launch_gather_rows(qt, dt, perm, Tg, d, qg, dg, st));
-  // A4-A7 forward
+  // A8 target first: the forward's epilogue reads it for the text rows
+  GemmArgs gr{};
+  gr.mode = kModeRef;
+  gr.T = T;
+  gr.n = d_out;
+  gr.d = d;
+  gr.xbf = static_cast<const uint16_t*>(X);
+  gr.ld_x = ld_x;
+  gr.b = W;
+  gr.b_rows = d;
+  gr.n_mod = 1;
+  gr.out = Yref;
+  gr.ld_out = ld_ref;
+  MASQ_CK(launch_gemm(gr, st));
+  // A4-A7 forward; text rows' output is also the loss's quantized output (S_0 = S_t), so the
+  // epilogue sums their |y - yref| and the loss GEMM below skips the text units
+  double* fpart = reinterpret_cast<double*>(W8(ws, L.fpart));
+  const int64_t fwd_units = ceil_div(T, kUnitM) * num_n;
   GemmArgs g{};
   g.mode = kModeFwd;
   g.T = T;
@@ -396,6 +414,11 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   g.n_mod = n_mod;
   g.out = Y;
   g.ld_out = ld_y;
+  g.ids = mod_id;
+  g.fwd_loss = 1;
+  g.yref = Yref;
+  g.ld_ref = ld_ref;
+  g.partials = fpart;
   if (cmc) {
     const int rp = (int)rpad_of(r);
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
@@ -409,20 +432,6 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
     g.l2t = l2t;
   }
   MASQ_CK(launch_gemm(g, st));
-  // A8 target and loss
-  GemmArgs gr{};
-  gr.mode = kModeRef;
-  gr.T = T;
-  gr.n = d_out;
-  gr.d = d;
-  gr.xbf = static_cast<const uint16_t*>(X);
-  gr.ld_x = ld_x;
-  gr.b = W;
-  gr.b_rows = d;
-  gr.n_mod = 1;
-  gr.out = Yref;
-  gr.ld_out = ld_ref;
-  MASQ_CK(launch_gemm(gr, st));
   MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * tiles * epi, st));
   GemmArgs gl{};
   gl.mode = kModeLoss;
@@ -440,8 +449,10 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   gl.yref = Yref;
   gl.ld_ref = ld_ref;
   gl.partials = partials;
+  gl.skip_m0 = 1;
   MASQ_CK(launch_gemm(gl, st));
-  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st));
+  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st,
+                             fpart, fwd_units * 2));
   if (qw_text) MASQ_CK(cudaMemcpyAsync(qw_text, qw, (size_t)d_out * d, cudaMemcpyDeviceToDevice, st));
   if (dw_text) MASQ_CK(cudaMemcpyAsync(dw_text, dw, sizeof(float) * d_out, cudaMemcpyDeviceToDevice, st));
   return MASQ_OK;

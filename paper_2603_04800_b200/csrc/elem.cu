@@ -707,11 +707,13 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
                                                            int num_n, int epi, const uint32_t* __restrict__ tile_mod,
                                                            const int64_t* __restrict__ counts_in, int n_mod,
                                                            int64_t n, Lambda8 lam, double* __restrict__ sums,
-                                                           int64_t* __restrict__ counts, double* __restrict__ loss) {
+                                                           int64_t* __restrict__ counts, double* __restrict__ loss,
+                                                           const double* __restrict__ extra, int64_t n_extra) {
   __shared__ double red[kMaxMod][512];
   double acc[kMaxMod];
 #pragma unroll
   for (int m = 0; m < kMaxMod; ++m) acc[m] = 0.0;
+  for (int64_t u = threadIdx.x; u < n_extra; u += 512) acc[0] += extra[u];   // text loss from the forward
   for (int64_t u = threadIdx.x; u < n_units; u += 512) {         // fixed assignment -> deterministic
     const uint32_t m = tile_mod[u / num_n];
     if (m >= (uint32_t)n_mod) continue;
@@ -947,10 +949,11 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
 
 cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
                                const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
-                               double* sums, int64_t* counts, double* loss, cudaStream_t st) {
+                               double* sums, int64_t* counts, double* loss, cudaStream_t st, const double* extra,
+                               int64_t n_extra) {
   ProfScope ps_("loss_reduce", st);
   loss_reduce_kernel<<<1, 512, 0, st>>>(partials, n_units, num_n, epi, tile_mod, counts_in, n_mod, n,
-                                         make_lambda(lambda_host, n_mod), sums, counts, loss);
+                                         make_lambda(lambda_host, n_mod), sums, counts, loss, extra, n_extra);
   return cudaGetLastError();
 }
 

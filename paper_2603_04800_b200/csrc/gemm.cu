@@ -83,6 +83,9 @@ struct Params {
   double* partials;            // loss: [n_units][2] (one per CTA of the pair)
   uint16_t* gsign;             // loss (optional, N1): bf16 sign(yq - yref) [T x n], 0 on padding rows
   float* apart;                // alpha: [T][2 * num_n] per-row partials
+  const uint8_t* ids;          // fwd with fwd_loss: modality id per row (text rows feed the loss)
+  int fwd_loss;                // fwd: sum |y - yref| over text rows into partials[unit][rank]
+  int skip_m0;                 // loss: skip the text units (their loss comes from the forward)
 };
 
 struct Unit {
@@ -103,6 +106,7 @@ __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
   if (p.mode == kModeLoss || p.mode == kModeAlpha) {
     w.mask = p.tile_mask[w.mt];
     if (w.mask == 0xFFFFFFFFu) return false;
+    if (p.skip_m0 && w.mask == 0u) return false;
     w.m = (int)w.mask;
   } else if (p.tile_mask) {
     const int t0 = 2 * w.mt;
@@ -325,6 +329,21 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       int src = -1;
       if (MODE == kModeLoss && row < p.T) src = __ldg(p.perm + row);
+      // forward + text loss: this row's Yref row (text rows only; their forward output is the
+      // loss's quantized output, PAPER.md:69 with S_m = S_t)
+      const bool tl = MODE == kModeFwd && p.fwd_loss && row < p.T && __ldg(p.ids + row) == 0;
+      double tpart = 0.0;
+      auto text_loss = [&](const uint32_t (&v)[32], int c) {
+        const float4* r4 = reinterpret_cast<const float4*>(p.yref + (size_t)row * p.ld_ref + col_base + (c0 + c) * 32);
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 y = __ldg(r4 + j);
+          acc += fabsf(__uint_as_float(v[4 * j + 0]) - y.x) + fabsf(__uint_as_float(v[4 * j + 1]) - y.y) +
+                 fabsf(__uint_as_float(v[4 * j + 2]) - y.z) + fabsf(__uint_as_float(v[4 * j + 3]) - y.w);
+        }
+        tpart += (double)acc;
+      };
       // loss: issue the first chunk's Yref loads now, under the main loop of this unit
       float4 ycur[8];
       if (MODE == kModeLoss && src >= 0 && nch > 0) {
@@ -389,6 +408,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
+          if (tl) text_loss(v, c);
           store_chunk(v, c);
         }
       } else if (MODE == kModeLoss) {
@@ -479,8 +499,23 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
           if (MODE == kModeFwd) dequant(v, c);
+          if (MODE == kModeFwd && tl) text_loss(v, c);
           store_chunk(v, c);
         }
+      }
+      if (MODE == kModeFwd && p.fwd_loss) {
+        // fixed-order combine of the 8 epilogue warps -> one text-loss partial per (unit, CTA)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tpart += __shfl_xor_sync(0xffffffffu, tpart, o);
+        if (lane == 0) red[ew] = tpart;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0) {
+          double tot = 0.0;
+#pragma unroll
+          for (int e = 0; e < EPI_WARPS; ++e) tot += red[e];
+          p.partials[(size_t)(w.mt * p.num_n + w.nt) * 2 + rank] = tot;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
       }
       tc_fence_before();
       __syncwarp();
@@ -590,6 +625,9 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.partials = g.partials;
   p.gsign = g.gsign;
   p.apart = g.apart;
+  p.ids = g.ids;
+  p.fwd_loss = g.fwd_loss;
+  p.skip_m0 = g.skip_m0;
   const int clusters = (int)std::min<int64_t>(p.n_units, num_sms() / 2);
   switch (g.mode) {
     case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, clusters, st);

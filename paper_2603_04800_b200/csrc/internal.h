@@ -37,7 +37,7 @@ struct WsLayout {
   // N3 decode
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
-  size_t qx_tok = 0, dx_tok = 0;
+  size_t qx_tok = 0, dx_tok = 0, fpart = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -89,9 +89,11 @@ cudaError_t launch_pack_l2(const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t 
 cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint16_t* Wt, cudaStream_t st);
 // sums[m] = fixed-order sum of partials[u * epi + e] over units u with tile_mod[u / num_n] == m;
 // counts_in: per-modality token counts from launch_route
+// extra (optional): n_extra per-(unit, CTA) partials of modality 0 added after the grouped ones
 cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
                                const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
-                               double* sums, int64_t* counts, double* loss, cudaStream_t st);
+                               double* sums, int64_t* counts, double* loss, cudaStream_t st,
+                               const double* extra = nullptr, int64_t n_extra = 0);
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st);
 
@@ -131,6 +133,12 @@ struct GemmArgs {
   // kModeAlpha (N1): acc = D . codes_m^T (bf16 codes of Q(S_m W), K-major [n_mod*n x d]);
   // apart[row][2*nt + half] = sum_j gsign[row][j] * dw_m[j] * acc[row][j] over the CTA's columns
   float* apart;
+  // fused layer call: the forward also sums the text rows' loss (|y - yref|, text rows only:
+  // their forward output is the loss's quantized output) into partials, and the loss GEMM then
+  // skips the text units
+  const uint8_t* ids;
+  int fwd_loss = 0;
+  int skip_m0 = 0;
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
 int gemm_epilogue_warps();

@@ -1,6 +1,7 @@
 """GPU: the fused per-linear calibration call (masq_calib_layer) equals the separate calls
-(quantize_weight(s[0]) + linear_forward + reference_output + calib_loss) bit for bit, and
-therefore the oracle within the bars those calls are tested to."""
+(quantize_weight(s[0]) + linear_forward + reference_output + calib_loss): weight codes, Y, Yref
+and counts bit for bit; the loss sums to 1e-12 relative (the text rows' |y - yref| is summed in
+the forward's epilogue, in token order, instead of in the loss GEMM's grouped order)."""
 import numpy as np
 import pytest
 import torch
@@ -31,6 +32,7 @@ def test_calib_layer_equals_separate_calls(name, use_cmc):
     s2, c2, l2 = m.calib_loss(X, ids, s, W, c["wbits"], c["abits"], Yr2)
     assert torch.equal(qt, qw) and torch.equal(dt, dw)
     assert torch.equal(Y, Y2) and torch.equal(Yref, Yr2)
-    assert torch.equal(sums, s2) and torch.equal(counts, c2) and torch.equal(loss, l2)
+    assert torch.equal(counts, c2)
+    assert torch.allclose(sums, s2, rtol=1e-12, atol=0) and torch.allclose(loss, l2, rtol=1e-12, atol=0)
     _, _, lo = O.calib_loss(c["X"], c["ids"], so, c["W"], c["wbits"], c["abits"])
     assert abs(float(loss.cpu()[0]) - lo) <= 1e-3 * abs(lo)
