@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // api.cu — the C ABI (include/masq.h): argument validation, workspace carving and the launch
 // sequence of every entry point.  All compute runs in the kernels of elem.cu, zgemm.cu, gemm.cu.
 #include <cstring>
@@ -150,9 +152,23 @@ inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) 
 inline cudaStream_t S(masq_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 inline uint8_t* W8(void* ws, size_t off) { return static_cast<uint8_t*>(ws) + off; }
 inline uint32_t* status_of(void* ws) { return static_cast<uint32_t*>(ws); }
-#define MASQ_CK(x)                                   \
-  do {                                               \
-    if ((x) != cudaSuccess) return MASQ_ERR_CUDA;    \
+// MASQ_DEBUG=1 in the environment prints the failing call and the CUDA error to stderr
+static bool masq_debug_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MASQ_DEBUG");
+    on = e && atoi(e) ? 1 : 0;
+  }
+  return on == 1;
+}
+#define MASQ_CK(x)                                                                              \
+  do {                                                                                          \
+    const cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                                    \
+      if (masq_debug_on()) fprintf(stderr, "[masq] %s:%d %s -> %s\n", __FILE__, __LINE__, #x,   \
+                                   cudaGetErrorString(e_));                                     \
+      return MASQ_ERR_CUDA;                                                                     \
+    }                                                                                           \
   } while (0)
 
 masq_status check_bits(int32_t b) {

@@ -1,7 +1,9 @@
 // prof.cu — opt-in kernel timing.  When enabled (masq_profile_enable), every kernel launch of
 // the library is bracketed by a cudaEvent pair recorded on the launching stream; the durations
 // are aggregated per kernel name by masq_profile_collect.  This is the only process-global
-// state in the library and it is off by default.
+// state in the library and it is off by default.  Launches inside a CUDA-graph capture record
+// their pairs as graph nodes (the pool is pre-filled), so each replay re-times them and a
+// collect after replays reports the last replay.
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -33,11 +35,22 @@ cudaEvent_t get_event() {
 }
 }  // namespace
 
+namespace {
+// inside a stream capture the record must be an external event node to stay timeable at replay
+void record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, st);
+}
+}  // namespace
+
 ProfScope::ProfScope(const char* name, cudaStream_t st) : name_(name), st_(st) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_on) return;
   a_ = get_event();
-  if (a_) cudaEventRecord(static_cast<cudaEvent_t>(a_), st_);
+  if (a_) record(static_cast<cudaEvent_t>(a_), st_);
 }
 
 ProfScope::~ProfScope() {
@@ -45,7 +58,7 @@ ProfScope::~ProfScope() {
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEvent_t b = get_event();
   if (!b) return;
-  cudaEventRecord(b, st_);
+  record(b, st_);
   g_recs.push_back(Rec{name_, static_cast<cudaEvent_t>(a_), b});
 }
 
@@ -61,6 +74,13 @@ int32_t masq_profile_enable(int32_t on) {
   g_on = on != 0;
   for (auto& r : g_recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
   g_recs.clear();
+  // pre-create the events so that launches recorded inside a CUDA-graph capture never need
+  // cudaEventCreate (not a capturable call); the records then become graph nodes
+  while (g_on && g_pool.size() < 2048) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    g_pool.push_back(e);
+  }
   return prev;
 }
 
@@ -69,10 +89,14 @@ int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms,
   std::vector<std::string> keys;
   std::vector<double> ms;
   std::vector<int64_t> cnt;
+  int failed = 0;
   for (auto& r : g_recs) {
-    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
     float t = 0.f;
-    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return -1;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) {
+      cudaGetLastError();                           // do not leave a sticky error for the caller
+      ++failed;
+      continue;
+    }
     size_t k = 0;
     while (k < keys.size() && keys[k] != r.name) ++k;
     if (k == keys.size()) { keys.emplace_back(r.name); ms.push_back(0.0); cnt.push_back(0); }
@@ -82,6 +106,7 @@ int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms,
     g_pool.push_back(r.b);
   }
   g_recs.clear();
+  if (failed && keys.empty()) return -1;
   const int32_t n = (int32_t)std::min<size_t>(keys.size(), (size_t)std::max(max_entries, 0));
   for (int32_t i = 0; i < n; ++i) {
     if (names) {
