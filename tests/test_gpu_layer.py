@@ -36,3 +36,54 @@ def test_calib_layer_equals_separate_calls(name, use_cmc):
     assert torch.allclose(sums, s2, rtol=1e-12, atol=0) and torch.allclose(loss, l2, rtol=1e-12, atol=0)
     _, _, lo = O.calib_loss(c["X"], c["ids"], so, c["W"], c["wbits"], c["abits"])
     assert abs(float(loss.cpu()[0]) - lo) <= 1e-3 * abs(lo)
+
+
+@pytest.mark.parametrize("profile", [False, True])
+def test_calib_layer_cuda_graph_replay(profile):
+    """The library is stream-ordered and allocation-free, so a calibration step can be captured
+    as a CUDA graph (also with the opt-in profiler on) and replayed: results equal the eager run."""
+    import ctypes
+    from paper_2603_04800_b200._lib import lib
+    m = M()
+    c = case("ragged3")
+    _, _, so, _, _ = oracle_state(c)
+    X, W, ids, s = bf(c["X"]), bf(c["W"]), tt(c["ids"]), tt(so)
+    L1, L2 = bf(c["L1"]), bf(c["L2"])
+    ws = m.Workspace(torch.device("cuda", 0))
+    n = W.shape[1]
+    outs = [torch.empty(X.shape[0], n, device="cuda") for _ in range(2)]
+    sums = torch.empty(3, dtype=torch.float64, device="cuda")
+    counts = torch.empty(3, dtype=torch.int64, device="cuda")
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    R = torch.empty(3, X.shape[1], device="cuda")
+    cnt = torch.empty(3, dtype=torch.int64, device="cuda")
+
+    def step():
+        m.calibrate_stats(X, ids, 3, R=R, count=cnt, ws=ws)
+        m.calib_layer(X, ids, s, W, 8, 8, L1, L2, Y=outs[0], Yref=outs[1], sums=sums, counts=counts, loss=loss,
+                      ws=ws)
+
+    step()
+    torch.cuda.synchronize()
+    ref = [t.clone() for t in (outs[0], outs[1], sums, counts, loss, R)]
+    if profile:
+        lib().masq_profile_enable(1)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for t in (outs[0], outs[1], sums, loss, R):
+        t.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    if profile:
+        names = ctypes.create_string_buffer(32 * 64)
+        tot = (ctypes.c_double * 64)()
+        cn = (ctypes.c_int64 * 64)()
+        assert lib().masq_profile_collect(64, names, tot, cn) > 0
+        lib().masq_profile_enable(0)
+    for a, b in zip((outs[0], outs[1], sums, counts, loss, R), ref):
+        assert torch.equal(a, b)
+    m.check(ws)
+    step()                                              # eager again after the graph
+    torch.cuda.synchronize()
