@@ -133,7 +133,11 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       const int64_t nkeys = (int64_t)n_mod * n + Tg;
       L.keys = take(sizeof(int32_t) * nkeys);
       L.vals = take(sizeof(double) * nkeys);
-      L.bucket = take(sizeof(double) * (size_t)bucket_chunks(nkeys) * n_mod * d);
+      L.bucket = take(sizeof(double) * (size_t)n_mod * d);          // per-channel scale-term contributions
+      L.skeys = take(sizeof(uint32_t) * nkeys);
+      L.svals = take(sizeof(double) * nkeys);
+      L.stemp_bytes = bucket_temp_bytes(nkeys);
+      L.stemp = take(L.stemp_bytes);
       break;
     }
     default:
@@ -604,8 +608,9 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     MASQ_CK(launch_gemm(ga, st));
     MASQ_CK(launch_gradkeys(bpart, 4 * gradgemm_ntiles_i(d), kj, colmax, wbits, apart, 2 * num_n, ktkey, n_mod, d,
                             d_out, Tg, keys, vals, st));
-    MASQ_CK(launch_bucket(keys, vals, nkeys, (int64_t)n_mod * d, bucket, st));
-    MASQ_CK(launch_gradreduce(gpart, bucket, bucket_chunks(nkeys), count_norm ? count_norm : cnt, lambda, n_mod,
+    MASQ_CK(launch_bucket(keys, vals, nkeys, (int64_t)n_mod * d, reinterpret_cast<uint32_t*>(W8(ws, L.skeys)),
+                          reinterpret_cast<double*>(W8(ws, L.svals)), W8(ws, L.stemp), L.stemp_bytes, bucket, st));
+    MASQ_CK(launch_gradreduce(gpart, bucket, count_norm ? count_norm : cnt, lambda, n_mod,
                               gradgemm_ntiles_j(d_out), d, d_out, grad, st));
   }
   return MASQ_OK;

@@ -20,6 +20,7 @@
 // TMEM accumulators (Q' in columns 0..255, P in 256..511).  The epilogue reads W and the tile
 // of Q(S_m W) (TMA) and reduces over j into one partial per (modality, j-tile, i); a
 // fixed-order reduction forms the gradient (deterministic).
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -52,7 +53,7 @@ struct GParams {
   const float* dw;               // [M][n]
   const uint32_t* colmax;        // [M][n] f32 bits of max_i |s_i w_ij|
   double* partial;               // [M][nj][d]
-  float* bpart;                  // [M][4 * ni][n]
+  float* bpart;                  // [M][4 * ni][n]  (one row per 32-row warp group)
   int32_t* kj;                   // [M][n]
 };
 
@@ -350,64 +351,63 @@ __global__ void codes16_kernel(const int8_t* __restrict__ q, int64_t count, uint
   *reinterpret_cast<uint4*>(out + i) = make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// keys / values of the scale terms (fixed-order partial sums)
-__global__ void gradkeys_kernel(const float* __restrict__ bpart, int nb, const int32_t* __restrict__ kj,
-                                const uint32_t* __restrict__ colmax, float qw, const float* __restrict__ apart, int na,
-                                const int32_t* __restrict__ ktkey, int n_mod, int64_t d, int64_t n, int64_t Tg,
-                                int32_t* __restrict__ keys, double* __restrict__ vals) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nj = (int64_t)n_mod * n;
-  if (idx < nj) {
-    const int64_t m = idx / n, j = idx - m * n;
+// beta keys / values: one CTA per (modality, 32 columns); thread (r0 = tid >> 5, lane = column)
+// sums the row groups r = r0, r0 + 8, ...; the 8 partial sums are added in a fixed order
+__global__ void __launch_bounds__(256) betakeys_kernel(const float* __restrict__ bpart, int nb,
+                                                       const int32_t* __restrict__ kj,
+                                                       const uint32_t* __restrict__ colmax, float qw, int64_t d,
+                                                       int64_t n, int32_t* __restrict__ keys,
+                                                       double* __restrict__ vals) {
+  __shared__ double sh[8][32];
+  const int64_t cb = (int64_t)blockIdx.x * 32;                 // column base in [0, n_mod * n)
+  const int64_t m = cb / n, j = cb - m * n + (threadIdx.x & 31);
+  const int r0 = threadIdx.x >> 5;
+  double a = 0.0;
+  for (int r = r0; r < nb; r += 8) a += (double)bpart[((int64_t)m * nb + r) * n + j];
+  sh[r0][threadIdx.x & 31] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
     double b = 0.0;
-    for (int r = 0; r < nb; ++r) b += (double)bpart[((int64_t)m * nb + r) * n + j];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) b += sh[q][threadIdx.x];
+    const int64_t idx = m * n + j;
     const int32_t k = kj[idx];
     const bool live = k >= 0 && k < d && __fdiv_rn(__uint_as_float(colmax[idx]), qw) >= 1e-12f;
     keys[idx] = live ? (int32_t)(m * d + k) : -1;
     vals[idx] = b;
-  } else if (idx < nj + Tg) {
-    const int64_t t = idx - nj;
-    double a = 0.0;
-    for (int r = 0; r < na; ++r) a += (double)apart[t * na + r];
-    keys[idx] = ktkey[t];
-    vals[idx] = -a;
   }
 }
 
-constexpr int kBucketChunk = 2048;
-
-// bucket[c][l] = sum_{k in chunk c, keys[k] == l} vals[k]   (fixed order within the chunk)
-__global__ void __launch_bounds__(256) bucket_kernel(const int32_t* __restrict__ keys, const double* __restrict__ vals,
-                                                     int64_t nkeys, int64_t nl, double* __restrict__ bucket) {
-  __shared__ int32_t sk[kBucketChunk];
-  __shared__ double sv[kBucketChunk];
-  const int64_t k0 = (int64_t)blockIdx.y * kBucketChunk;
-  const int nk = (int)(nkeys - k0 < kBucketChunk ? nkeys - k0 : kBucketChunk);
-  const int64_t lbase = (int64_t)blockIdx.x * 256;
-  int cnt = 0;
-  for (int k = threadIdx.x; k < nk; k += 256) {
-    const int32_t key = keys[k0 + k];
-    sk[k] = key;
-    sv[k] = vals[k0 + k];
-    cnt += (key >= lbase && key < lbase + 256) ? 1 : 0;
-  }
-  cnt = __syncthreads_or(cnt);
-  const int64_t l = lbase + threadIdx.x;
-  if (l >= nl) return;
+// alpha keys / values: (ktkey[t], -alpha_t), alpha_t = the row's partials summed in order
+__global__ void alphakeys_kernel(const float* __restrict__ apart, int na, const int32_t* __restrict__ ktkey,
+                                 int64_t Tg, int32_t* __restrict__ keys, double* __restrict__ vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Tg) return;
   double a = 0.0;
-  if (cnt)
-    for (int k = 0; k < nk; ++k)
-      if (sk[k] == (int32_t)l) a += sv[k];
-  bucket[(int64_t)blockIdx.y * nl + l] = a;
+  for (int r = 0; r < na; ++r) a += (double)apart[t * na + r];
+  keys[t] = ktkey[t];
+  vals[t] = -a;
 }
 
 struct Lam8 {
   float v[kMaxMod];
 };
 
-// grad[m][i] = lambda_m / (counts_m * n) * (sum_jt partial[m][jt][i] + sum_c bucket[c][m*d + i])
-// (fixed order)
-__global__ void gradreduce_kernel(const double* __restrict__ partial, const double* __restrict__ bucket, int nchunks,
+// contrib[l] = sum of vals over the run of keys == l in the (stably) sorted key list, in the
+// original order of the keys (radix sort is stable) -> deterministic; keys -1 sort last
+__global__ void runsum_kernel(const uint32_t* __restrict__ skeys, const double* __restrict__ svals, int64_t nkeys,
+                              int64_t nl, double* __restrict__ contrib) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nkeys) return;
+  const uint32_t k = skeys[i];
+  if (k >= (uint32_t)nl || (i > 0 && skeys[i - 1] == k)) return;     // not a run start
+  double a = 0.0;
+  for (int64_t j = i; j < nkeys && skeys[j] == k; ++j) a += svals[j];
+  contrib[k] = a;
+}
+
+// grad[m][i] = lambda_m / (counts_m * n) * (sum_jt partial[m][jt][i] + contrib[m*d + i])  (fixed order)
+__global__ void gradreduce_kernel(const double* __restrict__ partial, const double* __restrict__ contrib,
                                   const int64_t* __restrict__ counts, Lam8 lam, int n_mod, int nj, int64_t d,
                                   int64_t n, double* __restrict__ grad) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -416,7 +416,7 @@ __global__ void gradreduce_kernel(const double* __restrict__ partial, const doub
   const int64_t i = idx - (int64_t)m * d;
   double a = 0.0;
   for (int jt = 0; jt < nj; ++jt) a += partial[((int64_t)m * nj + jt) * d + i];
-  for (int c = 0; c < nchunks; ++c) a += bucket[(int64_t)c * n_mod * d + idx];
+  a += contrib[idx];
   const int64_t c = counts[m];
   grad[idx] = c > 0 ? (double)lam.v[m] * a / ((double)c * (double)n) : 0.0;
 }
@@ -495,20 +495,31 @@ cudaError_t launch_gradkeys(const float* bpart, int nb, const int32_t* kj, const
                             const float* apart, int na, const int32_t* ktkey, int n_mod, int64_t d, int64_t n,
                             int64_t Tg, int32_t* keys, double* vals, cudaStream_t st) {
   ProfScope ps_("gradkeys", st);
-  const int64_t count = (int64_t)n_mod * n + Tg;
-  gradkeys_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(bpart, nb, kj, colmax,
-                                                                  (float)((1 << (wbits - 1)) - 1), apart, na, ktkey,
-                                                                  n_mod, d, n, Tg, keys, vals);
+  betakeys_kernel<<<(unsigned)((int64_t)n_mod * n / 32), 256, 0, st>>>(bpart, nb, kj, colmax,
+                                                                      (float)((1 << (wbits - 1)) - 1), d, n, keys,
+                                                                      vals);
+  const int64_t nj = (int64_t)n_mod * n;
+  alphakeys_kernel<<<(unsigned)ceil_div(Tg, 256), 256, 0, st>>>(apart, na, ktkey, Tg, keys + nj, vals + nj);
   return cudaGetLastError();
 }
 
-int bucket_chunks(int64_t nkeys) { return (int)ceil_div(nkeys, kBucketChunk); }
+size_t bucket_temp_bytes(int64_t nkeys) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const double*)nullptr,
+                                  (double*)nullptr, (int)nkeys, 0, 32);
+  return bytes;
+}
 
-cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys, int64_t nl, double* bucket,
-                          cudaStream_t st) {
+cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys, int64_t nl, uint32_t* skeys,
+                          double* svals, void* temp, size_t temp_bytes, double* contrib, cudaStream_t st) {
   ProfScope ps_("bucket", st);
-  dim3 grid((unsigned)ceil_div(nl, 256), (unsigned)bucket_chunks(nkeys));
-  bucket_kernel<<<grid, 256, 0, st>>>(keys, vals, nkeys, nl, bucket);
+  cudaError_t e = cudaMemsetAsync(contrib, 0, sizeof(double) * nl, st);
+  if (e != cudaSuccess) return e;
+  size_t tb = temp_bytes;
+  e = cub::DeviceRadixSort::SortPairs(temp, tb, reinterpret_cast<const uint32_t*>(keys), skeys, vals, svals,
+                                      (int)nkeys, 0, 32, st);
+  if (e != cudaSuccess) return e;
+  runsum_kernel<<<(unsigned)ceil_div(nkeys, 256), 256, 0, st>>>(skeys, svals, nkeys, nl, contrib);
   return cudaGetLastError();
 }
 
@@ -554,15 +565,15 @@ cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* 
 int gradgemm_ntiles_j(int64_t n) { return (int)ceil_div(n, GN); }
 int gradgemm_ntiles_i(int64_t d) { return (int)ceil_div(d, GM); }
 
-cudaError_t launch_gradreduce(const double* partial, const double* bucket, int nchunks, const int64_t* counts,
+cudaError_t launch_gradreduce(const double* partial, const double* contrib, const int64_t* counts,
                               const float* lambda_host, int n_mod, int nj, int64_t d, int64_t n, double* grad,
                               cudaStream_t st) {
   Lam8 l;
   for (int m = 0; m < kMaxMod; ++m) l.v[m] = (lambda_host && m < n_mod) ? lambda_host[m] : 1.0f;
   const int64_t count = (int64_t)n_mod * d;
   ProfScope ps_("gradreduce", st);
-  gradreduce_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(partial, bucket, nchunks, counts, l, n_mod, nj, d,
-                                                                    n, grad);
+  gradreduce_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(partial, contrib, counts, l, n_mod, nj, d, n,
+                                                                    grad);
   return cudaGetLastError();
 }
 

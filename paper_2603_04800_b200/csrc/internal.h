@@ -29,7 +29,8 @@ struct WsLayout {
   size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, cnt = 0, total = 0;
   size_t gsign = 0, planes = 0, gpartial = 0;
   // N1 scale terms
-  size_t codes16 = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0;
+  size_t codes16 = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0, skeys = 0, svals = 0,
+         stemp = 0, stemp_bytes = 0;
   // N2 CMC factors (f64)
   size_t a64 = 0, g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
          work = 0, info = 0, dot = 0;
@@ -160,15 +161,16 @@ cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* 
 int gradgemm_ntiles_j(int64_t n);
 int gradgemm_ntiles_i(int64_t d);
 // keys/vals [n_mod*n + Tg]: (m*d + k_j, +beta_j) for every weight column, (ktkey[t], -alpha_t) for
-// every grouped row; alpha_t = sum of apart[t][0..na), beta = sum of bpart over the 4*ni row groups
+// every grouped row; alpha_t = sum of apart[t][0..na), beta = sum of bpart over the nb row groups
 cudaError_t launch_gradkeys(const float* bpart, int nb, const int32_t* kj, const uint32_t* colmax, int wbits,
                             const float* apart, int na, const int32_t* ktkey, int n_mod, int64_t d, int64_t n,
                             int64_t Tg, int32_t* keys, double* vals, cudaStream_t st);
-int bucket_chunks(int64_t nkeys);
-// bucket[c][l] = sum over keys of chunk c equal to l of vals (fixed order), l in [0, n_mod*d)
-cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys, int64_t nl, double* bucket,
-                          cudaStream_t st);
-cudaError_t launch_gradreduce(const double* partial, const double* bucket, int nchunks, const int64_t* counts,
+size_t bucket_temp_bytes(int64_t nkeys);
+// contrib[l] = sum of vals over keys == l (l in [0, nl)), summed in key order after a stable radix
+// sort (deterministic); skeys / svals / temp are workspace
+cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys, int64_t nl, uint32_t* skeys,
+                          double* svals, void* temp, size_t temp_bytes, double* contrib, cudaStream_t st);
+cudaError_t launch_gradreduce(const double* partial, const double* contrib, const int64_t* counts,
                               const float* lambda_host, int n_mod, int nj, int64_t d, int64_t n, double* grad,
                               cudaStream_t st);
 cudaError_t launch_adam_init(const float* s, double* theta, double* m1, double* m2, int64_t count, cudaStream_t st);
