@@ -337,3 +337,33 @@ def test_forward_max_tokens_sampled():
     assert max_abs_norm(Y.cpu().numpy()[rows], Yo) <= TOL_Y
     qxo, _ = O.quantize_activations(O.decode(X)[rows], ids[rows], so, 8)
     assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), O.int_gemm(qxo, qwo))
+
+
+def test_eight_modalities_end_to_end():
+    """n_mod = 8 (the ABI maximum), ragged modality runs, CMC for 7 non-text modalities: stats,
+    factors and codes bit-exact, forward and loss against the oracle."""
+    m = M()
+    n_mod, d, n, r = 8, 96, 160, 16
+    pattern = [(0, 40), (3, 70), (1, 33), (7, 90), (2, 64), (5, 17), (4, 120), (6, 55), (0, 23)]
+    ids = synth.modality_ids(pattern, repeat=3)
+    X = synth.activations(ids, d, n_mod, 4242, gamma=dict(enumerate([1.0, 20.0, 0.3, 5.0, 2.0, 50.0, 0.1, 8.0])))
+    W = synth.weight(d, n, 4243)
+    L1, L2 = synth.lowrank(d, n, r, n_mod, 4244)
+    R, cnt = O.calibrate_stats(X, ids, n_mod)
+    s = O.init_factors(R, cnt, W)
+    Rg, cg = m.calibrate_stats(bf(X), tt(ids), n_mod)
+    sg = m.init_factors(Rg, cg, bf(W))
+    m.check()
+    assert np.array_equal(Rg.cpu().numpy(), R) and np.array_equal(sg.cpu().numpy(), s)
+    qw, dw = O.quantize_weight(W, s[0], 8)
+    qwg, dwg = m.quantize_weight(bf(W), sg[0], 8)
+    assert np.array_equal(qwg.cpu().numpy(), qw) and np.array_equal(dwg.cpu().numpy(), dw)
+    Y = m.linear_forward(bf(X), tt(ids), sg, qwg, dwg, 8, 8, bf(L1), bf(L2)).cpu().numpy()
+    Yo = O.linear_forward(X, ids, s, qw, dw, 8, list(L1), list(L2))
+    assert max_abs_norm(Y, Yo) <= TOL_Y
+    Yref = m.reference_output(bf(X), bf(W))
+    sums, counts, loss = m.calib_loss(bf(X), tt(ids), sg, bf(W), 8, 8, Yref)
+    so, co, lo = O.calib_loss(X, ids, s, W, 8, 8)
+    assert np.array_equal(counts.cpu().numpy(), co)
+    assert np.all(np.abs(sums.cpu().numpy() - so) <= TOL_L * np.abs(so))
+    assert abs(float(loss.cpu()[0]) - lo) <= TOL_L * abs(lo)
