@@ -71,7 +71,8 @@ typedef void* masq_stream;      /* cudaStream_t */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
   MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,
-  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9, MASQ_OP_DECODE = 10, MASQ_OP_LAYER = 11
+  MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9, MASQ_OP_DECODE = 10, MASQ_OP_LAYER = 11,
+  MASQ_OP_CMC_GRAM = 12, MASQ_OP_CMC_FACTORS = 13
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -267,6 +268,20 @@ masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64
                                const float* s_t, const uint8_t* packed, const float* scales, int32_t group,
                                int32_t abits, float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
                                masq_stream stream);
+
+/* The two phases of masq_cmc_factors, for token-sharded / multi-batch runs: G[(m-1) d d] (+)=
+ * A_m^T A_m for every non-text modality m (f64, lower triangle; accumulate != 0 adds to G) —
+ * all-reduce G with SUM across ranks / batches — then the factors and the Theorem-2 residual
+ * <E, G E> from G alone (the activations enter only through their Gram matrix).  "Lower" is in
+ * column-major (cuBLAS) order, i.e. the upper triangle of a row-major [d x d] array. */
+masq_status masq_cmc_gram(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                          int64_t d, int32_t n_mod, const float* s, double* G, int32_t accumulate,
+                          void* ws, size_t ws_bytes, masq_stream stream);
+masq_status masq_cmc_factors_from_gram(const double* G, int64_t d, int64_t d_out, int32_t n_mod,
+                                       const float* s, const void* W, masq_dtype wt,
+                                       const int8_t* qw_text, const float* dw_text, int32_t r,
+                                       double eps_rel, void* L1, void* L2, masq_dtype lt, double* resid,
+                                       void* ws, size_t ws_bytes, masq_stream stream);
 
 /* ---------------------------------------------------------------- N4: baseline factor methods
  * — the closed forms the paper compares MASQuant against, on the same data. */

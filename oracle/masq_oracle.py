@@ -446,7 +446,13 @@ def whitening_transform(A, eps_rel: float = 1e-8):
     before the square roots, eps = eps_rel * lambda_max (reading Q27).
     A = X_m S_m^-1 (f64 of the f32 smoothed activations).  Returns (T, T^-1, lambda)."""
     A = np.asarray(A, F64)
-    lam, P = np.linalg.eigh(A.T @ A)
+    return whitening_from_gram(A.T @ A, eps_rel)
+
+
+def whitening_from_gram(G, eps_rel: float = 1e-8):
+    """The same transform from the Gram matrix G = A^T A (token-sharded runs SUM their shards'
+    Grams)."""
+    lam, P = np.linalg.eigh(np.asarray(G, F64))
     lam = np.maximum(lam, 0.0)
     lam_r = lam + eps_rel * lam.max()
     T = (P * np.sqrt(lam_r)[None, :]).T
@@ -457,7 +463,13 @@ def whitening_transform(A, eps_rel: float = 1e-8):
 def cmc_factors(A, dW, r: int, eps_rel: float = 1e-8):
     """PAPER.md:143-149 (eq:l1l2): SVD(T dW) = U Sigma V^T ~ U_r Sigma_r V_r^T,
     L1 = T^-1 U_r [d x r], L2 = Sigma_r V_r^T [r x n]; r = 0 -> empty factors."""
-    T, T_inv, _ = whitening_transform(A, eps_rel)
+    A = np.asarray(A, F64)
+    return cmc_factors_from_gram(A.T @ A, dW, r, eps_rel)
+
+
+def cmc_factors_from_gram(G, dW, r: int, eps_rel: float = 1e-8):
+    """cmc_factors with the activations entering only through G = A^T A."""
+    T, T_inv, _ = whitening_from_gram(G, eps_rel)
     d, n = dW.shape
     if r == 0:
         return np.zeros((d, 0)), np.zeros((0, n))
@@ -469,6 +481,12 @@ def reconstruction_loss(A, dW, L1, L2) -> float:
     """Theorem 2 objective ||A (dW - L1 L2)||_F^2 in f64."""
     A = np.asarray(A, F64)
     return float(np.sum((A @ (dW - L1 @ L2)) ** 2))
+
+
+def reconstruction_loss_from_gram(G, dW, L1, L2) -> float:
+    """The same objective as <E, G E> with E = dW - L1 L2 (no T x n product)."""
+    E = dW - L1 @ L2
+    return float(np.sum(E * (np.asarray(G, F64) @ E)))
 
 
 def naive_svd_factors(dW, r: int):

@@ -51,6 +51,11 @@ SIGNATURES = {
     "masq_unpack_int4": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
     "masq_linear_decode": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p,
                                      c_void_p, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_size_t, c_void_p]),
+    "masq_cmc_gram": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
+                                c_int32, c_void_p, c_size_t, c_void_p]),
+    "masq_cmc_factors_from_gram": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_int32,
+                                             c_void_p, c_void_p, c_int32, ctypes.c_double, c_void_p, c_void_p,
+                                             c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),
     "masq_smooth_factors": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, ctypes.c_double, c_void_p, c_void_p]),
     "masq_calibrate_meanabs": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),

@@ -24,56 +24,33 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     case MASQ_OP_STATS:
     case MASQ_OP_INIT:
       break;
-    case MASQ_OP_CMC: {
-      L.inv_s = take(sizeof(float) * n_mod * d);
-      L.a64 = take(sizeof(double) * (size_t)T * d);
-      L.g = take(sizeof(double) * (size_t)d * d);
-      L.c = take(sizeof(double) * (size_t)d * d);
-      L.lam = take(sizeof(double) * d);
-      L.sig2 = take(sizeof(double) * d);
-      L.sq = take(sizeof(double) * d);
-      L.isq = take(sizeof(double) * d);
-      L.dw64 = take(sizeof(double) * (size_t)d * n);
-      L.m64 = take(sizeof(double) * (size_t)d * n);
-      L.l1t64 = take(sizeof(double) * (size_t)d * r);
-      L.urs = take(sizeof(double) * (size_t)d * r);
-      L.l2t64 = take(sizeof(double) * (size_t)r * n);
-      L.lwork = cmc_syevd_lwork(d);
-      L.work = take(sizeof(double) * (L.lwork + 1));
-      L.info = take(sizeof(int) * 2);
-      L.dot = take(sizeof(double) * cmc_dot_blocks());
-      break;
-    }
-    case MASQ_OP_LAYER: {
-      const int64_t Tg = grouped_rows(T, n_mod);
-      L.inv_s = take(sizeof(float) * n_mod * d);
-      L.qx_tok = take((size_t)T * d);
-      L.dx_tok = take(sizeof(float) * T);
-      L.mask = take(sizeof(uint32_t) * tiles_m);
-      L.qx = take((size_t)Tg * d);
-      L.dx = take(sizeof(float) * Tg);
-      L.perm = take(sizeof(int32_t) * Tg);
-      L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
-      L.cnt = take(sizeof(int64_t) * n_mod);
-      L.qw_all = take((size_t)n_mod * n * d);
-      L.dw_all = take(sizeof(float) * n_mod * n);
-      L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
-      L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
-      L.fpart = take(sizeof(double) * ceil_div(T, kUnitM) * ceil_div(n, kTileN) * 2);
-      if (rp > 0 && nnt > 0) {
-        L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
-        L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
-        L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
+    case MASQ_OP_CMC:
+    case MASQ_OP_CMC_GRAM:
+    case MASQ_OP_CMC_FACTORS: {
+      if (op != MASQ_OP_CMC_FACTORS) {
+        L.inv_s = take(sizeof(float) * n_mod * d);
+        L.a64 = take(sizeof(double) * (size_t)T * d);
+      }
+      if (op == MASQ_OP_CMC) L.gall = take(sizeof(double) * (size_t)(n_mod > 1 ? n_mod - 1 : 1) * d * d);
+      if (op != MASQ_OP_CMC_GRAM) {
+        L.g = take(sizeof(double) * (size_t)d * d);
+        L.c = take(sizeof(double) * (size_t)d * d);
+        L.lam = take(sizeof(double) * d);
+        L.sig2 = take(sizeof(double) * d);
+        L.sq = take(sizeof(double) * d);
+        L.isq = take(sizeof(double) * d);
+        L.dw64 = take(sizeof(double) * (size_t)d * n);
+        L.m64 = take(sizeof(double) * (size_t)d * n);
+        L.l1t64 = take(sizeof(double) * (size_t)d * r);
+        L.urs = take(sizeof(double) * (size_t)d * r);
+        L.l2t64 = take(sizeof(double) * (size_t)r * n);
+        L.lwork = cmc_syevd_lwork(d);
+        L.work = take(sizeof(double) * (L.lwork + 1));
+        L.info = take(sizeof(int) * 2);
+        L.dot = take(sizeof(double) * cmc_dot_blocks());
       }
       break;
     }
-    case MASQ_OP_DECODE:
-      L.inv_s = take(sizeof(float) * d);
-      L.ids0 = take((size_t)T);
-      L.qx = take((size_t)T * d);
-      L.dx = take(sizeof(float) * T);
-      L.dpart = take(sizeof(float) * (size_t)decode_kchunks(d) * (n / 8) * 128);
-      break;
     case MASQ_OP_MEANABS:
       L.partials = take(sizeof(float) * (size_t)meanabs_slabs(T) * n_mod * d);
       break;
@@ -664,37 +641,15 @@ masq_status masq_keep_best(const double* loss, double* best_loss, const float* s
   return MASQ_OK;
 }
 
-masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
-                             int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
-                             const int8_t* qw_text, const float* dw_text, int32_t r, double eps_rel, void* L1,
-                             void* L2, masq_dtype lt, double* resid, void* ws, size_t ws_bytes, masq_stream stream) {
-  MASQ_TRY(check_common(T, d, n_mod));
-  if (n_mod < 2) return MASQ_ERR_SHAPE;
-  if (d_out <= 0 || r < 1 || r > d || r > d_out || !(eps_rel >= 0.0)) return MASQ_ERR_SHAPE;
-  if (d > 2147483647 / 8 || d_out > 2147483647 / 8 || T > 2147483647) return MASQ_ERR_SHAPE;
-  if (!s || !W || !qw_text || !dw_text || !L1 || !L2) return MASQ_ERR_NULL;
-  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
-  if (lt != MASQ_BF16 && lt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
-  if (T > 0) {
-    MASQ_TRY(check_x(X, xt, ld_x, d));
-    if (!mod_id) return MASQ_ERR_NULL;
-  }
-  if (!cmc_linalg_available()) return MASQ_ERR_UNSUPPORTED;
-  const WsLayout L = ws_layout(MASQ_OP_CMC, T, d, d_out, n_mod, r);
-  if (L.lwork == 0) return MASQ_ERR_UNSUPPORTED;
-  MASQ_TRY(check_ws(ws, ws_bytes, L));
-  cudaStream_t st = S(stream);
+namespace {
+CmcArgs cmc_factor_args(const WsLayout& L, void* ws, int64_t d, int64_t d_out, int32_t n_mod, const float* s,
+                        const void* W, masq_dtype wt, const int8_t* qw_text, const float* dw_text, int32_t r,
+                        double eps_rel, void* L1, void* L2, masq_dtype lt, double* resid) {
   CmcArgs a{};
-  a.X = X;
-  a.xt = xt;
-  a.ld_x = ld_x;
-  a.ids = mod_id;
-  a.T = T;
   a.d = d;
   a.n = d_out;
   a.n_mod = n_mod;
   a.r = r;
-  a.inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
   a.s = s;
   a.W = W;
   a.wt = wt;
@@ -705,7 +660,6 @@ masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const u
   a.L2 = L2;
   a.lt = lt;
   a.resid = resid;
-  a.A64 = reinterpret_cast<double*>(W8(ws, L.a64));
   a.G = reinterpret_cast<double*>(W8(ws, L.g));
   a.C = reinterpret_cast<double*>(W8(ws, L.c));
   a.lam = reinterpret_cast<double*>(W8(ws, L.lam));
@@ -721,8 +675,96 @@ masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const u
   a.info = reinterpret_cast<int*>(W8(ws, L.info));
   a.dot = reinterpret_cast<double*>(W8(ws, L.dot));
   a.lwork = L.lwork;
-  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, const_cast<float*>(a.inv), st));
-  const cudaError_t e = launch_cmc_factors(a, st);
+  return a;
+}
+
+masq_status cmc_factor_checks(int64_t d, int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
+                              const int8_t* qw_text, const float* dw_text, int32_t r, double eps_rel,
+                              const void* L1, const void* L2, masq_dtype lt) {
+  MASQ_TRY(check_common(0, d, n_mod));
+  if (n_mod < 2) return MASQ_ERR_SHAPE;
+  if (d_out <= 0 || r < 1 || r > d || r > d_out || !(eps_rel >= 0.0)) return MASQ_ERR_SHAPE;
+  if (d > 2147483647 / 8 || d_out > 2147483647 / 8) return MASQ_ERR_SHAPE;
+  if (!s || !W || !qw_text || !dw_text || !L1 || !L2) return MASQ_ERR_NULL;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (lt != MASQ_BF16 && lt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (!cmc_linalg_available()) return MASQ_ERR_UNSUPPORTED;
+  return MASQ_OK;
+}
+
+masq_status cmc_gram_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                          int32_t n_mod, const float* s, double* G, int32_t accumulate, const WsLayout& L, void* ws,
+                          cudaStream_t st) {
+  CmcArgs a{};
+  a.X = X;
+  a.xt = xt;
+  a.ld_x = ld_x;
+  a.ids = mod_id;
+  a.T = T;
+  a.d = d;
+  a.n_mod = n_mod;
+  a.inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  a.A64 = reinterpret_cast<double*>(W8(ws, L.a64));
+  if (T > 0) MASQ_CK(launch_inv(s, (int64_t)n_mod * d, const_cast<float*>(a.inv), st));
+  const cudaError_t e = launch_cmc_gram(a, G, accumulate, st);
+  if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
+  MASQ_CK(e);
+  return MASQ_OK;
+}
+}  // namespace
+
+masq_status masq_cmc_gram(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                          int32_t n_mod, const float* s, double* G, int32_t accumulate, void* ws, size_t ws_bytes,
+                          masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  if (n_mod < 2) return MASQ_ERR_SHAPE;
+  if (d > 2147483647 / 8 || T > 2147483647) return MASQ_ERR_SHAPE;
+  if (!s || !G) return MASQ_ERR_NULL;
+  if (T > 0) {
+    MASQ_TRY(check_x(X, xt, ld_x, d));
+    if (!mod_id) return MASQ_ERR_NULL;
+  }
+  if (!cmc_linalg_available()) return MASQ_ERR_UNSUPPORTED;
+  const WsLayout L = ws_layout(MASQ_OP_CMC_GRAM, T, d, 0, n_mod, 0);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  return cmc_gram_core(X, xt, ld_x, mod_id, T, d, n_mod, s, G, accumulate, L, ws, S(stream));
+}
+
+masq_status masq_cmc_factors_from_gram(const double* G, int64_t d, int64_t d_out, int32_t n_mod, const float* s,
+                                       const void* W, masq_dtype wt, const int8_t* qw_text, const float* dw_text,
+                                       int32_t r, double eps_rel, void* L1, void* L2, masq_dtype lt, double* resid,
+                                       void* ws, size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(cmc_factor_checks(d, d_out, n_mod, s, W, wt, qw_text, dw_text, r, eps_rel, L1, L2, lt));
+  if (!G) return MASQ_ERR_NULL;
+  const WsLayout L = ws_layout(MASQ_OP_CMC_FACTORS, 0, d, d_out, n_mod, r);
+  if (L.lwork == 0) return MASQ_ERR_UNSUPPORTED;
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  const CmcArgs a = cmc_factor_args(L, ws, d, d_out, n_mod, s, W, wt, qw_text, dw_text, r, eps_rel, L1, L2, lt, resid);
+  const cudaError_t e = launch_cmc_from_gram(a, G, S(stream));
+  if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
+  MASQ_CK(e);
+  return MASQ_OK;
+}
+
+masq_status masq_cmc_factors(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T, int64_t d,
+                             int64_t d_out, int32_t n_mod, const float* s, const void* W, masq_dtype wt,
+                             const int8_t* qw_text, const float* dw_text, int32_t r, double eps_rel, void* L1,
+                             void* L2, masq_dtype lt, double* resid, void* ws, size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  MASQ_TRY(cmc_factor_checks(d, d_out, n_mod, s, W, wt, qw_text, dw_text, r, eps_rel, L1, L2, lt));
+  if (T > 2147483647) return MASQ_ERR_SHAPE;
+  if (T > 0) {
+    MASQ_TRY(check_x(X, xt, ld_x, d));
+    if (!mod_id) return MASQ_ERR_NULL;
+  }
+  const WsLayout L = ws_layout(MASQ_OP_CMC, T, d, d_out, n_mod, r);
+  if (L.lwork == 0) return MASQ_ERR_UNSUPPORTED;
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  double* G = reinterpret_cast<double*>(W8(ws, L.gall));
+  MASQ_TRY(cmc_gram_core(X, xt, ld_x, mod_id, T, d, n_mod, s, G, 0, L, ws, st));
+  const CmcArgs a = cmc_factor_args(L, ws, d, d_out, n_mod, s, W, wt, qw_text, dw_text, r, eps_rel, L1, L2, lt, resid);
+  const cudaError_t e = launch_cmc_from_gram(a, G, st);
   if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
   MASQ_CK(e);
   return MASQ_OK;

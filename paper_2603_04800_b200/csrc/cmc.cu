@@ -11,6 +11,8 @@
 //   the eigenvalues its squared singular values (only the leading r are needed)
 //   L2 = U_r^T M = Sigma_r V_r^T,  L1 = T^-1 U_r = P diag(1/sqrt Lambda') U_r
 //   resid (optional) = ||A_m (dW - L1 L2)||_F^2 = <E, G E>, E = dW - L1 L2 (Dsymm + reduction).
+// Two phases so that token-sharded runs can SUM the Grams between them:
+// launch_cmc_gram (per shard / batch, accumulating) and launch_cmc_from_gram.
 // cuBLAS / cuSOLVER are plain library linear algebra here (GEMM, SYRK, symmetric eigensolver);
 // they are loaded with dlopen on first use so that libmasq.so itself has no link dependency on
 // them (a box without them fails this call with MASQ_ERR_UNSUPPORTED, nothing else).
@@ -210,20 +212,23 @@ size_t cmc_syevd_lwork(int64_t d) {
   return (size_t)lw;
 }
 
-cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st) {
+// phase 1: G[m-1] (+)= A_m^T A_m (lower triangle) for m = 1..n_mod-1
+cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStream_t st) {
   LinAlg* L = linalg(st);
   if (!L) return cudaErrorNotSupported;
-  const int dev = cur_dev();
-  cublasHandle_t hb = L->hb[dev];
-  cusolverDnHandle_t hs = L->hs[dev];
-  const int64_t T = a.T, d = a.d, n = a.n;
-  const int r = a.r;
-  const int di = (int)d, ni = (int)n, Ti = (int)T;
-  const double one = 1.0, zero = 0.0, mone = -1.0;
-#define CK_B(x) do { if ((x) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
-#define CK_S(x) do { if ((x) != CUSOLVER_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
+  cublasHandle_t hb = L->hb[cur_dev()];
+  const int64_t T = a.T, d = a.d;
+  const int di = (int)d, Ti = (int)T;
+  const double one = 1.0, beta = accumulate ? 1.0 : 0.0;
   for (int m = 1; m < a.n_mod; ++m) {
-    // A_m and its Gram matrix
+    double* Gm = G + (int64_t)(m - 1) * d * d;
+    if (T == 0) {
+      if (!accumulate) {
+        cudaError_t e = cudaMemsetAsync(Gm, 0, sizeof(double) * d * d, st);
+        if (e != cudaSuccess) return e;
+      }
+      continue;
+    }
     {
       ProfScope ps_("cmc_xs64", st);
       const unsigned g = (unsigned)ceil_div(T * d, 256);
@@ -232,10 +237,31 @@ cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st) {
       else
         xs64_kernel<<<g, 256, 0, st>>>(static_cast<const float*>(a.X), a.ld_x, a.ids, T, d, m, a.inv, a.A64);
     }
-    {
-      ProfScope ps_("cmc_gram", st);
-      CK_B(L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, Ti, &one, a.A64, di, &zero, a.G, di));
-    }
+    ProfScope ps_("cmc_gram", st);
+    if (L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, Ti, &one, a.A64, di, &beta, Gm, di) !=
+        CUBLAS_STATUS_SUCCESS)
+      return cudaErrorUnknown;
+  }
+  return cudaGetLastError();
+}
+
+// phase 2: factors (and the Theorem-2 residual <E, G E>) from the Gram matrices
+cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStream_t st) {
+  LinAlg* L = linalg(st);
+  if (!L) return cudaErrorNotSupported;
+  const int dev = cur_dev();
+  cublasHandle_t hb = L->hb[dev];
+  cusolverDnHandle_t hs = L->hs[dev];
+  const int64_t d = a.d, n = a.n;
+  const int r = a.r;
+  const int di = (int)d, ni = (int)n;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+#define CK_B(x) do { if ((x) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
+#define CK_S(x) do { if ((x) != CUSOLVER_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
+  for (int m = 1; m < a.n_mod; ++m) {
+    const double* Gm = Gall + (int64_t)(m - 1) * d * d;
+    cudaError_t e = cudaMemcpyAsync(a.G, Gm, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
     {
       ProfScope ps_("cmc_eig_gram", st);
       CK_S(L->syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, di, a.G, di, a.lam, a.work, (int)a.lwork,
@@ -286,11 +312,10 @@ cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st) {
                                               static_cast<float*>(a.L2) + (int64_t)(m - 1) * r * n);
     }
     if (a.resid) {
-      // E = dW - L1t L2t (in place), G again (the eigensolver overwrote it), F = G E, <E, F>
+      // E = dW - L1t L2t (in place), F = G E with the (caller's) Gram, <E, F>
       ProfScope ps_("cmc_resid", st);
       CK_B(L->dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, di, ni, r, &mone, a.L1t, di, a.L2t, r, &one, a.dW, di));
-      CK_B(L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, Ti, &one, a.A64, di, &zero, a.C, di));
-      CK_B(L->dsymm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, di, ni, &one, a.C, di, a.dW, di, &zero, a.Mb, di));
+      CK_B(L->dsymm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, di, ni, &one, Gm, di, a.dW, di, &zero, a.Mb, di));
       dot_partial_kernel<<<kDotBlocks, 256, 0, st>>>(a.dW, a.Mb, d * n, a.dot);
       dot_final_kernel<<<1, 32, 0, st>>>(a.dot, kDotBlocks, a.resid + (m - 1));
     }

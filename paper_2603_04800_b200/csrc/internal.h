@@ -35,6 +35,7 @@ struct WsLayout {
   size_t a64 = 0, g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
          work = 0, info = 0, dot = 0;
   size_t lwork = 0;   // doubles
+  size_t gall = 0;    // CMC: the (n_mod-1) Gram matrices of the one-call path
   // N3 decode
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
@@ -206,7 +207,8 @@ struct CmcArgs {
 bool cmc_linalg_available();
 size_t cmc_syevd_lwork(int64_t d);
 int cmc_dot_blocks();
-cudaError_t launch_cmc_factors(const CmcArgs& a, cudaStream_t st);
+cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStream_t st);
+cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* G, cudaStream_t st);
 
 // ---------------------------------------------------------------- N3 int4 decode (decode.cu)
 int decode_kchunks(int64_t d);

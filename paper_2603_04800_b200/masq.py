@@ -13,7 +13,7 @@ from ._lib import MasqDebug, lib
 
 MASQ_F32, MASQ_BF16 = 0, 1
 (OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS,
- OP_CMC, OP_DECODE, OP_LAYER) = range(12)
+ OP_CMC, OP_DECODE, OP_LAYER, OP_CMC_GRAM, OP_CMC_FACTORS) = range(14)
 
 
 class MasqError(RuntimeError):
@@ -340,6 +340,35 @@ def linear_decode(X, s_t, packed, scales, abits: int = 8, group: int = 128, Y=No
     _ck(lib().masq_linear_decode(_p(X), _dt(X), X.stride(0), T, d, n, _p(s_t.contiguous()), _p(packed), _p(scales),
                                  group, abits, _p(Y), Y.stride(0), p, nb, _stream(stream)), "masq_linear_decode")
     return Y
+
+
+def cmc_gram(X, mod_id, s, G=None, accumulate: bool = False, ws=None, stream=None):
+    """G f64 [M-1, d, d] (lower triangle) += / = A_m^T A_m for the non-text modalities."""
+    T, d = X.shape
+    n_mod = s.shape[0]
+    G = torch.zeros(n_mod - 1, d, d, dtype=torch.float64, device=X.device) if G is None else G
+    ws = ws or default_workspace(X.device)
+    p, nb = ws.ptr_size(workspace_size(OP_CMC_GRAM, T, d, 0, n_mod))
+    _ck(lib().masq_cmc_gram(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, n_mod, _p(s.contiguous()), _p(G),
+                            1 if accumulate else 0, p, nb, _stream(stream)), "masq_cmc_gram")
+    return G
+
+
+def cmc_factors_from_gram(G, s, W, qw_text, dw_text, r: int, eps_rel: float = 1e-8, dtype=torch.bfloat16,
+                          with_resid: bool = True, ws=None, stream=None):
+    """(L1, L2, resid) from the (all-reduced) Gram matrices."""
+    d, n = W.shape
+    n_mod = s.shape[0]
+    dev = W.device
+    L1 = torch.empty(n_mod - 1, d, r, dtype=dtype, device=dev)
+    L2 = torch.empty(n_mod - 1, r, n, dtype=dtype, device=dev)
+    resid = torch.empty(n_mod - 1, dtype=torch.float64, device=dev) if with_resid else None
+    ws = ws or default_workspace(dev)
+    p, nb = ws.ptr_size(workspace_size(OP_CMC_FACTORS, 0, d, n, n_mod, r))
+    _ck(lib().masq_cmc_factors_from_gram(_p(G), d, n, n_mod, _p(s.contiguous()), _p(W.contiguous()), _dt(W),
+                                         _p(qw_text), _p(dw_text), r, float(eps_rel), _p(L1), _p(L2), _dt(L1),
+                                         _p(resid), p, nb, _stream(stream)), "masq_cmc_factors_from_gram")
+    return L1, L2, resid
 
 
 # ----------------------------------------------------------------------------- N4

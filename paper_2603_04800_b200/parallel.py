@@ -75,6 +75,14 @@ def reduce_grad(grad, group=None):
     dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
 
 
+def reduce_gram(G, group=None):
+    """All-reduce the CMC Gram matrices (f64 [M-1 x d x d], N2): SUM over the token shards."""
+    _, ws = world()
+    if ws == 1:
+        return
+    dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
+
+
 def max_over_ranks(x: float, device=None) -> float:
     """Max of a host float over ranks (timings: the slowest rank defines the step)."""
     _, ws = world()

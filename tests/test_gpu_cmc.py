@@ -80,3 +80,36 @@ def test_cmc_factors_errors():
     with pytest.raises(m.MasqError) as e:
         m.cmc_factors(X, ids, s, W, qw, dw, 65)
     assert e.value.status == 2
+
+
+def test_cmc_two_phase_sharded_equals_one_call():
+    """Token-sharded N2: the Grams of two halves accumulated (the single-GPU stand-in for the SUM
+    all-reduce) then masq_cmc_factors_from_gram equal the one-call factors (A-weighted norm)
+    and the oracle's Gram-route factors."""
+    m = M()
+    c = _case()
+    n_mod = c["n_mod"]
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], n_mod)
+    s = O.init_factors(R, cnt, c["W"])
+    X, W, ids = bf(c["X"]), bf(c["W"]), tt(c["ids"])
+    qw, dw = m.quantize_weight(W, tt(s[0]), c["wbits"])
+    L1, L2, res1 = m.cmc_factors(X, ids, tt(s), W, qw, dw, 16, dtype=torch.float32)
+    h = c["T"] // 2
+    G = m.cmc_gram(X[:h], ids[:h], tt(s))
+    G = m.cmc_gram(X[h:], ids[h:], tt(s), G=G, accumulate=True)
+    P1, P2, res2 = m.cmc_factors_from_gram(G, tt(s), W, qw, dw, 16, dtype=torch.float32)
+    m.check()
+    xs = O.smooth_activations(O.decode(c["X"]), c["ids"], s)
+    qwo, dwo = O.quantize_weight(c["W"], s[0], c["wbits"])
+    for k in range(n_mod - 1):
+        A = xs[c["ids"] == k + 1].astype(np.float64)
+        dW = O.weight_residual(c["W"], s[k + 1], qwo, dwo)
+        base = np.linalg.norm(A @ dW)
+        a = L1[k].double().cpu().numpy() @ L2[k].double().cpu().numpy()
+        b = P1[k].double().cpu().numpy() @ P2[k].double().cpu().numpy()
+        assert np.linalg.norm(A @ (a - b)) <= 1e-6 * base
+        Gk = np.triu(G[k].cpu().numpy())                         # column-major lower = row-major upper
+        Gk = Gk + np.triu(Gk, 1).T
+        Go = A.T @ A
+        assert np.abs(Gk - Go).max() <= 1e-10 * np.abs(Go).max()
+        assert abs(float(res2[k]) - float(res1[k])) <= 1e-6 * base ** 2

@@ -669,3 +669,17 @@ def test_linear_decode_brute_force():
                 acc += float(dl[j, gg]) * int(np.dot(qa[t, sl].astype(np.int64), q[j, sl].astype(np.int64)))
             ref[t, j] = float(da[t]) * acc
     assert np.allclose(Y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_cmc_from_gram_equals_from_activations():
+    """The Gram route (what token-sharded runs use after a SUM of the shards' Grams) gives the
+    same factors and the same Theorem-2 loss; the shards' Grams add up to the batch Gram."""
+    g = np.random.Generator(np.random.PCG64(35))
+    A = _aniso(g, 240, 20)
+    dW = g.normal(size=(20, 30))
+    L1, L2 = O.cmc_factors(A, dW, 5)
+    G = A[:100].T @ A[:100] + A[100:].T @ A[100:]
+    M1, M2 = O.cmc_factors_from_gram(G, dW, 5)
+    assert np.abs(M1 @ M2 - L1 @ L2).max() <= 1e-9 * np.abs(L1 @ L2).max()
+    l_a = O.reconstruction_loss(A, dW, L1, L2)
+    assert abs(O.reconstruction_loss_from_gram(G, dW, L1, L2) - l_a) <= 1e-9 * l_a

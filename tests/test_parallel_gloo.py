@@ -5,7 +5,9 @@ which need a B200), then the real reduction code runs over gloo:
   * R after the MAX all-reduce is bit-identical to the single-process R; counts add up;
   * the loss from SUM-reduced per-modality sums/counts equals the single-process loss;
   * output-column shards of the forward concatenate to the full forward;
-  * N1 gradients of the token shards (global-count normalised) SUM to the full gradient.
+  * N1 gradients of the token shards (global-count normalised) SUM to the full gradient;
+  * N2: the shards' Gram matrices SUM to the batch Gram, and the CMC factors from it equal the
+    single-process factors.
 """
 import os
 import socket
@@ -50,6 +52,11 @@ def _worker(rank, world_size, port, q):
         _, g = O.calib_loss_grad(c["X"][a:b], c["ids"][a:b], s, c["W"], 8, 8, count_norm=cf)
         gt = torch.from_numpy(g.copy())
         P.reduce_grad(gt)
+        # N2: this rank's Gram of the smoothed image tokens, SUM-reduced -> the batch Gram
+        xs = O.smooth_activations(O.decode(c["X"][a:b]), c["ids"][a:b], s)
+        A = xs[c["ids"][a:b] == 1].astype(np.float64)
+        Gt = torch.from_numpy(A.T @ A)
+        P.reduce_gram(Gt)
         # forward column shard
         qw, dw = O.quantize_weight(c["W"], s[0], 8)
         j0, j1 = P.column_shards(c["n"], world_size)[rank]
@@ -57,7 +64,7 @@ def _worker(rank, world_size, port, q):
                               [c["L1"][0], c["L1"][1]], [c["L2"][0][:, j0:j1], c["L2"][1][:, j0:j1]])
         parts = [None] * world_size
         dist.all_gather_object(parts, (j0, j1, Ys))
-        q.put((rank, Rt.numpy(), ct.numpy(), st.numpy(), nt.numpy(), parts, gt.numpy()))
+        q.put((rank, Rt.numpy(), ct.numpy(), st.numpy(), nt.numpy(), parts, gt.numpy(), Gt.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -82,8 +89,15 @@ def test_two_rank_exchange_matches_single_process():
     qw, dw = O.quantize_weight(c["W"], s[0], 8)
     Y1 = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, [c["L1"][0], c["L1"][1]], [c["L2"][0], c["L2"][1]])
     _, g1 = O.calib_loss_grad(c["X"], c["ids"], s, c["W"], 8, 8)
-    for rank, R, cnt, sums, counts, parts, g in res:
+    xs1 = O.smooth_activations(O.decode(c["X"]), c["ids"], s)
+    A1 = xs1[c["ids"] == 1].astype(np.float64)
+    qw0, dw0 = O.quantize_weight(c["W"], s[0], 8)
+    dW = O.weight_residual(c["W"], s[1], qw0, dw0)
+    F1, F2 = O.cmc_factors(A1, dW, 8)
+    for rank, R, cnt, sums, counts, parts, g, G in res:
         assert np.allclose(g, g1, rtol=1e-9, atol=1e-12 * np.abs(g1).max())
+        H1, H2 = O.cmc_factors_from_gram(G, dW, 8)               # CMC factors from the reduced Gram
+        assert np.linalg.norm(A1 @ (H1 @ H2 - F1 @ F2)) <= 1e-9 * np.linalg.norm(A1 @ dW)
         assert np.array_equal(R, R1), "MAX all-reduce of R must be bit-identical to one process"
         assert np.array_equal(cnt, c1)
         assert np.array_equal(counts, counts1)
