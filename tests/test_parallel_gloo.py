@@ -7,7 +7,8 @@ which need a B200), then the real reduction code runs over gloo:
   * output-column shards of the forward concatenate to the full forward;
   * N1 gradients of the token shards (global-count normalised) SUM to the full gradient;
   * N2: the shards' Gram matrices SUM to the batch Gram, and the CMC factors from it equal the
-    single-process factors.
+    single-process factors;
+  * N4: the shards' mean-abs sums and counts SUM to the batch statistic.
 """
 import os
 import socket
@@ -57,6 +58,10 @@ def _worker(rank, world_size, port, q):
         A = xs[c["ids"][a:b] == 1].astype(np.float64)
         Gt = torch.from_numpy(A.T @ A)
         P.reduce_gram(Gt)
+        # N4: AWQ's mean-abs statistic, SUM of the shards' sums and counts
+        Sa, ca = O.meanabs_stats(c["X"][a:b], c["ids"][a:b], 3)
+        Sat, cat = torch.from_numpy(Sa.copy()), torch.from_numpy(ca.copy())
+        P.reduce_loss(Sat, cat)
         # forward column shard
         qw, dw = O.quantize_weight(c["W"], s[0], 8)
         j0, j1 = P.column_shards(c["n"], world_size)[rank]
@@ -64,7 +69,8 @@ def _worker(rank, world_size, port, q):
                               [c["L1"][0], c["L1"][1]], [c["L2"][0][:, j0:j1], c["L2"][1][:, j0:j1]])
         parts = [None] * world_size
         dist.all_gather_object(parts, (j0, j1, Ys))
-        q.put((rank, Rt.numpy(), ct.numpy(), st.numpy(), nt.numpy(), parts, gt.numpy(), Gt.numpy()))
+        q.put((rank, Rt.numpy(), ct.numpy(), st.numpy(), nt.numpy(), parts, gt.numpy(), Gt.numpy(), Sat.numpy(),
+               cat.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -94,7 +100,9 @@ def test_two_rank_exchange_matches_single_process():
     qw0, dw0 = O.quantize_weight(c["W"], s[0], 8)
     dW = O.weight_residual(c["W"], s[1], qw0, dw0)
     F1, F2 = O.cmc_factors(A1, dW, 8)
-    for rank, R, cnt, sums, counts, parts, g, G in res:
+    Sf, cf_ = O.meanabs_stats(c["X"], c["ids"], 3)
+    for rank, R, cnt, sums, counts, parts, g, G, Sa, ca in res:
+        assert np.allclose(Sa, Sf, rtol=1e-12) and np.array_equal(ca, cf_)
         assert np.allclose(g, g1, rtol=1e-9, atol=1e-12 * np.abs(g1).max())
         H1, H2 = O.cmc_factors_from_gram(G, dW, 8)               # CMC factors from the reduced Gram
         assert np.linalg.norm(A1 @ (H1 @ H2 - F1 @ F2)) <= 1e-9 * np.linalg.norm(A1 @ dW)
