@@ -306,6 +306,12 @@ masq_status masq_calibrate_meanabs(const void* X, masq_dtype xt, int64_t ld_x, c
                                    float* mean, float* mean_unified, int32_t reset,
                                    void* ws, size_t ws_bytes, masq_stream stream);
 
+/* count[m] (+)= number of tokens with id m (i64, device); reset != 0 zeroes first.  Bad ids set
+ * MASQ_ERR_BAD_MODALITY in the sticky status.  Workspace: masq_workspace_size(MASQ_OP_STATS, ...).
+ * (Token-sharded N1 runs use it to normalise each batch's gradient by the global counts.) */
+masq_status masq_count_modalities(const uint8_t* mod_id, int64_t T, int32_t n_mod, int64_t* count,
+                                  int32_t reset, void* ws, size_t ws_bytes, masq_stream stream);
+
 /* Channel statistics across modalities from R [n_mod x d] (each output optional):
  * alpha[i] = R[dominant][i] / max(R[other][i], 1e-12) (f32 division; Theorem 1 range
  * ratio); r_unified[i] = max_m R[m][i]; dom_counts[m] = number of

@@ -59,6 +59,8 @@ SIGNATURES = {
     "masq_smooth_factors": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, ctypes.c_double, c_void_p, c_void_p]),
     "masq_calibrate_meanabs": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t, c_void_p]),
+    "masq_count_modalities": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_int32, c_void_p, c_size_t,
+                                        c_void_p]),
     "masq_range_stats": (c_int32, [c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                    c_void_p]),
     "masq_calib_layer": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p,

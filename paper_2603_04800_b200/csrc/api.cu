@@ -849,6 +849,17 @@ masq_status masq_calibrate_meanabs(const void* X, masq_dtype xt, int64_t ld_x, c
   return MASQ_OK;
 }
 
+masq_status masq_count_modalities(const uint8_t* mod_id, int64_t T, int32_t n_mod, int64_t* count, int32_t reset,
+                                  void* ws, size_t ws_bytes, masq_stream stream) {
+  MASQ_TRY(check_common(T, 16, n_mod));
+  if (!count || (T > 0 && !mod_id)) return MASQ_ERR_NULL;
+  MASQ_TRY(check_ws(ws, ws_bytes, ws_layout(MASQ_OP_STATS, T, 16, 0, n_mod, 0)));
+  cudaStream_t st = S(stream);
+  if (reset) MASQ_CK(cudaMemsetAsync(count, 0, sizeof(int64_t) * n_mod, st));
+  if (T > 0) MASQ_CK(launch_count_modalities(mod_id, T, n_mod, count, status_of(ws), st));
+  return MASQ_OK;
+}
+
 masq_status masq_range_stats(const float* R, int32_t n_mod, int64_t d, int32_t dominant, int32_t other,
                              float* alpha, float* r_unified, int64_t* dom_counts, masq_stream stream) {
   MASQ_TRY(check_common(0, d, n_mod));

@@ -186,6 +186,14 @@ cudaError_t launch_meanabs(const void* X, masq_dtype xt, int64_t ld_x, const uin
   return cudaGetLastError();
 }
 
+cudaError_t launch_count_modalities(const uint8_t* ids, int64_t T, int n_mod, int64_t* cnt, uint32_t* status,
+                                   cudaStream_t st) {
+  ProfScope ps_("count_modalities", st);
+  count_ids_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(T, 256), 1024)), 256, 0, st>>>(
+      ids, T, n_mod, cnt, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_range_stats(const float* R, int n_mod, int64_t d, int dominant, int other, float* alpha,
                                float* runi, int64_t* dom, cudaStream_t st) {
   if (dom) {

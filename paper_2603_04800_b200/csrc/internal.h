@@ -226,6 +226,8 @@ cudaError_t launch_smooth_factors(const float* num, int64_t rows, int64_t d, con
 cudaError_t launch_meanabs(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                            int n_mod, double* S, int64_t* cnt, float* mean, float* uni, float* part,
                            uint32_t* status, cudaStream_t st);
+cudaError_t launch_count_modalities(const uint8_t* ids, int64_t T, int n_mod, int64_t* cnt, uint32_t* status,
+                                   cudaStream_t st);
 cudaError_t launch_range_stats(const float* R, int n_mod, int64_t d, int dominant, int other, float* alpha,
                                float* runi, int64_t* dom, cudaStream_t st);
 

@@ -399,6 +399,17 @@ def calibrate_meanabs(X, mod_id, n_mod: int, sumabs=None, count=None, reset: boo
     return sumabs, count, mean, uni
 
 
+def count_modalities(mod_id, n_mod: int, count=None, reset: bool = True, ws=None, stream=None):
+    """i64 [M] token counts per modality (device)."""
+    T = mod_id.shape[0]
+    count = torch.zeros(n_mod, dtype=torch.int64, device=mod_id.device) if count is None else count
+    ws = ws or default_workspace(mod_id.device)
+    p, nb = ws.ptr_size(workspace_size(OP_STATS, T, 16, 0, n_mod))
+    _ck(lib().masq_count_modalities(_p(mod_id), T, n_mod, _p(count), 1 if reset else 0, p, nb, _stream(stream)),
+        "masq_count_modalities")
+    return count
+
+
 def range_stats(R, dominant: int = 0, other: int = 1, stream=None):
     """(alpha f32 [d] or None, r_unified f32 [d], dom_counts i64 [M + 1])."""
     n_mod, d = R.shape

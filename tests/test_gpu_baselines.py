@@ -89,3 +89,12 @@ def test_unified_factors_and_awq_grid():
     bo, lo = O.awq_grid_search(c["X"], c["ids"], c["W"], 4, 8, betas, n_mod)
     assert np.allclose(losses, lo, rtol=1e-3)
     assert b == bo
+
+
+def test_count_modalities():
+    m = M()
+    c = case("ragged3")
+    cnt = m.count_modalities(tt(c["ids"]), 3)
+    assert cnt.cpu().tolist() == np.bincount(c["ids"], minlength=3).tolist()
+    cnt = m.count_modalities(tt(c["ids"][:100]), 3, count=cnt, reset=False)
+    assert cnt.cpu().tolist() == (np.bincount(c["ids"], minlength=3) + np.bincount(c["ids"][:100], minlength=3)).tolist()
