@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-n1", action="store_true", help="skip the N1 S-optimisation step timing")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="CUDA streams the step's linears are spread over (>1 overlaps one linear's GEMM tail with "
+                         "the next linear's work)")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one captured CUDA graph (N=1; measured slower here: the launch "
                          "gaps are ~2%% of the step and the captured profiler event nodes cost more)")
@@ -252,6 +255,7 @@ def workload_config(args, linears):
         "tokens_per_gpu": args.tokens,
         "parallelism": f"dp{args.gpus} (token-sharded calibration; replicated weights)",
         "l2": "inputs larger than L2 (each step streams >1 GB of activations/weights; no flush)",
+        "streams": args.streams,
     }
 
 
@@ -434,19 +438,33 @@ def main():
     losses = torch.zeros(nl, dtype=torch.float64, device=dev)
     ws = M.Workspace(dev)
 
+    nstreams = max(1, args.streams)
+    side = [torch.cuda.Stream(device=dev) for _ in range(nstreams)] if nstreams > 1 else []
+    wss = [ws] + [M.Workspace(dev) for _ in range(nstreams - 1)]
+
     def step(X_override=None, ids_override=None):
         idt = ids if ids_override is None else ids_override
         for li, e in enumerate(L):
             X = e["X"] if X_override is None else X_override[li]
             M.calibrate_stats(X, idt, N_MOD, R=Rv[li], count=Cbuf[li], reset=True, ws=ws)
         P.reduce_stats([Rbuf], Cbuf)                    # one batched exchange per step (max is order-free)
+        main = torch.cuda.current_stream()
+        if side:
+            ready = torch.cuda.Event()
+            ready.record(main)
         for li, e in enumerate(L):
             X = e["X"] if X_override is None else X_override[li]
-            s = M.init_factors(Rv[li], Cbuf[li], e["W"], ws=ws)
-            e["s"] = s
-            # A3 (every modality's weight codes, one W read) + A4-A7 forward + A8 target and loss
-            M.calib_layer(X, idt, s, e["W"], WBITS, ABITS, e["L1"], e["L2"], Y=e["Y"], Yref=e["Yref"],
-                          sums=Sbuf[li], counts=Nbuf[li], loss=losses[li:li + 1], ws=ws)
+            k = li % nstreams
+            if side:
+                side[k].wait_event(ready)
+            with torch.cuda.stream(side[k] if side else main):
+                s = M.init_factors(Rv[li], Cbuf[li], e["W"], ws=wss[k])
+                e["s"] = s
+                # A3 (every modality's weight codes, one W read) + A4-A7 forward + A8 target and loss
+                M.calib_layer(X, idt, s, e["W"], WBITS, ABITS, e["L1"], e["L2"], Y=e["Y"], Yref=e["Yref"],
+                              sums=Sbuf[li], counts=Nbuf[li], loss=losses[li:li + 1], ws=wss[k])
+        for st_ in side:                                 # join before the exchange / the step's end
+            main.wait_stream(st_)
         if world > 1:
             P.reduce_loss(Sbuf, Nbuf)
             for li, e in enumerate(L):

@@ -51,6 +51,36 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       }
       break;
     }
+    case MASQ_OP_LAYER: {
+      const int64_t Tg = grouped_rows(T, n_mod);
+      L.inv_s = take(sizeof(float) * n_mod * d);
+      L.qx_tok = take((size_t)T * d);
+      L.dx_tok = take(sizeof(float) * T);
+      L.mask = take(sizeof(uint32_t) * tiles_m);
+      L.qx = take((size_t)Tg * d);
+      L.dx = take(sizeof(float) * Tg);
+      L.perm = take(sizeof(int32_t) * Tg);
+      L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
+      L.cnt = take(sizeof(int64_t) * n_mod);
+      L.qw_all = take((size_t)n_mod * n * d);
+      L.dw_all = take(sizeof(float) * n_mod * n);
+      L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
+      L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
+      L.fpart = take(sizeof(double) * ceil_div(T, kUnitM) * ceil_div(n, kTileN) * 2);
+      if (rp > 0 && nnt > 0) {
+        L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
+        L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
+        L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
+      }
+      break;
+    }
+    case MASQ_OP_DECODE:
+      L.inv_s = take(sizeof(float) * d);
+      L.ids0 = take((size_t)T);
+      L.qx = take((size_t)T * d);
+      L.dx = take(sizeof(float) * T);
+      L.dpart = take(sizeof(float) * (size_t)decode_kchunks(d) * (n / 8) * 128);
+      break;
     case MASQ_OP_MEANABS:
       L.partials = take(sizeof(float) * (size_t)meanabs_slabs(T) * n_mod * d);
       break;

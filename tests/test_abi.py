@@ -84,3 +84,24 @@ def test_argument_errors_return_before_launch(so):
                                  None, None) == 2
     # workspace too small -> WORKSPACE
     assert L.masq_quantize_weight(p, 1, p, 64, 128, 8, p, p, p, 16, None) == 5
+
+
+def test_every_workspace_op_has_a_layout(so):
+    """Every MASQ_OP_* the header declares has its own workspace layout (a switch case lost in an
+    edit would silently hand the op a 256-byte layout and overlapping buffers)."""
+    from paper_2603_04800_b200._lib import lib
+    L = lib()
+    src = open(HEADER).read()
+    ops = {k: int(v) for k, v in re.findall(r"\b(MASQ_OP_[A-Z_]+)\s*=\s*(\d+)", src)}
+    assert len(ops) >= 14
+    T, d, n, M, r = 4096, 1024, 2048, 2, 64
+    stateless = {"MASQ_OP_STATS", "MASQ_OP_INIT", "MASQ_OP_REFERENCE"}   # only the status word
+    cpu_only_unknown = {"MASQ_OP_CMC", "MASQ_OP_CMC_FACTORS"}   # need the eigensolver's query (GPU)
+    for name, op in ops.items():
+        size = L.masq_workspace_size(op, T, d, n, M, r)
+        if name in stateless:
+            assert size == 256, name
+        elif name in cpu_only_unknown:
+            assert size >= 256, name
+        else:
+            assert size > 4096, (name, size)
