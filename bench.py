@@ -188,7 +188,7 @@ def oracle_threads():
         return os.cpu_count() or 1
 
 
-def time_oracle(T, r, linears, repeats=3, k_small=128, k_large=512):
+def time_oracle(T, r, linears, repeats=4, k_small=128, k_large=512):
     """Returns (tokens/s extrapolated to the full layer at T tokens, seconds of CPU work, desc).
     ~10-15 s of oracle work: `repeats` steps at 2*k_small and at 2*k_large tokens."""
     sample = oracle_sample(T, r)
