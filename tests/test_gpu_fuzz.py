@@ -72,3 +72,40 @@ def test_random_problem_parity(seed):
         Yl, Yr2, s2, c2, l2 = m.calib_layer(Xg, ids, sg, bf(c["W"]), wbits, abits, L1, L2)
         assert torch.equal(Yr2, Yref) and torch.equal(c2, counts)
         assert abs(float(l2.cpu()[0]) - lo) <= TOL_L * abs(lo) + 1e-300
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_gradient_parity(seed):
+    """N1 on random shapes: loss and straight-through gradient (with the scale terms)."""
+    from test_gpu_grad import TOL_G, _grad_err
+    m = M()
+    c = _problem(100 + seed)
+    if c["f32x"] or c["T"] < 8:
+        pytest.skip("bf16 X and a few tokens per modality needed")
+    n_mod, wbits, abits = c["n_mod"], c["wbits"], c["abits"]
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], n_mod)
+    s = O.init_factors(R, cnt, c["W"])
+    X, W = bf(c["X"]), bf(c["W"])
+    Yref = m.reference_output(X, W)
+    _, _, loss, grad = m.calib_loss_grad(X, tt(c["ids"]), tt(s), W, wbits, abits, Yref)
+    lo, go = O.calib_loss_grad(c["X"], c["ids"], s, c["W"], wbits, abits)
+    assert abs(float(loss.cpu()[0]) - lo) <= TOL_L * abs(lo) + 1e-300
+    assert _grad_err(grad.cpu().numpy(), go) <= TOL_G
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_decode_parity(seed):
+    """N3 on random shapes: grouped int4 codes bit-exact, decode output vs the oracle."""
+    m = M()
+    g = np.random.Generator(np.random.PCG64(7000 + seed))
+    d, n, T = 128 * int(g.integers(1, 40)), 8 * int(g.integers(1, 200)), int(g.integers(1, 17))
+    ids = np.zeros(T, np.uint8)
+    X = synth.activations(ids, d, 1, 7100 + seed)
+    W = synth.weight(d, n, 7200 + seed)
+    s = np.exp(g.normal(0, 0.5, d)).astype(np.float32)
+    packed, scales = m.quantize_weight_int4(bf(W), tt(s))
+    q, dl = O.quantize_weight_grouped(W, s, 4, 128)
+    assert np.array_equal(m.unpack_int4(packed, d, n).cpu().numpy(), q)
+    Y = m.linear_decode(bf(X), tt(s), packed, scales).cpu().numpy()
+    Yo = O.linear_decode(X, s, q, dl, 8, 128)
+    assert max_abs_norm(Y, Yo) <= TOL_Y
