@@ -133,7 +133,8 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.gsign = take(sizeof(uint16_t) * (size_t)Tg * n);
       L.planes = take(sizeof(uint16_t) * 2 * (size_t)Tg * d);
       L.gpartial = take(sizeof(double) * n_mod * gradgemm_ntiles_j(n) * d);
-      L.codes16 = take(sizeof(uint16_t) * (size_t)n_mod * n * d);
+      L.dq = take((size_t)Tg * d);
+      L.de = take(sizeof(float) * Tg);
       L.apart = take(sizeof(float) * (size_t)Tg * 2 * ceil_div(n, kTileN));
       L.bpart = take(sizeof(float) * (size_t)n_mod * 4 * gradgemm_ntiles_i(d) * n);
       L.kj = take(sizeof(int32_t) * (size_t)n_mod * n);
@@ -582,7 +583,8 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
   if (grad) {
     uint16_t* planes = reinterpret_cast<uint16_t*>(W8(ws, L.planes));
     double* gpart = reinterpret_cast<double*>(W8(ws, L.gpartial));
-    uint16_t* codes16 = reinterpret_cast<uint16_t*>(W8(ws, L.codes16));
+    int8_t* dq = reinterpret_cast<int8_t*>(W8(ws, L.dq));
+    float* de = reinterpret_cast<float*>(W8(ws, L.de));
     float* apart = reinterpret_cast<float*>(W8(ws, L.apart));
     float* bpart = reinterpret_cast<float*>(W8(ws, L.bpart));
     int32_t* kj = reinterpret_cast<int32_t*>(W8(ws, L.kj));
@@ -593,20 +595,19 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     int32_t* ktkey = keys + nj;
     const uint32_t* colmax = amax;                     // first half of the scratch: column maxima
     MASQ_CK(launch_gradprep(static_cast<const uint16_t*>(X), ld_x, mod_id, perm, qx, dx, inv, Tg, d, abits, planes,
-                            ktkey, st));
-    MASQ_CK(launch_codes16(qw, (int64_t)n_mod * d_out * d, codes16, st));
+                            ktkey, dq, de, st));
     MASQ_CK(cudaMemsetAsync(kj, 0x7F, sizeof(int32_t) * nj, st));
     MASQ_CK(launch_gradgemm(planes, Tg, gsign, qw, tmod, n_mod, d, d_out, s, inv, static_cast<const uint16_t*>(W), dw,
                             colmax, gpart, bpart, kj, st));
     GemmArgs ga{};
-    ga.mode = kModeAlpha;
+    ga.mode = kModeAlphaI8;                            // D (int8, row step Delta_t / 254) . codes^T
     ga.T = Tg;
     ga.n = d_out;
     ga.d = d;
-    ga.xbf = planes;                                   // plane 0 = D
-    ga.ld_x = d;
-    ga.b = codes16;
+    ga.qx = dq;
+    ga.b = qw;
     ga.b_rows = (int64_t)n_mod * d_out;
+    ga.dx = de;
     ga.dw = dw;
     ga.tile_mask = tmod;
     ga.n_mod = n_mod;

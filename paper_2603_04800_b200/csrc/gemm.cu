@@ -14,6 +14,9 @@
 //   kModeAlpha N1 scale term: rows grouped as for the loss, acc = D . codes(Q(S_m W))^T
 //             (kind::f16, both K-major; D = Ahat - X S^-1 as bf16), and the epilogue reduces
 //             sum_j sign(E)_tj * dw_m[j] * acc_tj per row into per-(row, CTA column half) partials.
+//   kModeAlphaI8 the same contraction on the int8 path: D quantized per row with the fixed step
+//             Delta_t / 254 (|D| <= Delta_t / 2), B = the int8 weight codes themselves; the
+//             epilogue applies the row step (dx = e_t).
 //
 // A cluster of two CTAs (one per SM of a TPC) computes a 256 x 256 output unit with
 // tcgen05.mma.cta_group::2 (M = 256, N = 256): CTA r loads rows [128r, 128r+128) of the A tile
@@ -103,7 +106,7 @@ __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
   w.mt = rem / gsz;
   w.nt = nt0 + (rem - w.mt * gsz);
   w.m = 0;
-  if (p.mode == kModeLoss || p.mode == kModeAlpha) {
+  if (p.mode == kModeLoss || p.mode == kModeAlpha || p.mode == kModeAlphaI8) {
     w.mask = p.tile_mask[w.mt];
     if (w.mask == 0xFFFFFFFFu) return false;
     if (p.skip_m0 && w.mask == 0u) return false;
@@ -156,7 +159,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (MODE != kModeLoss && MODE != kModeAlpha) tma_prefetch(&tmY);
+    if (MODE != kModeLoss && MODE != kModeAlpha && MODE != kModeAlphaI8) tma_prefetch(&tmY);
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -173,7 +176,8 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t tmem_base = *tmem_slot;
 
   constexpr int KELEMS = (MODE == kModeRef || MODE == kModeAlpha) ? 64 : 128;
-  constexpr bool kGrouped = MODE == kModeLoss || MODE == kModeAlpha;
+  constexpr bool kGrouped = MODE == kModeLoss || MODE == kModeAlpha || MODE == kModeAlphaI8;
+  constexpr bool kAlpha = MODE == kModeAlpha || MODE == kModeAlphaI8;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -470,7 +474,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           p.partials[(size_t)(w.mt * p.num_n + w.nt) * 2 + rank] = tot;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-      } else if (MODE == kModeAlpha) {
+      } else if (kAlpha) {
         float part = 0.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -487,9 +491,11 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const uint32_t gw = (&g4[i >> 3].x)[(i >> 1) & 3];
             const float g = __uint_as_float((i & 1) ? (gw & 0xFFFF0000u) : (gw << 16));   // +-1 or 0
             const float dws = __shfl_sync(0xffffffffu, dwr[c], i);
-            part = fmaf(g * dws, __uint_as_float(v[i]), part);
+            const float av = MODE == kModeAlphaI8 ? (float)(int)v[i] : __uint_as_float(v[i]);
+            part = fmaf(g * dws, av, part);
           }
         }
+        if (MODE == kModeAlphaI8) part *= dxr;                      // the row step e_t
         if (row < p.T) p.apart[(size_t)row * (2 * p.num_n) + 2 * w.nt + (ew >> 2)] = part;
       } else {
 #pragma unroll
@@ -543,7 +549,8 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  static const char* const kNames[5] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha"};
+  static const char* const kNames[6] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha",
+                                        "gemm_alpha_i8"};
   ProfScope ps_(kNames[MODE], st);
   masq_gemm_kernel<MODE><<<2 * clusters, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
   return cudaGetLastError();
@@ -578,7 +585,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, BM, 128, true);
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BNH, 128, true);
   }
-  if (g.mode != kModeLoss && g.mode != kModeAlpha) {
+  if (g.mode != kModeLoss && g.mode != kModeAlpha && g.mode != kModeAlphaI8) {
     ok &= make_tmap_2d(&ty, g.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.T, g.n, g.ld_out, 32, 32, true);
   } else {
     ty = ta;
@@ -635,6 +642,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     case kModeLoss: return launch_mode<kModeLoss>(ta, tb, ty, tz, tl2, p, clusters, st);
     case kModeRef: return launch_mode<kModeRef>(ta, tb, ty, tz, tl2, p, clusters, st);
     case kModeAlpha: return launch_mode<kModeAlpha>(ta, tb, ty, tz, tl2, p, clusters, st);
+    case kModeAlphaI8: return launch_mode<kModeAlphaI8>(ta, tb, ty, tz, tl2, p, clusters, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
                                                        const int32_t* __restrict__ perm, const int8_t* __restrict__ qx,
                                                        const float* __restrict__ dx, const float* __restrict__ inv,
                                                        int64_t Tg, int64_t d, float qa, uint16_t* __restrict__ planes,
-                                                       int32_t* __restrict__ ktkey) {
+                                                       int32_t* __restrict__ ktkey, int8_t* __restrict__ dq,
+                                                       float* __restrict__ de) {
   const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= Tg) return;
@@ -289,8 +290,14 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
   int bidx = 0x7FFFFFFF;
   uint16_t* pd = planes + p * d;
   uint16_t* px = planes + (Tg + p) * d;
+  // |D| <= Delta_t / 2 (a rounding residual), so D / (Delta_t / 254) fits int8: the alpha GEMM's
+  // operand (int8 tensor path), scale e_t = Delta_t / 254
+  const float estep = __fdiv_rn(dxv, 254.0f);
+  const float einv = dxv > 0.f ? __fdiv_rn(254.0f, dxv) : 0.f;
+  if (lane == 0) de[p] = estep;
   for (int64_t c = (int64_t)lane * 8; c < d; c += 256) {
     uint4 xv = make_uint4(0, 0, 0, 0), dv = make_uint4(0, 0, 0, 0);
+    uint2 qd = make_uint2(0, 0);
     if (src >= 0) {
       xv = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)src * ld_x + c));
       const uint2 q8 = __ldg(reinterpret_cast<const uint2*>(qx + p * d + c));
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
       const float iv[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
       const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
       const uint32_t qw[2] = {q8.x, q8.y};
-      uint32_t o[4];
+      uint32_t o[4], qb[2] = {0u, 0u};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         uint16_t h[2];
@@ -310,16 +317,21 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
           const float x = __uint_as_float(k ? (xw[e] & 0xFFFF0000u) : (xw[e] << 16));
           const float ah = __fmul_rn(dxv, (float)qv);
           const float xs = __fmul_rn(x, iv[idx]);
-          h[k] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(ah, xs)));
+          const float dd = __fsub_rn(ah, xs);
+          h[k] = __bfloat16_as_ushort(__float2bfloat16_rn(dd));
+          const int qi = max(-127, min(127, __float2int_rn(dd * einv)));
+          qb[idx >> 2] |= ((uint32_t)qi & 0xFFu) << (8 * (idx & 3));
           const uint32_t ab = __float_as_uint(xs) & 0x7FFFFFFFu;
           if (ab > best) { best = ab; bidx = (int)(c + idx); }
         }
         o[e] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
       }
       dv = make_uint4(o[0], o[1], o[2], o[3]);
+      qd = make_uint2(qb[0], qb[1]);
     }
     *reinterpret_cast<uint4*>(pd + c) = dv;
     *reinterpret_cast<uint4*>(px + c) = xv;
+    *reinterpret_cast<uint2*>(dq + p * d + c) = qd;
   }
   // first arg-max over the row: larger |xs| wins, ties -> smaller index
 #pragma unroll
@@ -333,22 +345,6 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
     const bool live = src >= 0 && __fdiv_rn(__uint_as_float(best), qa) >= 1e-12f;
     ktkey[p] = live ? mrow * (int)d + bidx : -1;
   }
-}
-
-__global__ void codes16_kernel(const int8_t* __restrict__ q, int64_t count, uint16_t* __restrict__ out) {
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (i >= count) return;
-  const uint2 v = __ldg(reinterpret_cast<const uint2*>(q + i));
-  const uint32_t w[2] = {v.x, v.y};
-  uint32_t o[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int a = (int)(int8_t)((w[e >> 1] >> (16 * (e & 1))) & 0xFF);
-    const int b = (int)(int8_t)((w[e >> 1] >> (16 * (e & 1) + 8)) & 0xFF);
-    o[e] = (uint32_t)__bfloat16_as_ushort(__int2bfloat16_rn(a)) |
-           ((uint32_t)__bfloat16_as_ushort(__int2bfloat16_rn(b)) << 16);
-  }
-  *reinterpret_cast<uint4*>(out + i) = make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 // beta keys / values: one CTA per (modality, 32 columns); thread (r0 = tid >> 5, lane = column)
@@ -478,18 +474,13 @@ cudaError_t launch_keep_best(const double* loss, double* best, const float* s, f
 
 cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
                             const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d, int abits,
-                            uint16_t* planes, int32_t* ktkey, cudaStream_t st) {
+                            uint16_t* planes, int32_t* ktkey, int8_t* dq, float* de, cudaStream_t st) {
   ProfScope ps_("gradprep", st);
   gradprep_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(X, ld_x, mod_id, perm, qx, dx, inv, Tg, d,
-                                                             (float)((1 << (abits - 1)) - 1), planes, ktkey);
+                                                             (float)((1 << (abits - 1)) - 1), planes, ktkey, dq, de);
   return cudaGetLastError();
 }
 
-cudaError_t launch_codes16(const int8_t* q, int64_t count, uint16_t* out, cudaStream_t st) {
-  ProfScope ps_("codes16", st);
-  codes16_kernel<<<(unsigned)ceil_div(count, 8 * 256), 256, 0, st>>>(q, count, out);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_gradkeys(const float* bpart, int nb, const int32_t* kj, const uint32_t* colmax, int wbits,
                             const float* apart, int na, const int32_t* ktkey, int n_mod, int64_t d, int64_t n,

@@ -29,7 +29,7 @@ struct WsLayout {
   size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, cnt = 0, total = 0;
   size_t gsign = 0, planes = 0, gpartial = 0;
   // N1 scale terms
-  size_t codes16 = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0, skeys = 0, svals = 0,
+  size_t dq = 0, de = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0, skeys = 0, svals = 0,
          stemp = 0, stemp_bytes = 0;
   // N2 CMC factors (f64)
   size_t a64 = 0, g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
@@ -106,7 +106,7 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, in
                   uint64_t cols, uint64_t ld, uint32_t box_rows, uint32_t box_cols, bool swizzle128);
 
 // ---------------------------------------------------------------- GEMM (gemm.cu)
-enum GemmMode { kModeFwd = 0, kModeAcc = 1, kModeLoss = 2, kModeRef = 3, kModeAlpha = 4 };
+enum GemmMode { kModeFwd = 0, kModeAcc = 1, kModeLoss = 2, kModeRef = 3, kModeAlpha = 4, kModeAlphaI8 = 5 };
 
 struct GemmArgs {
   int mode;
@@ -150,9 +150,7 @@ int gemm_epilogue_warps();
 // ktkey[Tg]: m*d + (first arg-max_i |xs_ti|) of every grouped row (-1: padding / floored scale)
 cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
                             const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d, int abits,
-                            uint16_t* planes, int32_t* ktkey, cudaStream_t st);
-// int8 codes [rows x d] -> bf16 [rows x d] (exact)
-cudaError_t launch_codes16(const int8_t* q, int64_t count, uint16_t* out, cudaStream_t st);
+                            uint16_t* planes, int32_t* ktkey, int8_t* dq, float* de, cudaStream_t st);
 // partial[m][jt][i] (sum_j of the direct terms), bpart[m][4*it + q][j] (beta_j over 32 rows i),
 // kj[m][j] = min i with |f32(s_i w_ij)| == colmax[m][j] (atomicMin; preset to INT_MAX)
 cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* gsign, const int8_t* qw_all,
