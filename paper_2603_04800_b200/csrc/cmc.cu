@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <dlfcn.h>
 
+#include <cstdlib>
+
 #include <mutex>
 
 #include "internal.h"
@@ -39,6 +41,11 @@ struct LinAlg {
   decltype(&cusolverDnSetStream) sv_set_stream = nullptr;
   decltype(&cusolverDnDsyevd_bufferSize) syevd_size = nullptr;
   decltype(&cusolverDnDsyevd) syevd = nullptr;
+  decltype(&cusolverDnDpotrf_bufferSize) potrf_size = nullptr;
+  decltype(&cusolverDnDpotrf) potrf = nullptr;
+  decltype(&cublasDtrmm_v2) dtrmm = nullptr;
+  decltype(&cublasDtrsm_v2) dtrsm = nullptr;
+  decltype(&cublasDsymv_v2) dsymv = nullptr;
   cublasHandle_t hb[64] = {};
   cusolverDnHandle_t hs[64] = {};
 };
@@ -74,8 +81,13 @@ LinAlg* linalg(cudaStream_t st) {
       L.sv_set_stream = reinterpret_cast<decltype(L.sv_set_stream)>(dlsym(hs, "cusolverDnSetStream"));
       L.syevd_size = reinterpret_cast<decltype(L.syevd_size)>(dlsym(hs, "cusolverDnDsyevd_bufferSize"));
       L.syevd = reinterpret_cast<decltype(L.syevd)>(dlsym(hs, "cusolverDnDsyevd"));
+      L.potrf_size = reinterpret_cast<decltype(L.potrf_size)>(dlsym(hs, "cusolverDnDpotrf_bufferSize"));
+      L.potrf = reinterpret_cast<decltype(L.potrf)>(dlsym(hs, "cusolverDnDpotrf"));
+      L.dtrmm = reinterpret_cast<decltype(L.dtrmm)>(dlsym(hb, "cublasDtrmm_v2"));
+      L.dtrsm = reinterpret_cast<decltype(L.dtrsm)>(dlsym(hb, "cublasDtrsm_v2"));
+      L.dsymv = reinterpret_cast<decltype(L.dsymv)>(dlsym(hb, "cublasDsymv_v2"));
       L.ok = L.create && L.set_stream && L.dgemm && L.dsyrk && L.dsymm && L.sv_create && L.sv_set_stream &&
-             L.syevd_size && L.syevd;
+             L.syevd_size && L.syevd && L.potrf_size && L.potrf && L.dtrmm && L.dtrsm && L.dsymv;
     }
   }
   if (!L.ok) return nullptr;
@@ -137,6 +149,46 @@ __global__ void whiten_kernel(const double* __restrict__ lam, int64_t d, double 
   const double q = sqrt(l);
   sq[k] = q;
   isq[k] = q > 0.0 ? 1.0 / q : 0.0;
+}
+
+// power iteration on the (lower-stored) Gram matrix: w = G u computed by Dsymv; this single-CTA
+// kernel sets lam = u . w (Rayleigh quotient, u unit) and u = w / |w| (fixed-order reductions)
+__global__ void __launch_bounds__(1024) power_step_kernel(double* __restrict__ u, const double* __restrict__ w,
+                                                          int64_t d, double* __restrict__ lam) {
+  __shared__ double s1[1024], s2[1024];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += 1024) {
+    a += u[i] * w[i];
+    b += w[i] * w[i];
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  const double nrm = sqrt(s2[0]);
+  if (threadIdx.x == 0) *lam = s1[0];
+  const double sc = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += 1024) u[i] = w[i] * sc;
+}
+
+__global__ void fill_kernel(double* __restrict__ u, int64_t d, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) u[i] = v;
+}
+
+// G'[i][i] = G[i][i] + eps_rel * max(lam, 0) (the relative regulariser of Q27), other entries copied
+__global__ void regularize_kernel(const double* __restrict__ G, int64_t d, const double* __restrict__ lam,
+                                  double eps_rel, double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= d * d) return;
+  const int64_t i = idx % d, j = idx / d;
+  out[idx] = G[idx] + (i == j ? eps_rel * fmax(*lam, 0.0) : 0.0);
 }
 
 // column-major [rows x cols]: row k scaled by f[k]
@@ -205,11 +257,13 @@ bool cmc_linalg_available() { return linalg(0) != nullptr; }
 size_t cmc_syevd_lwork(int64_t d) {
   LinAlg* L = linalg(0);
   if (!L || d <= 0) return 0;
-  int lw = 0;
+  int lw = 0, lp = 0;
   if (L->syevd_size(L->hs[cur_dev()], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d,
                     nullptr, &lw) != CUSOLVER_STATUS_SUCCESS)
     return 0;
-  return (size_t)lw;
+  if (L->potrf_size(L->hs[cur_dev()], CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d, &lp) != CUSOLVER_STATUS_SUCCESS)
+    return 0;
+  return (size_t)(lw > lp ? lw : lp);
 }
 
 // phase 1: G[m-1] (+)= A_m^T A_m (lower triangle) for m = 1..n_mod-1
@@ -256,20 +310,18 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
   const int r = a.r;
   const int di = (int)d, ni = (int)n;
   const double one = 1.0, zero = 0.0, mone = -1.0;
+  static int eig_env = -1;                            // MASQ_CMC_EIG=1: the paper's eigen route (A/B)
+  if (eig_env < 0) {
+    const char* ev = getenv("MASQ_CMC_EIG");
+    eig_env = ev && atoi(ev) ? 1 : 0;
+  }
+  const bool use_eig = eig_env == 1;
 #define CK_B(x) do { if ((x) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
 #define CK_S(x) do { if ((x) != CUSOLVER_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
   for (int m = 1; m < a.n_mod; ++m) {
     const double* Gm = Gall + (int64_t)(m - 1) * d * d;
-    cudaError_t e = cudaMemcpyAsync(a.G, Gm, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) return e;
     {
-      ProfScope ps_("cmc_eig_gram", st);
-      CK_S(L->syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, di, a.G, di, a.lam, a.work, (int)a.lwork,
-                    a.info));
-    }
-    whiten_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(a.lam, d, a.eps_rel, a.sq, a.isq);
-    // dW and M = diag(sqrt Lambda') P^T dW
-    {
+      // dW = S_m W - Q(S_t W)
       ProfScope ps_("cmc_dw", st);
       dim3 grid((unsigned)ceil_div(d, 32), (unsigned)ceil_div(n, 32)), block(32, 8);
       const float* sm = a.s + (int64_t)m * d;
@@ -278,11 +330,37 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
       else
         dw64_kernel<<<grid, block, 0, st>>>(static_cast<const float*>(a.W), sm, a.qw_t, a.dw_t, d, n, a.dW);
     }
-    {
+    if (use_eig) {
+      // the paper's route: eig G = P Lambda P^T, T = diag(sqrt Lambda') P^T
+      cudaError_t e = cudaMemcpyAsync(a.G, Gm, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return e;
+      {
+        ProfScope ps_("cmc_eig_gram", st);
+        CK_S(L->syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, di, a.G, di, a.lam, a.work, (int)a.lwork,
+                      a.info));
+      }
+      whiten_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(a.lam, d, a.eps_rel, a.sq, a.isq);
       ProfScope ps_("cmc_whiten_gemm", st);
       CK_B(L->dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, di, ni, di, &one, a.G, di, a.dW, di, &zero, a.Mb, di));
+      scale_rows_kernel<<<(unsigned)ceil_div(d * n, 256), 256, 0, st>>>(a.Mb, d, n, a.sq, a.Mb);
+    } else {
+      // any T with T^T T = G + eps*lambda_max*I gives the same optimum L1 L2 (T' = Q T for an
+      // orthogonal Q): take the Cholesky factor, G' = Lc Lc^T, T = Lc^T.  lambda_max by 32
+      // power-iteration steps (the regulariser only needs it to O(1e-6))
+      ProfScope ps_("cmc_chol", st);
+      double* u = a.sq;                                            // scratch vectors (d)
+      double* w = a.isq;
+      fill_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(u, d, 1.0 / sqrt((double)d));
+      for (int it = 0; it < 32; ++it) {
+        CK_B(L->dsymv(hb, CUBLAS_FILL_MODE_LOWER, di, &one, Gm, di, u, 1, &zero, w, 1));
+        power_step_kernel<<<1, 1024, 0, st>>>(u, w, d, a.lam);
+      }
+      regularize_kernel<<<(unsigned)ceil_div(d * d, 256), 256, 0, st>>>(Gm, d, a.lam, a.eps_rel, a.G);
+      CK_S(L->potrf(hs, CUBLAS_FILL_MODE_LOWER, di, a.G, di, a.work, (int)a.lwork, a.info));
+      // M = Lc^T dW
+      CK_B(L->dtrmm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, di, ni, &one, a.G,
+                    di, a.dW, di, a.Mb, di));
     }
-    scale_rows_kernel<<<(unsigned)ceil_div(d * n, 256), 256, 0, st>>>(a.Mb, d, n, a.sq, a.Mb);
     // top-r left singular vectors of M from eig(M M^T)
     {
       ProfScope ps_("cmc_mmt", st);
@@ -297,8 +375,16 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
     {
       ProfScope ps_("cmc_factors_gemm", st);
       CK_B(L->dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, r, ni, di, &one, Ur, di, a.Mb, di, &zero, a.L2t, r));
-      scale_rows_kernel<<<(unsigned)ceil_div(d * r, 256), 256, 0, st>>>(Ur, d, r, a.isq, a.Urs);
-      CK_B(L->dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, di, r, di, &one, a.G, di, a.Urs, di, &zero, a.L1t, di));
+      if (use_eig) {
+        scale_rows_kernel<<<(unsigned)ceil_div(d * r, 256), 256, 0, st>>>(Ur, d, r, a.isq, a.Urs);
+        CK_B(L->dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, di, r, di, &one, a.G, di, a.Urs, di, &zero, a.L1t, di));
+      } else {
+        // L1 = Lc^-T U_r
+        cudaError_t e = cudaMemcpyAsync(a.L1t, Ur, sizeof(double) * d * r, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+        CK_B(L->dtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, di, r, &one,
+                      a.G, di, a.L1t, di));
+      }
     }
     {
       const int64_t cnt = d * r + (int64_t)r * n;
