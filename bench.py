@@ -279,10 +279,18 @@ def run_c4(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MASQ_BENCH_FUNCTIONAL=1: exercise the N>1 code path on one GPU (every rank on cuda:0, gloo
+    # exchanges through the host) — a functional check of the multi-rank logic, never a timing
+    functional = os.environ.get("MASQ_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     T = args.tokens
     linears = layer_linears(args.linears.split(","))
     ids_h = synth.modality_ids(synth.CONFIGS[CFG]["pattern"], T=T)
@@ -403,10 +411,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MASQ_BENCH_FUNCTIONAL=1: exercise the N>1 code path on one GPU (every rank on cuda:0, gloo
+    # exchanges through the host) — a functional check of the multi-rank logic, never a timing
+    functional = os.environ.get("MASQ_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     linears = layer_linears(args.linears.split(","))
     T, r = args.tokens, args.rank_cmc
