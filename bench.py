@@ -62,8 +62,10 @@ def parse():
                     help="replay the step as one captured CUDA graph (N=1; measured slower here: the launch "
                          "gaps are ~2%% of the step and the captured profiler event nodes cost more)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines)")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
-                    help="c3: one Qwen2.5-VL-7B layer, every §8(a) row (default); c4: 28-layer calibration sweep")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c4s"],
+                    help="c3: one Qwen2.5-VL-7B layer, every §8(a) row (default); c4: 28-layer calibration sweep "
+                         "(2 loss passes at perturbed factors); c4s: the same sweep with 2 real S-optimisation "
+                         "epochs per layer (N1: loss + straight-through gradient + Adam)")
     ap.add_argument("--layers", type=int, default=28, help="c4: number of decoder layers")
     return ap.parse_args()
 
@@ -328,6 +330,10 @@ def run_c4(args):
                      for _ in range(2)])
     ws = M.Workspace(dev)
 
+    optimise = args.workload == "c4s"
+    grads = [torch.empty(N_MOD, e["d"], dtype=torch.float64, device=dev) for e in layers[0]]
+    adam = [None] * nl
+
     def sweep():
         for l in range(args.layers):
             for li, e in enumerate(layers[l]):
@@ -338,6 +344,25 @@ def run_c4(args):
             for li, e in enumerate(layers[l]):
                 svec.append(M.init_factors(Rv[l * nl + li], Cbuf[l * nl + li], e["W"], ws=ws))
                 M.reference_output(e["X"], e["W"], Yref=Yref[li], ws=ws)
+            if optimise:
+                # N1: 2 epochs of loss + straight-through gradient + log-space Adam,
+                # the gradient normalised by the global counts and SUM-reduced (token-sharded)
+                for li in range(nl):
+                    adam[li] = M.adam_init(svec[li])
+                for p_ in range(2):
+                    for li, e in enumerate(layers[l]):
+                        M.calib_loss_grad(e["X"], ids, svec[li], e["W"], WBITS, ABITS, Yref[li], grad=grads[li],
+                                          sums=Sbuf[li], counts=Nbuf[li], loss=losses[l, p_, li:li + 1],
+                                          count_norm=Cbuf[l * nl + li], ws=ws)
+                    if world > 1:
+                        P.reduce_loss(Sbuf, Nbuf)
+                    for li, e in enumerate(layers[l]):
+                        if world > 1:
+                            P.reduce_grad(grads[li])
+                            M.loss_finalize(Sbuf[li], Nbuf[li], e["n"], loss=losses[l, p_, li:li + 1])
+                        th, m1, m2 = adam[li]
+                        M.adam_step(th, grads[li], m1, m2, p_ + 1, 1e-2, s_out=svec[li])
+                continue
             for p_ in range(2):
                 for li, e in enumerate(layers[l]):
                     sp = svec[li] * pert[l][p_][li]
@@ -384,8 +409,10 @@ def run_c4(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic (device-generated, seeded)",
             "config": {"workload": (f"c4 (BASELINE configs[3]): {args.layers}-layer Qwen2.5-VL-7B-shaped calibration "
                                     f"sweep, {T} tokens/GPU (16 x [text 64 | image 768 | text 192]), per layer: stats "
-                                    "of 4 inputs, init, X W once, 2 loss passes (W4A8); one MAX/SUM exchange for all "
-                                    "layers' stats, one SUM per loss pass"),
+                                    "of 4 inputs, init, X W once, "
+                                    + ("2 S-optimisation epochs (loss + straight-through gradient + Adam, N1)"
+                                       if optimise else "2 loss passes")
+                                    + " (W4A8); one MAX/SUM exchange for all layers' stats, one SUM per pass"),
                        "tokens_per_gpu": T, "parallelism": f"dp{world}"},
             "kernels": kern, "gpu_launches": int(sum(v["launches_per_sweep"] for v in kern.values()) * args.steps),
             "clocks": clocks, "losses_layer0": [float(x) for x in losses[0].flatten().cpu().tolist()]}), flush=True)
@@ -398,7 +425,7 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if args.workload == "c4":
+    if args.workload in ("c4", "c4s"):
         return run_c4(args)
 
     import torch
