@@ -13,6 +13,17 @@
  *   A8  masq_calib_loss        sum_m lambda_m MAE(Q(X_m S_m^-1) Q(S_m W), X_m W)
  *                                                                          PAPER.md:62-70
  *       masq_reference_output  X W (f32), the loss target, computed once per batch
+ *   A3-A8 masq_calib_layer     one fused calibration pass of a linear (what bench.py runs)
+ *
+ * and the SURVEY §8(f) "next" rows on the same data:
+ *   N1  masq_calib_loss_grad, masq_adam_init / masq_adam_step, masq_keep_best,
+ *       masq_count_modalities                 S-optimisation (straight-through gradient, Adam)
+ *   N2  masq_cmc_factors (= masq_cmc_gram + masq_cmc_factors_from_gram)
+ *                                             whitened truncated-SVD CMC factors (Theorem 2)
+ *   N3  masq_quantize_weight_int4, masq_unpack_int4, masq_linear_decode
+ *                                             int4 weights in 128-channel groups, decode path
+ *   N4  masq_smooth_factors, masq_calibrate_meanabs, masq_range_stats
+ *                                             SmoothQuant / unified / AWQ baselines, dominance
  *
  * Conventions (apply to every entry point unless stated):
  *  - Shapes follow the paper's problem statement: X is [T x d]
