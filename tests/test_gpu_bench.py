@@ -33,9 +33,21 @@ def test_bench_single_gpu_contract():
 def test_bench_two_rank_code_path():
     env = dict(os.environ, MASQ_BENCH_FUNCTIONAL="1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2", *SMALL,
-                        "--no-n1"], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2", *SMALL],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
-    assert len(d["losses"]) == 2
+    assert len(d["losses"]) == 2 and d["n1_s_opt_step"]["ms_per_step"] > 0
+
+
+def test_bench_c4s_two_rank_code_path():
+    """The sweep workloads' exchanges (stats MAX/SUM, gradient and loss SUMs) with two ranks."""
+    env = dict(os.environ, MASQ_BENCH_FUNCTIONAL="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29534", "bench.py", "--gpus", "2",
+                        "--workload", "c4s", "--layers", "2", "--steps", "1", "--warmup", "1", "--tokens", "2048",
+                        "--linears", "qkv,o"], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and len(d["losses_layer0"]) == 4
