@@ -43,10 +43,10 @@ constexpr int kTileCodes = (kKChunk / kGroup) * 512;              // 16 KB
 constexpr int kTileScales = (kKChunk / kGroup) * 8 * 4;           // 1 KB
 
 constexpr int kDecThreads = 32 * (kDecWarps + 1);
-template <int kSub, int kStages>
+template <int kSub, int kStages, int kRed = 2>
 struct DecCfg {
   static constexpr int kStageBytes = kSub * (kTileCodes + kTileScales);
-  static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8 + 2 * kSub * kDecWarps * 32 * 4 * 4 + 64;
+  static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8 + kRed * kSub * kDecWarps * 32 * 4 * 4 + 64;
   static_assert(kSmem <= 232448, "decode shared memory");
 };
 
@@ -156,14 +156,14 @@ __device__ __forceinline__ void mma_s8u8(int (&c)[4], const uint32_t (&a)[4], ui
 // grid (x: CTAs streaming 32-column super tiles, y: K-chunks of 4096 channels); warps 0-7
 // consume, warp 8 (one lane) produces.  A stage holds up to 4 sub-tiles (8 columns each) of the
 // CTA's K-chunk: codes at [sub][group][512 B], scales at [sub][group][8 f32].
-template <int kSub, int kStages>
+template <int kSub, int kStages, int kRed = 2>
 __global__ void __launch_bounds__(kDecThreads) decode_kernel(const int8_t* __restrict__ qa,
                                                              const float* __restrict__ dx, int T, int64_t d,
                                                              int64_t n, const uint8_t* __restrict__ packed,
                                                              const float* __restrict__ scales,
                                                              float* __restrict__ part, float* __restrict__ Y,
                                                              int64_t ldy) {
-  constexpr int kStageBytes = DecCfg<kSub, kStages>::kStageBytes;
+  constexpr int kStageBytes = DecCfg<kSub, kStages, kRed>::kStageBytes;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* ring = dsm;
   uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kStages * kStageBytes);
@@ -251,7 +251,9 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const int8_t* __res
     const int ns = (int)(ntiles - jt0 < kSub ? ntiles - jt0 : kSub);
     mbar_wait(&full[st], ph);
     const uint8_t* sbase = ring + st * kStageBytes;
-    float* rb = red + (it & 1u) * (kSub * kDecWarps * 32 * 4);
+    // kRed == 1: one partials buffer; the reducers of the previous stage must be done with it
+    if (kRed == 1 && it > 0) asm volatile("bar.sync 1, %0;" ::"n"(32 * kDecWarps) : "memory");
+    float* rb = red + (kRed == 2 ? (it & 1u) : 0u) * (kSub * kDecWarps * 32 * 4);
 #pragma unroll
     for (int sub = 0; sub < kSub; ++sub) {
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -399,24 +401,26 @@ cudaError_t launch_decode(const int8_t* qa, const float* dx, int T, int64_t d, i
   cudaError_t err = cudaSuccess;
   {
     ProfScope ps_("decode_w4a8", st);
-#define DEC(S, K)                                                                                             \
+#define DEC(S, K, RD)                                                                                         \
   {                                                                                                           \
     static bool attr = false;                                                                                 \
     if (!attr) {                                                                                              \
-      err = cudaFuncSetAttribute(decode_kernel<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,            \
-                                 DecCfg<S, K>::kSmem);                                                        \
+      err = cudaFuncSetAttribute(decode_kernel<S, K, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                 DecCfg<S, K, RD>::kSmem);                                                    \
       if (err != cudaSuccess) return err;                                                                     \
       attr = true;                                                                                            \
     }                                                                                                         \
-    decode_kernel<S, K><<<grid, kDecThreads, DecCfg<S, K>::kSmem, st>>>(qa, dx, T, d, n, packed, scales, part, \
-                                                                      Y, ldy);                               \
+    decode_kernel<S, K, RD><<<grid, kDecThreads, DecCfg<S, K, RD>::kSmem, st>>>(qa, dx, T, d, n, packed,      \
+                                                                              scales, part, Y, ldy);         \
   }
     switch (cfg) {
-      case 33: DEC(3, 3) break;
-      case 24: DEC(2, 4) break;
-      case 25: DEC(2, 5) break;
-      case 16: DEC(1, 6) break;
-      default: DEC(4, 2) break;
+      case 33: DEC(3, 3, 2) break;
+      case 24: DEC(2, 4, 2) break;
+      case 25: DEC(2, 5, 2) break;
+      case 16: DEC(1, 6, 2) break;
+      case 431: DEC(4, 3, 1) break;
+      case 531: DEC(5, 2, 1) break;
+      default: DEC(4, 2, 2) break;
     }
 #undef DEC
   }
