@@ -7,7 +7,10 @@
 // so codes and scales are bit-exact against the CPU oracle.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace masq {
 namespace {
@@ -530,6 +533,224 @@ __global__ void __launch_bounds__(1024) aquant_row_kernel(const XT* __restrict__
   }
 }
 
+// ---- packed f32x2 arithmetic (sm_100: FMUL2/FFMA2/FADD2 issue two IEEE f32 ops per instruction).
+// Each op rounds once (RN) per lane.  ptxas contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into
+// one FFMA2, so the kernel below never feeds a packed product into a packed add: every place that
+// wants a product-then-add spells the fused form it means (fma.rn.f32x2).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// bf16 row kernel, one token row per CTA iteration over rows [r0, r1) contiguous per CTA (so the
+// modality changes rarely and each thread's chunk of the factors 1/s^m stays in registers, INVR).
+// X rows stream into a shared-memory ring of S stages by 1D TMA bulk copies (S rows in flight per
+// CTA: the register-fed version kept only ~1 row per CTA in flight and sat at 45% of HBM); the
+// smoothed row xs = x * (1/s) is kept in registers between the absmax and the code pass, so a
+// stage is refilled as soon as the CTA has passed the absmax barrier.
+// Per element: 1 unpack + 1/2 FMUL2 + 1/2 FMNMX3 (absmax); 1/2 FFMA2 (t = xs*rcp + 1.5*2^23) +
+// 1/2 FADD2 (r = t - 1.5*2^23) + 1/2 FFMA2 (e = xs*rcp - r) + 1/2 FMNMX3 (max |e|) + 3/4 PRMT.
+// Code proof: p = xs*rcp exactly (the FFMA2 product is not rounded); t rounds p to the nearest
+// integer r (ulp of t is 1, |p| < 2^22) and its low byte is r's two's complement; e = fl(p - r),
+// |e - (p - r)| <= 2^-25.  With |xs/delta| <= q_max (1 + 2^-22) < 128: rcp = fl(1/delta) gives
+// |p - xs/delta| <= 128 * 2^-24 = 2^-17 and the IEEE quotient q* = fl(xs/delta) is within half an
+// ulp (<= 2^-18) of xs/delta, so |p - q*| < 2^-16.  If every |e| <= 1/2 - 2^-15 then
+// |q* - r| <= 1/2 - 2^-15 + 2^-25 + 2^-16 < 1/2: rha(q*) = r with no tie (and no clamp,
+// |r| <= q_max).  Otherwise the chunk is recomputed with the exact division (quant8_exact); with
+// uniform fractional parts that is 2^-14 of the elements.
+// out of line: the rare exact path of 8 codes (keeps the unrolled hot loop small; the inlined
+// divisions of every chunk overflowed the instruction cache)
+__device__ __noinline__ uint2 quant8_exact(uint64_t a, uint64_t b, uint64_t c, uint64_t e, float delta, float rcp,
+                                           int qmin, int qmax) {
+  float f[8];
+  f2_unpack(a, f[0], f[1]);
+  f2_unpack(b, f[2], f[3]);
+  f2_unpack(c, f[4], f[5]);
+  f2_unpack(e, f[6], f[7]);
+  return make_uint2(quant4_exact(f[0], f[1], f[2], f[3], delta, rcp, qmin, qmax),
+                    quant4_exact(f[4], f[5], f[6], f[7], delta, rcp, qmin, qmax));
+}
+
+constexpr int kAqMaxStages = 16;
+constexpr int kAqMaxThreads = 384;                    // 170 registers per thread at CPL = 8
+template <int CPL>
+__global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
+    const __nv_bfloat16* __restrict__ X, int64_t ld_x, const uint8_t* __restrict__ ids, int64_t d, int n_mod,
+    const float* __restrict__ inv_s, float qaf, int qmin, int qmax, int8_t* __restrict__ qx,
+    float* __restrict__ dx, uint32_t* __restrict__ mask, uint32_t* __restrict__ status,
+    const int32_t* __restrict__ perm, int64_t T_out, int64_t rows_per_cta, int S) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ uint64_t full[kAqMaxStages];
+  __shared__ uint32_t s_red[2][32];
+  constexpr float kMagic = 12582912.0f;               // 1.5 * 2^23
+  constexpr float kLim = 0.5f - 0.000030517578125f;   // 1/2 - 2^-15 (see the proof above)
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = r0 + rows_per_cta < T_out ? r0 + rows_per_cta : T_out;
+  if (r0 >= r1) return;
+  const uint32_t rowb = (uint32_t)(d * 2);
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) sm100::mbar_init(&full[st], 1);
+    sm100::fence_mbar_init();
+    for (int64_t row = r0; row < r1 && row < r0 + S; ++row) {
+      const int st = (int)(row - r0);
+      const int64_t src = perm ? (int64_t)__ldg(perm + row) : row;
+      if (src >= 0) {
+        sm100::mbar_expect_tx(&full[st], rowb);
+        sm100::bulk_load_1d(ring + (size_t)st * rowb, X + src * ld_x, rowb, &full[st]);
+      } else {
+        sm100::mbar_arrive(&full[st]);                 // padding row: complete the phase, no data
+      }
+    }
+  }
+  __syncthreads();
+  // this thread's chunks: columns c_k = (k * nthr + tid) * 8; every chunk but the last is valid
+  // (CPL = ceil(chunks / nthr)); the last one is valid while c_{CPL-1} < d
+  const bool last_ok = ((CPL - 1) * nthr + tid) * 8 < d;
+  const uint32_t sbase = sm100::smem_u32(ring) + (uint32_t)tid * 16u;
+  const uint64_t magic2 = f2_pack(kMagic, kMagic);
+  uint64_t inv2[CPL][4];
+  int mc = -1;
+  int par = 0, st = 0;
+  uint32_t ph = 0;
+  for (int64_t row = r0; row < r1; ++row) {
+    const int64_t src = perm ? (int64_t)__ldg(perm + row) : row;
+    const int m = src >= 0 ? (int)__ldg(ids + src) : 0;
+    const bool skip = src < 0 || m >= n_mod;             // CTA-uniform
+    if (!skip && m != mc) {                              // CTA-uniform, once per modality run
+      mc = m;
+      const float* inv = inv_s + (int64_t)m * d + tid * 8;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        if (k < CPL - 1 || last_ok) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(inv + k * nthr * 8));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(inv + k * nthr * 8 + 4));
+          inv2[k][0] = f2_pack(a.x, a.y);
+          inv2[k][1] = f2_pack(a.z, a.w);
+          inv2[k][2] = f2_pack(b.x, b.y);
+          inv2[k][3] = f2_pack(b.z, b.w);
+        }
+      }
+    }
+    sm100::mbar_wait(&full[st], ph);
+    // pass 1: xs = x * (1/s) (f32, one rounding), running max |xs| (two independent chains)
+    uint64_t xs[CPL][4];
+    float am0 = 0.f, am1 = 0.f;
+    const uint32_t srow = sbase + (uint32_t)st * rowb;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      if (k < CPL - 1 || last_ok) {
+        uint32_t w[4];
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "r"(srow + (uint32_t)(k * nthr * 16)));
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          xs[k][p] = f2_mul(f2_pack(__uint_as_float(w[p] << 16), __uint_as_float(w[p] & 0xFFFF0000u)), inv2[k][p]);
+          float lo, hi;
+          f2_unpack(xs[k][p], lo, hi);
+          if (p & 1) am1 = fmax3(am1, fabsf(lo), fabsf(hi));
+          else am0 = fmax3(am0, fabsf(lo), fabsf(hi));
+        }
+      }
+    }
+    const float amax = fmaxf(am0, am1);
+    uint32_t ab = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));   // non-negative: u32 order
+    if (nw > 1) {
+      if (lane == 0) s_red[par][warp] = ab;
+    }
+    __syncthreads();                                     // every thread is done with the stage
+    if (tid == 0 && row + S < r1) {                      // refill it with row + S
+      const int64_t nrow = row + S;
+      const int64_t nsrc = perm ? (int64_t)__ldg(perm + nrow) : nrow;
+      if (nsrc >= 0) {
+        sm100::mbar_expect_tx(&full[st], rowb);
+        sm100::bulk_load_1d(ring + (size_t)st * rowb, X + nsrc * ld_x, rowb, &full[st]);
+      } else {
+        sm100::mbar_arrive(&full[st]);
+      }
+    }
+    if (++st == S) { st = 0; ph ^= 1u; }
+    if (nw > 1) {
+      ab = __reduce_max_sync(0xffffffffu, lane < nw ? s_red[par][lane] : 0u);
+      par ^= 1;
+    }
+    if (skip) {
+      if (src >= 0) {                                    // bad modality id: zero codes, flag
+        if (tid == 0) { atomicOr(status, kStBadModality); dx[row] = 0.f; }
+        int8_t* qr = qx + row * d;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          const int c = (k * nthr + tid) * 8;
+          if (c < d) *reinterpret_cast<uint2*>(qr + c) = make_uint2(0, 0);
+        }
+      }
+      continue;
+    }
+    const float delta = fmaxf(__fdiv_rn(__uint_as_float(ab), qaf), kFloor);
+    const float rcp = __fdiv_rn(1.0f, delta);
+    const uint64_t rcp2 = f2_pack(rcp, rcp);
+    int8_t* qr = qx + row * d;
+    // pass 2: codes
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = (k * nthr + tid) * 8;
+      if (k < CPL - 1 || last_ok) {
+        uint32_t tb[8];
+        float emax = 0.f;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint64_t t = f2_fma(xs[k][p], rcp2, magic2);
+          const uint64_t nr = f2_sub(magic2, t);               // -r, exact
+          const uint64_t e = f2_fma(xs[k][p], rcp2, nr);
+          float t0, t1, e0, e1;
+          f2_unpack(t, t0, t1);
+          f2_unpack(e, e0, e1);
+          tb[2 * p] = __float_as_uint(t0);
+          tb[2 * p + 1] = __float_as_uint(t1);
+          emax = fmax3(emax, fabsf(e0), fabsf(e1));
+        }
+        uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+        uint32_t w1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+        if (emax > kLim) {                                   // rare: exact IEEE quotient + rha
+          const uint2 wx = quant8_exact(xs[k][0], xs[k][1], xs[k][2], xs[k][3], delta, rcp, qmin, qmax);
+          w0 = wx.x;
+          w1 = wx.y;
+        }
+        *reinterpret_cast<uint2*>(qr + c) = make_uint2(w0, w1);
+      }
+    }
+    if (tid == 0) {
+      dx[row] = delta;
+      if (mask) atomicOr(mask + (row >> 7), 1u << m);
+    }
+  }
+}
+
 // one warp per token row; two passes over the row (absmax, then codes; the 2nd read hits L1/L2)
 template <typename XT>
 __global__ void __launch_bounds__(256) aquant_kernel(const XT* __restrict__ X, int64_t ld_x,
@@ -866,6 +1087,74 @@ static cudaError_t aquant_reg_dispatch(const XT* X, int64_t ld_x, const uint8_t*
   return cudaGetLastError();
 }
 
+// bf16 X: aquant_bf16_kernel with the smallest CPL (16-byte chunks per thread) that fits the row in
+// <= 512 threads with the factors in registers, else <= 1024 threads with the factors read per row
+template <int CPL>
+static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, const uint8_t* ids, int64_t d, int n_mod,
+                                      const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx, float* dx,
+                                      uint32_t* mask, uint32_t* status, const int32_t* perm, int64_t T_out, int nthr,
+                                      cudaStream_t st) {
+  auto kern = aquant_bf16_kernel<CPL>;
+  const int64_t rowb = 2 * d;
+  constexpr int64_t kRingPerSm = 192 * 1024;            // shared memory for row stages per SM
+  // register-limited CTAs per SM for this block size (queried once per instantiation and size;
+  // the launch configuration is a pure function of (CPL, nthr, d))
+  static thread_local int cached_nthr = -1, cached_occ = 0;
+  static thread_local bool attr_set = false;
+  if (cached_nthr != nthr) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, 0);
+    if (e != cudaSuccess) return e;
+    cached_nthr = nthr;
+    cached_occ = occ;
+  }
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingPerSm);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int per_sm = std::max(1, std::min(cached_occ, 16));
+  int S = 0;
+  for (; per_sm >= 1; --per_sm) {
+    S = (int)std::min<int64_t>(kAqMaxStages, kRingPerSm / per_sm / rowb);
+    if (S >= 2) break;
+  }
+  if (per_sm < 1 || S < 2) return cudaErrorNotSupported;
+  const int smem = (int)(S * rowb);
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(T_out, (int64_t)num_sms() * per_sm));
+  const int64_t rows = ceil_div(T_out, ctas);
+  kern<<<(unsigned)ceil_div(T_out, rows), nthr, smem, st>>>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx,
+                                                            mask, status, perm, T_out, rows, S);
+  return cudaGetLastError();
+}
+
+// bf16 X: the fewest warps per row with <= 8 16-byte chunks per thread (the smoothed row and the
+// thread's factor chunk stay in registers), rows up to 384 x 8 x 8 = 24576 channels
+static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, const uint8_t* ids, int64_t d,
+                                        int n_mod, const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx,
+                                        float* dx, uint32_t* mask, uint32_t* status, const int32_t* perm,
+                                        int64_t T_out, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(X) & 15) || (ld_x & 7) || (d & 7)) return cudaErrorNotSupported;  // 16-B rows
+  const int64_t ch = d / 8;
+  static const int target = [] {
+    const char* e = getenv("MASQ_AQ_CPL");               // measurement knob (chunks per thread)
+    const int v = e ? atoi(e) : 8;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  int64_t nthr = 32 * ceil_div(ch, (int64_t)target * 32);
+  if (nthr > kAqMaxThreads) nthr = 32 * ceil_div(ch, 8 * 32);
+  if (nthr > kAqMaxThreads) return cudaErrorNotSupported;
+  const int cpl = (int)ceil_div(ch, nthr);
+  ProfScope ps_("aquant", st);
+#define AQB(C) case C: return aquant_bf16_launch<C>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out, (int)nthr, st)
+  switch (cpl) {
+    AQB(1); AQB(2); AQB(3); AQB(4); AQB(5); AQB(6); AQB(7); AQB(8);
+    default: break;
+  }
+#undef AQB
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
                           uint32_t* status, cudaStream_t st, const int32_t* perm, int64_t T_out) {
@@ -876,7 +1165,12 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
     if (e != cudaSuccess) return e;
   }
   const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
-  cudaError_t er;
+  cudaError_t er = cudaErrorNotSupported;
+  static const bool v1 = getenv("MASQ_AQUANT_V1") != nullptr;   // measurement switch: previous kernel
+  if (xt == MASQ_BF16 && !v1)
+    er = aquant_bf16_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax, qmin,
+                              qmax, qx, dx, mask, status, perm, T_out, st);
+  if (er != cudaErrorNotSupported) return er;
   if (xt == MASQ_BF16) er = aquant_reg_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s,
                                                 (float)qmax, qmin, qmax, qx, dx, mask, status, perm, T_out, st);
   else er = aquant_reg_dispatch(static_cast<const float*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax, qmin, qmax,
