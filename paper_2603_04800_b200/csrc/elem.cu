@@ -98,6 +98,47 @@ __device__ __forceinline__ uint32_t quant4_exact(float x0, float x1, float x2, f
 __device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ float to_f32(float v) { return v; }
 
+// ---- packed f32x2 arithmetic (sm_100: FMUL2/FFMA2/FADD2 issue two IEEE f32 ops per instruction).
+// Each op rounds once (RN) per lane.  ptxas contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into
+// one FFMA2, so the kernel below never feeds a packed product into a packed add: every place that
+// wants a product-then-add spells the fused form it means (fma.rn.f32x2).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// out of line: the rare exact path of 4 codes from two packed pairs of f32 values
+__device__ __noinline__ uint32_t quant4_exact_ool(uint64_t a, uint64_t b, float delta, float rcp, int qmin, int qmax) {
+  float f[4];
+  f2_unpack(a, f[0], f[1]);
+  f2_unpack(b, f[2], f[3]);
+  return quant4_exact(f[0], f[1], f[2], f[3], delta, rcp, qmin, qmax);
+}
+
 // =============================================================== A1 stats
 // |x| max over packed words: bf16 pairs compare as unsigned 16-bit halves once the sign bits are
 // cleared (non-negative bf16 / f32 order == unsigned bit-pattern order), so the max is exact.
@@ -289,13 +330,20 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
       float f[U][V];
 #pragma unroll
       for (int u = 0; u < U; ++u) Vec<WT>::load(W + (sb + r + u) * n + j0, f[u]);
+      // |s_i w_ij| for two rows at a time: FMUL2 on column pairs, FMNMX3 folds both rows
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; u += 2)
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const float si = ss[k][r + u];
+          const uint64_t s0 = f2_pack(ss[k][r + u], ss[k][r + u]), s1 = f2_pack(ss[k][r + u + 1], ss[k][r + u + 1]);
 #pragma unroll
-          for (int e = 0; e < V; ++e) m[k][e] = fmaxf(m[k][e], fabsf(__fmul_rn(si, f[u][e])));
+          for (int e = 0; e < V; e += 2) {
+            float a0, a1, b0, b1;
+            f2_unpack(f2_mul(f2_pack(f[u][e], f[u][e + 1]), s0), a0, a1);
+            f2_unpack(f2_mul(f2_pack(f[u + 1][e], f[u + 1][e + 1]), s1), b0, b1);
+            m[k][e] = fmax3(m[k][e], fabsf(a0), fabsf(b0));
+            m[k][e + 1] = fmax3(m[k][e + 1], fabsf(a1), fabsf(b1));
+          }
         }
     }
     for (; r < nr; ++r) {
@@ -381,29 +429,30 @@ __global__ void __launch_bounds__(256) wquant_kernel(const WT* __restrict__ W, c
 #pragma unroll
       for (int e = 0; e < CPT; ++e) rcv[e] = 1.f;
     }
-    uint32_t nearmask = 0;
+    // codes of rows 4ty..4ty+3 at column e: ws = f32(s_i w_ij) on row pairs (FMUL2), then the
+    // exact-product rounding of aquant_bf16_kernel (FFMA2 t / FADD2 -r / FFMA2 e, 2^-15 margin);
+    // a flagged quad is recomputed from the registers by the out-of-line exact path
+    constexpr float kMagic = 12582912.0f;
+    constexpr float kLim = 0.5f - 0.000030517578125f;
+    const uint64_t magic2 = f2_pack(kMagic, kMagic);
+    const uint64_t s01 = f2_pack(si[0], si[1]), s23 = f2_pack(si[2], si[3]);
 #pragma unroll
     for (int e = 0; e < CPT; ++e) {
-      const float rc = rcv[e];
-      bool nr;
-      tile[tx * CPT + e][ty] = quant4_fast(__fmul_rn(si[0], f[0][e]), __fmul_rn(si[1], f[1][e]),
-                                           __fmul_rn(si[2], f[2][e]), __fmul_rn(si[3], f[3][e]), rc, qmin, qmax, nr);
-      nearmask |= (uint32_t)nr << e;
-    }
-#pragma unroll 1
-    while (nearmask) {                                       // rare exact fix-up of flagged quads
-      const int e = __ffs(nearmask) - 1;
-      nearmask &= nearmask - 1;
-      const int64_t j = jb + e;
-      const float dv = __ldg(dw + (int64_t)k * n + j);
-      const float rc = __ldg(rcp + (int64_t)k * n + j);
-      float x[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int64_t i = i0 + 4 * ty + r;
-        x[r] = i < d ? __fmul_rn(__ldg(s + (int64_t)k * d + i), to_f32(W[i * n + j])) : 0.f;
-      }
-      tile[tx * CPT + e][ty] = quant4_exact(x[0], x[1], x[2], x[3], dv, rc, qmin, qmax);
+      const uint64_t rc2 = f2_pack(rcv[e], rcv[e]);
+      const uint64_t a = f2_mul(f2_pack(f[0][e], f[1][e]), s01);
+      const uint64_t b = f2_mul(f2_pack(f[2][e], f[3][e]), s23);
+      const uint64_t ta = f2_fma(a, rc2, magic2), tb = f2_fma(b, rc2, magic2);
+      const uint64_t ea = f2_fma(a, rc2, f2_sub(magic2, ta)), eb = f2_fma(b, rc2, f2_sub(magic2, tb));
+      float t0, t1, t2, t3, e0, e1, e2, e3;
+      f2_unpack(ta, t0, t1);
+      f2_unpack(tb, t2, t3);
+      f2_unpack(ea, e0, e1);
+      f2_unpack(eb, e2, e3);
+      uint32_t word = __byte_perm(__byte_perm(__float_as_uint(t0), __float_as_uint(t1), 0x0040),
+                                  __byte_perm(__float_as_uint(t2), __float_as_uint(t3), 0x0040), 0x5410);
+      if (fmaxf(fmax3(fabsf(e0), fabsf(e1), fabsf(e2)), fabsf(e3)) > kLim)
+        word = quant4_exact_ool(a, b, __ldg(dw + (int64_t)k * n + jb + e), rcv[e], qmin, qmax);
+      tile[tx * CPT + e][ty] = word;
     }
     __syncthreads();
     // write JT rows (j) x 128 bytes (i): 8 threads per row, 16 bytes each
@@ -531,39 +580,6 @@ __global__ void __launch_bounds__(1024) aquant_row_kernel(const XT* __restrict__
       if (mask) atomicOr(mask + (row >> 7), 1u << m);
     }
   }
-}
-
-// ---- packed f32x2 arithmetic (sm_100: FMUL2/FFMA2/FADD2 issue two IEEE f32 ops per instruction).
-// Each op rounds once (RN) per lane.  ptxas contracts a mul.rn.f32x2 feeding an add.rn.f32x2 into
-// one FFMA2, so the kernel below never feeds a packed product into a packed add: every place that
-// wants a product-then-add spells the fused form it means (fma.rn.f32x2).
-__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
 }
 
 // bf16 row kernel, one token row per CTA iteration over rows [r0, r1) contiguous per CTA (so the
