@@ -389,17 +389,37 @@ struct Lam8 {
   float v[kMaxMod];
 };
 
-// contrib[l] = sum of vals over the run of keys == l in the (stably) sorted key list, in the
-// original order of the keys (radix sort is stable) -> deterministic; keys -1 sort last
-__global__ void runsum_kernel(const uint32_t* __restrict__ skeys, const double* __restrict__ svals, int64_t nkeys,
-                              int64_t nl, double* __restrict__ contrib) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nkeys) return;
-  const uint32_t k = skeys[i];
-  if (k >= (uint32_t)nl || (i > 0 && skeys[i - 1] == k)) return;     // not a run start
-  double a = 0.0;
-  for (int64_t j = i; j < nkeys && skeys[j] == k; ++j) a += svals[j];
-  contrib[k] = a;
+// contrib[l] = sum of vals over the run of keys == l in the (stably) sorted key list; keys -1
+// sort last.  The warp whose 32 elements hold a run's first key sums the whole run: lane q takes
+// elements start + q, start + q + 32, ... in order, then a fixed xor-shuffle tree -> the same
+// association on every run, so the result is deterministic.  (A run can be as long as every
+// column of the weight: the columns' arg-max rows concentrate on the outlier channels.)
+__global__ void __launch_bounds__(256) runsum_kernel(const uint32_t* __restrict__ skeys,
+                                                     const double* __restrict__ svals, int64_t nkeys, int64_t nl,
+                                                     double* __restrict__ contrib) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+  const int64_t i = base + lane;
+  uint32_t k = 0xFFFFFFFFu;
+  bool start = false;
+  if (i < nkeys) {
+    k = skeys[i];
+    start = k < (uint32_t)nl && (i == 0 || skeys[i - 1] != k);
+  }
+  uint32_t bal = __ballot_sync(0xffffffffu, start);
+  while (bal) {
+    const int src = __ffs(bal) - 1;
+    bal &= bal - 1;
+    const uint32_t kk = __shfl_sync(0xffffffffu, k, src);
+    double a = 0.0;
+    for (int64_t j = base + src + lane; j < nkeys; j += 32) {
+      if (skeys[j] != kk) break;                       // sorted: no later element of this lane matches
+      a += svals[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) contrib[kk] = a;
+  }
 }
 
 // grad[m][i] = lambda_m / (counts_m * n) * (sum_jt partial[m][jt][i] + contrib[m*d + i])  (fixed order)
