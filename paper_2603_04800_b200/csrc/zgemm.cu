@@ -49,6 +49,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   if (!(tmask & want)) return;                   // CTA-uniform: no modality of this pass here
 
   const int N = per * rpad;                      // accumulator columns (= B box rows)
+  const bool combined = 2 * N <= 256;            // [hi; lo] planes as one B operand
   const int BB = N * 128;                        // one B plane chunk
   const int SB = ((a_planes * XCH + 2 * BB) + 1023) & ~1023;
 
@@ -94,7 +95,11 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, N);
+      // B = [L1'hi ; L1'lo] (2N rows, the two TMA boxes are contiguous): one N = 2N MMA per
+      // k-step accumulates X.L1'hi into columns [0, N) and X.L1'lo into [N, 2N); the epilogue
+      // adds the halves
+      // (ranks above 128: two N-column MMAs into the same accumulator, as before)
+      const uint32_t idesc = idesc_bf16(128, combined ? 2 * N : N);
       uint32_t st = 0, ph = 0;
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&full[st], ph);
@@ -104,7 +109,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bh + k * 32), idesc, (kc | k) != 0);
-          mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bl + k * 32), idesc, 1u);
+          if (!combined) mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bl + k * 32), idesc, 1u);
           if (a_planes == 2)
             mma_bf16(tmem, umma_desc_sw128(base + XCH + k * 32), umma_desc_sw128(bh + k * 32), idesc, 1u);
         }
@@ -128,8 +133,14 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
       const bool mine = mid == mm;
       uint16_t* zr = Z + (int64_t)g * zld + (int64_t)(mm - 1) * 2 * rpad;
       for (int c = 0; c < rpad / 32; ++c) {
-        uint32_t v[32];
+        uint32_t v[32], w[32];
         tmem_ld32(taddr + (mm - m0) * rpad + c * 32, v);
+        if (combined) {
+          tmem_ld32(taddr + N + (mm - m0) * rpad + c * 32, w);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__fadd_rn(__uint_as_float(v[e]), __uint_as_float(w[e])));
+        }
         tmem_wait_ld();
         if (g < T) {
 #pragma unroll
@@ -228,7 +239,9 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
                          cudaStream_t st) {
   if (T <= 0 || n_mod < 2 || rpad <= 0) return cudaSuccess;
   const int n_nt = n_mod - 1;
-  const int per = std::max(1, std::min(n_nt, 256 / rpad));
+  // modalities per pass: 2 * per * rpad <= 256 MMA columns (the combined [hi; lo] form), else
+  // per * rpad <= 256 with two MMAs per k-step
+  const int per = rpad <= 128 ? std::max(1, std::min(n_nt, 128 / rpad)) : std::max(1, std::min(n_nt, 256 / rpad));
   const int passes = (int)ceil_div(n_nt, per);
   const int a_planes = A1 ? 2 : 1;
   CUtensorMap ta0, ta1, tb;
@@ -245,8 +258,9 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   const int smem = stages * SB + 2048;
   cudaError_t e = cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  const int acc_cols = 2 * N <= 256 ? 2 * N : N;
   uint32_t cols = 32;
-  while ((int)cols < N) cols <<= 1;
+  while ((int)cols < acc_cols) cols <<= 1;
   dim3 grid((unsigned)ceil_div(T, 128), (unsigned)passes);
   ProfScope ps_("zgemm", st);
   zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols, stages,
