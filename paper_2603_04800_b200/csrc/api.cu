@@ -67,6 +67,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.amax = take(2 * sizeof(uint32_t) * n_mod * n);
       L.partials = take(sizeof(double) * (Tg / kUnitM) * ceil_div(n, kTileN) * 16);
       L.fpart = take(sizeof(double) * ceil_div(T, kUnitM) * ceil_div(n, kTileN) * 2);
+      L.ipos = take(sizeof(int32_t) * T);
       if (rp > 0 && nnt > 0) {
         L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
         L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
@@ -405,11 +406,19 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   const int epi = gemm_epilogue_warps();
   // shared front half: factors, routing, every modality's weight codes (set 0 = the forward's
   // Q(S_t W)), the token-order activation codes (forward) and their grouped copy (loss)
+  int32_t* ipos = reinterpret_cast<int32_t*>(W8(ws, L.ipos));
   MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
-  MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, cnt, st));
+  MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, cnt, st, ipos));
   MASQ_CK(launch_wquant(W, MASQ_BF16, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
-  MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask, status_of(ws), st));
-  MASQ_CK(launch_gather_rows(qt, dt, perm, Tg, d, qg, dg, st));
+  // the loss GEMM below skips the text units, so only the non-text rows need the grouped copy
+  const cudaError_t qe = launch_aquant_dual(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask,
+                                            status_of(ws), perm, tmod, ipos, Tg, qg, dg, st);
+  if (qe == cudaErrorNotSupported) {
+    MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask, status_of(ws), st));
+    MASQ_CK(launch_gather_rows(qt, dt, perm, Tg, d, qg, dg, st));
+  } else {
+    MASQ_CK(qe);
+  }
   // A8 target first: the forward's epilogue reads it for the text rows
   GemmArgs gr{};
   gr.mode = kModeRef;

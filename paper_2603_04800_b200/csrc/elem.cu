@@ -618,7 +618,8 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
     const __nv_bfloat16* __restrict__ X, int64_t ld_x, const uint8_t* __restrict__ ids, int64_t d, int n_mod,
     const float* __restrict__ inv_s, float qaf, int qmin, int qmax, int8_t* __restrict__ qx,
     float* __restrict__ dx, uint32_t* __restrict__ mask, uint32_t* __restrict__ status,
-    const int32_t* __restrict__ perm, int64_t T_out, int64_t rows_per_cta, int S) {
+    const int32_t* __restrict__ perm, int64_t T_out, int64_t rows_per_cta, int S, int8_t* __restrict__ qg,
+    float* __restrict__ dg, const int32_t* __restrict__ ipos) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ uint64_t full[kAqMaxStages];
   __shared__ uint32_t s_red[2][32];
@@ -731,6 +732,10 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
     const float rcp = __fdiv_rn(1.0f, delta);
     const uint64_t rcp2 = f2_pack(rcp, rcp);
     int8_t* qr = qx + row * d;
+    // optional second copy of a non-text row at its modality-grouped position (the loss GEMM's
+    // operand of the fused layer call; CTA-uniform)
+    const int64_t gp = (qg != nullptr && m != 0) ? (int64_t)__ldg(ipos + row) : -1;
+    int8_t* qgr = gp >= 0 ? qg + gp * d : nullptr;
     // pass 2: codes
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
@@ -758,10 +763,12 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
           w1 = wx.y;
         }
         *reinterpret_cast<uint2*>(qr + c) = make_uint2(w0, w1);
+        if (qgr) *reinterpret_cast<uint2*>(qgr + c) = make_uint2(w0, w1);
       }
     }
     if (tid == 0) {
       dx[row] = delta;
+      if (qgr) dg[gp] = delta;
       if (mask) atomicOr(mask + (row >> 7), 1u << m);
     }
   }
@@ -839,7 +846,8 @@ __global__ void __launch_bounds__(256) aquant_kernel(const XT* __restrict__ X, i
 // unit boundary so every loss unit (one CTA pair) holds a single modality (uses its Q(S_m W)).
 __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__ ids, int64_t T, int n_mod,
                                                      int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
-                                                     int64_t n_tiles, int64_t* __restrict__ counts) {
+                                                     int64_t n_tiles, int64_t* __restrict__ counts,
+                                                     int32_t* __restrict__ ipos) {
   __shared__ int s_warp[kMaxMod][32];
   __shared__ int s_tot[kMaxMod], s_seg[kMaxMod + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -899,7 +907,10 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
     const int m = ids[t];
 #pragma unroll
     for (int mm = 0; mm < kMaxMod; ++mm)
-      if (m == mm && mm < n_mod) perm[pos[mm]++] = (int32_t)t;
+      if (m == mm && mm < n_mod) {
+        if (ipos) ipos[t] = pos[mm];
+        perm[pos[mm]++] = (int32_t)t;
+      }
   }
   for (int64_t tile = tid; tile < n_tiles; tile += 1024) {
     const int64_t r = tile * kUnitM;
@@ -1109,7 +1120,7 @@ template <int CPL>
 static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, const uint8_t* ids, int64_t d, int n_mod,
                                       const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx, float* dx,
                                       uint32_t* mask, uint32_t* status, const int32_t* perm, int64_t T_out, int nthr,
-                                      cudaStream_t st) {
+                                      int8_t* qg, float* dg, const int32_t* ipos, cudaStream_t st) {
   auto kern = aquant_bf16_kernel<CPL>;
   const int64_t rowb = 2 * d;
   constexpr int64_t kRingPerSm = 192 * 1024;            // shared memory for row stages per SM
@@ -1140,7 +1151,7 @@ static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, cons
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(T_out, (int64_t)num_sms() * per_sm));
   const int64_t rows = ceil_div(T_out, ctas);
   kern<<<(unsigned)ceil_div(T_out, rows), nthr, smem, st>>>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx,
-                                                            mask, status, perm, T_out, rows, S);
+                                                            mask, status, perm, T_out, rows, S, qg, dg, ipos);
   return cudaGetLastError();
 }
 
@@ -1149,7 +1160,8 @@ static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, cons
 static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, const uint8_t* ids, int64_t d,
                                         int n_mod, const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx,
                                         float* dx, uint32_t* mask, uint32_t* status, const int32_t* perm,
-                                        int64_t T_out, cudaStream_t st) {
+                                        int64_t T_out, cudaStream_t st, int8_t* qg = nullptr, float* dg = nullptr,
+                                        const int32_t* ipos = nullptr) {
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (ld_x & 7) || (d & 7)) return cudaErrorNotSupported;  // 16-B rows
   const int64_t ch = d / 8;
   static const int target = [] {
@@ -1162,7 +1174,7 @@ static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, co
   if (nthr > kAqMaxThreads) return cudaErrorNotSupported;
   const int cpl = (int)ceil_div(ch, nthr);
   ProfScope ps_("aquant", st);
-#define AQB(C) case C: return aquant_bf16_launch<C>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out, (int)nthr, st)
+#define AQB(C) case C: return aquant_bf16_launch<C>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out, (int)nthr, qg, dg, ipos, st)
   switch (cpl) {
     AQB(1); AQB(2); AQB(3); AQB(4); AQB(5); AQB(6); AQB(7); AQB(8);
     default: break;
@@ -1203,6 +1215,42 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
   return cudaGetLastError();
 }
 
+// padding rows of the grouped copy (perm < 0): zero codes and scale, rows of modality >= m_lo only
+__global__ void __launch_bounds__(256) pad_rows_kernel(const int32_t* __restrict__ perm,
+                                                       const uint32_t* __restrict__ tile_mod, int64_t Tg, int64_t d,
+                                                       int m_lo, int8_t* __restrict__ qg, float* __restrict__ dg) {
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= Tg || __ldg(perm + p) >= 0) return;
+  const uint32_t tm = __ldg(tile_mod + p / kUnitM);
+  if (tm == 0xFFFFFFFFu || (int)tm < m_lo) return;
+  uint4* out = reinterpret_cast<uint4*>(qg + p * d);
+  for (int64_t c = lane; c < d / 16; c += 32) out[c] = make_uint4(0, 0, 0, 0);
+  if (lane == 0) dg[p] = 0.f;
+}
+
+// A4 once for the fused layer call: token-order codes (forward) and, for non-text rows, their
+// modality-grouped copy (loss), in one pass over X; cudaErrorNotSupported when the TMA row
+// kernel does not apply (the caller then quantizes and gathers)
+cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                               int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
+                               uint32_t* status, const int32_t* perm, const uint32_t* tile_mod, const int32_t* ipos,
+                               int64_t Tg, int8_t* qg, float* dg, cudaStream_t st) {
+  static const bool v1 = getenv("MASQ_AQUANT_V1") != nullptr;
+  if (xt != MASQ_BF16 || v1 || T <= 0) return cudaErrorNotSupported;
+  if (mask) {
+    cudaError_t e = cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ceil_div(T, kTileM), st);
+    if (e != cudaSuccess) return e;
+  }
+  const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
+  cudaError_t e = aquant_bf16_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax,
+                                       qmin, qmax, qx, dx, mask, status, nullptr, T, st, qg, dg, ipos);
+  if (e != cudaSuccess) return e;
+  ProfScope ps_("pad_rows", st);
+  pad_rows_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(perm, tile_mod, Tg, d, 1, qg, dg);
+  return cudaGetLastError();
+}
+
 // grouped copy of token-order codes: row p of qg = row perm[p] of qt (zeros and dx 0 for padding)
 __global__ void __launch_bounds__(256) gather_rows_kernel(const int8_t* __restrict__ qt, const float* __restrict__ dt,
                                                           const int32_t* __restrict__ perm, int64_t Tg, int64_t d,
@@ -1225,12 +1273,12 @@ cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t*
 }
 
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
-                         int64_t* counts, cudaStream_t st) {
+                         int64_t* counts, cudaStream_t st, int32_t* ipos) {
   const int64_t Tg = grouped_rows(T, n_mod);
   cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
   if (e != cudaSuccess) return e;
   ProfScope ps_("route", st);
-  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM, counts);
+  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM, counts, ipos);
   return cudaGetLastError();
 }
 

@@ -39,7 +39,7 @@ struct WsLayout {
   // N3 decode
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
-  size_t qx_tok = 0, dx_tok = 0, fpart = 0;
+  size_t qx_tok = 0, dx_tok = 0, fpart = 0, ipos = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -71,6 +71,13 @@ cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_se
 // the call), then the f32 reciprocals of the scales used by the quantizer
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st);
 // qg[p] = qt[perm[p]] (rows of d bytes, d % 16 == 0), dg[p] = dt[perm[p]]; zeros for perm < 0
+// fused layer call: A4 once, writing the token-order codes and the grouped copy of the non-text
+// rows (ipos[t] = grouped row of token t from launch_route); zeroes the grouped padding rows of
+// modalities >= 1.  cudaErrorNotSupported when the TMA row kernel does not apply.
+cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                               int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
+                               uint32_t* status, const int32_t* perm, const uint32_t* tile_mod, const int32_t* ipos,
+                               int64_t Tg, int8_t* qg, float* dg, cudaStream_t st);
 cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t* perm, int64_t Tg, int64_t d, int8_t* qg,
                                float* dg, cudaStream_t st);
 // perm (optional): output row p quantizes input token perm[p] (-1: padding row, left untouched);
@@ -83,7 +90,7 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
 inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kUnitM) * kUnitM + (int64_t)n_mod * kUnitM; }
 // counts (optional): per-modality token counts [n_mod] (int64)
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
-                         int64_t* counts, cudaStream_t st);
+                         int64_t* counts, cudaStream_t st, int32_t* ipos = nullptr);
 // L2 [(M-1) x r x ld] -> L2t [(M-1)*n x 2*rpad] (the same L2^T for the Zhi and Zlo K-blocks)
 cudaError_t launch_pack_l2(const uint16_t* L2, int64_t ld_l2, int n_nt, int64_t n, int r, int rpad, uint16_t* L2t,
                            cudaStream_t st);
