@@ -70,6 +70,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.ipos = take(sizeof(int32_t) * T);
       if (rp > 0 && nnt > 0) {
         L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
+        L.zpart = take(zgemm_part_bytes(T, d, n_mod, (int)rp));
         L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
         L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
       }
@@ -98,6 +99,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.mask = take(sizeof(uint32_t) * tiles_m);
       if (rp > 0 && nnt > 0) {
         L.z = take(sizeof(uint16_t) * (size_t)T * nnt * 2 * rp);
+        L.zpart = take(zgemm_part_bytes(T, d, n_mod, (int)rp));
         L.l1t = take(sizeof(uint16_t) * 2 * (size_t)nnt * rp * d);
         L.l2t = take(sizeof(uint16_t) * (size_t)nnt * n * 2 * rp);
         if (f32_x) L.xsplit = take(sizeof(uint16_t) * 2 * (size_t)T * d);
@@ -341,12 +343,12 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
     MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), inv, d, r, rp, n_mod - 1, l1t, st));
     MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
     if (xt == MASQ_BF16) {
-      MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st));
+      MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     } else {
       uint16_t* xh = reinterpret_cast<uint16_t*>(W8(ws, L.xsplit));
       uint16_t* xl = xh + (size_t)T * d;
       MASQ_CK(launch_split_f32(static_cast<const float*>(X), ld_x, T, d, xh, xl, st));
-      MASQ_CK(launch_zgemm(xh, d, xl, mod_id, T, d, n_mod, l1t, rp, mask, z, st));
+      MASQ_CK(launch_zgemm(xh, d, xl, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     }
     g.rpad = rp;
     g.z = z;
@@ -463,7 +465,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
     MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), inv, d, r, rp, n_mod - 1, l1t, st));
     MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
-    MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st));
+    MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     g.rpad = rp;
     g.z = z;
     g.l2t = l2t;

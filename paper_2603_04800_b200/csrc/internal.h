@@ -39,7 +39,7 @@ struct WsLayout {
   // N3 decode
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
-  size_t qx_tok = 0, dx_tok = 0, fpart = 0, ipos = 0;
+  size_t qx_tok = 0, dx_tok = 0, fpart = 0, ipos = 0, zpart = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -247,6 +247,10 @@ cudaError_t launch_split_f32(const float* X, int64_t ld_x, int64_t T, int64_t d,
 // zeros for the other rows of tiles that contain modality m.  A0 (and A1 for f32 X) are bf16 planes.
 cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, const uint8_t* ids, int64_t T,
                          int64_t d, int n_mod, const uint16_t* L1s, int rpad, const uint32_t* tile_mask, uint16_t* Z,
-                         cudaStream_t st);
+                         cudaStream_t st, float* zpart = nullptr);
+// split-K of the CMC first factor for small T (too few 128-row tiles to fill the GPU): number of
+// K splits and the f32 partial workspace it needs (0 when not split)
+int zgemm_splits(int64_t T, int64_t d);
+size_t zgemm_part_bytes(int64_t T, int64_t d, int n_mod, int rpad);
 
 }  // namespace masq

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(ZT, 1)
 zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
              const __grid_constant__ CUtensorMap tmB, const uint8_t* __restrict__ ids, int T, int d, int n_mod,
              int rpad, int per, int a_planes, uint32_t tmem_cols, int stages,
-             const uint32_t* __restrict__ tile_mask, uint16_t* __restrict__ Z) {
+             const uint32_t* __restrict__ tile_mask, uint16_t* __restrict__ Z, float* __restrict__ zpart,
+             int splits) {
   const int mt = blockIdx.x;
   const int m0 = 1 + blockIdx.y * per;
   const int m1 = min(m0 + per, n_mod);           // exclusive
@@ -74,13 +75,18 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const int nk = (d + 63) / 64;
+  // split-K (small T): CTA z takes k-chunks [kc0, kc1) and writes an f32 partial; a combine kernel
+  // adds the partials in split order
+  const int nk_all = (d + 63) / 64;
+  const int kc0 = (int)((int64_t)nk_all * blockIdx.z / splits);
+  const int kc1 = (int)((int64_t)nk_all * (blockIdx.z + 1) / splits);
+  const int nk = kc1 - kc0;
   const int lo_row0 = (n_mod - 1) * rpad;        // lo plane starts after the hi plane
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t st = 0, ph = 0;
-      for (int kc = 0; kc < nk; ++kc) {
+      for (int kc = kc0; kc < kc1; ++kc) {
         mbar_wait(&empty[st], ph ^ 1u);
         mbar_expect_tx(&full[st], a_planes * XCH + 2 * BB);
         uint8_t* base = smem + st * SB;
@@ -128,8 +134,29 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
     tc_fence_after();
     const uint32_t taddr = tmem + ((q * 32u) << 16);
     const int zld = (n_mod - 1) * 2 * rpad;
+    const int nnt = n_mod - 1;
     for (int mm = m0; mm < m1; ++mm) {
       if (!((tmask >> mm) & 1u)) continue;                     // block never read by the GEMM
+      if (splits > 1) {                                        // raw f32 partial of this K range
+        float* zp = zpart + (((int64_t)blockIdx.z * gridDim.x * 128 + g) * nnt + (mm - 1)) * rpad;
+        for (int c = 0; c < rpad / 32; ++c) {
+          uint32_t v[32], w[32];
+          tmem_ld32(taddr + (mm - m0) * rpad + c * 32, v);
+          if (combined) tmem_ld32(taddr + N + (mm - m0) * rpad + c * 32, w);
+          tmem_wait_ld();
+          if (combined) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              v[e] = __float_as_uint(__fadd_rn(__uint_as_float(v[e]), __uint_as_float(w[e])));
+          }
+          if (g < T) {
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq)
+              *reinterpret_cast<uint4*>(zp + c * 32 + qq * 4) = make_uint4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
+          }
+        }
+        continue;
+      }
       const bool mine = mid == mm;
       uint16_t* zr = Z + (int64_t)g * zld + (int64_t)(mm - 1) * 2 * rpad;
       for (int c = 0; c < rpad / 32; ++c) {
@@ -212,7 +239,54 @@ __global__ void split_f32_kernel(const float* __restrict__ X, int64_t ld_x, int6
   hi[idx] = __bfloat16_as_ushort(h);
   lo[idx] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(v, __bfloat162float(h))));
 }
+// split-K combine: Z rows of the blocks the forward reads = hi/lo of sum_s zpart[s] (fixed order),
+// zeros for rows of other modalities; one warp per (row, non-text modality), lanes over columns
+__global__ void __launch_bounds__(256) zcombine_kernel(const float* __restrict__ zpart, int splits, int64_t T_pad,
+                                                       const uint8_t* __restrict__ ids, int64_t T, int n_mod,
+                                                       int rpad, const uint32_t* __restrict__ tile_mask,
+                                                       uint16_t* __restrict__ Z) {
+  const int nnt = n_mod - 1;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= T * nnt) return;
+  const int64_t g = w / nnt;
+  const int mm = (int)(w - g * nnt) + 1;
+  const int64_t n_tiles = (T + 127) / 128, mt = g >> 7;
+  const uint32_t tmask = tile_mask[mt] | ((mt ^ 1) < n_tiles ? tile_mask[mt ^ 1] : 0u);
+  if (!((tmask >> mm) & 1u)) return;
+  const bool mine = (int)__ldg(ids + g) == mm;
+  uint16_t* zr = Z + g * (int64_t)nnt * 2 * rpad + (int64_t)(mm - 1) * 2 * rpad;
+  for (int c = lane; c < rpad; c += 32) {
+    float v[16];                                  // splits <= 16: all loads in flight, then the ordered sum
+#pragma unroll
+    for (int sp = 0; sp < 16; ++sp)
+      v[sp] = sp < splits ? __ldg(zpart + ((sp * T_pad + g) * nnt + (mm - 1)) * rpad + c) : 0.f;
+    float z = 0.f;
+#pragma unroll
+    for (int sp = 0; sp < 16; ++sp)
+      if (sp < splits) z += v[sp];
+    if (!mine) z = 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(z);
+    zr[c] = __bfloat16_as_ushort(h);
+    zr[rpad + c] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(z, __bfloat162float(h))));
+  }
+}
 }  // namespace
+
+int zgemm_splits(int64_t T, int64_t d) {
+  const int64_t tiles = ceil_div(T, 128), nk = ceil_div(d, 64);
+  if (tiles <= 0 || tiles * 2 > num_sms()) return 1;     // enough tiles to fill the GPU
+  int64_t sp = num_sms() / tiles;
+  sp = std::min<int64_t>(sp, 16);
+  sp = std::min<int64_t>(sp, nk / 4);                    // >= 4 k-chunks per split
+  return (int)std::max<int64_t>(sp, 1);
+}
+
+size_t zgemm_part_bytes(int64_t T, int64_t d, int n_mod, int rpad) {
+  const int sp = zgemm_splits(T, d);
+  if (sp <= 1 || n_mod < 2 || rpad <= 0) return 0;
+  return sizeof(float) * (size_t)sp * ceil_div(T, 128) * 128 * (n_mod - 1) * rpad;
+}
 
 cudaError_t launch_l1_fold(const uint16_t* L1, const float* inv_s, int64_t d, int r, int rpad, int n_nt,
                            uint16_t* L1s, cudaStream_t st) {
@@ -236,7 +310,7 @@ cudaError_t launch_split_f32(const float* X, int64_t ld_x, int64_t T, int64_t d,
 
 cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, const uint8_t* ids, int64_t T,
                          int64_t d, int n_mod, const uint16_t* L1s, int rpad, const uint32_t* tile_mask, uint16_t* Z,
-                         cudaStream_t st) {
+                         cudaStream_t st, float* zpart) {
   if (T <= 0 || n_mod < 2 || rpad <= 0) return cudaSuccess;
   const int n_nt = n_mod - 1;
   // modalities per pass: 2 * per * rpad <= 256 MMA columns (the combined [hi; lo] form), else
@@ -261,10 +335,21 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   const int acc_cols = 2 * N <= 256 ? 2 * N : N;
   uint32_t cols = 32;
   while ((int)cols < acc_cols) cols <<= 1;
-  dim3 grid((unsigned)ceil_div(T, 128), (unsigned)passes);
-  ProfScope ps_("zgemm", st);
-  zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols, stages,
-                                       tile_mask, Z);
+  const int splits = zpart ? zgemm_splits(T, d) : 1;
+  dim3 grid((unsigned)ceil_div(T, 128), (unsigned)passes, (unsigned)splits);
+  {
+    ProfScope ps_("zgemm", st);
+    zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols, stages,
+                                         tile_mask, Z, zpart, splits);
+  }
+  if (splits > 1) {
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t warps = T * n_nt;
+    ProfScope ps_("zcombine", st);
+    zcombine_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(zpart, splits, ceil_div(T, 128) * 128, ids, T,
+                                                                       n_mod, rpad, tile_mask, Z);
+  }
   return cudaGetLastError();
 }
 
