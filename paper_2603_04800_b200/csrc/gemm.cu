@@ -635,7 +635,14 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.ids = g.ids;
   p.fwd_loss = g.fwd_loss;
   p.skip_m0 = g.skip_m0;
-  const int clusters = (int)std::min<int64_t>(p.n_units, num_sms() / 2);
+  // MASQ_GEMM_CLUSTERS (measurement knob): fewer persistent CTA pairs than SM pairs, leaving SMs
+  // to HBM-bound kernels of another stream
+  static const int env_cl = [] {
+    const char* e = getenv("MASQ_GEMM_CLUSTERS");
+    return e ? atoi(e) : 0;
+  }();
+  const int max_cl = env_cl > 0 ? std::min(env_cl, num_sms() / 2) : num_sms() / 2;
+  const int clusters = (int)std::min<int64_t>(p.n_units, max_cl);
   switch (g.mode) {
     case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, clusters, st);
     case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, clusters, st);
