@@ -22,6 +22,7 @@ value = tokens of all ranks / device time of K steps (CUDA events, max over rank
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import subprocess
@@ -330,6 +331,27 @@ def run_c4(args):
         pert.append([[torch.exp(0.01 * torch.randn(N_MOD, e["d"], generator=gp, device=dev)) for e in layers[0]]
                      for _ in range(2)])
     ws = M.Workspace(dev)
+    # linear li of a layer runs on stream li % S with its own workspace (the linears of a layer are
+    # independent between the exchanges; 2 streams let one linear's HBM-bound kernels run beside
+    # another's GEMM)
+    nstreams = max(1, args.streams)
+    main = torch.cuda.current_stream()
+    side = [torch.cuda.Stream(device=dev) for _ in range(nstreams)] if nstreams > 1 else []
+    wss = [ws] + [M.Workspace(dev) for _ in range(nstreams - 1)]
+
+    def on(li):
+        return torch.cuda.stream(side[li % nstreams]) if side else contextlib.nullcontext()
+
+    def fork():
+        if side:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            for st_ in side:
+                st_.wait_event(ev)
+
+    def join():
+        for st_ in side:
+            main.wait_stream(st_)
 
     optimise = args.workload == "c4s"
     grads = [torch.empty(N_MOD, e["d"], dtype=torch.float64, device=dev) for e in layers[0]]
@@ -341,38 +363,43 @@ def run_c4(args):
                 M.calibrate_stats(e["X"], ids, N_MOD, R=Rv[l * nl + li], count=Cbuf[l * nl + li], reset=True, ws=ws)
         P.reduce_stats([Rbuf], Cbuf)
         for l in range(args.layers):
-            svec = []
+            fork()
+            svec = [None] * nl
             for li, e in enumerate(layers[l]):
-                svec.append(M.init_factors(Rv[l * nl + li], Cbuf[l * nl + li], e["W"], ws=ws))
-                M.reference_output(e["X"], e["W"], Yref=Yref[li], ws=ws)
-            if optimise:
-                # N1: 2 epochs of loss + straight-through gradient + log-space Adam,
-                # the gradient normalised by the global counts and SUM-reduced (token-sharded)
-                for li in range(nl):
-                    adam[li] = M.adam_init(svec[li])
-                for p_ in range(2):
-                    for li, e in enumerate(layers[l]):
-                        M.calib_loss_grad(e["X"], ids, svec[li], e["W"], WBITS, ABITS, Yref[li], grad=grads[li],
-                                          sums=Sbuf[li], counts=Nbuf[li], loss=losses[l, p_, li:li + 1],
-                                          count_norm=Cbuf[l * nl + li], ws=ws)
-                    if world > 1:
-                        P.reduce_loss(Sbuf, Nbuf)
-                    for li, e in enumerate(layers[l]):
-                        if world > 1:
-                            P.reduce_grad(grads[li])
-                            M.loss_finalize(Sbuf[li], Nbuf[li], e["n"], loss=losses[l, p_, li:li + 1])
-                        th, m1, m2 = adam[li]
-                        M.adam_step(th, grads[li], m1, m2, p_ + 1, 1e-2, s_out=svec[li])
-                continue
+                with on(li):
+                    wk = wss[li % nstreams]
+                    svec[li] = M.init_factors(Rv[l * nl + li], Cbuf[l * nl + li], e["W"], ws=wk)
+                    M.reference_output(e["X"], e["W"], Yref=Yref[li], ws=wk)
+                    if optimise:
+                        adam[li] = M.adam_init(svec[li])
             for p_ in range(2):
                 for li, e in enumerate(layers[l]):
-                    sp = svec[li] * pert[l][p_][li]
-                    M.calib_loss(e["X"], ids, sp, e["W"], WBITS, ABITS, Yref[li], sums=Sbuf[li], counts=Nbuf[li],
-                                 loss=losses[l, p_, li:li + 1], ws=ws)
+                    with on(li):
+                        wk = wss[li % nstreams]
+                        if optimise:
+                            # N1: 2 epochs of loss + straight-through gradient + log-space
+                            # Adam, the gradient normalised by the global counts and SUM-reduced
+                            M.calib_loss_grad(e["X"], ids, svec[li], e["W"], WBITS, ABITS, Yref[li], grad=grads[li],
+                                              sums=Sbuf[li], counts=Nbuf[li], loss=losses[l, p_, li:li + 1],
+                                              count_norm=Cbuf[l * nl + li], ws=wk)
+                        else:
+                            sp = svec[li] * pert[l][p_][li]
+                            M.calib_loss(e["X"], ids, sp, e["W"], WBITS, ABITS, Yref[li], sums=Sbuf[li],
+                                         counts=Nbuf[li], loss=losses[l, p_, li:li + 1], ws=wk)
                 if world > 1:
+                    join()
                     P.reduce_loss(Sbuf, Nbuf)
                     for li, e in enumerate(layers[l]):
+                        if optimise:
+                            P.reduce_grad(grads[li])
                         M.loss_finalize(Sbuf[li], Nbuf[li], e["n"], loss=losses[l, p_, li:li + 1])
+                    fork()
+                if optimise:
+                    for li, e in enumerate(layers[l]):
+                        with on(li):
+                            th, m1, m2 = adam[li]
+                            M.adam_step(th, grads[li], m1, m2, p_ + 1, 1e-2, s_out=svec[li])
+            join()
 
     for _ in range(max(args.warmup, 1)):
         sweep()
