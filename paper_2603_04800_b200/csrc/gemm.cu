@@ -32,7 +32,7 @@
 //                                  tcgen05.ld 32x32b -> dequant -> swizzled smem -> TMA store)
 // TMEM holds two 256-column accumulators (512 columns) so the epilogue of unit i overlaps the
 // main loop of unit i+1.  The CMC k-blocks of unit i are inserted into the k-block stream of
-// unit i+1 (after kCmcDefer main k-blocks), by which time both epilogues have converted unit i's
+// unit i+1 (after min(20, 5/8 of its main k-blocks)), by which time both epilogues have converted unit i's
 // int32 accumulator to f32 in place; no extra TMEM columns and no Y round trip are needed.
 #include <cstdio>
 #include <cstdlib>
@@ -81,6 +81,7 @@ struct Params {
   const uint32_t* tile_mask;   // fwd: modality bit set per 128-row tile; loss: modality per 256-row unit
   const int32_t* perm;         // loss: grouped row -> token (-1 = padding)
   int rpad, cmc_kb;
+  int cmc_defer;                      // main k-blocks of unit i+1 issued before unit i's CMC k-blocks
   const float* yref;
   long long ld_ref;
   double* partials;            // loss: [n_units][2] (one per CTA of the pair)
@@ -211,7 +212,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (!decode_unit(p, u, w)) continue;
         const int brow = (kGrouped ? w.m * p.n : 0) + w.nt * BN + (int)rank * BNH;
         const int arow = w.mt * UM + (int)rank * BM;
-        const int defer_at = min(kCmcDefer, p.num_kb - 1);
+        const int defer_at = min(p.cmc_defer, p.num_kb - 1);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
           stage_arm();
@@ -267,7 +268,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         mbar_wait(&tempty[buf], ph ^ 1u);
         tc_fence_after();
         const uint32_t dtm = tmem_base + buf * BN;
-        const int defer_at = min(kCmcDefer, p.num_kb - 1);
+        const int defer_at = min(p.cmc_defer, p.num_kb - 1);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (pend && kb == defer_at) { issue_cmc(pu, pbuf, pph); pend = false; }
           mbar_wait(&full[ring.stage], ring.phase);
@@ -627,6 +628,18 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.perm = g.perm;
   p.rpad = cmc ? g.rpad : 0;
   p.cmc_kb = cmc ? (2 * g.rpad) / 64 : 0;
+  {
+    // MASQ_CMC_DEFER (measurement knob): k-blocks of the next unit before the CMC MMAs; -1 = half
+    static const int env_def = [] {
+      const char* e = getenv("MASQ_CMC_DEFER");
+      return e ? atoi(e) : -1000;
+    }();
+    // measured (tools/defer_sweep.sh, r = 64): at K = 3584 (28 int8 k-blocks) 16-20 beats 4 by
+    // 1.5-2% (the epilogue's dequant pass is done by then, so the MMA issuer does not wait on it)
+    // and 24+ loses (the second epilogue pass then delays the unit after next); deep K is flat
+    const int dflt = std::min(20, std::max(kCmcDefer, p.num_kb * 5 / 8));
+    p.cmc_defer = env_def == -1000 ? dflt : (env_def < 0 ? p.num_kb / 2 : env_def);
+  }
   p.yref = g.yref;
   p.ld_ref = g.ld_ref;
   p.partials = g.partials;
