@@ -98,14 +98,27 @@ struct Unit {
 };
 
 __device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
-  // grouped raster: p.group consecutive n-tiles swept over all m-units
-  const int per_group = p.group * p.num_m;
-  const int g = u / per_group;
-  const int rem = u - g * per_group;
-  const int nt0 = g * p.group;
-  const int gsz = min(p.group, p.num_n - nt0);
-  w.mt = rem / gsz;
-  w.nt = nt0 + (rem - w.mt * gsz);
+  if (p.group > 0) {
+    // grouped raster: p.group consecutive n-tiles swept over all m-units
+    const int per_group = p.group * p.num_m;
+    const int g = u / per_group;
+    const int rem = u - g * per_group;
+    const int nt0 = g * p.group;
+    const int gsz = min(p.group, p.num_n - nt0);
+    w.mt = rem / gsz;
+    w.nt = nt0 + (rem - w.mt * gsz);
+  } else {
+    // m-grouped raster (-p.group consecutive m-units swept over all n-tiles): the A panels of the
+    // group stay in L2 while B streams once per group
+    const int gm = -p.group;
+    const int per_group = gm * p.num_n;
+    const int g = u / per_group;
+    const int rem = u - g * per_group;
+    const int mt0 = g * gm;
+    const int gsz = min(gm, p.num_m - mt0);
+    w.nt = rem / gsz;
+    w.mt = mt0 + (rem - w.nt * gsz);
+  }
   w.m = 0;
   if (p.mode == kModeLoss || p.mode == kModeAlpha || p.mode == kModeAlphaI8) {
     w.mask = p.tile_mask[w.mt];
@@ -614,12 +627,12 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.n_units = p.num_m * p.num_n;
   p.n_tiles128 = (int)ceil_div(g.T, kTileM);
   {
-    static int env_group = -1;
-    if (env_group < 0) {
-      const char* e = getenv("MASQ_RASTER_GROUP");         // tuning knob (measurement only)
-      env_group = e ? atoi(e) : 0;
+    static int env_group = -1000;
+    if (env_group == -1000) {
+      const char* e = getenv("MASQ_RASTER_GROUP");         // tuning knob (measurement only;
+      env_group = e ? atoi(e) : 0;                          // < 0: m-grouped with -value m-units)
     }
-    p.group = env_group > 0 ? env_group : kRasterGroupDefault;
+    p.group = env_group != 0 ? env_group : kRasterGroupDefault;
   }
   p.n_mod = g.n_mod;
   p.dx = g.dx;
