@@ -59,7 +59,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.mask = take(sizeof(uint32_t) * tiles_m);
       L.qx = take((size_t)Tg * d);
       L.dx = take(sizeof(float) * Tg);
-      L.perm = take(sizeof(int32_t) * Tg);
+      L.perm = take(sizeof(int32_t) * (Tg + route_scratch_ints(T)));
       L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
       L.cnt = take(sizeof(int64_t) * n_mod);
       L.qw_all = take((size_t)n_mod * n * d);
@@ -110,7 +110,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.inv_s = take(sizeof(float) * n_mod * d);
       L.qx = take((size_t)Tg * d);
       L.dx = take(sizeof(float) * Tg);
-      L.perm = take(sizeof(int32_t) * Tg);
+      L.perm = take(sizeof(int32_t) * (Tg + route_scratch_ints(T)));
       L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
       L.cnt = take(sizeof(int64_t) * n_mod);
       L.qw_all = take((size_t)n_mod * n * d);
@@ -126,7 +126,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.inv_s = take(sizeof(float) * n_mod * d);
       L.qx = take((size_t)Tg * d);
       L.dx = take(sizeof(float) * Tg);
-      L.perm = take(sizeof(int32_t) * Tg);
+      L.perm = take(sizeof(int32_t) * (Tg + route_scratch_ints(T)));
       L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
       L.cnt = take(sizeof(int64_t) * n_mod);
       L.qw_all = take((size_t)n_mod * n * d);

@@ -921,6 +921,123 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
   }
 }
 
+// ---- multi-CTA routing (same stable counting sort as route_kernel): chunk b of kRouteChunk tokens
+// per CTA, 8 consecutive tokens per thread
+__device__ __forceinline__ void route_load8(const uint8_t* __restrict__ ids, int64_t T, int64_t t0, int (&m)[8]) {
+  if (t0 + 8 <= T && (reinterpret_cast<uintptr_t>(ids + t0) & 7) == 0) {
+    const uint2 v = *reinterpret_cast<const uint2*>(ids + t0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      m[k] = (v.x >> (8 * k)) & 0xFF;
+      m[4 + k] = (v.y >> (8 * k)) & 0xFF;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = t0 + k < T ? ids[t0 + k] : 0xFF;
+  }
+}
+
+__global__ void __launch_bounds__(256) route_count_kernel(const uint8_t* __restrict__ ids, int64_t T,
+                                                          int32_t* __restrict__ bcnt) {
+  __shared__ int s_w[8][kMaxMod];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int m8[8];
+  route_load8(ids, T, (int64_t)blockIdx.x * kRouteChunk + tid * 8, m8);
+#pragma unroll
+  for (int mm = 0; mm < kMaxMod; ++mm) {
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += (m8[k] == mm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) s_w[warp][mm] = c;
+  }
+  __syncthreads();
+  if (tid < kMaxMod) {
+    int c = 0;
+    for (int w = 0; w < 8; ++w) c += s_w[w][tid];
+    bcnt[(int64_t)blockIdx.x * kMaxMod + tid] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256) route_scatter_kernel(const uint8_t* __restrict__ ids, int64_t T, int n_mod,
+                                                            const int32_t* __restrict__ bcnt, int nb,
+                                                            int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
+                                                            int64_t n_tiles, int64_t* __restrict__ counts,
+                                                            int32_t* __restrict__ ipos) {
+  __shared__ int s_tot[kMaxMod], s_off[kMaxMod], s_seg[kMaxMod + 1];
+  __shared__ int s_w[8][kMaxMod];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  if (tid < kMaxMod) {                                  // totals and this chunk's offset, fixed order
+    int tot = 0, off = 0;
+    for (int bb = 0; bb < nb; ++bb) {
+      const int c = bcnt[(int64_t)bb * kMaxMod + tid];
+      tot += c;
+      if (bb < b) off += c;
+    }
+    s_tot[tid] = tot;
+    s_off[tid] = off;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int m = 0; m < n_mod; ++m) {
+      s_seg[m] = acc;
+      acc += (s_tot[m] + kUnitM - 1) / kUnitM * kUnitM;
+    }
+    s_seg[n_mod] = acc;
+  }
+  const int64_t t0 = (int64_t)b * kRouteChunk + tid * 8;
+  int m8[8];
+  route_load8(ids, T, t0, m8);
+  // exclusive prefix of this thread's per-modality counts within the chunk
+  int excl[kMaxMod];
+#pragma unroll
+  for (int mm = 0; mm < kMaxMod; ++mm) {
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += (m8[k] == mm);
+    int v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    excl[mm] = v - c;
+    if (lane == 31) s_w[warp][mm] = v;
+  }
+  __syncthreads();
+  int pos[kMaxMod];
+#pragma unroll
+  for (int mm = 0; mm < kMaxMod; ++mm) {
+    int wo = 0;
+    for (int w = 0; w < warp; ++w) wo += s_w[w][mm];
+    pos[mm] = (mm < n_mod ? s_seg[mm] + s_off[mm] : 0) + wo + excl[mm];
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int64_t t = t0 + k;
+    const int m = m8[k];
+#pragma unroll
+    for (int mm = 0; mm < kMaxMod; ++mm)
+      if (m == mm && mm < n_mod && t < T) {
+        if (ipos) ipos[t] = pos[mm];
+        perm[pos[mm]++] = (int32_t)t;
+      }
+  }
+  if (b == 0) {
+    if (tid < n_mod && counts) counts[tid] = s_tot[tid];
+    for (int64_t tile = tid; tile < n_tiles; tile += blockDim.x) {
+      const int64_t r = tile * kUnitM;
+      uint32_t v = 0xFFFFFFFFu;
+      for (int m = 0; m < n_mod; ++m)
+        if (r >= s_seg[m] && r < s_seg[m + 1] && s_tot[m] > 0) v = (uint32_t)m;
+      tile_mod[tile] = v;
+    }
+  }
+}
+
 // =============================================================== packing / transpose
 // out[c * ld_out + r] = in[r * ld_in + c]  (bf16), optional duplicate at out + dup_off
 __global__ void transpose_bf16_kernel(const uint16_t* __restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
@@ -1278,6 +1395,16 @@ cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm
   cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
   if (e != cudaSuccess) return e;
   ProfScope ps_("route", st);
+  if (!getenv("MASQ_ROUTE_V1")) {
+    // two passes over token chunks (per-chunk counts, then scan + scatter); the chunk counts live
+    // right after the Tg perm entries (route_scratch_ints)
+    int32_t* bcnt = perm + Tg;
+    const int64_t nb = route_blocks(T);
+    route_count_kernel<<<(unsigned)nb, 256, 0, st>>>(ids, T, bcnt);
+    route_scatter_kernel<<<(unsigned)nb, 256, 0, st>>>(ids, T, n_mod, bcnt, (int)nb, perm, tile_mod, Tg / kUnitM,
+                                                        counts, ipos);
+    return cudaGetLastError();
+  }
   route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM, counts, ipos);
   return cudaGetLastError();
 }

@@ -1,6 +1,7 @@
 // internal.h — host-side contracts between the C ABI (api.cu) and the kernel translation
 // units (elem.cu, gemm.cu, zgemm.cu).  Not part of the public ABI.
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <cuda.h>
@@ -88,6 +89,11 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
 // rows grouped by modality, each segment padded to a multiple of kUnitM (256) rows:
 // perm[Tg] (grouped row -> token, -1 padding), tile_mod[Tg/256] (modality of the unit, ~0u empty)
 inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kUnitM) * kUnitM + (int64_t)n_mod * kUnitM; }
+// routing scratch: per-chunk modality counts stored after the Tg perm entries (callers size perm
+// as grouped_rows(T, n_mod) + route_scratch_ints(T))
+constexpr int kRouteChunk = 2048;
+inline int64_t route_blocks(int64_t T) { return std::max<int64_t>(1, ceil_div(T, kRouteChunk)); }
+inline int64_t route_scratch_ints(int64_t T) { return route_blocks(T) * kMaxMod; }
 // counts (optional): per-modality token counts [n_mod] (int64)
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
                          int64_t* counts, cudaStream_t st, int32_t* ipos = nullptr);
