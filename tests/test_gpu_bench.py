@@ -51,3 +51,22 @@ def test_bench_c4s_two_rank_code_path():
     assert r.returncode == 0, r.stderr[-2000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0 and len(d["losses_layer0"]) == 4
+
+
+def test_bench_c5_column_shards():
+    """BASELINE configs[4]'s column-sharded forward: N = 1 line, then two ranks (functional) whose
+    shards cover the output columns."""
+    r = subprocess.run([sys.executable, "bench.py", "--workload", "c5", "--tokens", "4096", "--steps", "2",
+                        "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 1 and d["scaling"] == "strong" and d["unit"] == "TOP/s" and d["value"] > 0
+    assert d["roofline"]["bound"] == "tensor" and "gemm_fwd" in d["kernels"]
+    env = dict(os.environ, MASQ_BENCH_FUNCTIONAL="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29535", "bench.py", "--gpus", "2",
+                        "--workload", "c5", "--tokens", "4096", "--steps", "1", "--warmup", "1"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "column-shard x2"
