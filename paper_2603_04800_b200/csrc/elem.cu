@@ -16,6 +16,9 @@ namespace masq {
 namespace {
 
 constexpr float kFloor = 1e-12f;
+#ifndef MASQ_WCOLMAX_U
+#define MASQ_WCOLMAX_U 8                    // rows in flight per thread in wcolmax_kernel
+#endif
 #ifndef MASQ_STATS_U
 #define MASQ_STATS_U 8                      // rows in flight per thread (measured: 4 -> 8 is +8-10%, 12 is slower)
 #endif
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
                                                       int64_t d, int64_t n, int rows_per_strip,
                                                       uint32_t* __restrict__ amax) {
   constexpr int V = Vec<WT>::N;
-  constexpr int U = 8;
+  constexpr int U = MASQ_WCOLMAX_U;
   __shared__ float ss[NS][256];                       // factors of the current 256-row sub-strip
   const int64_t i0 = (int64_t)blockIdx.y * rows_per_strip;
   const int64_t i1 = min(d, i0 + rows_per_strip);

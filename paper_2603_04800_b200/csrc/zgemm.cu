@@ -275,6 +275,11 @@ __global__ void __launch_bounds__(256) zcombine_kernel(const float* __restrict__
 
 int zgemm_splits(int64_t T, int64_t d) {
   const int64_t tiles = ceil_div(T, 128), nk = ceil_div(d, 64);
+  static const int env_sp = [] {                         // measurement knob: forced split count
+    const char* e = getenv("MASQ_ZGEMM_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_sp > 0) return (int)std::max<int64_t>(1, std::min<int64_t>(env_sp, nk / 4));
   if (tiles <= 0 || tiles * 2 > num_sms()) return 1;     // enough tiles to fill the GPU
   int64_t sp = num_sms() / tiles;
   sp = std::min<int64_t>(sp, 16);
@@ -328,6 +333,11 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   const int SB = ((a_planes * XCH + 2 * N * 128) + 1023) & ~1023;
   int stages = (SMEM_CAP - 2048) / SB;
   stages = stages > 8 ? 8 : stages;
+  static const int env_st = [] {                         // measurement knob: ring stages
+    const char* e = getenv("MASQ_ZGEMM_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_st > 0) stages = std::min(stages, env_st);
   if (stages < 2) return cudaErrorInvalidValue;
   const int smem = stages * SB + 2048;
   cudaError_t e = cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
