@@ -69,3 +69,42 @@ def test_aquant_ties_round_half_away(abits):
     # and the oracle itself rounds those ties away from zero
     v = halves[:, 2:].astype(np.float64)
     assert np.array_equal(qxo[:, 2:].astype(np.float64), np.sign(v) * np.floor(np.abs(v) + 0.5))
+
+
+def test_aquant_edge_rows():
+    """All-zero rows (Delta floored at 1e-12, codes 0), a single token, the smallest width (d = 16),
+    a strided X view (ld_x > d) and an id >= n_mod (zero codes, Delta 0, sticky BAD_MODALITY)."""
+    import paper_2603_04800_b200 as m
+    g = np.random.Generator(np.random.PCG64(11))
+    for d in (16, 3584):
+        T = 37
+        ids = g.integers(0, 2, T).astype(np.uint8)
+        X = synth.activations(ids, d, 2, 5)
+        X[3] = 0                                            # bf16 +0 row
+        s = (g.random((2, d)) + 0.5).astype(np.float32)
+        qx, dx, _ = m.quantize_activations(bf(X), tt(ids), tt(s), 8)
+        m.check()
+        qxo, dxo = O.quantize_activations(X, ids, s, 8)
+        assert dxo[3] == np.float32(1e-12) and not qxo[3].any()
+        assert np.array_equal(dx.cpu().numpy(), dxo) and np.array_equal(qx.cpu().numpy(), qxo)
+        # single token
+        qx1, dx1, _ = m.quantize_activations(bf(X[5:6]), tt(ids[5:6]), tt(s), 8)
+        assert np.array_equal(qx1.cpu().numpy(), qxo[5:6]) and np.array_equal(dx1.cpu().numpy(), dxo[5:6])
+        # strided rows: a column window of a wider activation matrix
+        Xw = np.zeros((T, d + 64), np.uint16)
+        Xw[:, 32:32 + d] = X
+        Xv = bf(Xw)[:, 32:32 + d]
+        assert Xv.stride(0) == d + 64
+        qx2, dx2, _ = m.quantize_activations(Xv, tt(ids), tt(s), 8)
+        assert np.array_equal(qx2.cpu().numpy(), qxo) and np.array_equal(dx2.cpu().numpy(), dxo)
+    # bad modality id: zero codes, Delta 0, sticky status 6
+    bad = ids.copy()
+    bad[9] = 7
+    qx3, dx3, _ = m.quantize_activations(bf(X), tt(bad), tt(s), 8)
+    with pytest.raises(m.MasqError) as e:
+        m.check()
+    assert e.value.status == 6
+    m.check()
+    assert not qx3.cpu().numpy()[9].any() and float(dx3[9]) == 0.0
+    keep = np.arange(T) != 9
+    assert np.array_equal(qx3.cpu().numpy()[keep], qxo[keep])
