@@ -526,9 +526,13 @@ cudaError_t launch_bucket(const int32_t* keys, const double* vals, int64_t nkeys
   ProfScope ps_("bucket", st);
   cudaError_t e = cudaMemsetAsync(contrib, 0, sizeof(double) * nl, st);
   if (e != cudaSuccess) return e;
+  // sort on the low B bits only, 2^B - 1 >= nl: valid keys (< nl) keep their order and the
+  // invalid ones (-1, low bits all ones >= nl) still sort after them (radix sort is stable)
+  int bits = 1;
+  while (bits < 32 && ((1LL << bits) - 1) < nl) ++bits;
   size_t tb = temp_bytes;
   e = cub::DeviceRadixSort::SortPairs(temp, tb, reinterpret_cast<const uint32_t*>(keys), skeys, vals, svals,
-                                      (int)nkeys, 0, 32, st);
+                                      (int)nkeys, 0, bits, st);
   if (e != cudaSuccess) return e;
   runsum_kernel<<<(unsigned)ceil_div(nkeys, 256), 256, 0, st>>>(skeys, svals, nkeys, nl, contrib);
   return cudaGetLastError();
