@@ -403,13 +403,8 @@ cudaError_t launch_decode(const int8_t* qa, const float* dx, int T, int64_t d, i
     ProfScope ps_("decode_w4a8", st);
 #define DEC(S, K, RD)                                                                                         \
   {                                                                                                           \
-    static bool attr = false;                                                                                 \
-    if (!attr) {                                                                                              \
-      err = cudaFuncSetAttribute(decode_kernel<S, K, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                 DecCfg<S, K, RD>::kSmem);                                                    \
-      if (err != cudaSuccess) return err;                                                                     \
-      attr = true;                                                                                            \
-    }                                                                                                         \
+    err = set_max_dyn_smem(reinterpret_cast<const void*>(decode_kernel<S, K, RD>), DecCfg<S, K, RD>::kSmem);    \
+    if (err != cudaSuccess) return err;                                                                       \
     decode_kernel<S, K, RD><<<grid, kDecThreads, DecCfg<S, K, RD>::kSmem, st>>>(qa, dx, T, d, n, packed,      \
                                                                               scales, part, Y, ldy);         \
   }

@@ -1253,7 +1253,6 @@ static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, cons
   // register-limited CTAs per SM for this block size (queried once per instantiation and size;
   // the launch configuration is a pure function of (CPL, nthr, d))
   static thread_local int cached_nthr = -1, cached_occ = 0;
-  static thread_local bool attr_set = false;
   if (cached_nthr != nthr) {
     int occ = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, 0);
@@ -1261,10 +1260,9 @@ static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, cons
     cached_nthr = nthr;
     cached_occ = occ;
   }
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingPerSm);
+  {
+    cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(kern), (int)kRingPerSm);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   int per_sm = std::max(1, std::min(cached_occ, 16));
   int S = 0;

@@ -35,6 +35,8 @@
 // unit i+1 (after min(20, 5/8 of its main k-blocks)), by which time both epilogues have converted unit i's
 // int32 accumulator to f32 in place; no extra TMEM columns and no Y round trip are needed.
 #include <cstdio>
+#include <mutex>
+#include <vector>
 #include <cstdlib>
 
 #include "internal.h"
@@ -556,12 +558,9 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 template <int MODE>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
                         const CUtensorMap& l2, const Params& p, int clusters, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(masq_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_ALLOC);
+  {
+    cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(masq_gemm_kernel<MODE>), SMEM_ALLOC);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   static const char* const kNames[6] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha",
                                         "gemm_alpha_i8"};
@@ -572,6 +571,24 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
 }  // namespace
 
 int gemm_epilogue_warps() { return 2; }   // loss partial slots per unit (one per CTA of the pair)
+
+cudaError_t set_max_dyn_smem(const void* func, int bytes) {
+  struct Entry {
+    const void* f;
+    int dev, bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& x : done)
+    if (x.f == func && x.dev == dev && x.bytes >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({func, dev, bytes});
+  return e;
+}
 
 int num_sms() {
   static int n = 0;

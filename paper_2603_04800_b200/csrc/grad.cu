@@ -547,11 +547,9 @@ cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* 
   ok &= make_tmap_2d(&tb, gsign, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Tg, n, n, 64, 64, true);
   ok &= make_tmap_2d(&tq, qw_all, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)n_mod * n, d, d, GN, GM, false);
   if (!ok) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gradgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_ALLOC);
+  {
+    cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(gradgemm_kernel), G_ALLOC);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   GParams p{};
   p.d = (int)d;

@@ -45,6 +45,10 @@ struct WsLayout {
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size): the attribute
+// is per device, so one host thread driving several GPUs must set it on each (gemm.cu)
+cudaError_t set_max_dyn_smem(const void* func, int bytes);
+
 // ---------------------------------------------------------------- opt-in kernel timing (prof.cu)
 // RAII: records a cudaEvent pair around a kernel launch when masq_profile_enable(1) is active.
 class ProfScope {

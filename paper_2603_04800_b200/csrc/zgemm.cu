@@ -340,7 +340,7 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   if (env_st > 0) stages = std::min(stages, env_st);
   if (stages < 2) return cudaErrorInvalidValue;
   const int smem = stages * SB + 2048;
-  cudaError_t e = cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(zgemm_kernel), smem);
   if (e != cudaSuccess) return e;
   const int acc_cols = 2 * N <= 256 ? 2 * N : N;
   uint32_t cols = 32;
