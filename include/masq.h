@@ -366,7 +366,9 @@ const char* masq_status_string(masq_status s);
  * around every kernel the library launches (and discards earlier records); it returns the
  * previous state.  masq_profile_collect() waits for the recorded events and aggregates them
  * by kernel name: names[i*32 .. i*32+31] (NUL-terminated), total_ms[i], launches[i] for
- * i < return value (at most max_entries); it clears the records.  Returns -1 on a CUDA error.
+ * i < return value (at most max_entries); it clears the records.  A name may cover a short
+ * sequence of library kernels (routing: the count and scatter passes); launches[i] counts them
+ * all, total_ms[i] is the bracketed time.  Returns -1 on a CUDA error.
  */
 int32_t masq_profile_enable(int32_t on);
 int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms, int64_t* launches);

@@ -1401,8 +1401,9 @@ cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm
   const int64_t Tg = grouped_rows(T, n_mod);
   cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
   if (e != cudaSuccess) return e;
-  ProfScope ps_("route", st);
-  if (!getenv("MASQ_ROUTE_V1")) {
+  const bool v1 = getenv("MASQ_ROUTE_V1") != nullptr;
+  ProfScope ps_("route", st, v1 ? 1 : 2);
+  if (!v1) {
     // two passes over token chunks (per-chunk counts, then scan + scatter); the chunk counts live
     // right after the Tg perm entries (route_scratch_ints)
     int32_t* bcnt = perm + Tg;

@@ -505,7 +505,7 @@ cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_
 cudaError_t launch_gradkeys(const float* bpart, int nb, const int32_t* kj, const uint32_t* colmax, int wbits,
                             const float* apart, int na, const int32_t* ktkey, int n_mod, int64_t d, int64_t n,
                             int64_t Tg, int32_t* keys, double* vals, cudaStream_t st) {
-  ProfScope ps_("gradkeys", st);
+  ProfScope ps_("gradkeys", st, 2);
   betakeys_kernel<<<(unsigned)((int64_t)n_mod * n / 32), 256, 0, st>>>(bpart, nb, kj, colmax,
                                                                       (float)((1 << (wbits - 1)) - 1), d, n, keys,
                                                                       vals);

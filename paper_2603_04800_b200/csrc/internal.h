@@ -53,7 +53,8 @@ cudaError_t set_max_dyn_smem(const void* func, int bytes);
 // RAII: records a cudaEvent pair around a kernel launch when masq_profile_enable(1) is active.
 class ProfScope {
  public:
-  ProfScope(const char* name, cudaStream_t st);
+  // launches: library kernels the scope brackets (counted into masq_profile_collect's launches)
+  ProfScope(const char* name, cudaStream_t st, int launches = 1);
   ~ProfScope();
   ProfScope(const ProfScope&) = delete;
   ProfScope& operator=(const ProfScope&) = delete;
@@ -62,6 +63,7 @@ class ProfScope {
   const char* name_;
   cudaStream_t st_;
   void* a_ = nullptr;
+  int launches_ = 1;
 };
 
 // ---------------------------------------------------------------- elementwise kernels (elem.cu)

@@ -17,6 +17,7 @@ namespace {
 struct Rec {
   const char* name;
   cudaEvent_t a, b;
+  int launches;
 };
 std::mutex g_mu;
 bool g_on = false;
@@ -46,7 +47,7 @@ void record(cudaEvent_t e, cudaStream_t st) {
 }
 }  // namespace
 
-ProfScope::ProfScope(const char* name, cudaStream_t st) : name_(name), st_(st) {
+ProfScope::ProfScope(const char* name, cudaStream_t st, int launches) : name_(name), st_(st), launches_(launches) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_on) return;
   a_ = get_event();
@@ -59,7 +60,7 @@ ProfScope::~ProfScope() {
   cudaEvent_t b = get_event();
   if (!b) return;
   record(b, st_);
-  g_recs.push_back(Rec{name_, static_cast<cudaEvent_t>(a_), b});
+  g_recs.push_back(Rec{name_, static_cast<cudaEvent_t>(a_), b, launches_});
 }
 
 }  // namespace masq
@@ -101,7 +102,7 @@ int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms,
     while (k < keys.size() && keys[k] != r.name) ++k;
     if (k == keys.size()) { keys.emplace_back(r.name); ms.push_back(0.0); cnt.push_back(0); }
     ms[k] += t;
-    cnt[k] += 1;
+    cnt[k] += r.launches;
     g_pool.push_back(r.a);
     g_pool.push_back(r.b);
   }
