@@ -103,6 +103,10 @@ def make_host_inputs(T, rank, linears, r):
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and clock-event reasons during the timed region.  nvidia-smi -lms 100 runs as the
+    profiling recipe's clocks line; an NVML thread samples every 5 ms so the short timed regions
+    get enough samples.  mark() brackets the timed region; the summary uses the NVML samples
+    inside it (else every sample)."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -111,6 +115,24 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.nv = []                      # (t, sm_mhz, reasons bitmask)
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.handle = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(gpu_index)
+            try:
+                bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.nvml = pynvml
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.handle = None
 
     def start(self):
         try:
@@ -121,21 +143,58 @@ class ClockSampler:
             self.th.start()
         except Exception:
             self.proc = None
+        if self.handle is not None:
+            self.nth = threading.Thread(target=self._nvml, daemon=True)
+            self.nth.start()
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def _nvml(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle))
+                self.nv.append((time.time(), mhz, rs))
+            except Exception:
+                return
+            time.sleep(0.005)
+
+    def mark(self, begin: bool):
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def stop(self):
+        self._stop.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nv:
+            nv = self.nvml
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            sel = [x for x in self.nv if self.t0 is not None and self.t1 is not None and self.t0 <= x[0] <= self.t1]
+            inside = bool(sel)
+            sel = sel or self.nv
+            sm = [x[1] for x in sel]
+            reasons = sorted(nm for nm, b in bits.items() if any(x[2] & b for x in sel))
+            return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(sm), "source": "NVML every 5 ms" +
+                    (" inside the timed region" if inside else " (whole run)"),
+                    "nvidia_smi_samples": len(self.lines)}
         if self.proc is None:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
@@ -150,7 +209,8 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi -lms 100"}
 
 
 # --------------------------------------------------------------------------- oracle arm
@@ -415,11 +475,15 @@ def run_c4(args):
         time.sleep(0.3)
     lib().masq_profile_enable(1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.mark(True)
     a.record()
     for _ in range(args.steps):
         sweep()
     b.record()
     torch.cuda.synchronize()
+    if clk:
+        clk.mark(False)
     if world > 1:
         dist.barrier()
     clocks = clk.stop() if clk else None
@@ -512,11 +576,15 @@ def run_c5(args):
         time.sleep(0.3)
     lib().masq_profile_enable(1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.mark(True)
     a.record()
     for _ in range(args.steps):
         fwd()
     b.record()
     torch.cuda.synchronize()
+    if clk:
+        clk.mark(False)
     if world > 1:
         dist.barrier()
     clocks = clk.stop() if clk else None
@@ -695,6 +763,8 @@ def main():
         lib().masq_profile_enable(1)
     prof_steps = 1 if use_graph else args.steps
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.mark(True)
     ev0.record()
     for _ in range(args.steps):
         if use_graph:
@@ -703,6 +773,8 @@ def main():
             step()
     ev1.record()
     torch.cuda.synchronize()
+    if clk:
+        clk.mark(False)
     barrier()
     clocks = clk.stop() if clk else None
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
