@@ -51,7 +51,17 @@ constexpr int UM = 2 * BM;                           // rows per cluster unit
 constexpr int BN = kTileN;                           // columns per unit (MMA N)
 constexpr int BNH = BN / 2;                          // B rows held by each CTA
 constexpr int BKB = 128;                             // k-block bytes (128 int8 / 64 bf16)
-constexpr int STAGES = 6;
+#ifndef MASQ_GEMM_STAGES
+#define MASQ_GEMM_STAGES 6
+#endif
+#ifndef MASQ_GEMM_NSTG
+#define MASQ_GEMM_NSTG 1
+#endif
+constexpr int STAGES = MASQ_GEMM_STAGES;
+// Y staging tiles per epilogue warp; measured (tools/ab_gemm.sh): 6 stages x 1 staging tile beats
+// 5 x 2 and 4 x 2 by 3-8% on the int8 GEMMs (ring depth matters more), and per-lane direct
+// global stores of Y (no staging, 7 stages) lose 25-30%
+constexpr int NSTG = MASQ_GEMM_NSTG;
 constexpr int A_BYTES = BM * BKB;
 constexpr int B_BYTES = BNH * BKB;
 constexpr int EPI_WARPS = 8;
@@ -60,7 +70,7 @@ constexpr int STG_BYTES = 32 * 32 * 4;               // one 32-row x 32-column f
 constexpr int SMEM_A = 0;
 constexpr int SMEM_B = SMEM_A + STAGES * A_BYTES;
 constexpr int SMEM_STG = SMEM_B + STAGES * B_BYTES;
-constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * STG_BYTES;
+constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * NSTG * STG_BYTES;
 constexpr int SMEM_USED = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr int kCmcDefer = 4;
@@ -322,10 +332,9 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t q = warp & 3u;                       // TMEM lane quarter this warp may access
     const uint32_t ew = warp - 2u;                      // 0..7
     const int c0 = (int)(ew >> 2) * 4;                  // this warp's 4 column chunks: c0 .. c0+3
-    uint8_t* sb = smS + ew * STG_BYTES;
-    const uint32_t sbase = smem_u32(sb) + lane * 128u;
+    uint8_t* const sb0 = smS + ew * NSTG * STG_BYTES;
+    uint32_t nst = 0;                                   // Y chunks this warp has staged so far
     uint32_t local = 0, cmc_cnt[2] = {0u, 0u};
-    bool stored = false;
     const uint64_t pol_y = policy_evict_first();          // Y is written once, never re-read here
     for (int u = cid; u < p.n_units; u += ncl) {
       Unit w;
@@ -384,8 +393,12 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
       };
       auto store_chunk = [&](const uint32_t (&v)[32], int c) {
-        if (stored) {                                   // staging tile free again?
-          if (lane == 0) bulk_wait_read<0>();
+        // NSTG staging tiles per warp, used round robin: before refilling one, the TMA store
+        // issued NSTG chunks ago (its last user) must have finished reading it
+        uint8_t* sb = sb0 + (nst % NSTG) * STG_BYTES;
+        const uint32_t sbase = smem_u32(sb) + lane * 128u;
+        if (nst >= (uint32_t)NSTG) {
+          if (lane == 0) bulk_wait_read<NSTG - 1>();
           __syncwarp();
         }
 #pragma unroll
@@ -401,7 +414,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           tma_store_2d_hint(&tmY, sb, col_base + (c0 + c) * 32, row0, pol_y);
           bulk_commit();
         }
-        stored = true;
+        ++nst;
       };
 
       if (MODE == kModeFwd && unit_has_cmc(p, w)) {
