@@ -385,39 +385,15 @@ __global__ void wscale_kernel(const uint32_t* __restrict__ amax, float* __restri
 // pass 2: one 128 (i) x JT (j) tile of W read once (JT = 8 * CPT: 256-byte bf16 row segments
 // for CPT = 16, which keeps the DRAM access pattern page-friendly); for every set k the codes
 // are packed 4 rows per 32-bit word into a smem tile [JT j][128 i] and written K-major.
-template <typename WT, int NS, int CPT>
-#ifndef MASQ_WQ_MINB
-#define MASQ_WQ_MINB 3                      // 3 CTAs per SM (80 registers, a few spills): measured -9% on the 2-set weight quantization
-#endif
-__global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __restrict__ W, const float* __restrict__ s,
-                                                     int64_t d, int64_t n, int qmin, int qmax,
-                                                     const float* __restrict__ rcp, int8_t* __restrict__ qw,
-                                                     const float* __restrict__ dw) {
-  constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
-  constexpr int LPT = CPT / V;                  // loads per row per thread
-  constexpr int JT = 8 * CPT;                   // tile columns
-  __shared__ __align__(16) uint32_t tile[JT][33];   // [j][i/4] packed codes (+1 word pad)
-  const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * JT;
-  const int tx = threadIdx.x & 7;               // column group: j = j0 + 8*tx + e
-  const int ty = threadIdx.x >> 3;              // rows 4*ty .. 4*ty+3 of the tile
-  const int64_t jb = j0 + tx * CPT;
-  const bool colok = jb < n;                    // n % 32 == 0 -> whole CPT-column groups
-  float f[4][CPT];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int64_t i = i0 + 4 * ty + r;
-#pragma unroll
-    for (int l = 0; l < LPT; ++l) {
-      float g[V];
-      if (colok && i < d) Vec<WT>::load(W + i * n + jb + l * V, g);
-      else {
-#pragma unroll
-        for (int e = 0; e < V; ++e) g[e] = 0.f;
-      }
-#pragma unroll
-      for (int e = 0; e < V; ++e) f[r][l * V + e] = g[e];
-    }
-  }
+// the NS factor sets of one 128 (i) x JT (j) tile held as f[4][CPT] (rows 4ty..4ty+3, columns
+// jb..jb+CPT-1 of this thread): codes -> smem transpose -> K-major 16-byte stores
+template <int NS, int CPT>
+__device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64_t i0, int64_t j0, int tx, int ty,
+                                                 int64_t jb, bool colok, const float* __restrict__ s, int64_t d,
+                                                 int64_t n, int qmin, int qmax, const float* __restrict__ rcp,
+                                                 int8_t* __restrict__ qw, const float* __restrict__ dw,
+                                                 uint32_t (*tile)[33]) {
+  constexpr int JT = 8 * CPT;
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
     float si[4];
@@ -475,6 +451,116 @@ __global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __r
       }
     }
     __syncthreads();
+  }
+}
+
+#ifndef MASQ_WQ_MINB
+#define MASQ_WQ_MINB 3                      // 3 CTAs per SM (80 registers, a few spills): measured -9% on the 2-set weight quantization
+#endif
+template <typename WT, int NS, int CPT>
+__global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __restrict__ W, const float* __restrict__ s,
+                                                     int64_t d, int64_t n, int qmin, int qmax,
+                                                     const float* __restrict__ rcp, int8_t* __restrict__ qw,
+                                                     const float* __restrict__ dw) {
+  constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
+  constexpr int LPT = CPT / V;                  // loads per row per thread
+  constexpr int JT = 8 * CPT;                   // tile columns
+  __shared__ __align__(16) uint32_t tile[JT][33];   // [j][i/4] packed codes (+1 word pad)
+  const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * JT;
+  const int tx = threadIdx.x & 7;               // column group: j = j0 + 8*tx + e
+  const int ty = threadIdx.x >> 3;              // rows 4*ty .. 4*ty+3 of the tile
+  const int64_t jb = j0 + tx * CPT;
+  const bool colok = jb < n;                    // n % 32 == 0 -> whole CPT-column groups
+  float f[4][CPT];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t i = i0 + 4 * ty + r;
+#pragma unroll
+    for (int l = 0; l < LPT; ++l) {
+      float g[V];
+      if (colok && i < d) Vec<WT>::load(W + i * n + jb + l * V, g);
+      else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) g[e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) f[r][l * V + e] = g[e];
+    }
+  }
+  wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile);
+}
+
+// TMA-fed persistent variant (bf16 W): 128 x 128 tiles of W stream through a shared-memory ring
+// of kWqStages 32 KB stages by 2D TMA (no swizzle: row-major [128 i][128 j]), the next tiles in
+// flight while the current one is quantized; the same per-set code path as wquant_kernel.
+#ifndef MASQ_WQ_STAGES
+#define MASQ_WQ_STAGES 2
+#endif
+constexpr int kWqStages = MASQ_WQ_STAGES;
+constexpr int kWqTileBytes = 128 * 128 * 2;
+constexpr int kWqSmem = kWqStages * kWqTileBytes + 128 * 33 * 4 + 64;
+template <int NS>
+__global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                            const float* __restrict__ s, int64_t d, int64_t n,
+                                                            int qmin, int qmax, const float* __restrict__ rcp,
+                                                            int8_t* __restrict__ qw, const float* __restrict__ dw,
+                                                            int64_t tiles_j, int64_t ntiles) {
+  constexpr int CPT = 16;
+  extern __shared__ __align__(128) uint8_t wsm[];
+  uint8_t* ring = wsm;
+  uint32_t (*tile)[33] = reinterpret_cast<uint32_t(*)[33]>(wsm + kWqStages * kWqTileBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + kWqStages * kWqTileBytes + 128 * 33 * 4);
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  auto issue = [&](int64_t t, int st) {                // thread 0: tile t -> stage st
+    const int64_t jt = t % tiles_j, it = t / tiles_j;
+    sm100::mbar_expect_tx(&full[st], kWqTileBytes);
+    sm100::tma_load_2d(ring + st * kWqTileBytes, &tmW, &full[st], (int32_t)(jt * 128), (int32_t)(it * 128));
+  };
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch(&tmW);
+    for (int st = 0; st < kWqStages; ++st) sm100::mbar_init(&full[st], 1);
+    sm100::fence_mbar_init();
+    for (int st = 0; st < kWqStages; ++st) {
+      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
+      if (t < ntiles) issue(t, st);
+    }
+  }
+  __syncthreads();
+  int st = 0;
+  uint32_t ph = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t jt = t % tiles_j, it = t / tiles_j;
+    const int64_t i0 = it * 128, j0 = jt * 128;
+    const int64_t jb = j0 + tx * CPT;
+    const bool colok = jb < n;
+    sm100::mbar_wait(&full[st], ph);
+    float f[4][CPT];
+    const uint8_t* src = ring + st * kWqTileBytes;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint4* row = reinterpret_cast<const uint4*>(src + (4 * ty + r) * 256 + tx * 32);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 v = row[h];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          f[r][8 * h + 2 * q] = __uint_as_float(w[q] << 16);
+          f[r][8 * h + 2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+        }
+      }
+    }
+    // generic-proxy reads of the stage must be ordered before the TMA (async proxy) that refills
+    // it: without this fence the refill raced the still-pending reads (seen as a few corrupted
+    // codes in second-round tiles)
+    sm100::fence_proxy_async_smem();
+    __syncthreads();                                     // every thread has the stage in registers
+    if (threadIdx.x == 0) {
+      const int64_t tn = t + (int64_t)kWqStages * gridDim.x;
+      if (tn < ntiles) issue(tn, st);
+    }
+    if (++st == kWqStages) { st = 0; ph ^= 1u; }
+    wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile);
   }
 }
 
@@ -709,6 +795,7 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
     if (nw > 1) {
       if (lane == 0) s_red[par][warp] = ab;
     }
+    sm100::fence_proxy_async_smem();                     // stage reads before the TMA refill (WAR)
     __syncthreads();                                     // every thread is done with the stage
     if (tid == 0 && row + S < r1) {                      // refill it with row + S
       const int64_t nrow = row + S;
@@ -1168,7 +1255,24 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 8 * CPT), (unsigned)ceil_div(d, 128));
   { ProfScope ps_("wcolmax", st); wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
   { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, rcp, NS * n, (float)qmax); }
-  { ProfScope ps_("wquant", st); wquant_kernel<WT, NS, CPT><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, rcp, qw, dw); }
+  {
+    ProfScope ps_("wquant", st);
+    static const bool v1 = getenv("MASQ_WQUANT_V1") != nullptr;    // measurement switch
+    bool done = false;
+    if constexpr (sizeof(WT) == 2) {
+      CUtensorMap tm;
+      const int64_t tj = ceil_div(n, 128), ti = ceil_div(d, 128);
+      if (!v1 && make_tmap_2d(&tm, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, n, n, 128, 128, false)) {
+        cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(wquant_tma_kernel<NS>), kWqSmem);
+        if (e != cudaSuccess) return e;
+        const int64_t grid = std::min<int64_t>(tj * ti, (int64_t)num_sms() * 2);
+        wquant_tma_kernel<NS><<<(unsigned)grid, 256, kWqSmem, st>>>(tm, s, d, n, qmin, qmax, rcp, qw, dw, tj,
+                                                                     tj * ti);
+        done = true;
+      }
+    }
+    if (!done) wquant_kernel<WT, NS, CPT><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, rcp, qw, dw);
+  }
   return cudaGetLastError();
 }
 
