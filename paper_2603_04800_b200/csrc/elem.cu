@@ -564,6 +564,126 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
   }
 }
 
+// TMA-fed column maxima (bf16 W): unit = (128-column strip, run of RS 128-row tiles); each CTA walks
+// its units' tiles in order through the same 2-stage 2D-TMA ring as wquant_tma_kernel (prefetch
+// crosses unit boundaries); thread (tx, ty) keeps max_i |s_k[i] w_ij| of its 16 columns over its
+// 4 rows per tile in registers; at a unit's end: shuffle + smem reduce over ty, then atomicMax.
+template <int NS>
+__global__ void __launch_bounds__(256, 2) wcolmax_tma_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                             const float* __restrict__ s, int64_t d, int64_t n,
+                                                             int64_t tiles_j, int64_t tiles_i, int rs,
+                                                             int64_t units, uint32_t* __restrict__ amax) {
+  constexpr int CPT = 16;
+  extern __shared__ __align__(128) uint8_t wsm[];
+  uint8_t* ring = wsm;
+  float (*red)[NS * 128] = reinterpret_cast<float(*)[NS * 128]>(wsm + kWqStages * kWqTileBytes);   // [8 warps]
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + kWqStages * kWqTileBytes + 8 * NS * 128 * 4);
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t strips_i = (tiles_i + rs - 1) / rs;
+  // the CTA's tile sequence: units b, b + G, ...; unit u = (cs = u % tiles_j, strip = u / tiles_j)
+  auto tile_of = [&](int64_t u, int k, int64_t& it, int64_t& jt) {
+    jt = u % tiles_j;
+    it = (u / tiles_j) * rs + k;
+  };
+  auto unit_len = [&](int64_t u) -> int {
+    const int64_t it0 = (u / tiles_j) * rs;
+    return (int)((tiles_i - it0) < rs ? (tiles_i - it0) : rs);
+  };
+  (void)strips_i;
+  // producer cursor (thread 0)
+  int64_t pu = blockIdx.x;
+  int pk = 0;
+  auto next_issue = [&](int st) {
+    if (pu >= units) return;
+    int64_t it, jt;
+    tile_of(pu, pk, it, jt);
+    sm100::mbar_expect_tx(&full[st], kWqTileBytes);
+    sm100::tma_load_2d(ring + st * kWqTileBytes, &tmW, &full[st], (int32_t)(jt * 128), (int32_t)(it * 128));
+    if (++pk == unit_len(pu)) { pk = 0; pu += gridDim.x; }
+  };
+  if (threadIdx.x == 0) {
+    sm100::tma_prefetch(&tmW);
+    for (int st = 0; st < kWqStages; ++st) sm100::mbar_init(&full[st], 1);
+    sm100::fence_mbar_init();
+    for (int st = 0; st < kWqStages; ++st) next_issue(st);
+  }
+  __syncthreads();
+  int st = 0;
+  uint32_t ph = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int len = unit_len(u);
+    float m[NS][CPT];
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) m[k][e] = 0.f;
+    int64_t jt = 0;
+    for (int kt = 0; kt < len; ++kt) {
+      int64_t it;
+      tile_of(u, kt, it, jt);
+      sm100::mbar_wait(&full[st], ph);
+      const uint8_t* src = ring + st * kWqTileBytes;
+      uint4 raw[4][2];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          raw[r][h] = reinterpret_cast<const uint4*>(src + (4 * ty + r) * 256 + tx * 32)[h];
+      sm100::fence_proxy_async_smem();
+      __syncthreads();                                   // the stage is in registers: refill it
+      if (threadIdx.x == 0) next_issue(st);
+      if (++st == kWqStages) { st = 0; ph ^= 1u; }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        float si[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int64_t i = it * 128 + 4 * ty + r;
+          si[r] = i < d ? __ldg(s + (int64_t)k * d + i) : 0.f;
+        }
+#pragma unroll
+        for (int rp = 0; rp < 4; rp += 2) {
+          const uint64_t s0 = f2_pack(si[rp], si[rp]), s1 = f2_pack(si[rp + 1], si[rp + 1]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t w0[4] = {raw[rp][h].x, raw[rp][h].y, raw[rp][h].z, raw[rp][h].w};
+            const uint32_t w1[4] = {raw[rp + 1][h].x, raw[rp + 1][h].y, raw[rp + 1][h].z, raw[rp + 1][h].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float a0, a1, b0, b1;
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(w0[q] << 16), __uint_as_float(w0[q] & 0xFFFF0000u)), s0), a0, a1);
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(w1[q] << 16), __uint_as_float(w1[q] & 0xFFFF0000u)), s1), b0, b1);
+              const int e = 8 * h + 2 * q;
+              m[k][e] = fmax3(m[k][e], fabsf(a0), fabsf(b0));
+              m[k][e + 1] = fmax3(m[k][e + 1], fabsf(a1), fabsf(b1));
+            }
+          }
+        }
+      }
+    }
+    // reduce over ty: lanes tx + 8 * (ty % 4) within the warp, then the 8 warps through smem
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) {
+        float v = m[k][e];
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+        if (lane < 8) red[warp][k * 128 + tx * CPT + e] = v;
+      }
+    __syncthreads();
+    for (int c = threadIdx.x; c < NS * 128; c += 256) {
+      float v = red[0][c];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) v = fmaxf(v, red[w][c]);
+      const int k = c / 128;
+      const int64_t j = jt * 128 + (c - k * 128);
+      if (j < n && v > 0.f) atomicMax(amax + (int64_t)k * n + j, __float_as_uint(v));
+    }
+    __syncthreads();
+  }
+}
+
 // =============================================================== A4 activation quantization
 __global__ void inv_kernel(const float* __restrict__ s, int64_t count, float* __restrict__ inv) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1253,7 +1373,27 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   strips = (int)ceil_div(d, rows);
   constexpr int CPT = NS == 1 ? 8 : 16;            // measured: 16 columns per thread pays off for >= 2 sets
   dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 8 * CPT), (unsigned)ceil_div(d, 128));
-  { ProfScope ps_("wcolmax", st); wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax); }
+  {
+    ProfScope ps_("wcolmax", st);
+    static const bool v1 = getenv("MASQ_WCOLMAX_V1") != nullptr;   // measurement switch
+    bool done = false;
+    if constexpr (sizeof(WT) == 2 && NS <= 2) {          // 3-4 sets would spill the running maxima
+      CUtensorMap tm;
+      const int64_t tj = ceil_div(n, 128), ti = ceil_div(d, 128);
+      if (!v1 && make_tmap_2d(&tm, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, n, n, 128, 128, false)) {
+        const int smem = kWqStages * kWqTileBytes + 8 * NS * 128 * 4 + 64;
+        cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(wcolmax_tma_kernel<NS>), smem);
+        if (e != cudaSuccess) return e;
+        // row runs sized so that there are >= 2 units per SM (bounded atomic traffic)
+        const int rs = (int)std::max<int64_t>(1, std::min<int64_t>(ti, tj * ti / (2 * (int64_t)num_sms())));
+        const int64_t units = tj * ceil_div(ti, rs);
+        const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms() * 2);
+        wcolmax_tma_kernel<NS><<<(unsigned)grid, 256, smem, st>>>(tm, s, d, n, tj, ti, rs, units, amax);
+        done = true;
+      }
+    }
+    if (!done) wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax);
+  }
   { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, rcp, NS * n, (float)qmax); }
   {
     ProfScope ps_("wquant", st);
