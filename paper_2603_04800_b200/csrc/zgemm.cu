@@ -240,36 +240,48 @@ __global__ void split_f32_kernel(const float* __restrict__ X, int64_t ld_x, int6
   lo[idx] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(v, __bfloat162float(h))));
 }
 // split-K combine: Z rows of the blocks the forward reads = hi/lo of sum_s zpart[s] (fixed order),
-// zeros for rows of other modalities; one warp per (row, non-text modality), lanes over columns
+// zeros for rows of other modalities; one thread per (row, non-text modality, 4 columns)
 __global__ void __launch_bounds__(256) zcombine_kernel(const float* __restrict__ zpart, int splits, int64_t T_pad,
                                                        const uint8_t* __restrict__ ids, int64_t T, int n_mod,
                                                        int rpad, const uint32_t* __restrict__ tile_mask,
                                                        uint16_t* __restrict__ Z) {
   const int nnt = n_mod - 1;
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= T * nnt) return;
+  const int q4 = rpad / 4;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * nnt * q4) return;
+  const int c4 = (int)(idx % q4);
+  const int64_t w = idx / q4;
   const int64_t g = w / nnt;
   const int mm = (int)(w - g * nnt) + 1;
   const int64_t n_tiles = (T + 127) / 128, mt = g >> 7;
   const uint32_t tmask = tile_mask[mt] | ((mt ^ 1) < n_tiles ? tile_mask[mt ^ 1] : 0u);
   if (!((tmask >> mm) & 1u)) return;
   const bool mine = (int)__ldg(ids + g) == mm;
-  uint16_t* zr = Z + g * (int64_t)nnt * 2 * rpad + (int64_t)(mm - 1) * 2 * rpad;
-  for (int c = lane; c < rpad; c += 32) {
-    float v[16];                                  // splits <= 16: all loads in flight, then the ordered sum
+  float4 v[16];                                   // splits <= 16: all loads in flight, then the ordered sum
 #pragma unroll
-    for (int sp = 0; sp < 16; ++sp)
-      v[sp] = sp < splits ? __ldg(zpart + ((sp * T_pad + g) * nnt + (mm - 1)) * rpad + c) : 0.f;
-    float z = 0.f;
+  for (int sp = 0; sp < 16; ++sp)
+    if (sp < splits)
+      v[sp] = __ldg(reinterpret_cast<const float4*>(zpart + ((sp * T_pad + g) * nnt + (mm - 1)) * rpad) + c4);
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int sp = 0; sp < 16; ++sp)
-      if (sp < splits) z += v[sp];
-    if (!mine) z = 0.f;
-    const __nv_bfloat16 h = __float2bfloat16_rn(z);
-    zr[c] = __bfloat16_as_ushort(h);
-    zr[rpad + c] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(z, __bfloat162float(h))));
+  for (int sp = 0; sp < 16; ++sp)
+    if (sp < splits) {
+      z[0] += v[sp].x;
+      z[1] += v[sp].y;
+      z[2] += v[sp].z;
+      z[3] += v[sp].w;
+    }
+  uint16_t h[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float x = mine ? z[e] : 0.f;
+    const __nv_bfloat16 hb = __float2bfloat16_rn(x);
+    h[e] = __bfloat16_as_ushort(hb);
+    l[e] = __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(x, __bfloat162float(hb))));
   }
+  uint16_t* zr = Z + g * (int64_t)nnt * 2 * rpad + (int64_t)(mm - 1) * 2 * rpad + c4 * 4;
+  *reinterpret_cast<uint2*>(zr) = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+  *reinterpret_cast<uint2*>(zr + rpad) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
 }
 }  // namespace
 
@@ -355,10 +367,10 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   if (splits > 1) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int64_t warps = T * n_nt;
+    const int64_t threads = T * n_nt * (rpad / 4);
     ProfScope ps_("zcombine", st);
-    zcombine_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(zpart, splits, ceil_div(T, 128) * 128, ids, T,
-                                                                       n_mod, rpad, tile_mask, Z);
+    zcombine_kernel<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(zpart, splits, ceil_div(T, 128) * 128, ids, T,
+                                                                      n_mod, rpad, tile_mask, Z);
   }
   return cudaGetLastError();
 }
