@@ -36,7 +36,14 @@ def _problem(seed):
                 f32x=f32x)
 
 
-@pytest.mark.parametrize("seed", range(40))
+def _seeds():
+    # MASQ_FUZZ_SEEDS="a:b" widens the sweep for an extended run (default: seeds 0..39)
+    import os
+    a, b = (int(x) for x in os.environ.get("MASQ_FUZZ_SEEDS", "0:40").split(":"))
+    return range(a, b)
+
+
+@pytest.mark.parametrize("seed", _seeds())
 def test_random_problem_parity(seed):
     m = M()
     c = _problem(seed)
