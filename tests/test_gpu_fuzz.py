@@ -18,7 +18,7 @@ def _problem(seed):
     n_mod = int(g.integers(1, 5))
     d = 16 * int(g.integers(1, 40))
     n = 32 * int(g.integers(1, 20))
-    T = int(g.integers(1, 1400))
+    T = max(int(g.integers(1, 1400)), n_mod)           # room for every modality (the oracle rejects empty ones)
     runs, ids = [], []
     while sum(len(x) for x in ids) < T:
         m = int(g.integers(0, n_mod))
