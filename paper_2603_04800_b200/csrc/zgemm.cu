@@ -37,7 +37,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
              const __grid_constant__ CUtensorMap tmB, const uint8_t* __restrict__ ids, int T, int d, int n_mod,
              int rpad, int per, int a_planes, uint32_t tmem_cols, int stages,
              const uint32_t* __restrict__ tile_mask, uint16_t* __restrict__ Z, float* __restrict__ zpart,
-             int splits) {
+             int splits, int pair) {
   const int mt = blockIdx.x;
   const int m0 = 1 + blockIdx.y * per;
   const int m1 = min(m0 + per, n_mod);           // exclusive
@@ -135,7 +135,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
     const uint32_t taddr = tmem + ((q * 32u) << 16);
     const int zld = (n_mod - 1) * 2 * rpad;
     const int nnt = n_mod - 1;
-    for (int mm = m0; mm < m1; ++mm) {
+    for (int mm = m0; mm < m1 && !pair; ++mm) {
       if (!((tmask >> mm) & 1u)) continue;                     // block never read by the GEMM
       if (splits > 1) {                                        // raw f32 partial of this K range
         float* zp = zpart + (((int64_t)blockIdx.z * gridDim.x * 128 + g) * nnt + (mm - 1)) * rpad;
@@ -184,6 +184,82 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
             }
             *reinterpret_cast<uint4*>(zr + c * 32 + qq * 8) = make_uint4(ph2[0], ph2[1], ph2[2], ph2[3]);
             *reinterpret_cast<uint4*>(zr + rpad + c * 32 + qq * 8) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+          }
+        }
+      }
+    }
+  }
+  if (pair) {
+    // cluster pair = the two K halves of one 128-row tile: rank 1 adds its f32 accumulator into
+    // rank 0's (now idle) ring through DSMEM, rank 0 sums (own + partner, fixed order) and writes Z
+    const uint32_t rank = cluster_ctarank();
+    float* pbuf = reinterpret_cast<float*>(smem);              // [128 rows][N] f32 (<= 64 KB)
+    cluster_sync();                                            // both CTAs' MMAs are complete
+    if (warp >= 2 && rank == 1) {
+      const uint32_t q = warp & 3u;
+      const int rl = (int)(q * 32u + lane);
+      const uint32_t taddr = tmem + ((q * 32u) << 16);
+      for (int mm = m0; mm < m1; ++mm) {
+        if (!((tmask >> mm) & 1u)) continue;
+        for (int c = 0; c < rpad / 32; ++c) {
+          const int col = (mm - m0) * rpad + c * 32;
+          uint32_t v[32], w[32];
+          tmem_ld32(taddr + col, v);
+          tmem_ld32(taddr + N + col, w);                       // pair mode is the combined [hi; lo] form
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__fadd_rn(__uint_as_float(v[e]), __uint_as_float(w[e])));
+          uint32_t raddr;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(raddr) : "r"(smem_u32(pbuf + (size_t)rl * N + col)));
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq)
+            asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(raddr + 16u * qq),
+                         "r"(v[4 * qq]), "r"(v[4 * qq + 1]), "r"(v[4 * qq + 2]), "r"(v[4 * qq + 3])
+                         : "memory");
+        }
+      }
+    }
+    cluster_sync();                                            // partner partials visible in rank 0
+    if (warp >= 2 && rank == 0) {
+      const uint32_t q = warp & 3u;
+      const int rl = (int)(q * 32u + lane);
+      const int g = mt * 128 + rl;
+      const uint32_t taddr = tmem + ((q * 32u) << 16);
+      const int zld = (n_mod - 1) * 2 * rpad;
+      const int mid = g < T ? (int)__ldg(ids + g) : -1;
+      for (int mm = m0; mm < m1; ++mm) {
+        if (!((tmask >> mm) & 1u)) continue;
+        const bool mine = mid == mm;
+        uint16_t* zr = Z + (int64_t)g * zld + (int64_t)(mm - 1) * 2 * rpad;
+        for (int c = 0; c < rpad / 32; ++c) {
+          const int col = (mm - m0) * rpad + c * 32;
+          uint32_t v[32], w[32];
+          tmem_ld32(taddr + col, v);
+          tmem_ld32(taddr + N + col, w);
+          tmem_wait_ld();
+          const float* pr = pbuf + (size_t)rl * N + col;
+          if (g < T) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const float4 pa = *reinterpret_cast<const float4*>(pr + 8 * qq);
+              const float4 pb = *reinterpret_cast<const float4*>(pr + 8 * qq + 4);
+              const float pp[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+              uint32_t ph2[4], pl[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int k0 = 8 * qq + 2 * e;
+                const float o0 = __fadd_rn(__uint_as_float(v[k0]), __uint_as_float(w[k0]));
+                const float o1 = __fadd_rn(__uint_as_float(v[k0 + 1]), __uint_as_float(w[k0 + 1]));
+                const float z0 = mine ? __fadd_rn(o0, pp[2 * e]) : 0.f;
+                const float z1 = mine ? __fadd_rn(o1, pp[2 * e + 1]) : 0.f;
+                const float h0 = __bfloat162float(__float2bfloat16_rn(z0));
+                const float h1 = __bfloat162float(__float2bfloat16_rn(z1));
+                ph2[e] = pack_bf16(h0, h1);
+                pl[e] = pack_bf16(__fsub_rn(z0, h0), __fsub_rn(z1, h1));
+              }
+              *reinterpret_cast<uint4*>(zr + c * 32 + qq * 8) = make_uint4(ph2[0], ph2[1], ph2[2], ph2[3]);
+              *reinterpret_cast<uint4*>(zr + rpad + c * 32 + qq * 8) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+            }
           }
         }
       }
@@ -343,8 +419,18 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
                      true);
   if (!ok) return cudaErrorInvalidValue;
   const int SB = ((a_planes * XCH + 2 * N * 128) + 1023) & ~1023;
+  // cluster-pair split-K (two K halves per 128-row tile, reduced through DSMEM) when the tiles
+  // alone leave SMs idle but no global split is taken: 3 stages so two CTAs fit per SM
+  static const bool no_pair = [] {
+    const char* e = getenv("MASQ_ZGEMM_PAIR");
+    return e && e[0] == '0';
+  }();
+  const int64_t tiles = ceil_div(T, 128);
+  const bool pair = !no_pair && zpart != nullptr && zgemm_splits(T, d) == 1 && a_planes == 1 && 2 * N <= 256 &&
+                    tiles <= num_sms() && ceil_div(d, 64) >= 8;
   int stages = (SMEM_CAP - 2048) / SB;
   stages = stages > 8 ? 8 : stages;
+  if (pair) stages = std::min(stages, 3);
   static const int env_st = [] {                         // measurement knob: ring stages
     const char* e = getenv("MASQ_ZGEMM_STAGES");
     return e ? atoi(e) : 0;
@@ -357,14 +443,32 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   const int acc_cols = 2 * N <= 256 ? 2 * N : N;
   uint32_t cols = 32;
   while ((int)cols < acc_cols) cols <<= 1;
-  const int splits = zpart ? zgemm_splits(T, d) : 1;
+  const int splits = pair ? 2 : (zpart ? zgemm_splits(T, d) : 1);
   dim3 grid((unsigned)ceil_div(T, 128), (unsigned)passes, (unsigned)splits);
   {
     ProfScope ps_("zgemm", st);
-    zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols, stages,
-                                         tile_mask, Z, zpart, splits);
+    if (pair) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(ZT);
+      cfg.dynamicSmemBytes = (size_t)smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 2;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, zgemm_kernel, ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
+                             stages, tile_mask, Z, (float*)nullptr, 2, 1);
+      if (e != cudaSuccess) return e;
+    } else {
+      zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
+                                           stages, tile_mask, Z, zpart, splits, 0);
+    }
   }
-  if (splits > 1) {
+  if (splits > 1 && !pair) {
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int64_t threads = T * n_nt * (rpad / 4);
