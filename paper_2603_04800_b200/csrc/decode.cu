@@ -206,6 +206,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const int8_t* __res
     }
     return;
   }
+  // programmatic dependent launch: the producer above streams weights (inputs of earlier calls)
+  // while the activation quantizer that precedes this kernel may still run; the consumers wait
+  // for it here, before touching its codes and scales
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int gid = lane >> 2, tig = lane & 3;
   const int gw = warp * kGroupsPerWarp;                            // first group of this warp in the chunk
   const int remw = ngc - gw;
@@ -396,6 +400,7 @@ cudaError_t launch_decode(const int8_t* qa, const float* dx, int T, int64_t d, i
     const char* e = getenv("MASQ_DECODE_CFG");
     cfg = e ? atoi(e) : 42;
   }
+  static const bool pdl = getenv("MASQ_DECODE_PDL") == nullptr || getenv("MASQ_DECODE_PDL")[0] != '0';
   const int per = std::max(1, num_sms() / ky);                    // one CTA per SM in total
   dim3 grid((unsigned)std::min<int64_t>(ntiles, per), (unsigned)ky);
   cudaError_t err = cudaSuccess;
@@ -405,8 +410,18 @@ cudaError_t launch_decode(const int8_t* qa, const float* dx, int T, int64_t d, i
   {                                                                                                           \
     err = set_max_dyn_smem(reinterpret_cast<const void*>(decode_kernel<S, K, RD>), DecCfg<S, K, RD>::kSmem);    \
     if (err != cudaSuccess) return err;                                                                       \
-    decode_kernel<S, K, RD><<<grid, kDecThreads, DecCfg<S, K, RD>::kSmem, st>>>(qa, dx, T, d, n, packed,      \
-                                                                              scales, part, Y, ldy);         \
+    cudaLaunchConfig_t cfg_ = {};                                                                             \
+    cfg_.gridDim = grid;                                                                                      \
+    cfg_.blockDim = dim3(kDecThreads);                                                                        \
+    cfg_.dynamicSmemBytes = DecCfg<S, K, RD>::kSmem;                                                          \
+    cfg_.stream = st;                                                                                         \
+    cudaLaunchAttribute at_[1];                                                                               \
+    at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                           \
+    at_[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;                                          \
+    cfg_.attrs = at_;                                                                                         \
+    cfg_.numAttrs = 1;                                                                                        \
+    err = cudaLaunchKernelEx(&cfg_, decode_kernel<S, K, RD>, qa, dx, T, d, n, packed, scales, part, Y, ldy);  \
+    if (err != cudaSuccess) return err;                                                                       \
   }
     switch (cfg) {
       case 33: DEC(3, 3, 2) break;

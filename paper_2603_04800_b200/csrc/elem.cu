@@ -838,6 +838,9 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ uint64_t full[kAqMaxStages];
   __shared__ uint32_t s_red[2][32];
+  // a kernel launched after this one with programmatic stream serialization (the decode GEMM)
+  // may start now; it waits (griddepcontrol.wait) before reading this kernel's outputs
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr float kMagic = 12582912.0f;               // 1.5 * 2^23
   constexpr float kLim = 0.5f - 0.000030517578125f;   // 1/2 - 2^-15 (see the proof above)
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;
