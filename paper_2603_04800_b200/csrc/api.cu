@@ -851,9 +851,14 @@ masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64
   uint8_t* ids0 = reinterpret_cast<uint8_t*>(W8(ws, L.ids0));
   int8_t* qa = reinterpret_cast<int8_t*>(W8(ws, L.qx));
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
-  MASQ_CK(cudaMemsetAsync(ids0, 0, (size_t)T, st));
-  MASQ_CK(launch_inv(s_t, d, inv, st));
-  MASQ_CK(launch_aquant(X, xt, ld_x, ids0, T, d, 1, inv, abits, qa, dx, nullptr, status_of(ws), st, nullptr, T));
+  const cudaError_t qe = launch_aquant_direct(X, xt, ld_x, T, d, s_t, abits, qa, dx, status_of(ws), st);
+  if (qe == cudaErrorNotSupported) {
+    MASQ_CK(cudaMemsetAsync(ids0, 0, (size_t)T, st));
+    MASQ_CK(launch_inv(s_t, d, inv, st));
+    MASQ_CK(launch_aquant(X, xt, ld_x, ids0, T, d, 1, inv, abits, qa, dx, nullptr, status_of(ws), st, nullptr, T));
+  } else {
+    MASQ_CK(qe);
+  }
   MASQ_CK(launch_decode(qa, dx, (int)T, d, d_out, packed, scales, reinterpret_cast<float*>(W8(ws, L.dpart)), Y,
                         ld_y, st));
   return MASQ_OK;

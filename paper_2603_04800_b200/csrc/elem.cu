@@ -834,7 +834,9 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
     const float* __restrict__ inv_s, float qaf, int qmin, int qmax, int8_t* __restrict__ qx,
     float* __restrict__ dx, uint32_t* __restrict__ mask, uint32_t* __restrict__ status,
     const int32_t* __restrict__ perm, int64_t T_out, int64_t rows_per_cta, int S, int8_t* __restrict__ qg,
-    float* __restrict__ dg, const int32_t* __restrict__ ipos) {
+    float* __restrict__ dg, const int32_t* __restrict__ ipos, const float* __restrict__ s_raw) {
+  // ids == nullptr: every token is modality 0; inv_s == nullptr: 1/s is formed here from s_raw
+  // (the same IEEE division as inv_kernel) when a modality's factor chunk is (re)loaded
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ uint64_t full[kAqMaxStages];
   __shared__ uint32_t s_red[2][32];
@@ -874,16 +876,20 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
   uint32_t ph = 0;
   for (int64_t row = r0; row < r1; ++row) {
     const int64_t src = perm ? (int64_t)__ldg(perm + row) : row;
-    const int m = src >= 0 ? (int)__ldg(ids + src) : 0;
+    const int m = (src >= 0 && ids) ? (int)__ldg(ids + src) : 0;
     const bool skip = src < 0 || m >= n_mod;             // CTA-uniform
     if (!skip && m != mc) {                              // CTA-uniform, once per modality run
       mc = m;
-      const float* inv = inv_s + (int64_t)m * d + tid * 8;
+      const float* inv = (inv_s ? inv_s : s_raw) + (int64_t)m * d + tid * 8;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         if (k < CPL - 1 || last_ok) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(inv + k * nthr * 8));
-          const float4 b = __ldg(reinterpret_cast<const float4*>(inv + k * nthr * 8 + 4));
+          float4 a = __ldg(reinterpret_cast<const float4*>(inv + k * nthr * 8));
+          float4 b = __ldg(reinterpret_cast<const float4*>(inv + k * nthr * 8 + 4));
+          if (!inv_s) {
+            a = make_float4(__fdiv_rn(1.0f, a.x), __fdiv_rn(1.0f, a.y), __fdiv_rn(1.0f, a.z), __fdiv_rn(1.0f, a.w));
+            b = make_float4(__fdiv_rn(1.0f, b.x), __fdiv_rn(1.0f, b.y), __fdiv_rn(1.0f, b.z), __fdiv_rn(1.0f, b.w));
+          }
           inv2[k][0] = f2_pack(a.x, a.y);
           inv2[k][1] = f2_pack(a.z, a.w);
           inv2[k][2] = f2_pack(b.x, b.y);
@@ -1493,7 +1499,8 @@ template <int CPL>
 static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, const uint8_t* ids, int64_t d, int n_mod,
                                       const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx, float* dx,
                                       uint32_t* mask, uint32_t* status, const int32_t* perm, int64_t T_out, int nthr,
-                                      int8_t* qg, float* dg, const int32_t* ipos, cudaStream_t st) {
+                                      int8_t* qg, float* dg, const int32_t* ipos, const float* s_raw,
+                                      cudaStream_t st) {
   auto kern = aquant_bf16_kernel<CPL>;
   const int64_t rowb = 2 * d;
   constexpr int64_t kRingPerSm = 192 * 1024;            // shared memory for row stages per SM
@@ -1522,7 +1529,8 @@ static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, cons
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(T_out, (int64_t)num_sms() * per_sm));
   const int64_t rows = ceil_div(T_out, ctas);
   kern<<<(unsigned)ceil_div(T_out, rows), nthr, smem, st>>>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx,
-                                                            mask, status, perm, T_out, rows, S, qg, dg, ipos);
+                                                            mask, status, perm, T_out, rows, S, qg, dg, ipos,
+                                                            s_raw);
   return cudaGetLastError();
 }
 
@@ -1532,7 +1540,7 @@ static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, co
                                         int n_mod, const float* inv_s, float qaf, int qmin, int qmax, int8_t* qx,
                                         float* dx, uint32_t* mask, uint32_t* status, const int32_t* perm,
                                         int64_t T_out, cudaStream_t st, int8_t* qg = nullptr, float* dg = nullptr,
-                                        const int32_t* ipos = nullptr) {
+                                        const int32_t* ipos = nullptr, const float* s_raw = nullptr) {
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (ld_x & 7) || (d & 7)) return cudaErrorNotSupported;  // 16-B rows
   const int64_t ch = d / 8;
   static const int target = [] {
@@ -1545,7 +1553,7 @@ static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, co
   if (nthr > kAqMaxThreads) return cudaErrorNotSupported;
   const int cpl = (int)ceil_div(ch, nthr);
   ProfScope ps_("aquant", st);
-#define AQB(C) case C: return aquant_bf16_launch<C>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out, (int)nthr, qg, dg, ipos, st)
+#define AQB(C) case C: return aquant_bf16_launch<C>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx, mask, status, perm, T_out, (int)nthr, qg, dg, ipos, s_raw, st)
   switch (cpl) {
     AQB(1); AQB(2); AQB(3); AQB(4); AQB(5); AQB(6); AQB(7); AQB(8);
     default: break;
@@ -1598,6 +1606,17 @@ __global__ void __launch_bounds__(256) pad_rows_kernel(const int32_t* __restrict
   uint4* out = reinterpret_cast<uint4*>(qg + p * d);
   for (int64_t c = lane; c < d / 16; c += 32) out[c] = make_uint4(0, 0, 0, 0);
   if (lane == 0) dg[p] = 0.f;
+}
+
+// A4 of one modality (modality 0, no ids) with 1/s formed in the kernel: the decode path's
+// quantizer in one launch; cudaErrorNotSupported when the TMA row kernel does not apply
+cudaError_t launch_aquant_direct(const void* X, masq_dtype xt, int64_t ld_x, int64_t T, int64_t d, const float* s,
+                                 int abits, int8_t* qx, float* dx, uint32_t* status, cudaStream_t st) {
+  static const bool v1 = getenv("MASQ_AQUANT_V1") != nullptr;
+  if (xt != MASQ_BF16 || v1 || T <= 0) return cudaErrorNotSupported;
+  const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
+  return aquant_bf16_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, nullptr, d, 1, nullptr, (float)qmax, qmin,
+                              qmax, qx, dx, nullptr, status, nullptr, T, st, nullptr, nullptr, nullptr, s);
 }
 
 // A4 once for the fused layer call: token-order codes (forward) and, for non-text rows, their

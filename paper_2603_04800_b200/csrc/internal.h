@@ -81,6 +81,10 @@ cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t s
 // fused layer call: A4 once, writing the token-order codes and the grouped copy of the non-text
 // rows (ipos[t] = grouped row of token t from launch_route); zeroes the grouped padding rows of
 // modalities >= 1.  cudaErrorNotSupported when the TMA row kernel does not apply.
+// A4 for the decode path: every token modality 0, 1/s formed in the kernel (no ids, no inverse
+// factors); cudaErrorNotSupported when the TMA row kernel does not apply
+cudaError_t launch_aquant_direct(const void* X, masq_dtype xt, int64_t ld_x, int64_t T, int64_t d, const float* s,
+                                 int abits, int8_t* qx, float* dx, uint32_t* status, cudaStream_t st);
 cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                                int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
                                uint32_t* status, const int32_t* perm, const uint32_t* tile_mod, const int32_t* ipos,
