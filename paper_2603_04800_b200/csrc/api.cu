@@ -196,6 +196,20 @@ masq_status check_common(int64_t T, int64_t d, int32_t n_mod) {
   if (n_mod < 1 || n_mod > kMaxMod) return MASQ_ERR_SHAPE;
   return MASQ_OK;
 }
+// A4 with the inverse factors formed inside the bf16 row kernel; where that kernel does not apply
+// (f32 X, very wide rows, unaligned X) the inverse factors are computed into inv_ws first
+cudaError_t quantize_acts(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
+                          int n_mod, const float* s, float* inv_ws, int abits, int8_t* qx, float* dx,
+                          uint32_t* mask, uint32_t* status, cudaStream_t st) {
+  static const bool sep = getenv("MASQ_SEPARATE_INV") != nullptr;   // measurement switch
+  cudaError_t e = cudaErrorNotSupported;
+  if (!sep) e = launch_aquant(X, xt, ld_x, ids, T, d, n_mod, nullptr, abits, qx, dx, mask, status, st, nullptr, -1, s);
+  if (e != cudaErrorNotSupported) return e;
+  e = launch_inv(s, (int64_t)n_mod * d, inv_ws, st);
+  if (e != cudaSuccess) return e;
+  return launch_aquant(X, xt, ld_x, ids, T, d, n_mod, inv_ws, abits, qx, dx, mask, status, st);
+}
+
 masq_status check_x(const void* X, masq_dtype xt, int64_t ld_x, int64_t d) {
   if (!X) return MASQ_ERR_NULL;
   if (xt != MASQ_BF16 && xt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
@@ -283,8 +297,7 @@ masq_status masq_quantize_activations(const void* X, masq_dtype xt, int64_t ld_x
   const WsLayout L = ws_layout(MASQ_OP_QACT, T, d, 0, n_mod, 0);
   MASQ_TRY(check_ws(ws, ws_bytes, L));
   float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
-  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, S(stream)));
-  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, tile_mask, status_of(ws), S(stream)));
+  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, tile_mask, status_of(ws), S(stream)));
   return MASQ_OK;
 }
 
@@ -319,8 +332,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
   uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
-  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
-  MASQ_CK(launch_aquant(X, xt, ld_x, mod_id, T, d, n_mod, inv, abits, qx, dx, mask, status_of(ws), st));
+  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, mask, status_of(ws), st));
   GemmArgs g{};
   g.mode = use_acc ? kModeAcc : kModeFwd;
   g.T = T;
@@ -340,7 +352,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
-    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), inv, d, r, rp, n_mod - 1, l1t, st));
+    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t, st));
     MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
     if (xt == MASQ_BF16) {
       MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
@@ -409,13 +421,14 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   // shared front half: factors, routing, every modality's weight codes (set 0 = the forward's
   // Q(S_t W)), the token-order activation codes (forward) and their grouped copy (loss)
   int32_t* ipos = reinterpret_cast<int32_t*>(W8(ws, L.ipos));
-  MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
   MASQ_CK(launch_route(mod_id, T, n_mod, perm, tmod, cnt, st, ipos));
   MASQ_CK(launch_wquant(W, MASQ_BF16, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
-  // the loss GEMM below skips the text units, so only the non-text rows need the grouped copy
-  const cudaError_t qe = launch_aquant_dual(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask,
-                                            status_of(ws), perm, tmod, ipos, Tg, qg, dg, st);
+  // the loss GEMM below skips the text units, so only the non-text rows need the grouped copy;
+  // the row kernel forms 1/s itself (no inverse-factor launch)
+  const cudaError_t qe = launch_aquant_dual(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, nullptr, abits, qt, dt, mask,
+                                            status_of(ws), perm, tmod, ipos, Tg, qg, dg, st, s);
   if (qe == cudaErrorNotSupported) {
+    MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
     MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask, status_of(ws), st));
     MASQ_CK(launch_gather_rows(qt, dt, perm, Tg, d, qg, dg, st));
   } else {
@@ -463,7 +476,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
-    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), inv, d, r, rp, n_mod - 1, l1t, st));
+    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t, st));
     MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
     MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     g.rpad = rp;

@@ -1564,7 +1564,7 @@ static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, co
 
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
-                          uint32_t* status, cudaStream_t st, const int32_t* perm, int64_t T_out) {
+                          uint32_t* status, cudaStream_t st, const int32_t* perm, int64_t T_out, const float* s_raw) {
   if (T <= 0) return cudaSuccess;
   if (T_out < 0) T_out = T;
   if (mask) {
@@ -1576,8 +1576,10 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
   static const bool v1 = getenv("MASQ_AQUANT_V1") != nullptr;   // measurement switch: previous kernel
   if (xt == MASQ_BF16 && !v1)
     er = aquant_bf16_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax, qmin,
-                              qmax, qx, dx, mask, status, perm, T_out, st);
+                              qmax, qx, dx, mask, status, perm, T_out, st, nullptr, nullptr, nullptr,
+                              inv_s ? nullptr : s_raw);
   if (er != cudaErrorNotSupported) return er;
+  if (!inv_s) return cudaErrorNotSupported;             // the other kernels need the inverse factors
   if (xt == MASQ_BF16) er = aquant_reg_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s,
                                                 (float)qmax, qmin, qmax, qx, dx, mask, status, perm, T_out, st);
   else er = aquant_reg_dispatch(static_cast<const float*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax, qmin, qmax,
@@ -1625,7 +1627,7 @@ cudaError_t launch_aquant_direct(const void* X, masq_dtype xt, int64_t ld_x, int
 cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                                int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
                                uint32_t* status, const int32_t* perm, const uint32_t* tile_mod, const int32_t* ipos,
-                               int64_t Tg, int8_t* qg, float* dg, cudaStream_t st) {
+                               int64_t Tg, int8_t* qg, float* dg, cudaStream_t st, const float* s_raw) {
   static const bool v1 = getenv("MASQ_AQUANT_V1") != nullptr;
   if (xt != MASQ_BF16 || v1 || T <= 0) return cudaErrorNotSupported;
   if (mask) {
@@ -1634,7 +1636,8 @@ cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const
   }
   const int qmax = (1 << (abits - 1)) - 1, qmin = -(1 << (abits - 1));
   cudaError_t e = aquant_bf16_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax,
-                                       qmin, qmax, qx, dx, mask, status, nullptr, T, st, qg, dg, ipos);
+                                       qmin, qmax, qx, dx, mask, status, nullptr, T, st, qg, dg, ipos,
+                                       inv_s ? nullptr : s_raw);
   if (e != cudaSuccess) return e;
   ProfScope ps_("pad_rows", st);
   pad_rows_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(perm, tile_mod, Tg, d, 1, qg, dg);

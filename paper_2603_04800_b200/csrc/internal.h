@@ -88,14 +88,17 @@ cudaError_t launch_aquant_direct(const void* X, masq_dtype xt, int64_t ld_x, int
 cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                                int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
                                uint32_t* status, const int32_t* perm, const uint32_t* tile_mod, const int32_t* ipos,
-                               int64_t Tg, int8_t* qg, float* dg, cudaStream_t st);
+                               int64_t Tg, int8_t* qg, float* dg, cudaStream_t st, const float* s_raw = nullptr);
 cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t* perm, int64_t Tg, int64_t d, int8_t* qg,
                                float* dg, cudaStream_t st);
 // perm (optional): output row p quantizes input token perm[p] (-1: padding row, left untouched);
 // T_out = number of output rows (T when perm == NULL)
 cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T, int64_t d,
                           int n_mod, const float* inv_s, int abits, int8_t* qx, float* dx, uint32_t* mask,
-                          uint32_t* status, cudaStream_t st, const int32_t* perm = nullptr, int64_t T_out = -1);
+                          uint32_t* status, cudaStream_t st, const int32_t* perm = nullptr, int64_t T_out = -1,
+                          const float* s_raw = nullptr);
+// (inv_s == nullptr: 1/s is formed in the bf16 TMA row kernel from s_raw; cudaErrorNotSupported
+//  when that kernel does not apply, and the caller computes the inverse factors and retries)
 // rows grouped by modality, each segment padded to a multiple of kUnitM (256) rows:
 // perm[Tg] (grouped row -> token, -1 padding), tile_mod[Tg/256] (modality of the unit, ~0u empty)
 inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kUnitM) * kUnitM + (int64_t)n_mod * kUnitM; }
@@ -254,7 +257,8 @@ cudaError_t launch_range_stats(const float* R, int n_mod, int64_t d, int dominan
 
 // ---------------------------------------------------------------- CMC first factor (zgemm.cu)
 // L1s planes: [2][(M-1)*rpad][d] bf16, plane 0 = hi, 1 = lo of diag(1/s^m) L1^m (transposed)
-cudaError_t launch_l1_fold(const uint16_t* L1, const float* inv_s, int64_t d, int r, int rpad, int n_nt,
+// s: the factors [n_mod][d]; 1/s is formed in the kernel (IEEE division, as inv_kernel)
+cudaError_t launch_l1_fold(const uint16_t* L1, const float* s, int64_t d, int r, int rpad, int n_nt,
                            uint16_t* L1s, cudaStream_t st);
 // f32 X -> bf16 hi / lo planes [T x d]
 cudaError_t launch_split_f32(const float* X, int64_t ld_x, int64_t T, int64_t d, uint16_t* hi, uint16_t* lo,

@@ -274,19 +274,19 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
 }
 
 // L1s[p][(m-1)*rpad + k][i] = plane p of inv_s[m][i] * L1^m[i][k] (p = 0 hi, 1 lo); zero for k >= r
-__global__ void l1_fold_kernel(const uint16_t* __restrict__ L1, const float* __restrict__ inv_s, int64_t d, int r,
+__global__ void l1_fold_kernel(const uint16_t* __restrict__ L1, const float* __restrict__ s_f, int64_t d, int r,
                                int rpad, int n_nt, uint16_t* __restrict__ L1s) {
   __shared__ float t[32][33];
   const int mb = blockIdx.z;                    // non-text modality index (m - 1)
   const int64_t i0 = (int64_t)blockIdx.x * 32;
   const int k0 = blockIdx.y * 32;
-  const float* inv = inv_s + (int64_t)(mb + 1) * d;
+  const float* sm = s_f + (int64_t)(mb + 1) * d;
   const uint16_t* src = L1 + (int64_t)mb * d * r;
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int64_t i = i0 + y;
     const int k = k0 + threadIdx.x;
     float v = 0.f;
-    if (i < d && k < r) v = __fmul_rn(__uint_as_float((uint32_t)src[i * r + k] << 16), inv[i]);
+    if (i < d && k < r) v = __fmul_rn(__uint_as_float((uint32_t)src[i * r + k] << 16), __fdiv_rn(1.0f, sm[i]));
     t[y][threadIdx.x] = v;
   }
   __syncthreads();
@@ -381,7 +381,7 @@ size_t zgemm_part_bytes(int64_t T, int64_t d, int n_mod, int rpad) {
   return sizeof(float) * (size_t)sp * ceil_div(T, 128) * 128 * (n_mod - 1) * rpad;
 }
 
-cudaError_t launch_l1_fold(const uint16_t* L1, const float* inv_s, int64_t d, int r, int rpad, int n_nt,
+cudaError_t launch_l1_fold(const uint16_t* L1, const float* s_f, int64_t d, int r, int rpad, int n_nt,
                            uint16_t* L1s, cudaStream_t st) {
   if (r < rpad) {
     cudaError_t e = cudaMemsetAsync(L1s, 0, sizeof(uint16_t) * 2 * (size_t)n_nt * rpad * d, st);
@@ -389,7 +389,7 @@ cudaError_t launch_l1_fold(const uint16_t* L1, const float* inv_s, int64_t d, in
   }
   dim3 grid((unsigned)ceil_div(d, 32), (unsigned)ceil_div(r, 32), n_nt), block(32, 8);
   ProfScope ps_("l1_fold", st);
-  l1_fold_kernel<<<grid, block, 0, st>>>(L1, inv_s, d, r, rpad, n_nt, L1s);
+  l1_fold_kernel<<<grid, block, 0, st>>>(L1, s_f, d, r, rpad, n_nt, L1s);
   return cudaGetLastError();
 }
 
