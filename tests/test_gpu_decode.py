@@ -74,3 +74,24 @@ def test_linear_decode_limits():
     with pytest.raises(m.MasqError) as e:
         m.linear_decode(bf(c["X"][:17]), tt(s[0]), packed, scales)
     assert e.value.status == 2
+
+
+def test_linear_decode_quantizer_paths_agree():
+    """The decode call's one-launch bf16 quantizer (1/s formed in the kernel, no ids buffer) and
+    the fallback path taken for f32 X (inverse-factor kernel + row kernel) see the same values
+    (bf16 -> f32 is exact), so they must give bit-identical Y; a strided bf16 X view too."""
+    m = M()
+    d, n, T = 3584, 4608, 7
+    c, s = _inputs(d, n)
+    packed, scales = m.quantize_weight_int4(bf(c["W"]), tt(s[0]))
+    Xh = c["X"][np.arange(T) * 53 % c["T"]]
+    Yb = m.linear_decode(bf(Xh), tt(s[0]), packed, scales).cpu().numpy()
+    Yf = m.linear_decode(tt(O.decode(Xh)), tt(s[0]), packed, scales).cpu().numpy()
+    Xw = np.zeros((T, d + 128), np.uint16)
+    Xw[:, 64:64 + d] = Xh
+    Yv = m.linear_decode(bf(Xw)[:, 64:64 + d], tt(s[0]), packed, scales).cpu().numpy()
+    m.check()
+    assert np.array_equal(Yb, Yf) and np.array_equal(Yb, Yv)
+    q, dl = O.quantize_weight_grouped(c["W"], s[0], 4, 128)
+    Yo = O.linear_decode(Xh, s[0], q, dl, 8, 128)
+    assert np.abs(Yb - Yo).max() / np.abs(Yo).max() <= 1e-3
