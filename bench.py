@@ -50,8 +50,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="masq", choices=["masq", "reference"])
-    ap.add_argument("--rank-cmc", type=int, default=64, help="CMC rank r (0 disables)")
-    ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
+    ap.add_argument("--rank-cmc", type=int, default=None, help="CMC rank r (0 disables; default c3 64, c2 0)")
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default c3 16384, c2 4096)")
     ap.add_argument("--linears", default="qkv,o,gate_up,down")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -66,12 +66,27 @@ def parse():
                          "gaps are ~2%% of the step and the captured profiler event nodes cost more)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines)")
     ap.add_argument("--c5-n", type=int, default=18944, help="c5: output channels of the d=3584 linear")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c4s", "c5"],
-                    help="c3: one Qwen2.5-VL-7B layer, every §8(a) row (default); c4: 28-layer calibration sweep "
-                         "(2 loss passes at perturbed factors); c4s: the same sweep with 2 real S-optimisation "
-                         "epochs per layer (N1: loss + straight-through gradient + Adam)")
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4", "c4s", "c5"],
+                    help="c3: one Qwen2.5-VL-7B layer, every §8(a) row (default); c2: the same step on one "
+                         "Qwen2.5-Omni-3B layer (text/image/audio, W8A8, 4096 tokens, r = 0); c4 (= c4s): 28-layer "
+                         "calibration sweep with 2 real S-optimisation epochs per layer (N1: loss + "
+                         "straight-through gradient + Adam)")
     ap.add_argument("--layers", type=int, default=28, help="c4: number of decoder layers")
-    return ap.parse_args()
+    args = ap.parse_args()
+    configure(args)
+    return args
+
+
+def configure(args):
+    """Select the layer workload: c3 (BASELINE configs[2], default) or c2 (configs[1])."""
+    global CFG, CI, WBITS, ABITS, N_MOD
+    if args.workload == "c2":
+        CFG, CI, WBITS, ABITS, N_MOD = "c2", 1, 8, 8, 3
+    cfg = synth.CONFIGS[CFG]
+    if args.tokens is None:
+        args.tokens = 16384 if args.workload in ("c3", "c4", "c4s", "c5") else cfg["T"]
+    if args.rank_cmc is None:
+        args.rank_cmc = 64 if args.workload != "c2" else cfg["r"]
 
 
 def load_peaks():
@@ -228,19 +243,18 @@ def oracle_sample_step(ids_s, lin_s, r):
 
 
 def oracle_sample(T, r, seed_rank=0):
-    """Sample = the qkv linear (3584 -> 4608) of the c3 layer on k text + k image tokens (two sizes
-    split the per-token from the per-step weight-side cost)."""
+    """Sample = the qkv linear of the layer on k tokens of every modality (two sizes split the
+    per-token from the per-step weight-side cost)."""
     cfg = synth.CONFIGS[CFG]
     name, d, n = layer_linears(["qkv"])[0]
     ids_full = synth.modality_ids(cfg["pattern"], T=T)
     X = synth.activations(ids_full, d, N_MOD, synth.seed_for(CI, 0, 0) + 100000 * seed_rank)
     W = synth.weight(d, n, synth.seed_for(CI, 0, 1))
     L1, L2 = synth.lowrank(d, n, r, N_MOD, synth.seed_for(CI, 0, 2)) if r > 0 else (None, None)
-    text = np.nonzero(ids_full == 0)[0]
-    img = np.nonzero(ids_full == 1)[0]
+    by_mod = [np.nonzero(ids_full == m)[0] for m in range(N_MOD)]
 
     def sample(k):
-        rows = np.concatenate([text[:k], img[:k]])
+        rows = np.concatenate([b[:k] for b in by_mod])
         return ids_full[rows], dict(X=X[rows], W=W, L1=L1, L2=L2)
     return sample
 
@@ -271,14 +285,15 @@ def time_oracle(T, r, linears, repeats=4, k_small=128, k_large=512):
         oracle_sample_step(ids_b, s_b, r)
     tb = (time.perf_counter() - t) / repeats
     total = time.perf_counter() - t0
-    na, nb = 2 * k_small, 2 * k_large
+    na, nb = N_MOD * k_small, N_MOD * k_large
     per_tok = max(tb - ta, 1e-9) / (nb - na)
     fixed = max(ta - na * per_tok, 0.0)
-    dn_qkv = 3584 * 4608
+    _, dq, nq = layer_linears(["qkv"])[0]
+    dn_qkv = dq * nq
     scale = sum(d * n for _, d, n in linears) / dn_qkv
     layer_time = scale * (fixed + T * per_tok)
     desc = (f"oracle step (stats, init, wquant, forward+CMC, loss incl. X W) on the qkv linear "
-            f"3584->4608 with {na} and {nb} tokens (half text, half image), {repeats} repeats each: "
+            f"{dq}->{nq} with {na} and {nb} tokens (equal shares of the {N_MOD} modalities), {repeats} repeats each: "
             f"{ta:.2f} s / {tb:.2f} s per step; extrapolated to the {len(linears)}-linear layer at {T} tokens "
             f"by sum(d*n) (x{scale:.1f}): {layer_time:.1f} s")
     return T / layer_time, total, desc
@@ -313,11 +328,18 @@ def run_reference(args):
 
 
 def workload_config(args, linears):
+    if CFG == "c2":
+        head = "c2 (BASELINE configs[1]): Qwen2.5-Omni-3B-shaped (thinker) decoder layer, linears "
+        lay = "4 x [text 64 | image 512 | audio 320 | text 128]"
+        mods = "3 modalities (text/image/audio)"
+    else:
+        head = "c3 (BASELINE configs[2]): Qwen2.5-VL-7B-shaped decoder layer, linears "
+        lay = "16 x [text 64 | image 768 | text 192]"
+        mods = "2 modalities (text/image)"
     return {
-        "workload": (f"c3 (BASELINE configs[2]): Qwen2.5-VL-7B-shaped decoder layer, linears "
-                     + ", ".join(f"{k} {d}->{n}" for k, d, n in linears)
-                     + f"; {args.tokens} tokens/GPU per step (16 x [text 64 | image 768 | text 192]); "
-                     f"W{WBITS}A{ABITS}; CMC rank {args.rank_cmc} for image tokens; 2 modalities"),
+        "workload": (head + ", ".join(f"{k} {d}->{n}" for k, d, n in linears)
+                     + f"; {args.tokens} tokens/GPU per step ({lay}); "
+                     f"W{WBITS}A{ABITS}; CMC rank {args.rank_cmc} for non-text tokens; {mods}"),
         "tokens_per_gpu": args.tokens,
         "parallelism": f"dp{args.gpus} (token-sharded calibration; replicated weights)",
         "l2": "inputs larger than L2 (each step streams >1 GB of activations/weights; no flush)",
@@ -331,8 +353,8 @@ def run_c4(args):
     """BASELINE configs[3]: full 28-layer Qwen2.5-VL-7B-shaped calibration sweep, 16384 tokens per
     GPU (128 samples x 1024 tokens over 8 GPUs).  Per sweep: A1 stats of every layer input, ONE
     batched MAX/SUM exchange for all layers, then per layer: A2 init, X W once (the loss target of
-    the batch), and 2 loss passes (2 epochs) at perturbed factors
-    s * exp(0.01 N(0,1)) standing in for optimiser iterates, each followed by a SUM exchange.
+    the batch), and 2 S-optimisation epochs (N1): loss + straight-through gradient
+    (global counts, SUM-reduced) + log-space Adam on every linear, each followed by a SUM exchange.
     Inputs are generated on the device (same recipe distribution as synth/, seeded per layer and
     rank): host generation of 28 layers would take minutes; parity is covered at c3 sizes."""
     import torch
@@ -386,12 +408,6 @@ def run_c4(args):
     Sbuf = torch.zeros(nl, N_MOD, dtype=torch.float64, device=dev)
     Nbuf = torch.zeros(nl, N_MOD, dtype=torch.int64, device=dev)
     losses = torch.zeros(args.layers, 2, nl, dtype=torch.float64, device=dev)
-    pert = []
-    for l in range(args.layers):
-        gp = torch.Generator(device=dev)
-        gp.manual_seed(synth.seed_for(3, l, 5))
-        pert.append([[torch.exp(0.01 * torch.randn(N_MOD, e["d"], generator=gp, device=dev)) for e in layers[0]]
-                     for _ in range(2)])
     ws = M.Workspace(dev)
     # linear li of a layer runs on stream li % S with its own workspace (the linears of a layer are
     # independent between the exchanges; 2 streams let one linear's HBM-bound kernels run beside
@@ -415,7 +431,8 @@ def run_c4(args):
         for st_ in side:
             main.wait_stream(st_)
 
-    optimise = args.workload == "c4s"
+    # every loss pass is a real S-optimisation step (N1): loss + straight-through gradient + Adam
+    optimise = True
     grads = [torch.empty(N_MOD, e["d"], dtype=torch.float64, device=dev) for e in layers[0]]
     adam = [None] * nl
 
@@ -438,16 +455,11 @@ def run_c4(args):
                 for li, e in enumerate(layers[l]):
                     with on(li):
                         wk = wss[li % nstreams]
-                        if optimise:
-                            # N1: 2 epochs of loss + straight-through gradient + log-space
-                            # Adam, the gradient normalised by the global counts and SUM-reduced
-                            M.calib_loss_grad(e["X"], ids, svec[li], e["W"], WBITS, ABITS, Yref[li], grad=grads[li],
-                                              sums=Sbuf[li], counts=Nbuf[li], loss=losses[l, p_, li:li + 1],
-                                              count_norm=Cbuf[l * nl + li], ws=wk)
-                        else:
-                            sp = svec[li] * pert[l][p_][li]
-                            M.calib_loss(e["X"], ids, sp, e["W"], WBITS, ABITS, Yref[li], sums=Sbuf[li],
-                                         counts=Nbuf[li], loss=losses[l, p_, li:li + 1], ws=wk)
+                        # N1: 2 epochs of loss + straight-through gradient + log-space
+                        # Adam, the gradient normalised by the global counts and SUM-reduced
+                        M.calib_loss_grad(e["X"], ids, svec[li], e["W"], WBITS, ABITS, Yref[li], grad=grads[li],
+                                          sums=Sbuf[li], counts=Nbuf[li], loss=losses[l, p_, li:li + 1],
+                                          count_norm=Cbuf[l * nl + li], ws=wk)
                 if world > 1:
                     join()
                     P.reduce_loss(Sbuf, Nbuf)
@@ -465,7 +477,8 @@ def run_c4(args):
 
     for _ in range(max(args.warmup, 1)):
         sweep()
-    M.check(ws)
+    for w in wss:
+        M.check(w)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -730,7 +743,8 @@ def main():
     # ------------------------------------------------------------------ warm-up
     for _ in range(max(args.warmup, 0)):
         step()
-    M.check(ws)
+    for w in wss:
+        M.check(w)
     torch.cuda.synchronize()
 
     if args.profile_only:
@@ -763,14 +777,17 @@ def main():
         lib().masq_profile_enable(1)
     prof_steps = 1 if use_graph else args.steps
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     if clk:
         clk.mark(True)
     ev0.record()
-    for _ in range(args.steps):
+    for k_ in range(args.steps):
         if use_graph:
             graph.replay()
         else:
             step()
+        if k_ < args.steps - 1:
+            evs[k_].record()
     ev1.record()
     torch.cuda.synchronize()
     if clk:
@@ -778,6 +795,8 @@ def main():
     barrier()
     clocks = clk.stop() if clk else None
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    marks = [ev0] + evs + [ev1]
+    ms_median = float(np.median([marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]))
     import ctypes
     cap = 64
     names = ctypes.create_string_buffer(32 * cap)
@@ -789,7 +808,8 @@ def main():
     for i in range(max(nk, 0)):
         nm = names.raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode()
         kern[nm] = dict(ms=tot[i], launches=int(cnt[i]))
-    M.check(ws)
+    for w in wss:
+        M.check(w)
     ms_step = ms_total / args.steps
     value = world * T * args.steps / (ms_total / 1e3)
 
@@ -862,16 +882,16 @@ def main():
         e2e = {"value": world * T * args.steps / (ms_e2e / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e / args.steps,
                "note": "pinned H2D of the step's activations+ids on a copy stream (double-buffered, overlapping "
-                       "the previous step's compute) + D2H of the losses, every step"}
+                       "the previous step's compute) + D2H of the per-linear losses (the step's result), every "
+                       "step; the forward outputs Y and the targets X W stay on the device (a calibration step "
+                       "consumes them there)"}
 
     # ------------------------------------------------------------------ N1 (S-optimisation step)
     loss_main = [float(x) for x in losses.cpu().tolist()]
     n1 = None
     if not args.no_n1:
         for e in L:
-            e["theta"] = torch.log(e["s"].double())
-            e["m1"] = torch.zeros_like(e["theta"])
-            e["m2"] = torch.zeros_like(e["theta"])
+            e["theta"], e["m1"], e["m2"] = M.adam_init(e["s"])
             e["grad"] = torch.empty_like(e["theta"])
         Gbuf = [e["grad"] for e in L]
         n1_state = {"t": 0}
@@ -930,6 +950,31 @@ def main():
             dist.destroy_process_group()
         return 0
 
+    # ------------------------------------------------------------------ INT8 ceiling, measured here
+    # cuBLAS's int8 GEMM (torch._int_mm) on the step's largest linear shape, timed in this process
+    # after the timed regions (a second, measured denominator beside the derived 2 x bf16 one)
+    int8_ceiling = None
+    try:
+        big = max(L, key=lambda e: e["d"] * e["n"])
+        a8 = torch.randint(-127, 128, (T, big["d"]), dtype=torch.int8, device=dev)
+        b8 = torch.randint(-8, 8, (big["n"], big["d"]), dtype=torch.int8, device=dev).t()
+        for _ in range(3):
+            torch._int_mm(a8, b8)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        c0.record()
+        for _ in range(reps):
+            torch._int_mm(a8, b8)
+        c1.record()
+        torch.cuda.synchronize()
+        ms_i = c0.elapsed_time(c1) / reps
+        int8_ceiling = {"tops": 2.0 * T * big["d"] * big["n"] / (ms_i * 1e-3) / 1e12,
+                        "shape": f"{T} x {big['d']} x {big['n']}", "ms": ms_i,
+                        "how": "torch._int_mm (cuBLAS s8 GEMM), 10 back-to-back calls after 3 warm-up, CUDA events"}
+        del a8, b8
+    except Exception as ex:
+        int8_ceiling = {"tops": None, "error": repr(ex)}
+
     # ------------------------------------------------------------------ roofline accounting
     peaks = load_peaks()
     int8_peak = 2.0 * peaks["bf16_sus"]          # INT8 = 2x bf16 (nominal ratio 4.5/2.25 PFLOP/s)
@@ -987,6 +1032,11 @@ def main():
         "frac_int8_peak_linear_forward_call": (ops / (fwd_call_ms / 1e3) / 1e12 / int8_peak) if fwd_call_ms else None,
         "frac_int8_spec_4500": (ops / (fwd_call_ms / 1e3) / 1e12 / 4500.0) if fwd_call_ms else None,
         "int8_peak_tops": int8_peak,
+        "int8_peak_source": "MEASURED_PEAKS.json bf16 sustained x 2 (the guide's INT8/bf16 nominal ratio)",
+        "frac_int8_spec_4500_gemm_kernel": (fwd.get("achieved") / 4500.0) if fwd.get("achieved") else None,
+        "int8_ceiling_cublas": int8_ceiling,
+        "frac_int8_ceiling_cublas_gemm_kernel": (fwd.get("achieved") / int8_ceiling["tops"])
+        if (fwd.get("achieved") and int8_ceiling and int8_ceiling.get("tops")) else None,
         "note": "algorithmic 2*T*d*n ops of the 4 linears; forward = inv + aquant + L1/L2 pack + zgemm + gemm_fwd "
                 "(the activation codes are computed once per step and shared with the loss)",
     }
@@ -998,6 +1048,15 @@ def main():
             v, secs, desc = time_oracle(T, r, linears)
             cpu = {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle", "sample": desc,
                    "seconds": secs}
+            try:                                    # the same sample on ONE host thread
+                from threadpoolctl import threadpool_limits
+                with threadpool_limits(limits=1):
+                    v1, secs1, _ = time_oracle(T, r, linears, repeats=2)
+                cpu["value_1thread"] = v1
+                cpu["seconds_1thread"] = secs1
+            except Exception as ex:
+                cpu["value_1thread"] = None
+                cpu["error_1thread"] = repr(ex)
         except Exception as ex:  # report, never hide
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {ex!r}"}
@@ -1006,9 +1065,11 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int8",
-        "dtype_detail": "s8 x s8 -> s32 tcgen05 GEMMs (W4A8 codes in int8 containers); f32 quantizer; "
+        "dtype_detail": f"s8 x s8 -> s32 tcgen05 GEMMs (W{WBITS}A{ABITS} codes in int8 containers); f32 quantizer; "
                         "bf16 -> f32 tcgen05 for CMC and X W",
-        "data": "synthetic (seeded, synth/; random-init weights of the Qwen2.5-VL-7B layer shapes)",
+        "data": "synthetic (seeded, synth/; random-init weights of the "
+                + ("Qwen2.5-Omni-3B" if CFG == "c2" else "Qwen2.5-VL-7B") + " layer shapes)",
+        "ms_per_step_median": ms_median,
         "config": workload_config(args, linears),
         "linear_forward": linear,
         "n1_s_opt_step": n1,

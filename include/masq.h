@@ -83,7 +83,10 @@ enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
   MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,
   MASQ_OP_MEANABS = 8, MASQ_OP_CMC = 9, MASQ_OP_DECODE = 10, MASQ_OP_LAYER = 11,
-  MASQ_OP_CMC_GRAM = 12, MASQ_OP_CMC_FACTORS = 13
+  MASQ_OP_CMC_GRAM = 12, MASQ_OP_CMC_FACTORS = 13,
+  /* flag OR-ed into MASQ_OP_LOSS / MASQ_OP_LOSS_GRAD: the workspace also holds the loss
+   * target X W (f32 [T x d_out]) for calls made with Yref == NULL */
+  MASQ_OP_SELF_REF = 0x100
 };
 size_t masq_workspace_size(int32_t op, int64_t T, int64_t d, int64_t d_out,
                            int32_t n_mod, int32_t r);
@@ -141,11 +144,13 @@ masq_status masq_quantize_activations(const void* X, masq_dtype xt, int64_t ld_x
                                       int32_t abits, int8_t* qx, float* dx, uint32_t* tile_mask,
                                       void* ws, size_t ws_bytes, masq_stream stream);
 
-/* Optional debug taps for masq_linear_forward (parity tests). */
+/* Optional debug taps for masq_linear_forward (parity tests); every field may be NULL / 0. */
 typedef struct masq_debug {
   int32_t* acc;        /* if non-NULL: write the int32 accumulators sum_i qx*qw [T x ld_acc]
                           instead of Y (CMC skipped) */
   int64_t ld_acc;
+  int8_t* qx;          /* if non-NULL: receives the activation codes A4 produced, [T x d] int8 */
+  float* dx;           /* if non-NULL: receives the per-token steps Delta_x, [T] f32 */
 } masq_debug;
 
 /*
@@ -156,7 +161,7 @@ typedef struct masq_debug {
  * masq_quantize_weight with s^text (qw [d_out x d] K-major, dw [d_out]).
  * L1: bf16 [(n_mod-1) x d x r] (L1^m = T^-1 U_r), row-major per modality;
  * L2: bf16 [(n_mod-1) x r x ld_l2] (L2^m = Sigma_r V_r^T), row-major per modality.
- * L1/L2 may be NULL iff r == 0.  The CMC term is computed in full precision
+ * L1/L2 may be NULL iff r == 0.  s, qw, dw, L1, L2, Y: 16-byte aligned (MASQ_ERR_ALIGN).  The CMC term is computed in full precision
  * from the f32 smoothed activations (split-bf16 tensor-core products, fp32
  * accumulation, reading Q13).  Y: f32 [T x ld_y], original token order.
  * Column sharding: pass qw + j0*d, dw + j0, L2 + j0, Y + j0 and d_out = shard width.
@@ -186,7 +191,11 @@ masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, in
  *   counts[m] = #{t : id_t = m}
  *   loss[0]   = sum_m lambda[m] * sums[m] / (counts[m] * d_out)   over m with counts[m] > 0
  * lambda: HOST array [n_mod] (NULL -> all 1.0).  Yref: f32 [T x ld_ref]
- * from masq_reference_output.  sums/counts/loss are device pointers; the sums are
+ * from masq_reference_output (computed once per batch and reused across the S-optimisation
+ * passes), or NULL: the call then computes X W itself (as masq_reference_output; X and W must
+ * be bf16, else MASQ_ERR_UNSUPPORTED) into the workspace, which must be sized with
+ * masq_workspace_size(MASQ_OP_LOSS | MASQ_OP_SELF_REF, ...) (else MASQ_ERR_WORKSPACE).
+ * sums/counts/loss are device pointers; the sums are
  * reduced in a fixed order (deterministic).  For token-sharded multi-GPU use,
  * all-reduce sums and counts (SUM) and call masq_loss_finalize.
  */
@@ -200,12 +209,18 @@ masq_status masq_calib_loss(const void* X, masq_dtype xt, int64_t ld_x, const ui
 
 /*
  * N1 (the next row after A8) — the S-optimisation step's gradient: everything
- * masq_calib_loss computes, plus grad[m*d + i] = dL/dtheta^m_i with theta^m = ln s^m (SPEC.md:
- * 307-316: log-space parameters, rounding treated as identity = straight-through; reading Q24:
- * the dynamic scales are held constant):
- *   grad_i = lambda_m/(N_m n) * sum_j [ (Ahat^T G)_ij (S_m W)_ij - (X_m^T G)_ij inv_i Bhat_ij ]
- * with G = sign(Ahat Bhat - X_m W), Ahat = Q(X_m S_m^-1), Bhat = Q(S_m W).  grad: device f64
- * [n_mod x d].  X and W must be bf16.  count_norm (device i64 [n_mod], optional): the token
+ * masq_calib_loss computes, plus grad[m*d + l] = dL/dtheta^m_l with theta^m = ln s^m (SPEC.md:
+ * 307-316: log-space parameters, rounding treated as identity = straight-through).  Reading
+ * Q24: ONLY round() is straight-through; the dynamic scales Delta = max|.|/q_max
+ * are differentiated through their first arg-max element (a floored Delta has zero derivative).
+ * Per modality m, with A = X_m S_m^-1, Ahat = Q(A), B = S_m W, Bhat = Q(B),
+ * G = lambda_m/(N_m n) sign(Ahat Bhat - X_m W):
+ *   grad_l = sum_j (Ahat^T G)_lj B_lj - sum_j (A^T G)_lj Bhat_lj
+ *          + sum_{j: k_j = l} beta_j - sum_{t: k_t = l} alpha_t,
+ *   beta_j = sum_i (Ahat^T G)_ij (Bhat - B)_ij,   alpha_t = sum_j G_tj ((Ahat - A) Bhat)_tj,
+ * k_j = first arg-max_i |B_ij| (weight column scale), k_t = first arg-max_i |A_ti| (token scale).
+ * grad: device f64 [n_mod x d], summed in a fixed order (bit-reproducible).  X and W must be
+ * bf16.  Yref may be NULL (as masq_calib_loss; workspace MASQ_OP_LOSS_GRAD | MASQ_OP_SELF_REF).  count_norm (device i64 [n_mod], optional): the token
  * counts N_m used in scale_m = lambda_m/(N_m n); NULL = this call's own counts.  Token-sharded
  * multi-GPU use passes the GLOBAL counts (known after the A1 exchange) so that a plain SUM
  * all-reduce of grad over ranks is the gradient of the whole batch.

@@ -477,6 +477,32 @@ def cmc_factors_from_gram(G, dW, r: int, eps_rel: float = 1e-8):
     return T_inv @ U[:, :r], sig[:r, None] * Vt[:r]
 
 
+def cmc_factors_small_side(A, dW, r: int, eps_rel: float = 1e-8):
+    """The eq:l1l2 optimum evaluated from the n x n side, for d > n (the c3 down
+    projection, d = 18944: the paper's d x d eigensolve is out of reach for a CPU oracle there).
+    With T^T T = A^T A + eps lambda_max I (PAPER.md:139-142 and reading Q27), the squared singular
+    values and right singular vectors of M = T dW are the eigenpairs of
+        M^T M = dW^T T^T T dW = (A dW)^T (A dW) + eps lambda_max dW^T dW        (n x n),
+    and L2 = Sigma_r V_r^T, L1 = T^-1 U_r = T^-1 M V_r Sigma_r^-1 = dW V_r Sigma_r^-1.
+    lambda_max = the largest eigenvalue of A^T A (= that of A A^T, the smaller Gram is used).
+    Pinned against cmc_factors (the paper's route) in tests/test_oracle_pins.py."""
+    A = np.asarray(A, F64)
+    dW = np.asarray(dW, F64)
+    n = dW.shape[1]
+    if r == 0:
+        return np.zeros((dW.shape[0], 0)), np.zeros((0, n))
+    small = A @ A.T if A.shape[0] < A.shape[1] else A.T @ A
+    lam_max = max(float(np.linalg.eigvalsh(small).max()), 0.0)
+    AdW = A @ dW
+    C = AdW.T @ AdW + eps_rel * lam_max * (dW.T @ dW)
+    sig2, V = np.linalg.eigh(C)                           # ascending
+    sig = np.sqrt(np.maximum(sig2[::-1][:r], 0.0))
+    Vr = V[:, ::-1][:, :r]
+    L2 = sig[:, None] * Vr.T
+    L1 = (dW @ Vr) * np.where(sig > 0, 1.0 / np.where(sig > 0, sig, 1.0), 0.0)[None, :]
+    return L1, L2
+
+
 def reconstruction_loss(A, dW, L1, L2) -> float:
     """Theorem 2 objective ||A (dW - L1 L2)||_F^2 in f64."""
     A = np.asarray(A, F64)

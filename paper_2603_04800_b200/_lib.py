@@ -80,7 +80,7 @@ SIGNATURES = {
 
 
 class MasqDebug(ctypes.Structure):
-    _fields_ = [("acc", c_void_p), ("ld_acc", c_int64)]
+    _fields_ = [("acc", c_void_p), ("ld_acc", c_int64), ("qx", c_void_p), ("dx", c_void_p)]
 
 
 _lib = None

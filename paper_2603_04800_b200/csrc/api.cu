@@ -20,6 +20,8 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
   const int64_t rp = rpad_of(r);
   const int64_t nnt = std::max(n_mod - 1, 0);
   L.status = take(kStatusBytes);
+  const bool self_ref = (op & MASQ_OP_SELF_REF) != 0;     // loss target X W computed into ws
+  op &= ~MASQ_OP_SELF_REF;
   switch (op) {
     case MASQ_OP_STATS:
     case MASQ_OP_INIT:
@@ -28,13 +30,20 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     case MASQ_OP_CMC_GRAM:
     case MASQ_OP_CMC_FACTORS: {
       if (op != MASQ_OP_CMC_FACTORS) {
+        // tensor-core Gram (gram.cu): routing, the bf16 hi/lo planes of X S^-1, fp32 partial tiles
+        const int64_t Tg = grouped_rows(T, n_mod);
         L.inv_s = take(sizeof(float) * n_mod * d);
-        L.a64 = take(sizeof(double) * (size_t)T * d);
+        L.perm = take(sizeof(int32_t) * (Tg + route_scratch_ints(T)));
+        L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
+        L.cnt = take(sizeof(int64_t) * n_mod);
+        L.planes = take(sizeof(uint16_t) * 2 * (size_t)Tg * d);
+        L.gram_part = take(cmc_gram_part_bytes(T, d, n_mod));
       }
       if (op == MASQ_OP_CMC) L.gall = take(sizeof(double) * (size_t)(n_mod > 1 ? n_mod - 1 : 1) * d * d);
       if (op != MASQ_OP_CMC_GRAM) {
         L.g = take(sizeof(double) * (size_t)d * d);
-        L.c = take(sizeof(double) * (size_t)d * d);
+        const int64_t ce = cmc_eig_route() ? d : std::min(d, n);     // the eigensolved matrix
+        L.c = take(sizeof(double) * (size_t)ce * ce);
         L.lam = take(sizeof(double) * d);
         L.sig2 = take(sizeof(double) * d);
         L.sq = take(sizeof(double) * d);
@@ -44,7 +53,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
         L.l1t64 = take(sizeof(double) * (size_t)d * r);
         L.urs = take(sizeof(double) * (size_t)d * r);
         L.l2t64 = take(sizeof(double) * (size_t)r * n);
-        L.lwork = cmc_syevd_lwork(d);
+        L.lwork = cmc_syevd_lwork(d, n);
         L.work = take(sizeof(double) * (L.lwork + 1));
         L.info = take(sizeof(int) * 2);
         L.dot = take(sizeof(double) * cmc_dot_blocks());
@@ -138,7 +147,9 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
       L.gpartial = take(sizeof(double) * n_mod * gradgemm_ntiles_j(n) * d);
       L.dq = take((size_t)Tg * d);
       L.de = take(sizeof(float) * Tg);
-      L.apart = take(sizeof(float) * (size_t)Tg * 2 * ceil_div(n, kTileN));
+      L.dq2 = take((size_t)Tg * d);
+      L.de2 = take(sizeof(float) * Tg);
+      L.apart = take(sizeof(float) * (size_t)Tg * 4 * ceil_div(n, kTileN));
       L.bpart = take(sizeof(float) * (size_t)n_mod * 4 * gradgemm_ntiles_i(d) * n);
       L.kj = take(sizeof(int32_t) * (size_t)n_mod * n);
       const int64_t nkeys = (int64_t)n_mod * n + Tg;
@@ -154,6 +165,8 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     default:
       break;
   }
+  // last, so every other offset is the same with and without the flag
+  if (self_ref && (op == MASQ_OP_LOSS || op == MASQ_OP_LOSS_GRAD)) L.yref = take(sizeof(float) * (size_t)T * n);
   L.total = off;
   return L;
 }
@@ -321,7 +334,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   float* out = use_acc ? reinterpret_cast<float*>(dbg->acc) : Y;
   const int64_t ld_out = use_acc ? dbg->ld_acc : ld_y;
   if (ld_out < d_out || ld_out % 4 != 0 || !al16(out)) return MASQ_ERR_ALIGN;
-  if (!al16(qw) || !al16(dw)) return MASQ_ERR_ALIGN;
+  if (!al16(qw) || !al16(dw) || !al16(s)) return MASQ_ERR_ALIGN;
   if (T == 0) return MASQ_OK;
   MASQ_TRY(check_x(X, xt, ld_x, d));
   if (!mod_id) return MASQ_ERR_NULL;
@@ -333,6 +346,8 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
   uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
   MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, mask, status_of(ws), st));
+  if (dbg && dbg->qx) MASQ_CK(cudaMemcpyAsync(dbg->qx, qx, (size_t)T * d, cudaMemcpyDeviceToDevice, st));
+  if (dbg && dbg->dx) MASQ_CK(cudaMemcpyAsync(dbg->dx, dx, sizeof(float) * T, cudaMemcpyDeviceToDevice, st));
   GemmArgs g{};
   g.mode = use_acc ? kModeAcc : kModeFwd;
   g.T = T;
@@ -563,7 +578,31 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     return MASQ_OK;
   }
   MASQ_TRY(check_x(X, xt, ld_x, d));
-  if (!mod_id || !Yref) return MASQ_ERR_NULL;
+  if (!mod_id) return MASQ_ERR_NULL;
+  if (!Yref) {
+    // the target X_m W is part of the loss; without a caller-supplied Yref it is
+    // computed here (bf16 tensor-core products, fp32 accumulation, reading Q16) into the
+    // workspace, which must then be sized with MASQ_OP_SELF_REF
+    if (xt != MASQ_BF16 || wt != MASQ_BF16) return MASQ_ERR_UNSUPPORTED;
+    const WsLayout Ls = ws_layout((grad ? MASQ_OP_LOSS_GRAD : MASQ_OP_LOSS) | MASQ_OP_SELF_REF, T, d, d_out, n_mod, 0);
+    MASQ_TRY(check_ws(ws, ws_bytes, Ls));
+    float* yr = reinterpret_cast<float*>(W8(ws, Ls.yref));
+    GemmArgs gr{};
+    gr.mode = kModeRef;
+    gr.T = T;
+    gr.n = d_out;
+    gr.d = d;
+    gr.xbf = static_cast<const uint16_t*>(X);
+    gr.ld_x = ld_x;
+    gr.b = W;
+    gr.b_rows = d;
+    gr.n_mod = 1;
+    gr.out = yr;
+    gr.ld_out = d_out;
+    MASQ_CK(launch_gemm(gr, st));
+    Yref = yr;
+    ld_ref = d_out;
+  }
   if (ld_ref < d_out || ld_ref % 4 != 0 || !al16(Yref)) return MASQ_ERR_ALIGN;
   float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
   int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
@@ -618,8 +657,10 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     const int64_t nj = (int64_t)n_mod * d_out, nkeys = nj + Tg;
     int32_t* ktkey = keys + nj;
     const uint32_t* colmax = amax;                     // first half of the scratch: column maxima
+    int8_t* dq2 = reinterpret_cast<int8_t*>(W8(ws, L.dq2));
+    float* de2 = reinterpret_cast<float*>(W8(ws, L.de2));
     MASQ_CK(launch_gradprep(static_cast<const uint16_t*>(X), ld_x, mod_id, perm, qx, dx, inv, Tg, d, abits, planes,
-                            ktkey, dq, de, st));
+                            ktkey, dq, de, dq2, de2, st));
     MASQ_CK(cudaMemsetAsync(kj, 0x7F, sizeof(int32_t) * nj, st));
     MASQ_CK(launch_gradgemm(planes, Tg, gsign, qw, tmod, n_mod, d, d_out, s, inv, static_cast<const uint16_t*>(W), dw,
                             colmax, gpart, bpart, kj, st));
@@ -637,8 +678,14 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     ga.n_mod = n_mod;
     ga.gsign = gsign;
     ga.apart = apart;
+    ga.apart_ld = 4 * num_n;
+    ga.apart_off = 0;
     MASQ_CK(launch_gemm(ga, st));
-    MASQ_CK(launch_gradkeys(bpart, 4 * gradgemm_ntiles_i(d), kj, colmax, wbits, apart, 2 * num_n, ktkey, n_mod, d,
+    ga.qx = dq2;                                       // the residual's codes on the step e_t / 254
+    ga.dx = de2;
+    ga.apart_off = 2 * num_n;
+    MASQ_CK(launch_gemm(ga, st));
+    MASQ_CK(launch_gradkeys(bpart, 4 * gradgemm_ntiles_i(d), kj, colmax, wbits, apart, 4 * num_n, ktkey, n_mod, d,
                             d_out, Tg, keys, vals, st));
     MASQ_CK(launch_bucket(keys, vals, nkeys, (int64_t)n_mod * d, reinterpret_cast<uint32_t*>(W8(ws, L.skeys)),
                           reinterpret_cast<double*>(W8(ws, L.svals)), W8(ws, L.stemp), L.stemp_bytes, bucket, st));
@@ -759,7 +806,11 @@ masq_status cmc_gram_core(const void* X, masq_dtype xt, int64_t ld_x, const uint
   a.d = d;
   a.n_mod = n_mod;
   a.inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
-  a.A64 = reinterpret_cast<double*>(W8(ws, L.a64));
+  a.perm = reinterpret_cast<int32_t*>(W8(ws, L.perm));
+  a.tile_mod = reinterpret_cast<uint32_t*>(W8(ws, L.tile_mod));
+  a.cnt = reinterpret_cast<int64_t*>(W8(ws, L.cnt));
+  a.planes = reinterpret_cast<uint16_t*>(W8(ws, L.planes));
+  a.gram_part = reinterpret_cast<float*>(W8(ws, L.gram_part));
   if (T > 0) MASQ_CK(launch_inv(s, (int64_t)n_mod * d, const_cast<float*>(a.inv), st));
   const cudaError_t e = launch_cmc_gram(a, G, accumulate, st);
   if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
@@ -854,7 +905,7 @@ masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64
   if (d <= 0 || d % 128 != 0 || d_out <= 0 || d_out % 8 != 0) return MASQ_ERR_SHAPE;
   MASQ_TRY(check_bits(abits));
   if (!s_t || !packed || !scales || !Y) return MASQ_ERR_NULL;
-  if (ld_y < d_out || !al16(packed)) return MASQ_ERR_ALIGN;
+  if (ld_y < d_out || !al16(packed) || !al16(s_t) || !al16(scales)) return MASQ_ERR_ALIGN;
   const WsLayout L = ws_layout(MASQ_OP_DECODE, T, d, d_out, 1, 0);
   MASQ_TRY(check_ws(ws, ws_bytes, L));
   if (T == 0) return MASQ_OK;

@@ -1,9 +1,10 @@
 // cmc.cu — N2: construction of the CMC factors L1^m, L2^m on the GPU
 // (eq:l1l2).
 //
-// For every non-text modality m, in f64 throughout the decomposition:
-//   A_m = X_m S_m^-1 (the f32 smoothed activations the path computes, other tokens zeroed)
-//   G = A_m^T A_m (cuBLAS Dsyrk)             -> eig G = P Lambda P^T (cuSOLVER Dsyevd)
+// For every non-text modality m:
+//   A_m = X_m S_m^-1 (the f32 smoothed activations the path computes)
+//   G = A_m^T A_m: tensor-core split-bf16 Gram, f64 chunk reduction (gram.cu), then in f64:
+//   eig G = P Lambda P^T (cuSOLVER Dsyevd; MASQ_CMC_EIG=1, else the Cholesky route below)
 //   Lambda' = max(Lambda, 0) + eps_rel * lambda_max (reading Q27)
 //   dW = S_m W - Q(S_t W) (exact in f64, this file's kernel, from the text codes and scales)
 //   M = T dW = diag(sqrt Lambda') P^T dW      (Dgemm + row scaling)
@@ -11,6 +12,10 @@
 //   the eigenvalues its squared singular values (only the leading r are needed)
 //   L2 = U_r^T M = Sigma_r V_r^T,  L1 = T^-1 U_r = P diag(1/sqrt Lambda') U_r
 //   resid (optional) = ||A_m (dW - L1 L2)||_F^2 = <E, G E>, E = dW - L1 L2 (Dsymm + reduction).
+// When n < d the same optimum comes from the n x n side: eig(dW^T G' dW) = V Sigma^2 V^T,
+// L2 = Sigma_r V_r^T, L1 = dW V_r Sigma_r^-1 (T^-1 M = dW, so no d x d factorisation is needed).
+// Default route for n >= d: G' = Lc Lc^T (Cholesky), T = Lc^T (any T with T^T T = G' gives the
+// same L1 L2), M = Lc^T dW, U_r from eig(M M^T), L2 = U_r^T M, L1 = Lc^-T U_r.
 // Two phases so that token-sharded runs can SUM the Grams between them:
 // launch_cmc_gram (per shard / batch, accumulating) and launch_cmc_from_gram.
 // cuBLAS / cuSOLVER are plain library linear algebra here (GEMM, SYRK, symmetric eigensolver);
@@ -106,21 +111,6 @@ int cur_dev() {
   return dev;
 }
 
-// A64 [T x d] row-major (= column-major d x T): xs of modality m, zeros elsewhere
-template <typename XT>
-__global__ void xs64_kernel(const XT* __restrict__ X, int64_t ld_x, const uint8_t* __restrict__ ids, int64_t T,
-                            int64_t d, int m, const float* __restrict__ inv, double* __restrict__ A) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= T * d) return;
-  const int64_t t = idx / d, i = idx - t * d;
-  double v = 0.0;
-  if (ids[t] == m) {
-    const float x = (float)X[t * ld_x + i];
-    v = (double)__fmul_rn(x, inv[(int64_t)m * d + i]);
-  }
-  A[idx] = v;
-}
-
 // dW column-major [d x n]: dW(i, j) = s_i w_ij - dw_j code_ji   (32 x 32 tiles, W transposed via smem)
 template <typename WT>
 __global__ void dw64_kernel(const WT* __restrict__ W, const float* __restrict__ s, const int8_t* __restrict__ qw,
@@ -199,6 +189,35 @@ __global__ void scale_rows_kernel(const double* in, int64_t rows, int64_t cols, 
   out[idx] = in[idx] * f[idx % rows];
 }
 
+// F += eps_rel * max(lam, 0) * dW  (the regulariser of Q27 applied to G dW)
+__global__ void add_reg_kernel(double* __restrict__ F, const double* __restrict__ dW, int64_t count,
+                               const double* __restrict__ lam, double eps_rel) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  F[idx] += eps_rel * fmax(*lam, 0.0) * dW[idx];
+}
+
+// small-side factors from V_r (n x r column-major, ascending eigen order) and sig2 (n):
+// L1t (d x r, column-major, = dW V_r on entry) column k scaled by 1 / sigma_k; L2t (r x n,
+// column-major) = Sigma_r V_r^T; sigma_k = sqrt(max(sig2[n - r + k], 0)) (0 -> zero factors)
+__global__ void small_side_factors_kernel(double* __restrict__ L1t, double* __restrict__ L2t,
+                                          const double* __restrict__ Vr, const double* __restrict__ sig2, int64_t d,
+                                          int64_t n, int r) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = d * r, n2 = (int64_t)r * n;
+  if (idx < n1) {
+    const int k = (int)(idx / d);
+    const double sg = sqrt(fmax(sig2[n - r + k], 0.0));
+    L1t[idx] = sg > 0.0 ? L1t[idx] / sg : 0.0;
+  } else if (idx < n1 + n2) {
+    const int64_t e = idx - n1;
+    const int64_t j = e / r;
+    const int k = (int)(e - j * r);
+    const double sg = sqrt(fmax(sig2[n - r + k], 0.0));
+    L2t[e] = sg * Vr[(int64_t)k * n + j];
+  }
+}
+
 template <typename OT>
 __device__ __forceinline__ OT cvt_out(double v);
 template <>
@@ -254,11 +273,21 @@ constexpr int kDotBlocks = 592;
 
 bool cmc_linalg_available() { return linalg(0) != nullptr; }
 
-size_t cmc_syevd_lwork(int64_t d) {
+bool cmc_eig_route() {
+  static const int env = [] {                         // MASQ_CMC_EIG=1: the paper's eigen route (A/B)
+    const char* ev = getenv("MASQ_CMC_EIG");
+    return ev && atoi(ev) ? 1 : 0;
+  }();
+  return env == 1;
+}
+
+size_t cmc_syevd_lwork(int64_t d, int64_t n) {
   LinAlg* L = linalg(0);
   if (!L || d <= 0) return 0;
+  // eigensolves: d x d (the eigen route's G and M M^T) or min(d, n) (Cholesky / small-side routes)
+  const int64_t e = cmc_eig_route() ? d : std::min(d, n);
   int lw = 0, lp = 0;
-  if (L->syevd_size(L->hs[cur_dev()], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d,
+  if (L->syevd_size(L->hs[cur_dev()], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)e, nullptr, (int)e,
                     nullptr, &lw) != CUSOLVER_STATUS_SUCCESS)
     return 0;
   if (L->potrf_size(L->hs[cur_dev()], CUBLAS_FILL_MODE_LOWER, (int)d, nullptr, (int)d, &lp) != CUSOLVER_STATUS_SUCCESS)
@@ -266,37 +295,18 @@ size_t cmc_syevd_lwork(int64_t d) {
   return (size_t)(lw > lp ? lw : lp);
 }
 
-// phase 1: G[m-1] (+)= A_m^T A_m (lower triangle) for m = 1..n_mod-1
+// phase 1: G[m-1] (+)= A_m^T A_m for m = 1..n_mod-1 (full symmetric, row-major) on the tensor
+// cores (gram.cu): route the tokens into modality-grouped order, then the split-bf16 Gram
 cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStream_t st) {
-  LinAlg* L = linalg(st);
-  if (!L) return cudaErrorNotSupported;
-  cublasHandle_t hb = L->hb[cur_dev()];
   const int64_t T = a.T, d = a.d;
-  const int di = (int)d, Ti = (int)T;
-  const double one = 1.0, beta = accumulate ? 1.0 : 0.0;
-  for (int m = 1; m < a.n_mod; ++m) {
-    double* Gm = G + (int64_t)(m - 1) * d * d;
-    if (T == 0) {
-      if (!accumulate) {
-        cudaError_t e = cudaMemsetAsync(Gm, 0, sizeof(double) * d * d, st);
-        if (e != cudaSuccess) return e;
-      }
-      continue;
-    }
-    {
-      ProfScope ps_("cmc_xs64", st);
-      const unsigned g = (unsigned)ceil_div(T * d, 256);
-      if (a.xt == MASQ_BF16)
-        xs64_kernel<<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.X), a.ld_x, a.ids, T, d, m, a.inv, a.A64);
-      else
-        xs64_kernel<<<g, 256, 0, st>>>(static_cast<const float*>(a.X), a.ld_x, a.ids, T, d, m, a.inv, a.A64);
-    }
-    ProfScope ps_("cmc_gram", st);
-    if (L->dsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, di, Ti, &one, a.A64, di, &beta, Gm, di) !=
-        CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;
+  if (T == 0) {
+    if (!accumulate) return cudaMemsetAsync(G, 0, sizeof(double) * (size_t)(a.n_mod - 1) * d * d, st);
+    return cudaSuccess;
   }
-  return cudaGetLastError();
+  cudaError_t e = launch_route(a.ids, T, a.n_mod, a.perm, a.tile_mod, a.cnt, st);
+  if (e != cudaSuccess) return e;
+  return launch_cmc_gram_tc(a.X, a.xt, a.ld_x, a.ids, T, d, a.n_mod, a.inv, a.perm, a.tile_mod, a.planes,
+                            a.gram_part, G, accumulate, st);
 }
 
 // phase 2: factors (and the Theorem-2 residual <E, G E>) from the Gram matrices
@@ -310,12 +320,7 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
   const int r = a.r;
   const int di = (int)d, ni = (int)n;
   const double one = 1.0, zero = 0.0, mone = -1.0;
-  static int eig_env = -1;                            // MASQ_CMC_EIG=1: the paper's eigen route (A/B)
-  if (eig_env < 0) {
-    const char* ev = getenv("MASQ_CMC_EIG");
-    eig_env = ev && atoi(ev) ? 1 : 0;
-  }
-  const bool use_eig = eig_env == 1;
+  const bool use_eig = cmc_eig_route();
 #define CK_B(x) do { if ((x) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
 #define CK_S(x) do { if ((x) != CUSOLVER_STATUS_SUCCESS) return cudaErrorUnknown; } while (0)
   for (int m = 1; m < a.n_mod; ++m) {
@@ -330,7 +335,32 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
       else
         dw64_kernel<<<grid, block, 0, st>>>(static_cast<const float*>(a.W), sm, a.qw_t, a.dw_t, d, n, a.dW);
     }
-    if (use_eig) {
+    if (!use_eig && n < d) {
+      // small side (n < d, e.g. the down projection 18944 -> 3584): with T^T T = G' = G +
+      // eps lambda_max I, the right singular vectors of M = T dW are the eigenvectors of
+      // M^T M = dW^T G' dW (n x n), and the best rank-r L1 L2 is T^-1 M V_r V_r^T = dW V_r V_r^T:
+      // L2 = Sigma_r V_r^T, L1 = dW V_r Sigma_r^-1 (no d x d factorisation or eigensolve)
+      ProfScope ps_("cmc_small_side", st);
+      double* u = a.sq;
+      double* w = a.isq;
+      fill_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(u, d, 1.0 / sqrt((double)d));
+      for (int it = 0; it < 32; ++it) {
+        CK_B(L->dsymv(hb, CUBLAS_FILL_MODE_LOWER, di, &one, Gm, di, u, 1, &zero, w, 1));
+        power_step_kernel<<<1, 1024, 0, st>>>(u, w, d, a.lam);
+      }
+      CK_B(L->dsymm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, di, ni, &one, Gm, di, a.dW, di, &zero, a.Mb, di));
+      add_reg_kernel<<<(unsigned)ceil_div(d * n, 256), 256, 0, st>>>(a.Mb, a.dW, d * n, a.lam, a.eps_rel);
+      CK_B(L->dgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, ni, ni, di, &one, a.dW, di, a.Mb, di, &zero, a.C, ni));
+      {
+        ProfScope ps2_("cmc_eig_small", st);
+        CK_S(L->syevd(hs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, ni, a.C, ni, a.sig2, a.work,
+                      (int)a.lwork, a.info + 1));
+      }
+      const double* Vr = a.C + (int64_t)(n - r) * n;              // columns n-r .. n-1 (ascending)
+      CK_B(L->dgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, di, r, ni, &one, a.dW, di, Vr, ni, &zero, a.L1t, di));
+      const int64_t cnt = d * r + (int64_t)r * n;
+      small_side_factors_kernel<<<(unsigned)ceil_div(cnt, 256), 256, 0, st>>>(a.L1t, a.L2t, Vr, a.sig2, d, n, r);
+    } else if (use_eig) {
       // the paper's route: eig G = P Lambda P^T, T = diag(sqrt Lambda') P^T
       cudaError_t e = cudaMemcpyAsync(a.G, Gm, sizeof(double) * d * d, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return e;
@@ -361,6 +391,7 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
       CK_B(L->dtrmm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, di, ni, &one, a.G,
                     di, a.dW, di, a.Mb, di));
     }
+    if (use_eig || n >= d) {
     // top-r left singular vectors of M from eig(M M^T)
     {
       ProfScope ps_("cmc_mmt", st);
@@ -385,6 +416,7 @@ cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* Gall, cudaStrea
         CK_B(L->dtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, di, r, &one,
                       a.G, di, a.L1t, di));
       }
+    }
     }
     {
       const int64_t cnt = d * r + (int64_t)r * n;

@@ -98,7 +98,8 @@ struct Params {
   long long ld_ref;
   double* partials;            // loss: [n_units][2] (one per CTA of the pair)
   uint16_t* gsign;             // loss (optional, N1): bf16 sign(yq - yref) [T x n], 0 on padding rows
-  float* apart;                // alpha: [T][2 * num_n] per-row partials
+  float* apart;                // alpha: [T][apart_ld] per-row partials, this pass at apart_off
+  int apart_ld, apart_off;
   const uint8_t* ids;          // fwd with fwd_loss: modality id per row (text rows feed the loss)
   int fwd_loss;                // fwd: sum |y - yref| over text rows into partials[unit][rank]
   int skip_m0;                 // loss: skip the text units (their loss comes from the forward)
@@ -525,7 +526,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
         if (MODE == kModeAlphaI8) part *= dxr;                      // the row step e_t
-        if (row < p.T) p.apart[(size_t)row * (2 * p.num_n) + 2 * w.nt + (ew >> 2)] = part;
+        if (row < p.T) p.apart[(size_t)row * p.apart_ld + p.apart_off + 2 * w.nt + (ew >> 2)] = part;
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -688,6 +689,8 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.partials = g.partials;
   p.gsign = g.gsign;
   p.apart = g.apart;
+  p.apart_ld = g.apart_ld > 0 ? g.apart_ld : 2 * p.num_n;
+  p.apart_off = g.apart_off;
   p.ids = g.ids;
   p.fwd_loss = g.fwd_loss;
   p.skip_m0 = g.skip_m0;

@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
                                                        const float* __restrict__ dx, const float* __restrict__ inv,
                                                        int64_t Tg, int64_t d, float qa, uint16_t* __restrict__ planes,
                                                        int32_t* __restrict__ ktkey, int8_t* __restrict__ dq,
-                                                       float* __restrict__ de) {
+                                                       float* __restrict__ de, int8_t* __restrict__ dq2,
+                                                       float* __restrict__ de2) {
   const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= Tg) return;
@@ -291,13 +292,21 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
   uint16_t* pd = planes + p * d;
   uint16_t* px = planes + (Tg + p) * d;
   // |D| <= Delta_t / 2 (a rounding residual), so D / (Delta_t / 254) fits int8: the alpha GEMM's
-  // operand (int8 tensor path), scale e_t = Delta_t / 254
+  // operand (int8 tensor path), scale e_t = Delta_t / 254.  Its rounding residual (<= e_t / 2) is
+  // quantized again on e_t / 254 and contracted by a second pass of the same GEMM, so D enters
+  // alpha_t to 1/254^2 of its range (one level alone is 1/254: ~1e-3 of the gradient when a
+  // modality has a single token, whose alpha lands on one channel undiluted)
   const float estep = __fdiv_rn(dxv, 254.0f);
   const float einv = dxv > 0.f ? __fdiv_rn(254.0f, dxv) : 0.f;
-  if (lane == 0) de[p] = estep;
+  const float estep2 = __fdiv_rn(estep, 254.0f);
+  const float einv2 = estep2 > 0.f ? __fdiv_rn(1.0f, estep2) : 0.f;
+  if (lane == 0) {
+    de[p] = estep;
+    de2[p] = estep2;
+  }
   for (int64_t c = (int64_t)lane * 8; c < d; c += 256) {
     uint4 xv = make_uint4(0, 0, 0, 0), dv = make_uint4(0, 0, 0, 0);
-    uint2 qd = make_uint2(0, 0);
+    uint2 qd = make_uint2(0, 0), qd2 = make_uint2(0, 0);
     if (src >= 0) {
       xv = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)src * ld_x + c));
       const uint2 q8 = __ldg(reinterpret_cast<const uint2*>(qx + p * d + c));
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
       const float iv[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
       const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
       const uint32_t qw[2] = {q8.x, q8.y};
-      uint32_t o[4], qb[2] = {0u, 0u};
+      uint32_t o[4], qb[2] = {0u, 0u}, qb2[2] = {0u, 0u};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         uint16_t h[2];
@@ -321,6 +330,9 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
           h[k] = __bfloat16_as_ushort(__float2bfloat16_rn(dd));
           const int qi = max(-127, min(127, __float2int_rn(dd * einv)));
           qb[idx >> 2] |= ((uint32_t)qi & 0xFFu) << (8 * (idx & 3));
+          const float rr = fmaf(-(float)qi, estep, dd);             // second level: the residual
+          const int q2 = max(-127, min(127, __float2int_rn(rr * einv2)));
+          qb2[idx >> 2] |= ((uint32_t)q2 & 0xFFu) << (8 * (idx & 3));
           const uint32_t ab = __float_as_uint(xs) & 0x7FFFFFFFu;
           if (ab > best) { best = ab; bidx = (int)(c + idx); }
         }
@@ -328,10 +340,12 @@ __global__ void __launch_bounds__(256) gradprep_kernel(const uint16_t* __restric
       }
       dv = make_uint4(o[0], o[1], o[2], o[3]);
       qd = make_uint2(qb[0], qb[1]);
+      qd2 = make_uint2(qb2[0], qb2[1]);
     }
     *reinterpret_cast<uint4*>(pd + c) = dv;
     *reinterpret_cast<uint4*>(px + c) = xv;
     *reinterpret_cast<uint2*>(dq + p * d + c) = qd;
+    *reinterpret_cast<uint2*>(dq2 + p * d + c) = qd2;
   }
   // first arg-max over the row: larger |xs| wins, ties -> smaller index
 #pragma unroll
@@ -494,10 +508,12 @@ cudaError_t launch_keep_best(const double* loss, double* best, const float* s, f
 
 cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
                             const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d, int abits,
-                            uint16_t* planes, int32_t* ktkey, int8_t* dq, float* de, cudaStream_t st) {
+                            uint16_t* planes, int32_t* ktkey, int8_t* dq, float* de, int8_t* dq2, float* de2,
+                            cudaStream_t st) {
   ProfScope ps_("gradprep", st);
   gradprep_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(X, ld_x, mod_id, perm, qx, dx, inv, Tg, d,
-                                                             (float)((1 << (abits - 1)) - 1), planes, ktkey, dq, de);
+                                                             (float)((1 << (abits - 1)) - 1), planes, ktkey, dq, de,
+                                                             dq2, de2);
   return cudaGetLastError();
 }
 

@@ -28,15 +28,16 @@ inline int64_t rpad_of(int64_t r) { return r > 0 ? ceil_div(r, 64) * 64 : 0; }
 struct WsLayout {
   size_t status = 0, inv_s = 0, qx = 0, dx = 0, mask = 0, z = 0, l1t = 0, l2t = 0, xsplit = 0;
   size_t qw_all = 0, dw_all = 0, amax = 0, partials = 0, wt = 0, perm = 0, tile_mod = 0, cnt = 0, total = 0;
-  size_t gsign = 0, planes = 0, gpartial = 0;
+  size_t gsign = 0, planes = 0, gpartial = 0, yref = 0;
   // N1 scale terms
-  size_t dq = 0, de = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0, skeys = 0, svals = 0,
+  size_t dq = 0, de = 0, dq2 = 0, de2 = 0, apart = 0, bpart = 0, kj = 0, keys = 0, vals = 0, bucket = 0, skeys = 0, svals = 0,
          stemp = 0, stemp_bytes = 0;
   // N2 CMC factors (f64)
-  size_t a64 = 0, g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
+  size_t g = 0, c = 0, lam = 0, sig2 = 0, sq = 0, isq = 0, dw64 = 0, m64 = 0, l1t64 = 0, urs = 0, l2t64 = 0,
          work = 0, info = 0, dot = 0;
   size_t lwork = 0;   // doubles
   size_t gall = 0;    // CMC: the (n_mod-1) Gram matrices of the one-call path
+  size_t gram_part = 0;   // CMC: fp32 partial Gram tiles (gram.cu)
   // N3 decode
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
@@ -159,8 +160,10 @@ struct GemmArgs {
   double* partials;                // [n_mod][tiles][4]
   uint16_t* gsign;                 // loss, optional (N1): bf16 sign(yq - yref), grouped rows [T x n]
   // kModeAlpha (N1): acc = D . codes_m^T (bf16 codes of Q(S_m W), K-major [n_mod*n x d]);
-  // apart[row][2*nt + half] = sum_j gsign[row][j] * dw_m[j] * acc[row][j] over the CTA's columns
+  // apart[row * apart_ld + apart_off + 2*nt + half] = sum_j gsign[row][j] * dw_m[j] * acc[row][j]
+  // over the CTA's columns (two passes: D's int8 codes and their residual's)
   float* apart;
+  int apart_ld = 0, apart_off = 0;
   // fused layer call: the forward also sums the text rows' loss (|y - yref|, text rows only:
   // their forward output is the loss's quantized output) into partials, and the loss GEMM then
   // skips the text units
@@ -176,7 +179,8 @@ int gemm_epilogue_warps();
 // ktkey[Tg]: m*d + (first arg-max_i |xs_ti|) of every grouped row (-1: padding / floored scale)
 cudaError_t launch_gradprep(const uint16_t* X, int64_t ld_x, const uint8_t* mod_id, const int32_t* perm,
                             const int8_t* qx, const float* dx, const float* inv, int64_t Tg, int64_t d, int abits,
-                            uint16_t* planes, int32_t* ktkey, int8_t* dq, float* de, cudaStream_t st);
+                            uint16_t* planes, int32_t* ktkey, int8_t* dq, float* de, int8_t* dq2, float* de2,
+                            cudaStream_t st);
 // partial[m][jt][i] (sum_j of the direct terms), bpart[m][4*it + q][j] (beta_j over 32 rows i),
 // kj[m][j] = min i with |f32(s_i w_ij)| == colmax[m][j] (atomicMin; preset to INT_MAX)
 cudaError_t launch_gradgemm(const uint16_t* planes, int64_t Tg, const uint16_t* gsign, const int8_t* qw_all,
@@ -224,14 +228,29 @@ struct CmcArgs {
   void* L2;                      // [(M-1) x r x n]
   masq_dtype lt;
   double* resid;                 // optional [(M-1)]
-  double *A64, *G, *C, *lam, *sig2, *sq, *isq, *dW, *Mb, *L1t, *Urs, *L2t, *work, *dot;
+  double *G, *C, *lam, *sig2, *sq, *isq, *dW, *Mb, *L1t, *Urs, *L2t, *work, *dot;
   int* info;
   size_t lwork;
+  // tensor-core Gram (gram.cu)
+  int32_t* perm;
+  uint32_t* tile_mod;
+  int64_t* cnt;
+  uint16_t* planes;
+  float* gram_part;
 };
 bool cmc_linalg_available();
-size_t cmc_syevd_lwork(int64_t d);
+size_t cmc_syevd_lwork(int64_t d, int64_t n);
+bool cmc_eig_route();
 int cmc_dot_blocks();
 cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStream_t st);
+// G[m-1] (+)= A_m^T A_m for m = 1..n_mod-1 on the tensor cores (split-bf16, fp32 partial tiles
+// over token chunks, f64 fixed-order reduction; both triangles written); perm / tile_mod from
+// launch_route, inv = 1/s, planes [2][Tg][d] bf16 and part (cmc_gram_part_bytes) scratch
+size_t cmc_gram_part_bytes(int64_t T, int64_t d, int n_mod);
+cudaError_t launch_cmc_gram_tc(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T,
+                               int64_t d, int n_mod, const float* inv, const int32_t* perm,
+                               const uint32_t* tile_mod, uint16_t* planes, float* part, double* G, int accumulate,
+                               cudaStream_t st);
 cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* G, cudaStream_t st);
 
 // ---------------------------------------------------------------- N3 int4 decode (decode.cu)

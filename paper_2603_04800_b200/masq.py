@@ -14,6 +14,7 @@ from ._lib import MasqDebug, lib
 MASQ_F32, MASQ_BF16 = 0, 1
 (OP_STATS, OP_INIT, OP_QWEIGHT, OP_QACT, OP_FORWARD, OP_LOSS, OP_REFERENCE, OP_LOSS_GRAD, OP_MEANABS,
  OP_CMC, OP_DECODE, OP_LAYER, OP_CMC_GRAM, OP_CMC_FACTORS) = range(14)
+OP_SELF_REF = 0x100
 
 
 class MasqError(RuntimeError):
@@ -61,7 +62,14 @@ class Workspace:
     def get(self, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 256)
         if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.zeros(nbytes + 256, dtype=torch.uint8, device=self.device)
+            new = torch.zeros(nbytes + 256, dtype=torch.uint8, device=self.device)
+            if self.buf is not None:
+                # kernels queued on any stream may still use the old block and its sticky status
+                # word: wait for them, then carry the status (at the 256-aligned base) across
+                torch.cuda.synchronize(self.device)
+                o_old, o_new = (-self.buf.data_ptr()) % 256, (-new.data_ptr()) % 256
+                new[o_new:o_new + 16].copy_(self.buf[o_old:o_old + 16])
+            self.buf = new
         return self.buf
 
     def ptr_size(self, nbytes: int):
@@ -149,11 +157,12 @@ def quantize_activations(X, mod_id, s, abits: int, ws=None, stream=None):
 
 # ----------------------------------------------------------------------------- A4-A7
 def linear_forward(X, mod_id, s, qw, dw, wbits: int, abits: int, L1=None, L2=None, Y=None,
-                   acc_debug: bool = False, ws=None, stream=None):
+                   acc_debug: bool = False, taps: bool = False, ws=None, stream=None):
     """Y = Q(X_m S_m^-1) Q(S_t W) [+ X_m S_m^-1 L1^m L2^m for m != text].
 
     L1: bf16 [n_mod-1, d, r]; L2: bf16 [n_mod-1, r, d_out] (or a column view with a row stride).
     acc_debug=True returns the raw int32 accumulators instead (CMC skipped).
+    taps=True returns (out, qx, dx): the activation codes / steps the call used (debug taps).
     """
     T, d = X.shape
     d_out = qw.shape[0]
@@ -161,20 +170,27 @@ def linear_forward(X, mod_id, s, qw, dw, wbits: int, abits: int, L1=None, L2=Non
     r = 0 if L1 is None else int(L1.shape[-1])
     ld_l2 = 0 if L2 is None else int(L2.stride(-2))
     dbg = None
+    qx = dx = None
+    if taps:
+        qx = torch.empty(T, d, dtype=torch.int8, device=X.device)
+        dx = torch.empty(T, dtype=torch.float32, device=X.device)
     if acc_debug:
         out = torch.empty(T, d_out, dtype=torch.int32, device=X.device)
-        dbg = MasqDebug(out.data_ptr(), out.stride(0))
+        dbg = MasqDebug(out.data_ptr(), out.stride(0), None if qx is None else qx.data_ptr(),
+                        None if dx is None else dx.data_ptr())
         Yp, ldy = None, d_out
     else:
         out = torch.empty(T, d_out, dtype=torch.float32, device=X.device) if Y is None else Y
         Yp, ldy = _p(out), out.stride(0)
+        if taps:
+            dbg = MasqDebug(None, 0, qx.data_ptr(), dx.data_ptr())
     ws = ws or default_workspace(X.device)
     p, n = ws.ptr_size(workspace_size(OP_FORWARD, T, d, d_out, n_mod, r if not acc_debug else 0))
     _ck(lib().masq_linear_forward(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod,
                                   _p(s.contiguous()), _p(qw), _p(dw), wbits, abits, _p(L1), _p(L2), ld_l2, r,
                                   Yp, ldy, p, n, ctypes.byref(dbg) if dbg is not None else None,
                                   _stream(stream)), "masq_linear_forward")
-    return out
+    return (out, qx, dx) if taps else out
 
 
 # ----------------------------------------------------------------------------- A8
@@ -196,10 +212,11 @@ def _lambda_arr(lam, n_mod):
     return arr
 
 
-def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, sums=None, counts=None, loss=None,
+def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref=None, lam=None, sums=None, counts=None, loss=None,
                ws=None, stream=None):
     """Per-modality sums of |Q(X_m S_m^-1) Q(S_m W) - X_m W|, counts and the weighted MAE loss
-    (PAPER.md:62-70).  Returns device tensors (sums f64 [M], counts i64 [M], loss f64 [1])."""
+    (PAPER.md:62-70).  Returns device tensors (sums f64 [M], counts i64 [M], loss f64 [1]).
+    Yref None: the library computes the target X W itself (workspace OP_LOSS | OP_SELF_REF)."""
     T, d = X.shape
     d_out = W.shape[1]
     n_mod = s.shape[0]
@@ -208,12 +225,12 @@ def calib_loss(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, sums=Non
     counts = torch.empty(n_mod, dtype=torch.int64, device=dev) if counts is None else counts
     loss = torch.empty(1, dtype=torch.float64, device=dev) if loss is None else loss
     ws = ws or default_workspace(dev)
-    p, n = ws.ptr_size(workspace_size(OP_LOSS, T, d, d_out, n_mod))
+    p, n = ws.ptr_size(workspace_size(OP_LOSS | (OP_SELF_REF if Yref is None else 0), T, d, d_out, n_mod))
     lam_arr = _lambda_arr(lam, n_mod)
     _ck(lib().masq_calib_loss(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod, _p(s.contiguous()),
                               _p(W.contiguous()), _dt(W), wbits, abits,
                               ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr is not None else None,
-                              _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), p, n, _stream(stream)),
+                              _p(Yref), 0 if Yref is None else Yref.stride(0), _p(sums), _p(counts), _p(loss), p, n, _stream(stream)),
         "masq_calib_loss")
     return sums, counts, loss
 
@@ -244,7 +261,7 @@ def calib_layer(X, mod_id, s, W, wbits: int, abits: int, L1=None, L2=None, lam=N
     return Y, Yref, sums, counts, loss
 
 
-def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, grad=None, sums=None, counts=None,
+def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref=None, lam=None, grad=None, sums=None, counts=None,
                     loss=None, count_norm=None, ws=None, stream=None):
     """N1: (sums, counts, loss, grad) with grad = dL/d ln s (straight-through), f64 [M x d].
 
@@ -259,12 +276,13 @@ def calib_loss_grad(X, mod_id, s, W, wbits: int, abits: int, Yref, lam=None, gra
     loss = torch.empty(1, dtype=torch.float64, device=dev) if loss is None else loss
     grad = torch.empty(n_mod, d, dtype=torch.float64, device=dev) if grad is None else grad
     ws = ws or default_workspace(dev)
-    p, n = ws.ptr_size(workspace_size(OP_LOSS_GRAD, T, d, d_out, n_mod))
+    p, n = ws.ptr_size(workspace_size(OP_LOSS_GRAD | (OP_SELF_REF if Yref is None else 0), T, d, d_out, n_mod))
     lam_arr = _lambda_arr(lam, n_mod)
     _ck(lib().masq_calib_loss_grad(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, d_out, n_mod, _p(s.contiguous()),
                                    _p(W.contiguous()), _dt(W), wbits, abits,
                                    ctypes.cast(lam_arr, ctypes.c_void_p) if lam_arr is not None else None,
-                                   _p(Yref), Yref.stride(0), _p(sums), _p(counts), _p(loss), _p(grad),
+                                   _p(Yref), 0 if Yref is None else Yref.stride(0), _p(sums), _p(counts),
+                                   _p(loss), _p(grad),
                                    _p(count_norm), p, n, _stream(stream)), "masq_calib_loss_grad")
     return sums, counts, loss, grad
 

@@ -92,7 +92,8 @@ def test_every_workspace_op_has_a_layout(so):
     from paper_2603_04800_b200._lib import lib
     L = lib()
     src = open(HEADER).read()
-    ops = {k: int(v) for k, v in re.findall(r"\b(MASQ_OP_[A-Z_]+)\s*=\s*(\d+)", src)}
+    ops = {k: int(v, 0) for k, v in re.findall(r"\b(MASQ_OP_[A-Z_]+)\s*=\s*(0x[0-9a-fA-F]+|\d+)", src)}
+    flag = ops.pop("MASQ_OP_SELF_REF")
     assert len(ops) >= 14
     T, d, n, M, r = 4096, 1024, 2048, 2, 64
     stateless = {"MASQ_OP_STATS", "MASQ_OP_INIT", "MASQ_OP_REFERENCE"}   # only the status word
@@ -105,3 +106,7 @@ def test_every_workspace_op_has_a_layout(so):
             assert size >= 256, name
         else:
             assert size > 4096, (name, size)
+    # the self-reference flag appends the loss target X W (f32 [T x n]) to the loss layouts
+    for name in ("MASQ_OP_LOSS", "MASQ_OP_LOSS_GRAD"):
+        base = L.masq_workspace_size(ops[name], T, d, n, M, 0)
+        assert L.masq_workspace_size(ops[name] | flag, T, d, n, M, 0) >= base + 4 * T * n

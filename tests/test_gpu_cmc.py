@@ -2,8 +2,15 @@
 oracle.cmc_layer_factors (Theorem 2).
 
 L1 and L2 are unique only up to the sign of each singular pair, so the product L1 L2 is
-compared in the norm Theorem 2 is stated in: ||A (P_gpu - P_oracle)||_F <= 1e-6 ||A dW||_F
+compared in the norm Theorem 2 is stated in: ||A (P_gpu - P_oracle)||_F <= TOL_P ||A dW||_F
 (f32 outputs), and the optional residual against the oracle's reconstruction loss.
+
+Reading Q29: the Gram A^T A is accumulated on the tensor cores from a split-bf16
+representation of A (each value to 2^-17, all four hi/lo products, fp32 accumulation over token
+chunks, f64 across chunks), so G carries ~1e-6 relative error (CPU emulation of the same
+arithmetic: 2e-7..3e-6 max-normalised; L1 L2 moves by 2e-7..7e-7 in the A-norm; the residual
+<E, G E> evaluated with that G by <= 1.2e-7 ||A dW||^2).  Bars: G 1e-4 (max-normalised), L1 L2
+1e-4 in the A-norm, residual 1e-6 ||A dW||^2 — all inside north_star's 1e-3 float bar.
 """
 import numpy as np
 import pytest
@@ -14,6 +21,9 @@ import synth
 from test_gpu_parity import M, bf, tt
 
 pytestmark = pytest.mark.gpu
+
+TOL_P = 1e-4
+TOL_G = 1e-4
 
 
 def _case(T=2048, d=128, n=192, shuffle=False):
@@ -41,7 +51,7 @@ def test_cmc_factors_parity(kw, r, eps):
         Pg = L1[k].double().cpu().numpy() @ L2[k].double().cpu().numpy()
         Po = L1o[k] @ L2o[k]
         base = np.linalg.norm(A @ dW)
-        assert np.linalg.norm(A @ (Pg - Po)) <= 1e-6 * base
+        assert np.linalg.norm(A @ (Pg - Po)) <= TOL_P * base
         assert abs(float(resid[k]) - lo[k]) <= 1e-6 * base ** 2
         n1, n2 = O.naive_svd_factors(dW, r)
         assert float(resid[k]) <= O.reconstruction_loss(A, dW, n1, n2)
@@ -107,9 +117,58 @@ def test_cmc_two_phase_sharded_equals_one_call():
         base = np.linalg.norm(A @ dW)
         a = L1[k].double().cpu().numpy() @ L2[k].double().cpu().numpy()
         b = P1[k].double().cpu().numpy() @ P2[k].double().cpu().numpy()
-        assert np.linalg.norm(A @ (a - b)) <= 1e-6 * base
-        Gk = np.triu(G[k].cpu().numpy())                         # column-major lower = row-major upper
-        Gk = Gk + np.triu(Gk, 1).T
+        assert np.linalg.norm(A @ (a - b)) <= TOL_P * base
+        Gk = G[k].cpu().numpy()                                  # full symmetric, exactly
+        assert np.array_equal(Gk, Gk.T)
         Go = A.T @ A
-        assert np.abs(Gk - Go).max() <= 1e-10 * np.abs(Go).max()
+        assert np.abs(Gk - Go).max() <= TOL_G * np.abs(Go).max()
         assert abs(float(res2[k]) - float(res1[k])) <= 1e-6 * base ** 2
+
+
+def test_cmc_gram_deterministic_and_accumulates():
+    """The tensor-core Gram is bit-reproducible (fixed-order chunk reduction) and accumulate=1 adds
+    onto the caller's matrix."""
+    m = M()
+    c = _case(T=3000, d=272, n=96)
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 3)
+    s = tt(O.init_factors(R, cnt, c["W"]))
+    X, ids = bf(c["X"]), tt(c["ids"])
+    G1 = m.cmc_gram(X, ids, s)
+    G2 = m.cmc_gram(X, ids, s)
+    assert torch.equal(G1, G2)
+    G3 = m.cmc_gram(X, ids, s, G=G1.clone(), accumulate=True)
+    assert torch.equal(G3, G1 + G2)
+
+
+@pytest.mark.parametrize("name,d,n,r", [("qkv", 3584, 4608, 64), ("down", 18944, 3584, 64)])
+def test_cmc_factors_at_c3_shapes(name, d, n, r):
+    """N2 at the c3 layer's shapes on a 4096-token calibration batch (3072 image tokens):
+    qkv 3584 -> 4608 (d <= n: Cholesky route) against the paper-route oracle, and the down
+    projection 18944 -> 3584 (n < d: the n x n route) against oracle.cmc_factors_small_side
+    (the paper route's d x d eigensolve is out of reach for the CPU there; the two routes are
+    pinned equal in tests/test_oracle_pins.py)."""
+    m = M()
+    c = synth.config_inputs("c3", d=d, n=n, T=4096, r=0, layer=7)
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 2)
+    s = O.init_factors(R, cnt, c["W"])
+    X, W, ids = bf(c["X"]), bf(c["W"]), tt(c["ids"])
+    qw, dw = m.quantize_weight(W, tt(s[0]), 4)
+    L1, L2, resid = m.cmc_factors(X, ids, tt(s), W, qw, dw, r, dtype=torch.float32)
+    m.check()
+    L1 = L1[0].double().cpu().numpy()
+    L2 = L2[0].double().cpu().numpy()
+    torch.cuda.empty_cache()
+    xs = O.smooth_activations(O.decode(c["X"]), c["ids"], s)
+    A = xs[c["ids"] == 1].astype(np.float64)
+    qwo, dwo = O.quantize_weight(c["W"], s[0], 4)
+    dW = O.weight_residual(c["W"], s[1], qwo, dwo)
+    if d <= n:
+        L1o, L2o = O.cmc_factors(A, dW, r)
+    else:
+        L1o, L2o = O.cmc_factors_small_side(A, dW, r)
+    AdW = A @ dW
+    base = np.linalg.norm(AdW)
+    err = np.linalg.norm(A @ (L1 @ L2) - (A @ L1o) @ L2o) / base
+    assert err <= TOL_P, err
+    lo = float(np.sum((AdW - (A @ L1o) @ L2o) ** 2))
+    assert abs(float(resid[0]) - lo) <= 1e-6 * base ** 2, (float(resid[0]), lo)

@@ -2,9 +2,10 @@
 of the calibration loss w.r.t. ln s (masq_calib_loss_grad) and the log-space Adam update
 (masq_adam_step) — against oracle.calib_loss_grad / oracle.adam_step on the same inputs.
 
-Bar: the loss within 1e-3 relative (as A8); the gradient within 2e-3 max-abs-normalised per
-modality (sign(E) may differ where E rounds to ~0 in f32 vs f64 and the P/Q
-contractions accumulate in fp32 over the tokens); Adam to f64 rounding.
+Bar: the loss within 1e-3 relative (as A8); the gradient within 1e-3 max-abs-normalised per
+modality (north_star's float bar; measured 1e-7 .. 4e-4, DESIGN.md §10 — sign(E) may differ
+where E rounds to ~0 in f32 vs f64 and the P/Q contractions accumulate in fp32 over the
+tokens); Adam to f64 rounding.
 """
 import numpy as np
 import pytest
@@ -15,7 +16,7 @@ from test_gpu_parity import M, bf, case, oracle_state, tt
 
 pytestmark = pytest.mark.gpu
 
-TOL_G = 2e-3
+TOL_G = 1e-3
 
 
 def _grad_err(g, go):
@@ -104,9 +105,10 @@ def test_adam_step_parity_trajectory():
         assert np.allclose(m1.cpu().numpy(), m1_o, rtol=1e-12, atol=1e-12 * np.abs(m1_o).max())
         assert np.allclose(m2.cpu().numpy(), m2_o, rtol=1e-12, atol=1e-12 * np.abs(m2_o).max())
         assert np.allclose(s_cur.cpu().numpy(), np.exp(th_o).astype(np.float32), rtol=2e-7)
-    # No descent assertion: a uniform rescale of s^m is an exact invariance of the per-token /
-    # per-channel absmax quantizers, but not of the straight-through surrogate, and Adam's
-    # sign-like first steps move mostly along it (Q24) — the loss stays ~flat.
+    # Descent over 5 steps at lr 1e-2 is not asserted here (a short trajectory can step over a
+    # minimum); the driver test below asserts it over 2 epochs.  With the scale terms of reading
+    # Q24 the uniform rescale of s^m — an exact invariance of the loss — is a null direction of
+    # the gradient (oracle pin), so Adam does not drift along it.
 
 
 def test_loss_grad_token_shards_sum_to_batch():

@@ -600,6 +600,23 @@ def test_cmc_factors_theorem2():
     assert np.abs(Lstar - L1 @ L2).max() <= 1e-8 * np.abs(Lstar).max()
 
 
+@pytest.mark.parametrize("T_,d,n,r,eps", [(300, 40, 24, 6, 1e-8), (300, 40, 24, 6, 0.0), (60, 48, 20, 5, 1e-8),
+                                           (200, 20, 28, 4, 1e-8)])
+def test_cmc_small_side_equals_paper_route(T_, d, n, r, eps):
+    """The n x n evaluation of eq:l1l2 (oracle.cmc_factors_small_side, used where the paper's d x d
+    eigensolve is out of reach: d = 18944) gives the paper route's L1 L2 and loss — for d > n,
+    d < n, a rank-deficient Gram (T < d, regularised) and eps = 0."""
+    g = np.random.Generator(np.random.PCG64(91 + T_ + d))
+    A = _aniso(g, T_, d)
+    dW = g.normal(size=(d, n))
+    L1, L2 = O.cmc_factors(A, dW, r, eps)
+    S1, S2 = O.cmc_factors_small_side(A, dW, r, eps)
+    base = np.linalg.norm(A @ dW)
+    assert np.linalg.norm(A @ (L1 @ L2 - S1 @ S2)) <= 1e-9 * base
+    assert abs(O.reconstruction_loss(A, dW, L1, L2) - O.reconstruction_loss(A, dW, S1, S2)) <= 1e-10 * base ** 2
+    assert np.allclose(np.abs(L2), np.abs(S2), rtol=1e-6, atol=1e-9 * np.abs(L2).max())   # Sigma_r V_r^T up to sign
+
+
 def test_cmc_isotropic_and_effective_rank():
     """isotropic activations -> whitened and naive losses agree; fig:effective_rank
     (SPEC.md:418): on anisotropic activations T dW has a lower effective rank than dW in >= 9 of
