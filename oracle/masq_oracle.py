@@ -598,3 +598,32 @@ def linear_decode(X, s_t, codes, delta, abits: int, group: int) -> np.ndarray:
     n, d = codes.shape
     What = (np.asarray(codes, F64).reshape(n, d // group, group) * np.asarray(delta, F64)[:, :, None]).reshape(n, d)
     return dequantize_rows(qx, dx) @ What.T
+
+
+def linear_forward_grouped(X, ids, s, codes, delta, abits: int, group: int, L1=None, L2=None, rows=None):
+    """N3 prefill — the routed forward of PAPER.md:177-185 with the group-quantized base weight
+    Q_g(S_t W) (codes int [n x d] K-major, delta [n x d/group] from quantize_weight_grouped with s[0];
+    reading Q28) for ANY token count and every modality:
+        Y_t = Q(x_t S_m^-1) . Q_g(S_t W)                                 m = text
+        Y_t = Q(x_t S_m^-1) . Q_g(S_t W) + x_t S_m^-1 . L1^m L2^m         m != text
+    f64 of the dequantized values (per-token activation scales, per-(channel, group) weight
+    scales).  rows: optional token subset.  With all tokens text and no CMC it is linear_decode;
+    with group = d it is linear_forward with the O3 weight (pinned in tests/test_oracle_pins.py).
+    Returns f64 [len(rows) x n]."""
+    Xf = decode(X)
+    ids = _check_ids(ids, np.asarray(s).shape[0])
+    if rows is not None:
+        rows = np.asarray(rows, np.int64)
+        Xf, ids = Xf[rows], ids[rows]
+    xs = smooth_activations(Xf, ids, s)
+    qx, dx = quantize_rows(xs, abits)
+    n, d = np.asarray(codes).shape
+    What = (np.asarray(codes, F64).reshape(n, d // group, group) * np.asarray(delta, F64)[:, :, None]).reshape(n, d)
+    Y = dequantize_rows(qx, dx) @ What.T
+    if L1 is not None and L2 is not None:
+        for m in range(1, np.asarray(s).shape[0]):
+            sel = np.nonzero(ids == m)[0]
+            if sel.size:
+                Y[sel] += cmc_term(xs[sel], L1[m - 1], L2[m - 1])
+    return Y
+

@@ -688,6 +688,45 @@ def test_linear_decode_brute_force():
     assert np.allclose(Y, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
 
 
+def test_linear_forward_grouped_pins():
+    """N3 prefill oracle: (1) group = d reduces to O3/O6 — the grouped codes / scales equal
+    quantize_weight's bit for bit and the output equals linear_forward's (with CMC) to f64 rounding;
+    (2) all-text tokens without CMC equal linear_decode; (3) a per-element loop over groups with
+    integer partial sums on a tiny 3-modality case (CMC included as its own term)."""
+    c = synth.config_inputs("c2", T=1024, d=256, n=96, r=16)
+    R, cnt = O.calibrate_stats(c["X"], c["ids"], 3)
+    s = O.init_factors(R, cnt, c["W"])
+    qd, dd = O.quantize_weight_grouped(c["W"], s[0], 4, 256)
+    qw, dw = O.quantize_weight(c["W"], s[0], 4)
+    assert np.array_equal(qd, qw) and np.array_equal(dd[:, 0], dw)
+    L1, L2 = list(c["L1"]), list(c["L2"])
+    Yg = O.linear_forward_grouped(c["X"], c["ids"], s, qd, dd, 8, 256, L1, L2)
+    Yf = O.linear_forward(c["X"], c["ids"], s, qw, dw, 8, L1, L2)
+    assert np.allclose(Yg, Yf, rtol=1e-12, atol=1e-12 * np.abs(Yf).max())
+    q, dl = O.quantize_weight_grouped(c["W"], s[0], 4, 128)
+    ids0 = np.zeros_like(c["ids"])
+    Yt = O.linear_forward_grouped(c["X"][:5], ids0[:5], s, q, dl, 8, 128)
+    Yd = O.linear_decode(c["X"][:5], s[0], q, dl, 8, 128)
+    assert np.array_equal(Yt, Yd)
+    rows = np.array([0, 70, 600, 1000])                     # text, image, audio, text
+    Yr = O.linear_forward_grouped(c["X"], c["ids"], s, q, dl, 8, 128, L1, L2, rows=rows)
+    xs = O.smooth_activations(O.decode(c["X"])[rows], c["ids"][rows], s)
+    qa, da = O.quantize_rows(xs, 8)
+    for a, t in enumerate(rows):
+        m = int(c["ids"][t])
+        for j in range(0, 96, 7):
+            acc = 0.0
+            for gg in range(2):
+                sl = slice(gg * 128, (gg + 1) * 128)
+                acc += float(dl[j, gg]) * int(np.dot(qa[a, sl].astype(np.int64), q[j, sl].astype(np.int64)))
+            ref = float(da[a]) * acc
+            if m:
+                l1 = O.decode(c["L1"][m - 1]).astype(np.float64)
+                l2 = O.decode(c["L2"][m - 1]).astype(np.float64)
+                ref += float(xs[a].astype(np.float64) @ l1 @ l2[:, j])
+            assert abs(Yr[a, j] - ref) <= 1e-12 * max(abs(ref), 1.0)
+
+
 def test_cmc_from_gram_equals_from_activations():
     """The Gram route (what token-sharded runs use after a SUM of the shards' Grams) gives the
     same factors and the same Theorem-2 loss; the shards' Grams add up to the batch Gram."""
