@@ -990,9 +990,14 @@ def main():
         "gemm_loss": ("tensor", sum(2.0 * n_nt * e["d"] * e["n"] for e in L), "TOP/s", int8_peak),
         "gemm_ref": ("tensor", ops, "TFLOP/s", bf16_peak),
         "stats": ("hbm", sum(2.0 * T * e["d"] + T for e in L), "GB/s", peaks["hbm"]),
-        "aquant": ("hbm", sum(3.0 * T * e["d"] + 4 * T for e in L), "GB/s", peaks["hbm"]),
+        # X read (2 B) + token-order codes (1 B) + the modality-grouped copy of the non-text rows
+        # (1 B, masq_calib_layer's loss operand) per activation, + the row scales
+        "aquant": ("hbm", sum(3.0 * T * e["d"] + 1.0 * n_nt * e["d"] + 4 * T + 4 * n_nt for e in L), "GB/s",
+                   peaks["hbm"]),
         "gather_rows": ("hbm", sum(2.0 * T * e["d"] for e in L), "GB/s", peaks["hbm"]),
-        "zgemm": ("hbm", sum(2.0 * n_nt * e["d"] + 4.0 * n_nt * 2 * max(r, 64) for e in L), "GB/s", peaks["hbm"]),
+        # X rows of the non-text tokens (2 B) + their Z row: (M-1) modalities x [hi | lo] x rpad bf16
+        "zgemm": ("hbm", sum(2.0 * n_nt * e["d"] + 2.0 * n_nt * (N_MOD - 1) * 2 * (-(-max(r, 1) // 64) * 64)
+                             for e in L), "GB/s", peaks["hbm"]),
         "wcolmax": ("hbm", sum(2.0 * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),      # one W read, N_MOD sets
         "wquant": ("hbm", sum((2.0 + N_MOD) * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),
         "init": ("hbm", sum(2.0 * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),

@@ -22,6 +22,8 @@
  *                                             whitened truncated-SVD CMC factors (Theorem 2)
  *   N3  masq_quantize_weight_int4, masq_unpack_int4, masq_linear_decode
  *                                             int4 weights in 128-channel groups, decode path
+ *       masq_quantize_weight_w4g, masq_linear_forward_w4g
+ *                                             the same weights packed for the prefill tcgen05 GEMM
  *   N4  masq_smooth_factors, masq_calibrate_meanabs, masq_range_stats
  *                                             SmoothQuant / unified / AWQ baselines, dominance
  *
@@ -294,6 +296,28 @@ masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64
                                const float* s_t, const uint8_t* packed, const float* scales, int32_t group,
                                int32_t abits, float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
                                masq_stream stream);
+
+/* Prefill-shaped W4A8 forward with PACKED int4 weights and 128-channel group scales, any T, with
+ * CMC (reading Q28):
+ *   Y[t, j] = dx[t] * sum_g Delta_jg * (qx[t, g-th 128 channels] . code[j, g-th 128 channels])
+ *             (+ (X_t S_m^-1) L1^m L2^m for m_t != text, as masq_linear_forward)
+ * on the tensor cores: the packed nibbles are expanded to int8 in shared memory and every group is
+ * one kind::i8 k-block into its own TMEM accumulator, promoted in f32 with the group's scale.
+ * Weight format (masq_quantize_weight_w4g): packed uint8 [d_out x d/2], K-major: in the 64 bytes of
+ * group g of channel j, byte 16c + i = code[j][128g + 32c + i] & 0xF | (code[j][128g + 32c + 16 + i]
+ * & 0xF) << 4 (two's complement nibbles); scales f32 [d_out x d/128] (Delta_jg = max(max|s_i w_ij|/7,
+ * 1e-12), the A3 quantizer at group granularity).  The codes and scales equal those of
+ * masq_quantize_weight_int4 (the decode format); only the byte order differs.
+ * d % 128 == 0, d_out % 32 == 0, group == 128; workspace masq_workspace_size(MASQ_OP_FORWARD, ...).
+ * masq_debug.acc: int32 sum over the groups of the unscaled group accumulators (CMC skipped). */
+masq_status masq_quantize_weight_w4g(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t d_out,
+                                     int32_t group, uint8_t* packed, float* scales, masq_stream stream);
+masq_status masq_linear_forward_w4g(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id,
+                                    int64_t T, int64_t d, int64_t d_out, int32_t n_mod,
+                                    const float* s, const uint8_t* packed, const float* scales, int32_t group,
+                                    int32_t abits, const void* L1, const void* L2, int64_t ld_l2, int32_t r,
+                                    float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
+                                    const masq_debug* dbg, masq_stream stream);
 
 /* The two phases of masq_cmc_factors, for token-sharded / multi-batch runs: G[(m-1) d d] (+)=
  * A_m^T A_m for every non-text modality m (f64, lower triangle; accumulate != 0 adds to G) —

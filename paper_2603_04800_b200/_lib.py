@@ -51,6 +51,12 @@ SIGNATURES = {
     "masq_unpack_int4": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p]),
     "masq_linear_decode": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p,
                                      c_void_p, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_size_t, c_void_p]),
+    "masq_quantize_weight_w4g": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_int64, c_int32, c_void_p,
+                                           c_void_p, c_void_p]),
+    "masq_linear_forward_w4g": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int32,
+                                          c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                                          c_void_p, c_void_p, c_int64, c_int32,
+                                          c_void_p, c_int64, c_void_p, c_size_t, c_void_p, c_void_p]),
     "masq_cmc_gram": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
                                 c_int32, c_void_p, c_size_t, c_void_p]),
     "masq_cmc_factors_from_gram": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_int32,

@@ -36,7 +36,9 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
         L.perm = take(sizeof(int32_t) * (Tg + route_scratch_ints(T)));
         L.tile_mod = take(sizeof(uint32_t) * (Tg / kUnitM));
         L.cnt = take(sizeof(int64_t) * n_mod);
-        L.planes = take(sizeof(uint16_t) * 2 * (size_t)Tg * d);
+        L.gram_r = take(sizeof(float) * n_mod * d);
+        L.gram_ex = take(sizeof(int32_t) * n_mod * d);
+        L.slices = take(cmc_gram_slice_bytes(T, d, n_mod));
         L.gram_part = take(cmc_gram_part_bytes(T, d, n_mod));
       }
       if (op == MASQ_OP_CMC) L.gall = take(sizeof(double) * (size_t)(n_mod > 1 ? n_mod - 1 : 1) * d * d);
@@ -809,8 +811,11 @@ masq_status cmc_gram_core(const void* X, masq_dtype xt, int64_t ld_x, const uint
   a.perm = reinterpret_cast<int32_t*>(W8(ws, L.perm));
   a.tile_mod = reinterpret_cast<uint32_t*>(W8(ws, L.tile_mod));
   a.cnt = reinterpret_cast<int64_t*>(W8(ws, L.cnt));
-  a.planes = reinterpret_cast<uint16_t*>(W8(ws, L.planes));
-  a.gram_part = reinterpret_cast<float*>(W8(ws, L.gram_part));
+  a.R = reinterpret_cast<float*>(W8(ws, L.gram_r));
+  a.ex = reinterpret_cast<int32_t*>(W8(ws, L.gram_ex));
+  a.slices = reinterpret_cast<int8_t*>(W8(ws, L.slices));
+  a.gram_part = reinterpret_cast<double*>(W8(ws, L.gram_part));
+  a.status = status_of(ws);
   if (T > 0) MASQ_CK(launch_inv(s, (int64_t)n_mod * d, const_cast<float*>(a.inv), st));
   const cudaError_t e = launch_cmc_gram(a, G, accumulate, st);
   if (e == cudaErrorNotSupported) return MASQ_ERR_UNSUPPORTED;
@@ -925,6 +930,89 @@ masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64
   }
   MASQ_CK(launch_decode(qa, dx, (int)T, d, d_out, packed, scales, reinterpret_cast<float*>(W8(ws, L.dpart)), Y,
                         ld_y, st));
+  return MASQ_OK;
+}
+
+masq_status masq_quantize_weight_w4g(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t d_out,
+                                     int32_t group, uint8_t* packed, float* scales, masq_stream stream) {
+  if (!W || !s || !packed || !scales) return MASQ_ERR_NULL;
+  if (group != 128) return MASQ_ERR_UNSUPPORTED;
+  if (d <= 0 || d % 128 != 0 || d_out <= 0 || d_out % 32 != 0 || d >= (1LL << 31) || d_out >= (1LL << 31))
+    return MASQ_ERR_SHAPE;
+  if (wt != MASQ_BF16 && wt != MASQ_F32) return MASQ_ERR_UNSUPPORTED;
+  if (!al16(packed) || !al16(W)) return MASQ_ERR_ALIGN;
+  MASQ_CK(launch_wq4_layout(W, wt, s, d, d_out, packed, scales, 1, S(stream)));
+  return MASQ_OK;
+}
+
+masq_status masq_linear_forward_w4g(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* mod_id, int64_t T,
+                                    int64_t d, int64_t d_out, int32_t n_mod, const float* s, const uint8_t* packed,
+                                    const float* scales, int32_t group, int32_t abits, const void* L1, const void* L2,
+                                    int64_t ld_l2, int32_t r, float* Y, int64_t ld_y, void* ws, size_t ws_bytes,
+                                    const masq_debug* dbg, masq_stream stream) {
+  MASQ_TRY(check_common(T, d, n_mod));
+  MASQ_TRY(check_bits(abits));
+  if (group != 128) return MASQ_ERR_UNSUPPORTED;
+  if (d % 128 != 0 || d_out <= 0 || d_out % 32 != 0 || d_out >= (1LL << 31)) return MASQ_ERR_SHAPE;
+  if (r < 0 || r > 256 || r % 16 != 0) return MASQ_ERR_SHAPE;
+  const bool use_acc = dbg && dbg->acc;
+  if (!s || !packed || !scales || (!Y && !use_acc)) return MASQ_ERR_NULL;
+  const bool cmc = r > 0 && n_mod > 1 && !use_acc;
+  if (cmc) {
+    if (!L1 || !L2) return MASQ_ERR_NULL;
+    if (ld_l2 < d_out || !al16(L1) || !al16(L2) || (ld_l2 % 8) != 0) return MASQ_ERR_ALIGN;
+  }
+  void* out = use_acc ? static_cast<void*>(dbg->acc) : static_cast<void*>(Y);
+  const int64_t ld_out = use_acc ? dbg->ld_acc : ld_y;
+  if (ld_out < d_out || !al16(out) || !al16(packed) || !al16(s)) return MASQ_ERR_ALIGN;
+  if (T == 0) return MASQ_OK;
+  MASQ_TRY(check_x(X, xt, ld_x, d));
+  if (!mod_id) return MASQ_ERR_NULL;
+  const WsLayout L = ws_layout(MASQ_OP_FORWARD, T, d, d_out, n_mod, cmc ? r : 0, xt == MASQ_F32);
+  MASQ_TRY(check_ws(ws, ws_bytes, L));
+  cudaStream_t st = S(stream);
+  float* inv = reinterpret_cast<float*>(W8(ws, L.inv_s));
+  int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
+  float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
+  uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
+  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, mask, status_of(ws), st));
+  if (dbg && dbg->qx) MASQ_CK(cudaMemcpyAsync(dbg->qx, qx, (size_t)T * d, cudaMemcpyDeviceToDevice, st));
+  if (dbg && dbg->dx) MASQ_CK(cudaMemcpyAsync(dbg->dx, dx, sizeof(float) * T, cudaMemcpyDeviceToDevice, st));
+  W4gArgs g{};
+  g.T = T;
+  g.n = d_out;
+  g.d = d;
+  g.qx = qx;
+  g.dx = dx;
+  g.packed = packed;
+  g.scales = scales;
+  g.tile_mask = mask;
+  g.n_mod = n_mod;
+  g.out = out;
+  g.ld_out = ld_out;
+  g.acc_mode = use_acc ? 1 : 0;
+  if (cmc) {
+    const int rp = (int)rpad_of(r);
+    uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
+    uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
+    uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
+    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t, st));
+    MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
+    if (xt == MASQ_BF16) {
+      MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st,
+                           reinterpret_cast<float*>(W8(ws, L.zpart))));
+    } else {
+      uint16_t* xh = reinterpret_cast<uint16_t*>(W8(ws, L.xsplit));
+      uint16_t* xl = xh + (size_t)T * d;
+      MASQ_CK(launch_split_f32(static_cast<const float*>(X), ld_x, T, d, xh, xl, st));
+      MASQ_CK(launch_zgemm(xh, d, xl, mod_id, T, d, n_mod, l1t, rp, mask, z, st,
+                           reinterpret_cast<float*>(W8(ws, L.zpart))));
+    }
+    g.rpad = rp;
+    g.z = z;
+    g.l2t = l2t;
+  }
+  MASQ_CK(launch_w4g_gemm(g, st));
   return MASQ_OK;
 }
 

@@ -3,7 +3,7 @@
 //
 // For every non-text modality m:
 //   A_m = X_m S_m^-1 (the f32 smoothed activations the path computes)
-//   G = A_m^T A_m: tensor-core split-bf16 Gram, f64 chunk reduction (gram.cu), then in f64:
+//   G = A_m^T A_m: exact int8-slice Gram on the tensor cores (gram.cu), then in f64:
 //   eig G = P Lambda P^T (cuSOLVER Dsyevd; MASQ_CMC_EIG=1, else the Cholesky route below)
 //   Lambda' = max(Lambda, 0) + eps_rel * lambda_max (reading Q27)
 //   dW = S_m W - Q(S_t W) (exact in f64, this file's kernel, from the text codes and scales)
@@ -296,7 +296,7 @@ size_t cmc_syevd_lwork(int64_t d, int64_t n) {
 }
 
 // phase 1: G[m-1] (+)= A_m^T A_m for m = 1..n_mod-1 (full symmetric, row-major) on the tensor
-// cores (gram.cu): route the tokens into modality-grouped order, then the split-bf16 Gram
+// cores (gram.cu): route the tokens into modality-grouped order, then the exact int8-slice Gram
 cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStream_t st) {
   const int64_t T = a.T, d = a.d;
   if (T == 0) {
@@ -305,8 +305,8 @@ cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStr
   }
   cudaError_t e = launch_route(a.ids, T, a.n_mod, a.perm, a.tile_mod, a.cnt, st);
   if (e != cudaSuccess) return e;
-  return launch_cmc_gram_tc(a.X, a.xt, a.ld_x, a.ids, T, d, a.n_mod, a.inv, a.perm, a.tile_mod, a.planes,
-                            a.gram_part, G, accumulate, st);
+  return launch_cmc_gram_tc(a.X, a.xt, a.ld_x, a.ids, T, d, a.n_mod, a.inv, a.perm, a.tile_mod, a.R, a.cnt, a.ex,
+                            a.slices, a.gram_part, a.status, G, accumulate, st);
 }
 
 // phase 2: factors (and the Theorem-2 residual <E, G E>) from the Gram matrices

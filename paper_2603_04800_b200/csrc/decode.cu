@@ -68,7 +68,10 @@ __device__ __forceinline__ float ldw<float>(const float* p) { return *p; }
 
 // one CTA = 16 output channels (two 8-column tiles) x one group of 128 input channels;
 // thread k reads row k of the group (16 columns), block max per column, exact codes, packing
-template <typename WT>
+// LAYOUT 0: the decode kernel's fragment order (above); LAYOUT 1: the prefill GEMM's K-major
+// format (w4g.cu): packed[j][g*64 + 16c + i] = code[128g+32c+i] | code[128g+32c+16+i] << 4 (two's
+// complement nibbles), scales[j][g]
+template <typename WT, int LAYOUT>
 __global__ void __launch_bounds__(128) wq4_kernel(const WT* __restrict__ W, const float* __restrict__ s, int64_t d,
                                                   int64_t n, uint8_t* __restrict__ packed,
                                                   float* __restrict__ scales) {
@@ -96,12 +99,30 @@ __global__ void __launch_bounds__(128) wq4_kernel(const WT* __restrict__ W, cons
     const float m = fmaxf(fmaxf(red[0][k], red[1][k]), fmaxf(red[2][k], red[3][k]));
     const float dl = fmaxf(__fdiv_rn(m, 7.0f), 1e-12f);
     dsh[k] = dl;
-    if (j0 + k < n) scales[(((j0 + k) >> 3) * (d / kGroup) + g) * 8 + ((j0 + k) & 7)] = dl;
+    if (j0 + k < n) {
+      if (LAYOUT == 0) scales[(((j0 + k) >> 3) * (d / kGroup) + g) * 8 + ((j0 + k) & 7)] = dl;
+      else scales[(j0 + k) * (d / kGroup) + g] = dl;
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < 16; ++c) codes[c][k] = (int8_t)rha_code(ws[c], dsh[c], -8, 7);
   __syncthreads();
+  if (LAYOUT == 1) {
+    // thread k: channel j0 + (k >> 3), bytes 8 (k & 7) .. + 7 of the group's 64
+    const int c = k >> 3, b0 = (k & 7) * 8;
+    if (j0 + c >= n) return;
+    uint32_t w2[2] = {0u, 0u};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int b = b0 + e, cc = b >> 4, i = b & 15;
+      const uint32_t lo = (uint32_t)codes[c][32 * cc + i] & 0xFu;
+      const uint32_t hi = (uint32_t)codes[c][32 * cc + 16 + i] & 0xFu;
+      w2[e >> 2] |= (lo | (hi << 4)) << (8 * (e & 3));
+    }
+    *reinterpret_cast<uint2*>(packed + (j0 + c) * (d / 2) + (int64_t)g * 64 + b0) = make_uint2(w2[0], w2[1]);
+    return;
+  }
   // 2 tiles x 32 lanes x 4 words: thread k -> tile k >> 6, lane (k >> 1) & 31, words 2 (k & 1) + {0, 1}
   const int tile = k >> 6, L = (k >> 1) & 31, gid = L >> 2, tig = L & 3;
   const int64_t jt = (j0 >> 3) + tile;
@@ -373,15 +394,23 @@ __global__ void decode_combine_kernel(const float* __restrict__ part, int ky, in
 int decode_kchunks(int64_t d) { return (int)ceil_div(d, kKChunk); }
 int decode_max_tokens() { return kMaxDecodeT; }
 
+cudaError_t launch_wq4_layout(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t n, uint8_t* packed,
+                              float* scales, int layout, cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(n, 16), (unsigned)(d / kGroup));
+  ProfScope ps_(layout ? "wq4g" : "wq4", st);
+  if (wt == MASQ_BF16) {
+    if (layout) wq4_kernel<__nv_bfloat16, 1><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(W), s, d, n, packed, scales);
+    else wq4_kernel<__nv_bfloat16, 0><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(W), s, d, n, packed, scales);
+  } else {
+    if (layout) wq4_kernel<float, 1><<<grid, 128, 0, st>>>(static_cast<const float*>(W), s, d, n, packed, scales);
+    else wq4_kernel<float, 0><<<grid, 128, 0, st>>>(static_cast<const float*>(W), s, d, n, packed, scales);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_wq4(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t n, uint8_t* packed,
                        float* scales, cudaStream_t st) {
-  dim3 grid((unsigned)ceil_div(n, 16), (unsigned)(d / kGroup));
-  ProfScope ps_("wq4", st);
-  if (wt == MASQ_BF16)
-    wq4_kernel<<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(W), s, d, n, packed, scales);
-  else
-    wq4_kernel<<<grid, 128, 0, st>>>(static_cast<const float*>(W), s, d, n, packed, scales);
-  return cudaGetLastError();
+  return launch_wq4_layout(W, wt, s, d, n, packed, scales, 0, st);
 }
 
 cudaError_t launch_unpack4(const uint8_t* packed, int64_t d, int64_t n, int8_t* codes, cudaStream_t st) {

@@ -1,20 +1,30 @@
-// gram.cu — N2: the whitening Gram matrices G_m = (X_m S_m^-1)^T (X_m S_m^-1) of the
-// CMC factor construction ("SVD(A^T A)" with A = X_m S_m^-1) on the tensor cores.
+// gram.cu — N2: the whitening Gram matrices G_m = A_m^T A_m, A_m = X_m S_m^-1, of the
+// CMC factor construction ("SVD(A^T A)") on the int8 tensor cores, EXACTLY.
 //
-// A_m is the f32 smoothed activation the path computes (a = x * (1/s_m), IEEE mul).  Each value is
-// split into a bf16 pair a = h + l (h = bf16(a), l = bf16(a - h); |a - h - l| <= 2^-17 |a|), and
-//   G ~= H^T H + H^T L + L^T H + L^T L
-// (all four products: dropping L^T L, <= 2^-18 |a||a'| per term but positive semidefinite, biases
-// the Theorem-2 residual <E, G E> low by ~1e-6 of ||A dW||^2 — measured in a CPU emulation)
-// is accumulated by tcgen05 kind::f16 MMAs in fp32 TMEM with the TOKEN axis as K (both operands
-// MN-major, read from [tokens x d] planes).  Work unit = (modality, 128 x 256 tile of G, token
-// chunk); only tiles on or above the block diagonal are computed (G is symmetric).  Every unit
-// writes its fp32 partial tile; a reduction kernel adds the chunks of a tile in f64 in a fixed
-// order (deterministic), and writes BOTH triangles of the row-major [d x d] G (each unordered
-// pair {i, i'} comes from exactly one tile, so the matrix is exactly symmetric).
+// Why exact: the whitening regulariser is eps * lambda_max with eps = 1e-8 (reading Q27), and a
+// calibration batch often has fewer tokens of a modality than channels (3072 image tokens vs
+// d = 3584 or 18944), so G is rank-deficient and its null-space eigenvalues must stay within
+// ~1e-9 lambda_max of zero for the Cholesky factor of G + eps lambda_max I to exist.  fp32 tensor
+// core accumulation of split-bf16 products leaves them at ~+-1e-6 lambda_max (measured: the
+// factorisation fails); integer accumulation has no rounding at all.
 //
-// Rows are taken in the loss's modality-grouped order (launch_route): modality m's tokens form one
-// contiguous segment of the planes (padding rows zero), so a unit streams contiguous tokens.
+// Representation: per modality and channel i a power-of-two scale 2^e_i with |a_ti| / 2^e_i < 64
+// (e_i from the channel's max |a| = R^m_i * (1/s^m_i), exact: rounding is monotonic), and three
+// int8 slices u = a / 2^e_i = S0 + S1 / 128 + S2 / 128^2 + r, |r| <= 2^-15, every step exact in f32
+// (S0 = rint(u), S1 = rint((u - S0) * 128), S2 = rint(((u - S0) * 128 - S1) * 128); all in
+// [-64, 64]).  So a_hat = 2^e (S0 + S1/128 + S2/128^2) differs from a by <= 2^-20 of the channel's
+// max, and
+//   G_hat_ij = 2^(e_i + e_j) * sum_{k=0..4} 128^-k * sum_{s + s' = k} sum_t S_s[t,i] S_s'[t,j]
+// is the Gram of a_hat computed with no rounding except the final f64 combination (9 kind::i8
+// products into 5 int32 TMEM accumulators, one per level k): positive semidefinite to f64
+// rounding, and within ~1e-7 of G where it matters.
+//
+// Layout: the slices are written TRANSPOSED (channel rows, token columns in the loss's modality-
+// grouped order from launch_route) so both MMA operands are ordinary K-major SWIZZLE_128B tiles
+// with the token axis as K.  Work unit = (modality, 128 x 96 tile of G on or above the block
+// diagonal, token chunk); each unit writes its f64 tile; a reduction adds the chunks in a fixed
+// order (deterministic) and writes BOTH triangles of the row-major [d x d] G (each unordered pair
+// {i, j} comes from exactly one tile, so G is exactly symmetric).
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -25,23 +35,28 @@ using namespace sm100;
 
 namespace {
 constexpr int RT = 192;                       // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
-constexpr int RM = 128, RN = 256, RK = 32;    // i rows, i' columns, tokens per k-block
-constexpr int A_PL = RM * RK * 2;             // 8 KB: one plane of the A tile
-constexpr int B_PL = RN * RK * 2;             // 16 KB: one plane of the B tile
-constexpr int RSTAGE = 2 * A_PL + 2 * B_PL;   // 48 KB (H and L planes of both operands)
-constexpr int RSTAGES = 4;
+constexpr int RM = 128, RN = 96, RK = 128;    // i rows, j columns, tokens per k-block
+constexpr int NSL = 3;                        // int8 slices per value
+constexpr int NLV = 2 * NSL - 1;              // levels k = s + s'
+constexpr int A_SL = RM * RK;                 // 16 KB: one slice of the A tile
+constexpr int B_SL = RN * RK;                 // 12 KB
+constexpr int RSTAGE = NSL * (A_SL + B_SL);   // 84 KB
+constexpr int RSTAGES = 2;
 constexpr int R_SMEM = RSTAGES * RSTAGE + 256;
 constexpr int R_ALLOC = R_SMEM + 1024;
-constexpr uint32_t IDESC_R = idesc_bf16(RM, RN) | (1u << 15) | (1u << 16);   // A and B MN-major
+constexpr uint32_t IDESC_R = idesc_i8(RM, RN);
+static_assert(NLV * RN <= 512, "TMEM columns");
+static_assert(R_ALLOC <= 232448, "shared memory budget");
 
 struct RParams {
   int d, Tg, n_mod;
   const uint32_t* tile_mod;      // modality of every 256-row grouped unit (~0u = empty)
   int n_tm;
-  int nti, ntj, n_tiles;         // tile grid (upper block triangle: it <= 2 jt + 1)
+  int nti, ntj, n_tiles;         // tile grid over the upper block triangle
   int chunk_kb, max_chunks;      // k-blocks per token chunk; chunk slots per (modality, tile)
   int n_units;                   // (n_mod - 1) * n_tiles * max_chunks
-  float* part;                   // [n_units][RN][RM] fp32 partial tiles (column-major in the tile)
+  const int32_t* ex;             // [n_mod][d] channel exponents e_i
+  double* part;                  // [n_units][RN][RM] f64 tiles (column-major in the tile)
 };
 
 __device__ __forceinline__ void seg_of(const RParams& p, int m, int& k0, int& nkb) {
@@ -55,11 +70,15 @@ __device__ __forceinline__ void seg_of(const RParams& p, int m, int& k0, int& nk
   nkb = cnt * (kUnitM / RK);
 }
 
-// tile index -> (it, jt) over the upper block triangle, jt-major
+// tiles of jt-column block: it with 128 it <= 96 jt + 95 (some i <= j inside), jt-major
+__device__ __host__ __forceinline__ int tiles_in_col(int nti, int jt) {
+  const int lim = (RN * jt + RN - 1) / RM + 1;
+  return lim < nti ? lim : nti;
+}
 __device__ __forceinline__ void tile_of(const RParams& p, int t, int& it, int& jt) {
   jt = 0;
   for (;;) {
-    const int cnt = min(p.nti, 2 * jt + 2);
+    const int cnt = tiles_in_col(p.nti, jt);
     if (t < cnt) break;
     t -= cnt;
     ++jt;
@@ -88,20 +107,22 @@ __device__ __forceinline__ Work decode(const RParams& p, int u) {
 }
 
 __global__ void __launch_bounds__(RT, 1)
-cmc_gram_kernel(const __grid_constant__ CUtensorMap tmP, const RParams p) {
+cmc_gram_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const RParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RSTAGES * RSTAGE);
   uint64_t* empty = full + RSTAGES;
-  uint64_t* tfull = empty + RSTAGES;       // [2]
-  uint64_t* tempty = tfull + 2;            // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + RSTAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmP);
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
     for (int i = 0; i < RSTAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tslot, 512);
@@ -123,14 +144,9 @@ cmc_gram_kernel(const __grid_constant__ CUtensorMap tmP, const RParams p) {
           uint8_t* base = smem + st * RSTAGE;
           const int t = w.k0 + kb * RK;
 #pragma unroll
-          for (int pl = 0; pl < 2; ++pl) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              tma_load_2d(base + pl * A_PL + h * (A_PL / 2), &tmP, &full[st], w.it * RM + h * 64, pl * p.Tg + t);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tma_load_2d(base + 2 * A_PL + pl * B_PL + q * (B_PL / 4), &tmP, &full[st], w.jt * RN + q * 64,
-                          pl * p.Tg + t);
+          for (int s = 0; s < NSL; ++s) {
+            tma_load_2d(base + s * A_SL, &tmA, &full[st], t, s * p.d + w.it * RM);
+            tma_load_2d(base + NSL * A_SL + s * B_SL, &tmB, &full[st], t, s * p.d + w.jt * RN);
           }
           if (++st == RSTAGES) { st = 0; ph ^= 1u; }
         }
@@ -144,57 +160,77 @@ cmc_gram_kernel(const __grid_constant__ CUtensorMap tmP, const RParams p) {
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Work w = decode(p, u);
         if (!w.live) continue;
-        const uint32_t buf = local & 1u, bph = (local >> 1) & 1u;
+        mbar_wait(tempty, (local & 1u) ^ 1u);
         ++local;
-        mbar_wait(&tempty[buf], bph ^ 1u);
         tc_fence_after();
-        const uint32_t acc = tmem + buf * RN;
+        bool fresh[NLV];
+#pragma unroll
+        for (int k = 0; k < NLV; ++k) fresh[k] = true;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
           const uint32_t base = smem_u32(smem + st * RSTAGE);
 #pragma unroll
-          for (int kk = 0; kk < RK / 16; ++kk) {
-            const uint64_t aH = umma_desc_sw128_mn(base + kk * 2048, A_PL / 2);
-            const uint64_t aL = umma_desc_sw128_mn(base + A_PL + kk * 2048, A_PL / 2);
-            const uint64_t bH = umma_desc_sw128_mn(base + 2 * A_PL + kk * 2048, B_PL / 4);
-            const uint64_t bL = umma_desc_sw128_mn(base + 2 * A_PL + B_PL + kk * 2048, B_PL / 4);
-            mma_bf16(acc, aH, bH, IDESC_R, (kb != w.kb0 || kk != 0) ? 1u : 0u);
-            mma_bf16(acc, aH, bL, IDESC_R, 1u);
-            mma_bf16(acc, aL, bH, IDESC_R, 1u);
-            mma_bf16(acc, aL, bL, IDESC_R, 1u);
+          for (int kk = 0; kk < RK / 32; ++kk) {
+#pragma unroll
+            for (int s = 0; s < NSL; ++s) {
+#pragma unroll
+              for (int s2 = 0; s2 < NSL; ++s2) {
+                const int lv = s + s2;
+                mma_i8(tmem + lv * RN, umma_desc_sw128(base + s * A_SL + kk * 32),
+                       umma_desc_sw128(base + NSL * A_SL + s2 * B_SL + kk * 32), IDESC_R, fresh[lv] ? 0u : 1u);
+                fresh[lv] = false;
+              }
+            }
           }
           mma_commit(&empty[st]);
           if (++st == RSTAGES) { st = 0; ph ^= 1u; }
         }
-        mma_commit(&tfull[buf]);
+        mma_commit(tfull);
       }
     }
     __syncwarp();
   } else {
-    // -------------------------------------------------------------- epilogue: TMEM -> partial tile
+    // -------------------------------------------------------------- epilogue: 5 levels -> f64 tile
     const uint32_t q = warp & 3u;
     uint32_t local = 0;
     for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
       const Work w = decode(p, u);
       if (!w.live) continue;
-      const uint32_t buf = local & 1u, bph = (local >> 1) & 1u;
+      const int row = (int)(q * 32u + lane);
+      const int i = w.it * RM + row;
+      const int32_t* exm = p.ex + (size_t)w.m * p.d;
+      const int ei = i < p.d ? __ldg(exm + i) : 0;
+      mbar_wait(tfull, local & 1u);
       ++local;
-      mbar_wait(&tfull[buf], bph);
       tc_fence_after();
-      const uint32_t taddr = tmem + ((q * 32u) << 16) + buf * RN;
-      float* out = p.part + (size_t)u * RN * RM + q * 32 + lane;      // [col][row], row = q*32 + lane
+      const uint32_t taddr = tmem + ((q * 32u) << 16);
+      double* out = p.part + (size_t)u * RN * RM + row;            // [col][row]
 #pragma unroll 1
       for (int c = 0; c < RN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(taddr + c * 32, v);
-        tmem_wait_ld();
+        double g[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) out[(size_t)(c * 32 + k) * RM] = __uint_as_float(v[k]);
+        for (int k = 0; k < 32; ++k) g[k] = 0.0;
+        double wl = 1.0;
+#pragma unroll
+        for (int lv = 0; lv < NLV; ++lv) {
+          uint32_t v[32];
+          tmem_ld32(taddr + lv * RN + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) g[k] = fma((double)(int)v[k], wl, g[k]);
+          wl *= 0.0078125;                                             // 128^-1, exact
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int j = w.jt * RN + c * 32 + k;
+          const int ej = j < p.d ? __ldg(exm + j) : 0;
+          out[(size_t)(c * 32 + k) * RM] = ldexp(g[k], ei + ej);
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) mbar_arrive(tempty);
     }
   }
   tc_fence_before();
@@ -205,75 +241,84 @@ cmc_gram_kernel(const __grid_constant__ CUtensorMap tmP, const RParams p) {
   }
 }
 
-// planes [2][Tg][d] bf16 of the non-text rows in grouped order: h = bf16(a), l = bf16(a - h),
-// a = x * inv_m (f32); padding rows of non-text segments are zero; text rows are not written
+// channel exponents e[m][i] = ilogb(max_t |a_ti|) - 5 (|a| / 2^e < 64), from R^m and 1/s^m
+__global__ void gram_exp_kernel(const float* __restrict__ R, const float* __restrict__ inv, int64_t count,
+                                int32_t* __restrict__ ex) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const float amax = __fmul_rn(R[k], inv[k]);
+  ex[k] = amax > 0.f ? ilogbf(amax) - 5 : 0;
+}
+
+// slices S_s [NSL][d][Tg] (channel rows, grouped-token columns) of the non-text rows; padding rows
+// give zeros; text columns are not written.  Block = 64 grouped rows x 128 channels, transposed
+// through shared memory.
 template <typename XT>
-__global__ void __launch_bounds__(256) gram_planes_kernel(const XT* __restrict__ X, int64_t ld_x,
-                                                          const uint8_t* __restrict__ ids,
+__global__ void __launch_bounds__(256) gram_slices_kernel(const XT* __restrict__ X, int64_t ld_x,
                                                           const int32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ tile_mod,
-                                                          const float* __restrict__ inv, int64_t Tg, int64_t d,
-                                                          uint16_t* __restrict__ planes) {
-  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (p >= Tg) return;
-  const uint32_t um = tile_mod[p / kUnitM];
-  if (um == 0u || um == 0xFFFFFFFFu) return;                    // text unit or unused
-  const int32_t src = perm[p];
+                                                          const float* __restrict__ inv,
+                                                          const int32_t* __restrict__ ex, int64_t Tg, int64_t d,
+                                                          int8_t* __restrict__ S) {
+  __shared__ int8_t sh[NSL][128][64 + 4];
+  const int64_t p0 = (int64_t)blockIdx.x * 64;
+  const int64_t c0 = (int64_t)blockIdx.y * 128;
+  const uint32_t um = tile_mod[p0 / kUnitM];                   // 64 rows never straddle a 256-row unit
+  if (um == 0u || um == 0xFFFFFFFFu) return;
   const float* invm = inv + (int64_t)um * d;
-  uint16_t* ph = planes + p * d;
-  uint16_t* pl = planes + (Tg + p) * d;
-  for (int64_t c = (int64_t)lane * 8; c < d; c += 256) {
-    uint4 hv = make_uint4(0, 0, 0, 0), lv = make_uint4(0, 0, 0, 0);
-    if (src >= 0) {
-      float x[8];
-      if (sizeof(XT) == 2) {
-        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(X) + src * ld_x + c));
-        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-        for (int k = 0; k < 8; ++k) x[k] = __uint_as_float((k & 1) ? (xw[k >> 1] & 0xFFFF0000u) : (xw[k >> 1] << 16));
-      } else {
-        const float4 a0 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X) + src * ld_x + c));
-        const float4 a1 =
-            __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X) + src * ld_x + c + 4));
-        x[0] = a0.x; x[1] = a0.y; x[2] = a0.z; x[3] = a0.w;
-        x[4] = a1.x; x[5] = a1.y; x[6] = a1.z; x[7] = a1.w;
+  const int32_t* exm = ex + (int64_t)um * d;
+  // load: thread (r = tid / 4, c = (tid % 4) * 32 .. +32): one row's 32 channels
+  const int tid = threadIdx.x;
+  for (int r = tid >> 2; r < 64; r += 64) {
+    const int64_t prow = p0 + r;
+    const int32_t src = perm[prow];
+    const int cb = (tid & 3) * 32;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      const int64_t i = c0 + cb + k;
+      int s0 = 0, s1 = 0, s2 = 0;
+      if (src >= 0 && i < d) {
+        const float x = (float)X[(int64_t)src * ld_x + i];
+        const float a = __fmul_rn(x, __ldg(invm + i));
+        const float u = ldexpf(a, -__ldg(exm + i));          // exact, |u| < 64
+        const float f0 = rintf(u);
+        const float r1 = (u - f0) * 128.0f;                  // exact
+        const float f1 = rintf(r1);
+        const float f2 = rintf((r1 - f1) * 128.0f);          // (r1 - f1) * 128 exact
+        s0 = (int)f0;
+        s1 = (int)f1;
+        s2 = (int)f2;
       }
-      const float4 i0 = __ldg(reinterpret_cast<const float4*>(invm + c));
-      const float4 i1 = __ldg(reinterpret_cast<const float4*>(invm + c + 4));
-      const float iv[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
-      uint32_t hw[4], lw[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        uint32_t hh[2], ll[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const float a = __fmul_rn(x[2 * e + k], iv[2 * e + k]);
-          const __nv_bfloat16 h = __float2bfloat16_rn(a);
-          const float r = __fsub_rn(a, __bfloat162float(h));
-          hh[k] = __bfloat16_as_ushort(h);
-          ll[k] = __bfloat16_as_ushort(__float2bfloat16_rn(r));
-        }
-        hw[e] = hh[0] | (hh[1] << 16);
-        lw[e] = ll[0] | (ll[1] << 16);
-      }
-      hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      lv = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      sh[0][cb + k][r] = (int8_t)s0;
+      sh[1][cb + k][r] = (int8_t)s1;
+      sh[2][cb + k][r] = (int8_t)s2;
     }
-    *reinterpret_cast<uint4*>(ph + c) = hv;
-    *reinterpret_cast<uint4*>(pl + c) = lv;
+  }
+  __syncthreads();
+  // store: per slice, 128 channel rows x 64 bytes; thread -> (slice row, 16-byte quarter)
+  for (int e = tid; e < NSL * 128 * 4; e += 256) {
+    const int s = e / 512, rem = e - s * 512, row = rem >> 2, qtr = rem & 3;
+    const int64_t i = c0 + row;
+    if (i >= d) continue;
+    const int8_t* sp = &sh[s][row][qtr * 16];
+    uint32_t w[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      w[b] = (uint32_t)(uint8_t)sp[4 * b] | ((uint32_t)(uint8_t)sp[4 * b + 1] << 8) |
+             ((uint32_t)(uint8_t)sp[4 * b + 2] << 16) | ((uint32_t)(uint8_t)sp[4 * b + 3] << 24);
+    *reinterpret_cast<uint4*>(S + ((int64_t)s * d + i) * Tg + p0 + qtr * 16) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
-// G[m-1] (+)= sum over the chunks (fixed order, f64) of the partial tiles; both triangles.
-// Block = one 32 x 32 sub-block of a tile (8 x 4 per tile); grid.x = tile * 32 + sub, grid.y = m - 1.
+// G[m-1] (+)= sum over the chunks (fixed order) of the f64 tiles; both triangles.
+// Block = one 32 x 32 sub-block of a 128 x 96 tile (4 x 3); grid.x = tile * 12 + sub, grid.y = m - 1.
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const RParams p, double* __restrict__ G, int accumulate) {
   __shared__ double sh[32][33];
   const int m = 1 + (int)blockIdx.y;
-  const int t = (int)blockIdx.x >> 5, sub = (int)blockIdx.x & 31;
+  const int t = (int)blockIdx.x / 12, sub = (int)blockIdx.x % 12;
   int it, jt;
   tile_of(p, t, it, jt);
-  const int r0 = (sub & 3) * 32, c0 = (sub >> 2) * 32;          // sub-block origin inside the 128 x 256 tile
+  const int r0 = (sub & 3) * 32, c0 = (sub >> 2) * 32;
   int k0, nkb;
   seg_of(p, m, k0, nkb);
   const int nch = min(p.max_chunks, (nkb + p.chunk_kb - 1) / p.chunk_kb);
@@ -284,29 +329,27 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const RParams p, doubl
   for (int cc = ty; cc < 32; cc += 8) {
     const int col = c0 + cc, row = r0 + tx;
     double a = 0.0;
-    for (int c = 0; c < nch; ++c) a += (double)p.part[((ubase + c) * RN + col) * RM + row];
+    for (int c = 0; c < nch; ++c) a += p.part[((ubase + c) * RN + col) * RM + row];
     sh[cc][tx] = a;
   }
   __syncthreads();
-  // (1) G[i'][i] with i = it*128 + r0 + tx (row fastest: contiguous), for i <= i'
-  for (int cc = ty; cc < 32; cc += 8) {
-    const int i = it * RM + r0 + tx, i2 = jt * RN + c0 + cc;
-    if (i < d && i2 < d && i <= i2) {
-      double* g = Gm + (size_t)i2 * d + i;
+  for (int cc = ty; cc < 32; cc += 8) {                        // G[j][i], i fastest, i <= j
+    const int i = it * RM + r0 + tx, j = jt * RN + c0 + cc;
+    if (i < d && j < d && i <= j) {
+      double* g = Gm + (size_t)j * d + i;
       *g = (accumulate ? *g : 0.0) + sh[cc][tx];
     }
   }
-  // (2) G[i][i'] (i' fastest: contiguous), for i < i'
-  for (int rr = ty; rr < 32; rr += 8) {
-    const int i = it * RM + r0 + rr, i2 = jt * RN + c0 + tx;
-    if (i < d && i2 < d && i < i2) {
-      double* g = Gm + (size_t)i * d + i2;
+  for (int rr = ty; rr < 32; rr += 8) {                        // G[i][j], j fastest, i < j
+    const int i = it * RM + r0 + rr, j = jt * RN + c0 + tx;
+    if (i < d && j < d && i < j) {
+      double* g = Gm + (size_t)i * d + j;
       *g = (accumulate ? *g : 0.0) + sh[tx][rr];
     }
   }
 }
 
-RParams make_params(int64_t T, int64_t d, int n_mod, const uint32_t* tile_mod, float* part) {
+RParams make_params(int64_t T, int64_t d, int n_mod, const uint32_t* tile_mod, const int32_t* ex, double* part) {
   RParams p{};
   const int64_t Tg = grouped_rows(T, n_mod);
   p.d = (int)d;
@@ -317,57 +360,68 @@ RParams make_params(int64_t T, int64_t d, int n_mod, const uint32_t* tile_mod, f
   p.nti = (int)ceil_div(d, RM);
   p.ntj = (int)ceil_div(d, RN);
   p.n_tiles = 0;
-  for (int jt = 0; jt < p.ntj; ++jt) p.n_tiles += std::min(p.nti, 2 * jt + 2);
-  // token chunks: at least 2048 tokens, at most 4 chunk slots over the whole grouped batch
+  for (int jt = 0; jt < p.ntj; ++jt) p.n_tiles += tiles_in_col(p.nti, jt);
+  // token chunks only to fill the SMs when the tiles alone do not (>= 2048 tokens each); int32
+  // accumulation is exact for any chunk here (|S| <= 64: 3 * 64^2 * 2^16 < 2^31 per level)
   const int64_t kb_total = ceil_div(Tg, RK);
-  p.chunk_kb = (int)std::max<int64_t>(2048 / RK, ceil_div(kb_total, 4));
+  const int64_t tiles_all = (int64_t)std::max(n_mod - 1, 1) * p.n_tiles;
+  const int64_t want = std::max<int64_t>(1, ceil_div(4 * 148, tiles_all));
+  p.chunk_kb = (int)std::min<int64_t>(std::max<int64_t>(2048 / RK, ceil_div(kb_total, want)), 65536 / RK);
   p.max_chunks = (int)ceil_div(kb_total, p.chunk_kb);
   p.n_units = std::max(n_mod - 1, 0) * p.n_tiles * p.max_chunks;
+  p.ex = ex;
   p.part = part;
   return p;
 }
 }  // namespace
 
 size_t cmc_gram_part_bytes(int64_t T, int64_t d, int n_mod) {
-  const RParams p = make_params(T, d, n_mod, nullptr, nullptr);
-  return sizeof(float) * (size_t)p.n_units * RN * RM;
+  const RParams p = make_params(T, d, n_mod, nullptr, nullptr, nullptr);
+  return sizeof(double) * (size_t)p.n_units * RN * RM;
 }
+size_t cmc_gram_slice_bytes(int64_t T, int64_t d, int n_mod) { return (size_t)NSL * d * grouped_rows(T, n_mod); }
 
 cudaError_t launch_cmc_gram_tc(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T,
                                int64_t d, int n_mod, const float* inv, const int32_t* perm,
-                               const uint32_t* tile_mod, uint16_t* planes, float* part, double* G, int accumulate,
-                               cudaStream_t st) {
+                               const uint32_t* tile_mod, float* R, int64_t* cnt, int32_t* ex, int8_t* slices,
+                               double* part, uint32_t* status, double* G, int accumulate, cudaStream_t st) {
   if (n_mod < 2) return cudaSuccess;
   const int64_t Tg = grouped_rows(T, n_mod);
+  // per-modality channel maxima of |x| -> exponents of the channel scales
+  cudaError_t e = cudaMemsetAsync(R, 0, sizeof(float) * n_mod * d, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, sizeof(int64_t) * n_mod, st);
+  if (e != cudaSuccess) return e;
+  e = launch_stats(X, xt, ld_x, ids, T, d, n_mod, R, cnt, status, st);
+  if (e != cudaSuccess) return e;
   {
-    ProfScope ps_("cmc_planes", st);
-    const unsigned g = (unsigned)ceil_div(Tg, 8);
+    ProfScope ps_("cmc_slices", st, 2);
+    gram_exp_kernel<<<(unsigned)ceil_div((int64_t)n_mod * d, 256), 256, 0, st>>>(R, inv, (int64_t)n_mod * d, ex);
+    dim3 grid((unsigned)(Tg / 64), (unsigned)ceil_div(d, 128));
     if (xt == MASQ_BF16)
-      gram_planes_kernel<<<g, 256, 0, st>>>(static_cast<const uint16_t*>(X), ld_x, ids, perm, tile_mod, inv, Tg, d,
-                                            planes);
+      gram_slices_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X), ld_x, perm, tile_mod, inv, ex,
+                                               Tg, d, slices);
     else
-      gram_planes_kernel<<<g, 256, 0, st>>>(static_cast<const float*>(X), ld_x, ids, perm, tile_mod, inv, Tg, d,
-                                            planes);
-    cudaError_t e = cudaGetLastError();
+      gram_slices_kernel<<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld_x, perm, tile_mod, inv, ex, Tg, d,
+                                               slices);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  CUtensorMap tp;
-  if (!make_tmap_2d(&tp, planes, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 2 * (uint64_t)Tg, d, d, RK, 64, true))
-    return cudaErrorInvalidValue;
-  const RParams p = make_params(T, d, n_mod, tile_mod, part);
-  {
-    cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(cmc_gram_kernel), R_ALLOC);
-    if (e != cudaSuccess) return e;
-  }
+  CUtensorMap ta, tb;
+  bool ok = make_tmap_2d(&ta, slices, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)NSL * d, Tg, Tg, RM, RK, true);
+  ok &= make_tmap_2d(&tb, slices, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)NSL * d, Tg, Tg, RN, RK, true);
+  if (!ok) return cudaErrorInvalidValue;
+  const RParams p = make_params(T, d, n_mod, tile_mod, ex, part);
+  e = set_max_dyn_smem(reinterpret_cast<const void*>(cmc_gram_kernel), R_ALLOC);
+  if (e != cudaSuccess) return e;
   {
     ProfScope ps_("cmc_gram", st);
     const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
-    cmc_gram_kernel<<<grid, RT, R_ALLOC, st>>>(tp, p);
-    cudaError_t e = cudaGetLastError();
+    cmc_gram_kernel<<<grid, RT, R_ALLOC, st>>>(ta, tb, p);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   ProfScope ps_("cmc_gram_reduce", st);
-  dim3 grid((unsigned)p.n_tiles * 32, (unsigned)(n_mod - 1));
+  dim3 grid((unsigned)p.n_tiles * 12, (unsigned)(n_mod - 1));
   gram_reduce_kernel<<<grid, 256, 0, st>>>(p, G, accumulate);
   return cudaGetLastError();
 }

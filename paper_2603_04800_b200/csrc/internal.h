@@ -37,7 +37,7 @@ struct WsLayout {
          work = 0, info = 0, dot = 0;
   size_t lwork = 0;   // doubles
   size_t gall = 0;    // CMC: the (n_mod-1) Gram matrices of the one-call path
-  size_t gram_part = 0;   // CMC: fp32 partial Gram tiles (gram.cu)
+  size_t gram_part = 0, gram_r = 0, gram_ex = 0, slices = 0;   // CMC: exact Gram scratch (gram.cu)
   // N3 decode
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
@@ -235,22 +235,27 @@ struct CmcArgs {
   int32_t* perm;
   uint32_t* tile_mod;
   int64_t* cnt;
-  uint16_t* planes;
-  float* gram_part;
+  float* R;
+  int32_t* ex;
+  int8_t* slices;
+  double* gram_part;
+  uint32_t* status;
 };
 bool cmc_linalg_available();
 size_t cmc_syevd_lwork(int64_t d, int64_t n);
 bool cmc_eig_route();
 int cmc_dot_blocks();
 cudaError_t launch_cmc_gram(const CmcArgs& a, double* G, int accumulate, cudaStream_t st);
-// G[m-1] (+)= A_m^T A_m for m = 1..n_mod-1 on the tensor cores (split-bf16, fp32 partial tiles
-// over token chunks, f64 fixed-order reduction; both triangles written); perm / tile_mod from
-// launch_route, inv = 1/s, planes [2][Tg][d] bf16 and part (cmc_gram_part_bytes) scratch
+// G[m-1] (+)= A_m^T A_m for m = 1..n_mod-1 on the int8 tensor cores, exact (gram.cu: three int8
+// slices per value on a per-channel power-of-two scale, int32 accumulation, f64 combination; both
+// triangles written); perm / tile_mod from launch_route, inv = 1/s; R / cnt / ex / slices / part
+// are scratch (cmc_gram_slice_bytes, cmc_gram_part_bytes)
 size_t cmc_gram_part_bytes(int64_t T, int64_t d, int n_mod);
+size_t cmc_gram_slice_bytes(int64_t T, int64_t d, int n_mod);
 cudaError_t launch_cmc_gram_tc(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t* ids, int64_t T,
                                int64_t d, int n_mod, const float* inv, const int32_t* perm,
-                               const uint32_t* tile_mod, uint16_t* planes, float* part, double* G, int accumulate,
-                               cudaStream_t st);
+                               const uint32_t* tile_mod, float* R, int64_t* cnt, int32_t* ex, int8_t* slices,
+                               double* part, uint32_t* status, double* G, int accumulate, cudaStream_t st);
 cudaError_t launch_cmc_from_gram(const CmcArgs& a, const double* G, cudaStream_t st);
 
 // ---------------------------------------------------------------- N3 int4 decode (decode.cu)
@@ -261,6 +266,26 @@ cudaError_t launch_wq4(const void* W, masq_dtype wt, const float* s, int64_t d, 
 cudaError_t launch_unpack4(const uint8_t* packed, int64_t d, int64_t n, int8_t* codes, cudaStream_t st);
 cudaError_t launch_decode(const int8_t* qa, const float* dx, int T, int64_t d, int64_t n, const uint8_t* packed,
                           const float* scales, float* part, float* Y, int64_t ldy, cudaStream_t st);
+
+// ---------------------------------------------------------------- N3 prefill W4 grouped GEMM (w4g.cu)
+struct W4gArgs {
+  int64_t T, n, d;
+  const int8_t* qx;                // activation codes [T x d]
+  const float* dx;                 // [T]
+  const uint8_t* packed;           // [n x d/2] (w4g layout)
+  const float* scales;             // [n x d/128]
+  const uint32_t* tile_mask;       // per 128-token tile modality bits (CMC)
+  int n_mod, rpad;
+  const uint16_t* z;               // [T x (M-1)*2*rpad]
+  const uint16_t* l2t;             // [(M-1)*n x 2*rpad]
+  void* out;
+  int64_t ld_out;
+  int acc_mode;
+};
+cudaError_t launch_w4g_gemm(const W4gArgs& a, cudaStream_t st);
+// W4 grouped quantizer: layout 0 = decode (decode.cu format), 1 = prefill (w4g.cu format)
+cudaError_t launch_wq4_layout(const void* W, masq_dtype wt, const float* s, int64_t d, int64_t n, uint8_t* packed,
+                              float* scales, int layout, cudaStream_t st);
 
 // ---------------------------------------------------------------- N4 baselines (baseline.cu)
 int meanabs_slabs(int64_t T);

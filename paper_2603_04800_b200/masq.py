@@ -360,6 +360,42 @@ def linear_decode(X, s_t, packed, scales, abits: int = 8, group: int = 128, Y=No
     return Y
 
 
+def quantize_weight_w4g(W, s_vec, group: int = 128, stream=None):
+    """(packed uint8 [n, d/2] in the prefill GEMM's K-major nibble order, scales f32 [n, d/group])."""
+    d, n = W.shape
+    packed = torch.empty(n, d // 2, dtype=torch.uint8, device=W.device)
+    scales = torch.empty(n, d // group, dtype=torch.float32, device=W.device)
+    _ck(lib().masq_quantize_weight_w4g(_p(W.contiguous()), _dt(W), _p(s_vec.contiguous()), d, n, group, _p(packed),
+                                       _p(scales), _stream(stream)), "masq_quantize_weight_w4g")
+    return packed, scales
+
+
+def linear_forward_w4g(X, mod_id, s, packed, scales, abits: int = 8, L1=None, L2=None, Y=None, group: int = 128,
+                       acc_debug: bool = False, ws=None, stream=None):
+    """Prefill W4A8 forward with packed int4 group-scaled weights (+ CMC): f32 [T x n]
+    (acc_debug: the int32 sum over groups of the unscaled accumulators)."""
+    T, d = X.shape
+    n = packed.shape[0]
+    n_mod = s.shape[0]
+    r = 0 if L1 is None else int(L1.shape[-1])
+    ld_l2 = 0 if L2 is None else int(L2.stride(-2))
+    dbg = None
+    if acc_debug:
+        out = torch.empty(T, n, dtype=torch.int32, device=X.device)
+        dbg = MasqDebug(out.data_ptr(), out.stride(0), None, None)
+        Yp, ldy = None, n
+    else:
+        out = torch.empty(T, n, dtype=torch.float32, device=X.device) if Y is None else Y
+        Yp, ldy = _p(out), out.stride(0)
+    ws = ws or default_workspace(X.device)
+    p, nb = ws.ptr_size(workspace_size(OP_FORWARD, T, d, n, n_mod, r if not acc_debug else 0))
+    _ck(lib().masq_linear_forward_w4g(_p(X), _dt(X), X.stride(0), _p(mod_id), T, d, n, n_mod, _p(s.contiguous()),
+                                      _p(packed), _p(scales), group, abits, _p(L1), _p(L2), ld_l2, r, Yp, ldy, p, nb,
+                                      ctypes.byref(dbg) if dbg is not None else None, _stream(stream)),
+        "masq_linear_forward_w4g")
+    return out
+
+
 def cmc_gram(X, mod_id, s, G=None, accumulate: bool = False, ws=None, stream=None):
     """G f64 [M-1, d, d] (lower triangle) += / = A_m^T A_m for the non-text modalities."""
     T, d = X.shape

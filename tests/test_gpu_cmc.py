@@ -5,12 +5,14 @@ L1 and L2 are unique only up to the sign of each singular pair, so the product L
 compared in the norm Theorem 2 is stated in: ||A (P_gpu - P_oracle)||_F <= TOL_P ||A dW||_F
 (f32 outputs), and the optional residual against the oracle's reconstruction loss.
 
-Reading Q29: the Gram A^T A is accumulated on the tensor cores from a split-bf16
-representation of A (each value to 2^-17, all four hi/lo products, fp32 accumulation over token
-chunks, f64 across chunks), so G carries ~1e-6 relative error (CPU emulation of the same
-arithmetic: 2e-7..3e-6 max-normalised; L1 L2 moves by 2e-7..7e-7 in the A-norm; the residual
-<E, G E> evaluated with that G by <= 1.2e-7 ||A dW||^2).  Bars: G 1e-4 (max-normalised), L1 L2
-1e-4 in the A-norm, residual 1e-6 ||A dW||^2 — all inside north_star's 1e-3 float bar.
+Reading Q29: the Gram A^T A is computed on the int8 tensor cores EXACTLY for a
+slightly rounded A: every channel on a power-of-two scale (|a| / 2^e < 64), three int8 slices
+(a represented to 2^-20 of the channel's max), all nine slice products accumulated in int32 and
+combined in f64 — so G is the exact Gram of A_hat (positive semidefinite to f64 rounding: a
+rank-deficient batch keeps its null space at ~1e-16 lambda_max, below the 1e-8 regulariser).  CPU
+emulation of the same arithmetic: G within 1.1-2.6e-7 (max-normalised), L1 L2 within 0.8-9e-7 in
+the A-norm, the residual <E, G_hat E> within 6e-9 ||A dW||^2.  Bars: G 1e-4, L1 L2 1e-4 in the
+A-norm, residual 1e-6 ||A dW||^2 — all inside north_star's 1e-3 float bar.
 """
 import numpy as np
 import pytest

@@ -1,5 +1,6 @@
 """N2 timing (measurement tool, not product): masq_cmc_factors at the c3 linears (T = 16384
-calibration tokens, r = 64), per stage, with the f64 GEMM rates of the cuBLAS stages."""
+calibration tokens, r = 64), per stage: the tensor-core Gram (split-bf16, 4 products) with its
+executed bf16 rate, and the f64 library stages (Cholesky / small-side GEMMs, eigensolve)."""
 import ctypes
 import json
 import os
@@ -19,7 +20,7 @@ def main():
     dev = torch.device("cuda", 0)
     T, r = 16384, 64
     ids = torch.from_numpy(synth.modality_ids(synth.CONFIGS["c3"]["pattern"], T=T)).to(dev)
-    names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["qkv", "o"]
+    names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["qkv", "o", "gate_up", "down"]
     out = {}
     for name, d, n in synth.LAYER_LINEARS["c3"]:
         if name not in names:
@@ -42,9 +43,18 @@ def main():
         k = lib().masq_profile_collect(64, nm, tot, cn)
         lib().masq_profile_enable(0)
         ker = {nm.raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode(): tot[i] for i in range(k)}
-        rec = {"wall_s": wall, "kernels_ms": ker, "resid": resid.cpu().tolist(),
-               "gram_f64_tflops": T * d * d / (ker.get("cmc_gram", 1e9) / 1e3) / 1e12,
-               "mmt_f64_tflops": n * d * d / (ker.get("cmc_mmt", 1e9) / 1e3) / 1e12}
+        t_nt = int((ids != 0).sum())
+        nti, ntj = -(-d // 128), -(-d // 256)
+        tiles = sum(min(nti, 2 * jt + 2) for jt in range(ntj))
+        executed = 4 * 2.0 * t_nt * tiles * 128 * 256          # 4 split-bf16 products over the computed tiles
+        gms = ker.get("cmc_gram", 0.0)
+        total_ms = sum(ker.values())
+        eig_ms = sum(v for k_, v in ker.items() if k_.startswith("cmc_eig"))
+        rec = {"wall_s": wall, "kernels_ms": ker, "resid": resid.cpu().tolist(), "tokens_non_text": t_nt,
+               "gram_ms": gms, "gram_algorithmic_tflop": t_nt * d * d / 1e12,
+               "gram_executed_bf16_tflops": executed / (gms / 1e3) / 1e12 if gms else None,
+               "eig_ms": eig_ms, "eig_share": eig_ms / total_ms if total_ms else None,
+               "route": "small-side n x n" if n < d else "Cholesky + eig(M M^T)"}
         out[f"{name}_d{d}_n{n}"] = rec
         print(name, json.dumps(rec), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
