@@ -303,9 +303,10 @@ masq_status masq_linear_decode(const void* X, masq_dtype xt, int64_t ld_x, int64
  *             (+ (X_t S_m^-1) L1^m L2^m for m_t != text, as masq_linear_forward)
  * on the tensor cores: the packed nibbles are expanded to int8 in shared memory and every group is
  * one kind::i8 k-block into its own TMEM accumulator, promoted in f32 with the group's scale.
- * Weight format (masq_quantize_weight_w4g): packed uint8 [d_out x d/2], K-major: in the 64 bytes of
- * group g of channel j, byte 16c + i = code[j][128g + 32c + i] & 0xF | (code[j][128g + 32c + 16 + i]
- * & 0xF) << 4 (two's complement nibbles); scales f32 [d_out x d/128] (Delta_jg = max(max|s_i w_ij|/7,
+ * Weight format (masq_quantize_weight_w4g): packed uint8 [d/128][d_out][64] (group-major: the 64
+ * bytes of group g of channel j at (g d_out + j) 64, so 128 channels of a group are one contiguous
+ * 8 KB block), byte 16c + i = code[j][128g + 32c + i] & 0xF | (code[j][128g + 32c + 16 + i] & 0xF)
+ * << 4 (two's complement nibbles); scales f32 [d_out x d/128] (Delta_jg = max(max|s_i w_ij|/7,
  * 1e-12), the A3 quantizer at group granularity).  The codes and scales equal those of
  * masq_quantize_weight_int4 (the decode format); only the byte order differs.
  * d % 128 == 0, d_out % 32 == 0, group == 128; workspace masq_workspace_size(MASQ_OP_FORWARD, ...).

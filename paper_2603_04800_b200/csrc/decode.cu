@@ -68,9 +68,9 @@ __device__ __forceinline__ float ldw<float>(const float* p) { return *p; }
 
 // one CTA = 16 output channels (two 8-column tiles) x one group of 128 input channels;
 // thread k reads row k of the group (16 columns), block max per column, exact codes, packing
-// LAYOUT 0: the decode kernel's fragment order (above); LAYOUT 1: the prefill GEMM's K-major
-// format (w4g.cu): packed[j][g*64 + 16c + i] = code[128g+32c+i] | code[128g+32c+16+i] << 4 (two's
-// complement nibbles), scales[j][g]
+// LAYOUT 0: the decode kernel's fragment order (above); LAYOUT 1: the prefill GEMM's group-major
+// format (w4g.cu): packed[(g*n + j)*64 + 16c + i] = code[j][128g+32c+i] | code[j][128g+32c+16+i] << 4
+// (two's complement nibbles), scales[j][g]
 template <typename WT, int LAYOUT>
 __global__ void __launch_bounds__(128) wq4_kernel(const WT* __restrict__ W, const float* __restrict__ s, int64_t d,
                                                   int64_t n, uint8_t* __restrict__ packed,
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128) wq4_kernel(const WT* __restrict__ W, cons
       const uint32_t hi = (uint32_t)codes[c][32 * cc + 16 + i] & 0xFu;
       w2[e >> 2] |= (lo | (hi << 4)) << (8 * (e & 3));
     }
-    *reinterpret_cast<uint2*>(packed + (j0 + c) * (d / 2) + (int64_t)g * 64 + b0) = make_uint2(w2[0], w2[1]);
+    *reinterpret_cast<uint2*>(packed + ((int64_t)g * n + j0 + c) * 64 + b0) = make_uint2(w2[0], w2[1]);
     return;
   }
   // 2 tiles x 32 lanes x 4 words: thread k -> tile k >> 6, lane (k >> 1) & 31, words 2 (k & 1) + {0, 1}

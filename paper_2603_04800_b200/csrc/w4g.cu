@@ -13,9 +13,10 @@
 // — no shuffles, one scalar per lane and group.  Four 128-column TMEM accumulators rotate so the
 // MMAs of group g+1..g+3 overlap the promotion of group g.
 //
-// Packed format (this kernel's, masq_quantize_weight_w4g): K-major, d/2 bytes per output channel;
-// in the 64 bytes of group g, byte 16c + i holds code[128g + 32c + i] in its low nibble and
-// code[128g + 32c + 16 + i] in its high nibble (two's complement).  Converter warps expand one
+// Packed format (this kernel's, masq_quantize_weight_w4g): group-major [d/128][n][64 B] — the 64
+// bytes of (group g, channel j) at (g n + j) 64, so a CTA's 128-channel group tile is one contiguous
+// 8 KB block; byte 16c + i holds code[j][128g + 32c + i] in its low nibble and code[j][128g + 32c +
+// 16 + i] in its high nibble (two's complement).  Converter warps expand one
 // group per stage in shared memory: (w << 4) & 0xF0F0F0F0 and w & 0xF0F0F0F0 are the int8 values
 // 16*code of 16 consecutive k (two ops per 8 codes, no sign extension, natural K order), written
 // into the SWIZZLE_128B K-major A tile the MMA reads; the factor 16 is removed exactly in the
@@ -26,6 +27,7 @@
 // tokens' Z rows), added in f32 after the dx scaling.  Y is written straight from registers (lane =
 // channel, so a warp stores 32 consecutive floats of a token row).
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.h"
@@ -43,15 +45,17 @@ constexpr int QK = 128;                 // one group = one k-block (128 int8 / 6
 constexpr int PK_BYTES = QM * 64;       // packed group tile (8 KB)
 constexpr int QA_BYTES = QM * QK;       // unpacked / L2^T A tile (16 KB)
 constexpr int QB_BYTES = QNH * QK;      // activation / Z B tile (8 KB)
-constexpr int QSTAGES = 5;
+constexpr int NP = 5;                   // input ring: packed group tile (or a CMC L2^T tile) + B tile
+constexpr int NA = 5;                   // unpacked A ring (the converters' output)
 constexpr int NBUF = 4;                 // 128-column TMEM accumulators
-constexpr int CONV_WARPS = 2;               // each thread expands 2 rows per group
+constexpr int CONV_WARPS = 2;
 constexpr int EPI_WARPS = 8;
 constexpr int QTHREADS = 64 + 32 * (CONV_WARPS + EPI_WARPS);
-constexpr int SM_PK = 0;
-constexpr int SM_A = SM_PK + QSTAGES * PK_BYTES;
-constexpr int SM_B = SM_A + QSTAGES * QA_BYTES;
-constexpr int SM_BAR = SM_B + QSTAGES * QB_BYTES;
+constexpr int P_A = QA_BYTES;           // input slot: 16 KB region (packed uses 8 KB, CMC A 16 KB) ...
+constexpr int P_SLOT = P_A + QB_BYTES;  // ... + the 8 KB B tile
+constexpr int SM_P = 0;
+constexpr int SM_A = SM_P + NP * P_SLOT;
+constexpr int SM_BAR = SM_A + NA * QA_BYTES;
 constexpr int SM_USED = SM_BAR + 512;
 constexpr int SM_ALLOC = SM_USED + 1024;
 constexpr uint32_t IDESC_Q = idesc_i8(QUM, QN);
@@ -69,8 +73,32 @@ struct WParams {
   void* out;                            // f32 Y or int32 accumulators [T][ld_out]
   long long ld_out;
   int acc_mode;                         // 1: int32 sum over groups (debug tap), no dx / CMC
+  int exp;                              // measurement knob (MASQ_W4G_EXP): 1 skip promotion, 2 skip unpack,
+                                        // 4 skip the TMEM loads, 8 skip the MMAs
 };
 
+
+__device__ __forceinline__ uint64_t w2_pack(uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void w2_unpack(uint64_t v, float& lo, float& hi) {
+  uint32_t a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(a), "=r"(b) : "l"(v));
+  lo = __uint_as_float(a);
+  hi = __uint_as_float(b);
+}
+__device__ __forceinline__ uint64_t w2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t w2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 struct WUnit {
   int mt, nt;
@@ -94,10 +122,11 @@ __device__ __forceinline__ WUnit w_unit(const WParams& p, int u) {
   return w;
 }
 
+template <int N>
 struct QRing {
   uint32_t stage = 0, phase = 0;
   __device__ __forceinline__ void advance() {
-    if (++stage == QSTAGES) { stage = 0; phase ^= 1u; }
+    if (++stage == N) { stage = 0; phase ^= 1u; }
   }
 };
 
@@ -108,14 +137,14 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* sPK = smem + SM_PK;
+  uint8_t* sP = smem + SM_P;
   uint8_t* sA = smem + SM_A;
-  uint8_t* sB = smem + SM_B;
-  uint64_t* pfull = reinterpret_cast<uint64_t*>(smem + SM_BAR);   // own: packed tile landed
-  uint64_t* full = pfull + QSTAGES;      // leader's: B (and CMC A) landed in both CTAs
-  uint64_t* aready = full + QSTAGES;     // leader's: both CTAs' converters wrote A
-  uint64_t* empty = aready + QSTAGES;    // both: the MMAs of the stage completed
-  uint64_t* tfull = empty + QSTAGES;     // [NBUF] both: accumulator ready
+  uint64_t* pfull = reinterpret_cast<uint64_t*>(smem + SM_BAR);   // own: packed tile landed (or CMC mark)
+  uint64_t* full = pfull + NP;           // leader's: B (and CMC A) landed in both CTAs
+  uint64_t* pempty = full + NP;          // own: the MMA (commit) and this CTA's converters are done with it
+  uint64_t* aready = pempty + NP;        // [NA] leader's: both CTAs' converters wrote the A slot
+  uint64_t* aempty = aready + NA;        // [NA] own: the MMA read the A slot
+  uint64_t* tfull = aempty + NA;         // [NBUF] both: accumulator ready
   uint64_t* tempty = tfull + NBUF;       // [NBUF] leader's: both CTAs' epilogues drained it
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
@@ -127,11 +156,14 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmPK);
     tma_prefetch(&tmX);
-    for (int i = 0; i < QSTAGES; ++i) {
+    for (int i = 0; i < NP; ++i) {
       mbar_init(&pfull[i], 1);
       mbar_init(&full[i], 1);
+      mbar_init(&pempty[i], 1 + CONV_WARPS);
+    }
+    for (int i = 0; i < NA; ++i) {
       mbar_init(&aready[i], 2 * CONV_WARPS);
-      mbar_init(&empty[i], 1);
+      mbar_init(&aempty[i], 1);
     }
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&tfull[i], 1);
@@ -148,28 +180,30 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------------- TMA producer (both CTAs)
-      QRing ring;
+      QRing<NP> ring;
       for (int u = cid; u < p.n_units; u += ncl) {
         const WUnit w = w_unit(p, u);
         const int crow = w.nt * QUM + (int)rank * QM;         // this CTA's output channels
         const int trow = w.mt * QN + (int)rank * QNH;         // this CTA's token rows
         for (int g = 0; g < p.ng; ++g) {
-          mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+          mbar_wait(&pempty[ring.stage], ring.phase ^ 1u);
+          uint8_t* slot = sP + ring.stage * P_SLOT;
           mbar_expect_tx(&pfull[ring.stage], PK_BYTES);
-          tma_load_2d(sPK + ring.stage * PK_BYTES, &tmPK, &pfull[ring.stage], g * 64, crow);
+          tma_load_2d(slot, &tmPK, &pfull[ring.stage], 0, g * p.n + crow);
           if (leader) mbar_expect_tx(&full[ring.stage], 2 * QB_BYTES);
-          tma_load_2d_2sm(sB + ring.stage * QB_BYTES, &tmX, &full[ring.stage], g * QK, trow);
+          tma_load_2d_2sm(slot + P_A, &tmX, &full[ring.stage], g * QK, trow);
           ring.advance();
         }
         if (w.cmc) {
           for (int mm = 1; mm < p.n_mod; ++mm) {
             if (!((w.mask >> mm) & 1u)) continue;
             for (int kb = 0; kb < p.cmc_kb; ++kb) {
-              mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+              mbar_wait(&pempty[ring.stage], ring.phase ^ 1u);
+              uint8_t* slot = sP + ring.stage * P_SLOT;
+              mbar_arrive(&pfull[ring.stage]);                  // CMC slot: the converters only release it
               if (leader) mbar_expect_tx(&full[ring.stage], 2 * (QA_BYTES + QB_BYTES));
-              tma_load_2d_2sm(sA + ring.stage * QA_BYTES, &tmL2, &full[ring.stage], kb * 64, (mm - 1) * p.n + crow);
-              tma_load_2d_2sm(sB + ring.stage * QB_BYTES, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64,
-                              trow);
+              tma_load_2d_2sm(slot, &tmL2, &full[ring.stage], kb * 64, (mm - 1) * p.n + crow);
+              tma_load_2d_2sm(slot + P_A, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64, trow);
               ring.advance();
             }
           }
@@ -180,10 +214,10 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
   } else if (warp == 1) {
     if (leader && lane == 0) {
       // ---------------------------------------------------------------- MMA issuer (leader CTA)
-      QRing ring;
-      uint32_t aph = 0;                 // per-stage phase bits of aready (group stages only)
+      QRing<NP> ring;
+      QRing<NA> aring;
       uint32_t acnt = 0;                // accumulator buffers used so far
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      const uint32_t p0 = smem_u32(sP), a0 = smem_u32(sA);
       for (int u = cid; u < p.n_units; u += ncl) {
         const WUnit w = w_unit(p, u);
         for (int g = 0; g < p.ng; ++g) {
@@ -191,17 +225,20 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
           ++acnt;
           mbar_wait(&tempty[buf], bph ^ 1u);
           mbar_wait(&full[ring.stage], ring.phase);
-          mbar_wait(&aready[ring.stage], (aph >> ring.stage) & 1u);
-          aph ^= 1u << ring.stage;
+          mbar_wait(&aready[aring.stage], aring.phase);
           tc_fence_after();
           const uint32_t dtm = tmem_base + buf * QN;
+          const uint32_t ab = a0 + aring.stage * QA_BYTES, bb = p0 + ring.stage * P_SLOT + P_A;
+          if (!(p.exp & 8)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_i8_2sm(dtm, umma_desc_sw128(a0 + ring.stage * QA_BYTES + k * 32),
-                       umma_desc_sw128(b0 + ring.stage * QB_BYTES + k * 32), IDESC_Q, k != 0);
-          mma_commit_2sm(&empty[ring.stage], kPair);
+            for (int k = 0; k < 4; ++k)
+              mma_i8_2sm(dtm, umma_desc_sw128(ab + k * 32), umma_desc_sw128(bb + k * 32), IDESC_Q, k != 0);
+          }
+          mma_commit_2sm(&pempty[ring.stage], kPair);
+          mma_commit_2sm(&aempty[aring.stage], kPair);
           mma_commit_2sm(&tfull[buf], kPair);
           ring.advance();
+          aring.advance();
         }
         if (w.cmc) {
           const uint32_t buf = acnt % NBUF, bph = (acnt / NBUF) & 1u;
@@ -215,13 +252,14 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
             for (int kb = 0; kb < p.cmc_kb; ++kb) {
               mbar_wait(&full[ring.stage], ring.phase);
               tc_fence_after();
+              const uint32_t ab = p0 + ring.stage * P_SLOT, bb = ab + P_A;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                mma_bf16_2sm(dtm, umma_desc_sw128(a0 + ring.stage * QA_BYTES + k * 32),
-                             umma_desc_sw128(b0 + ring.stage * QB_BYTES + k * 32), IDESC_QC, first ? 0u : 1u);
+                mma_bf16_2sm(dtm, umma_desc_sw128(ab + k * 32), umma_desc_sw128(bb + k * 32), IDESC_QC,
+                             first ? 0u : 1u);
                 first = false;
               }
-              mma_commit_2sm(&empty[ring.stage], kPair);
+              mma_commit_2sm(&pempty[ring.stage], kPair);
               ring.advance();
             }
           }
@@ -232,45 +270,61 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
     __syncwarp();
   } else if (warp < 2 + CONV_WARPS) {
     // ------------------------------------------------------------------ converters (both CTAs)
-    // thread = two output channel rows of this CTA's tile: 64 packed bytes -> 128 int8 (16 x code)
-    const uint32_t row0 = (warp - 2) * 32 + lane;
-    QRing ring;
-    uint32_t pph = 0;                   // per-stage phase bits of pfull (group stages only)
+    // per group: 128 rows x 4 input chunks of 16 B (64 packed bytes -> 128 int8 = 16 x code); thread
+    // t takes chunks q = t + 64 k (row q / 4, chunk q % 4): a warp's loads cover 512 contiguous bytes
+    // and its swizzled stores hit distinct banks (no shared-memory bank conflicts)
+    const uint32_t tid = (warp - 2) * 32 + lane;
+    QRing<NP> ring;
+    QRing<NA> aring;
     for (int u = cid; u < p.n_units; u += ncl) {
       const WUnit w = w_unit(p, u);
       for (int g = 0; g < p.ng; ++g) {
-        mbar_wait(&pfull[ring.stage], (pph >> ring.stage) & 1u);
-        pph ^= 1u << ring.stage;
+        mbar_wait(&pfull[ring.stage], ring.phase);
+        mbar_wait(&aempty[aring.stage], aring.phase ^ 1u);
+        const uint4* src = reinterpret_cast<const uint4*>(sP + ring.stage * P_SLOT);
+        const uint32_t dstA = smem_u32(sA + aring.stage * QA_BYTES);
+        // all loads first (the stores below are asm with a memory clobber, which would otherwise
+        // serialise every load behind the previous chunk's stores)
+        constexpr int KCH = (QM * 4) / (32 * CONV_WARPS);
+        uint4 xin[KCH];
 #pragma unroll
-        for (int rr = 0; rr < QM / (32 * CONV_WARPS); ++rr) {
-          const uint32_t row = row0 + rr * 32 * CONV_WARPS;
-          const uint4* src = reinterpret_cast<const uint4*>(sPK + ring.stage * PK_BYTES + row * 64);
-          const uint32_t dst = smem_u32(sA + ring.stage * QA_BYTES + row * QK);
+        for (int k = 0; k < KCH; ++k) xin[k] = (p.exp & 2) ? make_uint4(0, 0, 0, 0) : src[tid + k * 32 * CONV_WARPS];
+        fence_proxy_async_smem();                               // the reads before the slot's TMA refill
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[ring.stage]);        // packed bytes consumed
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 x = src[c];
-            const uint4 lo = make_uint4((x.x << 4) & 0xF0F0F0F0u, (x.y << 4) & 0xF0F0F0F0u,
-                                        (x.z << 4) & 0xF0F0F0F0u, (x.w << 4) & 0xF0F0F0F0u);
-            const uint4 hi = make_uint4(x.x & 0xF0F0F0F0u, x.y & 0xF0F0F0F0u, x.z & 0xF0F0F0F0u, x.w & 0xF0F0F0F0u);
-            const uint32_t d0 = dst + ((((uint32_t)(2 * c)) ^ (row & 7u)) << 4);
-            const uint32_t d1 = dst + ((((uint32_t)(2 * c + 1)) ^ (row & 7u)) << 4);
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d0), "r"(lo.x), "r"(lo.y), "r"(lo.z),
-                         "r"(lo.w)
-                         : "memory");
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d1), "r"(hi.x), "r"(hi.y), "r"(hi.z),
-                         "r"(hi.w)
-                         : "memory");
-          }
+        for (int k = 0; k < KCH; ++k) {
+          const uint32_t q = tid + k * 32 * CONV_WARPS;
+          const uint32_t row = q >> 2, c = q & 3u;
+          const uint4 x = xin[k];
+          const uint4 lo = make_uint4((x.x << 4) & 0xF0F0F0F0u, (x.y << 4) & 0xF0F0F0F0u,
+                                      (x.z << 4) & 0xF0F0F0F0u, (x.w << 4) & 0xF0F0F0F0u);
+          const uint4 hi = make_uint4(x.x & 0xF0F0F0F0u, x.y & 0xF0F0F0F0u, x.z & 0xF0F0F0F0u, x.w & 0xF0F0F0F0u);
+          const uint32_t d0 = dstA + row * QK + (((2u * c) ^ (row & 7u)) << 4);
+          const uint32_t d1 = dstA + row * QK + (((2u * c + 1u) ^ (row & 7u)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d0), "r"(lo.x), "r"(lo.y), "r"(lo.z),
+                       "r"(lo.w)
+                       : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d1), "r"(hi.x), "r"(hi.y), "r"(hi.z),
+                       "r"(hi.w)
+                       : "memory");
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&aready[ring.stage], 0);
+        if (lane == 0) mbar_arrive_cluster(&aready[aring.stage], 0);
         ring.advance();
+        aring.advance();
       }
       if (w.cmc) {
-        for (int mm = 1; mm < p.n_mod; ++mm)
-          if ((w.mask >> mm) & 1u)
-            for (int kb = 0; kb < p.cmc_kb; ++kb) ring.advance();
+        for (int mm = 1; mm < p.n_mod; ++mm) {
+          if (!((w.mask >> mm) & 1u)) continue;
+          for (int kb = 0; kb < p.cmc_kb; ++kb) {
+            mbar_wait(&pfull[ring.stage], ring.phase);            // (the producer's mark)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pempty[ring.stage]);
+            ring.advance();
+          }
+        }
       }
     }
   } else {
@@ -284,15 +338,24 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
       const int j = w.nt * QUM + (int)rank * QM + (int)q * 32 + (int)lane;    // this lane's channel
       const bool jv = j < p.n;
       const float* scp = p.scales + (size_t)(jv ? j : 0) * p.ng;
-      // ACC: exact int32 sums over the groups (the debug tap); else f32 promotion with the scale
-      typename std::conditional<ACC, int, float>::type y[64];
+      // ACC: exact int32 sums over the groups (the debug tap).  Else f32 promotion with the scale,
+      // on packed pairs: the int32 accumulator (a multiple of 16, |acc| < 2^22) becomes a float by
+      // the magic-number add (IADD: bits of 1.5 * 2^23 + acc, exact) and FADD2 (- 1.5 * 2^23,
+      // exact), then FFMA2 into y — one ALU and one FMA-pipe operation per element (I2FP, the
+      // conversion instruction, issues at a quarter of the ALU rate and bound this loop)
+      int yi[ACC ? 64 : 1];
+      uint64_t y2[ACC ? 1 : 32];
 #pragma unroll
-      for (int k = 0; k < 64; ++k) y[k] = 0;
+      for (int k = 0; k < (ACC ? 64 : 1); ++k) yi[k] = 0;
+#pragma unroll
+      for (int k = 0; k < (ACC ? 1 : 32); ++k) y2[k] = 0ull;
+      const uint64_t magic2 = w2_pack(0x4B400000u, 0x4B400000u);
       float sc_next = jv ? __ldg(scp) : 0.f;
       for (int g = 0; g < p.ng; ++g) {
         const uint32_t buf = acnt % NBUF, bph = (acnt / NBUF) & 1u;
         ++acnt;
         const float sc = sc_next * 0.0625f;               // Delta_jg / 16 (exact)
+        const uint64_t sc2 = w2_pack(__float_as_uint(sc), __float_as_uint(sc));
         if (g + 1 < p.ng) sc_next = jv ? __ldg(scp + g + 1) : 0.f;
         mbar_wait(&tfull[buf], bph);
         tc_fence_after();
@@ -300,26 +363,41 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t v[32];
-          tmem_ld32(taddr + half * 32, v);
-          tmem_wait_ld();
+          if (!(p.exp & 4)) {
+            tmem_ld32(taddr + half * 32, v);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = (uint32_t)k;
+          }
           if (half == 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
           }
+          if constexpr (ACC) {
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            if (ACC) y[half * 32 + k] += ((int)v[k]) >> 4;
-            else y[half * 32 + k] = fmaf((float)(int)v[k], sc, y[half * 32 + k]);
+            for (int k = 0; k < 32; ++k) yi[half * 32 + k] += ((int)v[k]) >> 4;
+          } else if (!(p.exp & 1)) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const uint64_t f = w2_sub(w2_pack(v[2 * k] + 0x4B400000u, v[2 * k + 1] + 0x4B400000u), magic2);
+              y2[half * 16 + k] = w2_fma(f, sc2, y2[half * 16 + k]);
+            }
           }
         }
+      }
+      float y[ACC ? 1 : 64];
+      if constexpr (!ACC) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) w2_unpack(y2[k], y[2 * k], y[2 * k + 1]);
       }
       const int t0 = w.mt * QN + h * 64;
       if constexpr (ACC) {
         int32_t* out = static_cast<int32_t*>(p.out);
 #pragma unroll
         for (int k = 0; k < 64; ++k)
-          if (jv && t0 + k < p.T) out[(size_t)(t0 + k) * p.ld_out + j] = (int)y[k];
+          if (jv && t0 + k < p.T) out[(size_t)(t0 + k) * p.ld_out + j] = yi[k];
       } else {
 #pragma unroll
         for (int k = 0; k < 64; ++k) y[k] *= (t0 + k < p.T) ? __ldg(p.dx + t0 + k) : 0.f;
@@ -363,7 +441,9 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
 cudaError_t launch_w4g_gemm(const W4gArgs& g, cudaStream_t st) {
   if (g.T <= 0 || g.n <= 0) return cudaSuccess;
   CUtensorMap tpk, tx, tl2, tz;
-  bool ok = make_tmap_2d(&tpk, g.packed, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.n, g.d / 2, g.d / 2, QM, 64, false);
+  // packed [ng][n][64 B] (group-major): a CTA's group tile is one contiguous 8 KB block
+  bool ok = make_tmap_2d(&tpk, g.packed, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)(g.d / QK) * g.n, 64, 64, QM,
+                         64, false);
   ok &= make_tmap_2d(&tx, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, QNH, 128, true);
   const bool cmc = !g.acc_mode && g.rpad > 0 && g.n_mod > 1;
   if (cmc) {
@@ -394,6 +474,13 @@ cudaError_t launch_w4g_gemm(const W4gArgs& g, cudaStream_t st) {
   p.out = g.out;
   p.ld_out = g.ld_out;
   p.acc_mode = g.acc_mode;
+  {
+    static const int env_exp = [] {                      // measurement knob only
+      const char* e = getenv("MASQ_W4G_EXP");
+      return e ? atoi(e) : 0;
+    }();
+    p.exp = env_exp;
+  }
   const void* fn = g.acc_mode ? reinterpret_cast<const void*>(w4g_gemm_kernel<true>)
                               : reinterpret_cast<const void*>(w4g_gemm_kernel<false>);
   {

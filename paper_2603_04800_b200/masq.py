@@ -361,9 +361,10 @@ def linear_decode(X, s_t, packed, scales, abits: int = 8, group: int = 128, Y=No
 
 
 def quantize_weight_w4g(W, s_vec, group: int = 128, stream=None):
-    """(packed uint8 [n, d/2] in the prefill GEMM's K-major nibble order, scales f32 [n, d/group])."""
+    """(packed uint8 [d/group, n, 64] in the prefill GEMM's group-major nibble order, scales f32
+    [n, d/group])."""
     d, n = W.shape
-    packed = torch.empty(n, d // 2, dtype=torch.uint8, device=W.device)
+    packed = torch.empty(d // group, n, 64, dtype=torch.uint8, device=W.device)
     scales = torch.empty(n, d // group, dtype=torch.float32, device=W.device)
     _ck(lib().masq_quantize_weight_w4g(_p(W.contiguous()), _dt(W), _p(s_vec.contiguous()), d, n, group, _p(packed),
                                        _p(scales), _stream(stream)), "masq_quantize_weight_w4g")
@@ -375,7 +376,7 @@ def linear_forward_w4g(X, mod_id, s, packed, scales, abits: int = 8, L1=None, L2
     """Prefill W4A8 forward with packed int4 group-scaled weights (+ CMC): f32 [T x n]
     (acc_debug: the int32 sum over groups of the unscaled accumulators)."""
     T, d = X.shape
-    n = packed.shape[0]
+    n = scales.shape[0]
     n_mod = s.shape[0]
     r = 0 if L1 is None else int(L1.shape[-1])
     ld_l2 = 0 if L2 is None else int(L2.stride(-2))

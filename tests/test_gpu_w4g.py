@@ -21,12 +21,14 @@ TOL_Y = 1e-3
 
 
 def pack_w4g(codes):
-    """The prefill layout of include/masq.h from integer codes [n x d]: in the 64 bytes of group g,
-    byte 16c + i = code[128g + 32c + i] & 0xF | (code[128g + 32c + 16 + i] & 0xF) << 4."""
+    """The prefill layout of include/masq.h from integer codes [n x d]: [d/128][n][64] with byte
+    16c + i of (group g, channel j) = code[j][128g + 32c + i] & 0xF | (code[j][128g + 32c + 16 + i]
+    & 0xF) << 4."""
     c = np.asarray(codes, np.int16) & 0xF
     n, d = c.shape
-    c = c.reshape(n, d // 32, 2, 16)                          # [n][32-code chunk][lo/hi half][16]
-    return (c[:, :, 0, :] | (c[:, :, 1, :] << 4)).astype(np.uint8).reshape(n, d // 2)
+    c = c.reshape(n, d // 128, 4, 2, 16)                      # [n][group][32-code chunk][lo/hi][16]
+    b = (c[:, :, :, 0, :] | (c[:, :, :, 1, :] << 4)).astype(np.uint8).reshape(n, d // 128, 64)
+    return np.ascontiguousarray(b.transpose(1, 0, 2))
 
 
 def per_modality_err(Y, Yo, ids):
