@@ -48,6 +48,25 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   uint32_t want = 0;
   for (int mm = m0; mm < m1; ++mm) want |= 1u << mm;
   if (!(tmask & want)) return;                   // CTA-uniform: no modality of this pass here
+  if (!(tile_mask[mt] & want)) {
+    // none of this tile's tokens belongs to the pass, only its pair tile's: the unit's CMC K-blocks
+    // need zero Z rows here, not a product (no X read, no MMA).  Split-K: the combine kernel
+    // writes them (rows of other modalities are zero there)
+    if (splits > 1 && !pair) return;
+    if (blockIdx.z != 0) return;
+    const int zld = (n_mod - 1) * 2 * rpad;
+    const int chunks = (2 * rpad) / 8;                          // 16-byte chunks per modality block
+    for (int mm = m0; mm < m1; ++mm) {
+      if (!((tmask >> mm) & 1u)) continue;
+      for (int e = threadIdx.x; e < 128 * chunks; e += blockDim.x) {
+        const int rl = e / chunks, c = e - rl * chunks;
+        const int g = mt * 128 + rl;
+        if (g < T)
+          *reinterpret_cast<uint4*>(Z + (int64_t)g * zld + (int64_t)(mm - 1) * 2 * rpad + c * 8) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    return;
+  }
 
   const int N = per * rpad;                      // accumulator columns (= B box rows)
   const bool combined = 2 * N <= 256;            // [hi; lo] planes as one B operand
