@@ -373,6 +373,17 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
 
 // dw[j] = max(amax[j] / q_max, 1e-12f) (the output scales) and rcp[j] = the f32 reciprocal
 // 1/dw[j] used by the fast quantizer path; amax (the column maxima) is kept for N1's arg-max
+// column panel [c0, c0 + ncols) of every set k (rows k * ss + j of amax / dw / rcp)
+__global__ void wscale_panel_kernel(const uint32_t* __restrict__ amax, float* __restrict__ dw, float* __restrict__ rcp,
+                                    int64_t ncols, int64_t ss, float qmaxf) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  const int64_t idx = (int64_t)blockIdx.y * ss + j;
+  const float dv = fmaxf(__fdiv_rn(__uint_as_float(amax[idx]), qmaxf), kFloor);
+  dw[idx] = dv;
+  rcp[idx] = __fdiv_rn(1.0f, dv);
+}
+
 __global__ void wscale_kernel(const uint32_t* __restrict__ amax, float* __restrict__ dw, float* __restrict__ rcp,
                               int64_t count, float qmaxf) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -387,12 +398,13 @@ __global__ void wscale_kernel(const uint32_t* __restrict__ amax, float* __restri
 // are packed 4 rows per 32-bit word into a smem tile [JT j][128 i] and written K-major.
 // the NS factor sets of one 128 (i) x JT (j) tile held as f[4][CPT] (rows 4ty..4ty+3, columns
 // jb..jb+CPT-1 of this thread): codes -> smem transpose -> K-major 16-byte stores
+// n: columns of this call (a panel of W); ss: the stride between factor sets (the full n)
 template <int NS, int CPT>
 __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64_t i0, int64_t j0, int tx, int ty,
                                                  int64_t jb, bool colok, const float* __restrict__ s, int64_t d,
                                                  int64_t n, int qmin, int qmax, const float* __restrict__ rcp,
                                                  int8_t* __restrict__ qw, const float* __restrict__ dw,
-                                                 uint32_t (*tile)[33]) {
+                                                 uint32_t (*tile)[33], int64_t ss) {
   constexpr int JT = 8 * CPT;
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
@@ -404,7 +416,7 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
     }
     float rcv[CPT];
     if (colok) {
-      const float4* r4 = reinterpret_cast<const float4*>(rcp + (int64_t)k * n + jb);
+      const float4* r4 = reinterpret_cast<const float4*>(rcp + (int64_t)k * ss + jb);
 #pragma unroll
       for (int q = 0; q < CPT / 4; ++q) {
         const float4 a = __ldg(r4 + q);
@@ -436,7 +448,7 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
       uint32_t word = __byte_perm(__byte_perm(__float_as_uint(t0), __float_as_uint(t1), 0x0040),
                                   __byte_perm(__float_as_uint(t2), __float_as_uint(t3), 0x0040), 0x5410);
       if (fmaxf(fmax3(fabsf(e0), fabsf(e1), fabsf(e2)), fabsf(e3)) > kLim)
-        word = quant4_exact_ool(a, b, __ldg(dw + (int64_t)k * n + jb + e), rcv[e], qmin, qmax);
+        word = quant4_exact_ool(a, b, __ldg(dw + (int64_t)k * ss + jb + e), rcv[e], qmin, qmax);
       tile[tx * CPT + e][ty] = word;
     }
     __syncthreads();
@@ -447,7 +459,7 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
       const int64_t j = j0 + jr, i = i0 + part * 16;
       if (j < n && i < d) {
         const uint32_t* t = &tile[jr][part * 4];
-        *reinterpret_cast<uint4*>(qw + ((int64_t)k * n + j) * d + i) = make_uint4(t[0], t[1], t[2], t[3]);
+        *reinterpret_cast<uint4*>(qw + ((int64_t)k * ss + j) * d + i) = make_uint4(t[0], t[1], t[2], t[3]);
       }
     }
     __syncthreads();
@@ -487,7 +499,7 @@ __global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __r
       for (int e = 0; e < V; ++e) f[r][l * V + e] = g[e];
     }
   }
-  wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile);
+  wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile, n);
 }
 
 // TMA-fed persistent variant (bf16 W): 128 x 128 tiles of W stream through a shared-memory ring
@@ -504,7 +516,7 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
                                                             const float* __restrict__ s, int64_t d, int64_t n,
                                                             int qmin, int qmax, const float* __restrict__ rcp,
                                                             int8_t* __restrict__ qw, const float* __restrict__ dw,
-                                                            int64_t tiles_j, int64_t ntiles) {
+                                                            int64_t tiles_j, int64_t ntiles, int64_t ss) {
   constexpr int CPT = 16;
   extern __shared__ __align__(128) uint8_t wsm[];
   uint8_t* ring = wsm;
@@ -560,7 +572,7 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
       if (tn < ntiles) issue(tn, st);
     }
     if (++st == kWqStages) { st = 0; ph ^= 1u; }
-    wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile);
+    wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile, ss);
   }
 }
 
@@ -572,7 +584,7 @@ template <int NS>
 __global__ void __launch_bounds__(256, 2) wcolmax_tma_kernel(const __grid_constant__ CUtensorMap tmW,
                                                              const float* __restrict__ s, int64_t d, int64_t n,
                                                              int64_t tiles_j, int64_t tiles_i, int rs,
-                                                             int64_t units, uint32_t* __restrict__ amax) {
+                                                             int64_t units, uint32_t* __restrict__ amax, int64_t ss) {
   constexpr int CPT = 16;
   extern __shared__ __align__(128) uint8_t wsm[];
   uint8_t* ring = wsm;
@@ -678,7 +690,7 @@ __global__ void __launch_bounds__(256, 2) wcolmax_tma_kernel(const __grid_consta
       for (int w = 1; w < 8; ++w) v = fmaxf(v, red[w][c]);
       const int k = c / 128;
       const int64_t j = jt * 128 + (c - k * 128);
-      if (j < n && v > 0.f) atomicMax(amax + (int64_t)k * n + j, __float_as_uint(v));
+      if (j < n && v > 0.f) atomicMax(amax + (int64_t)k * ss + j, __float_as_uint(v));
     }
     __syncthreads();
   }
@@ -1382,41 +1394,73 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   strips = (int)ceil_div(d, rows);
   constexpr int CPT = NS == 1 ? 8 : 16;            // measured: 16 columns per thread pays off for >= 2 sets
   dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 8 * CPT), (unsigned)ceil_div(d, 128));
+  if constexpr (sizeof(WT) == 2 && NS <= 2) {
+    // bf16 W: the TMA-fed column maxima and quantization kernels, one column panel of W at a time,
+    // the panel sized to stay L2-resident between the two passes (pass 2 then reads W from L2:
+    // one HBM read of W in total instead of two)
+    static const bool v1 = getenv("MASQ_WCOLMAX_V1") != nullptr || getenv("MASQ_WQUANT_V1") != nullptr;
+    static const int64_t panel_bytes = [] {
+      const char* e = getenv("MASQ_WQ_PANEL_MB");                   // measurement knob (0: no panels)
+      const int64_t mb = e ? atoll(e) : 0;                          // measured: panels lose (launch tails)
+      return mb > 0 ? mb << 20 : ((int64_t)1 << 62);
+    }();
+    if (!v1) {
+      int64_t P = std::max<int64_t>(128, (panel_bytes / (2 * d)) / 128 * 128);
+      if (P >= n) P = n;
+      const int smem_c = kWqStages * kWqTileBytes + 8 * NS * 128 * 4 + 64;
+      cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(wcolmax_tma_kernel<NS>), smem_c);
+      if (e != cudaSuccess) return e;
+      e = set_max_dyn_smem(reinterpret_cast<const void*>(wquant_tma_kernel<NS>), kWqSmem);
+      if (e != cudaSuccess) return e;
+      for (int64_t c0 = 0; c0 < n; c0 += P) {
+        const int64_t pc = std::min<int64_t>(P, n - c0);
+        CUtensorMap tm;
+        if (!make_tmap_2d(&tm, w + c0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, pc, n, 128, 128, false))
+          return cudaErrorInvalidValue;
+        const int64_t tj = ceil_div(pc, 128), ti = ceil_div(d, 128);
+        {
+          ProfScope ps_("wcolmax", st);
+          // row runs sized so that there are >= 2 units per SM (bounded atomic traffic)
+          const int rs = (int)std::max<int64_t>(1, std::min<int64_t>(ti, tj * ti / (2 * (int64_t)num_sms())));
+          const int64_t units = tj * ceil_div(ti, rs);
+          const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms() * 2);
+          wcolmax_tma_kernel<NS><<<(unsigned)grid, 256, smem_c, st>>>(tm, s, d, pc, tj, ti, rs, units, amax + c0, n);
+        }
+        {
+          ProfScope ps_("wscale", st);
+          wscale_panel_kernel<<<dim3((unsigned)ceil_div(pc, 256), NS), 256, 0, st>>>(amax + c0, dw + c0, rcp + c0, pc,
+                                                                                      n, (float)qmax);
+        }
+        {
+          ProfScope ps_("wquant", st);
+          const int64_t grid = std::min<int64_t>(tj * ti, (int64_t)num_sms() * 2);
+          wquant_tma_kernel<NS><<<(unsigned)grid, 256, kWqSmem, st>>>(tm, s, d, pc, qmin, qmax, rcp + c0, qw + c0 * d,
+                                                                       dw + c0, tj, tj * ti, n);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+  }
   {
     ProfScope ps_("wcolmax", st);
-    static const bool v1 = getenv("MASQ_WCOLMAX_V1") != nullptr;   // measurement switch
-    bool done = false;
-    if constexpr (sizeof(WT) == 2 && NS <= 2) {          // 3-4 sets would spill the running maxima
-      CUtensorMap tm;
-      const int64_t tj = ceil_div(n, 128), ti = ceil_div(d, 128);
-      if (!v1 && make_tmap_2d(&tm, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, n, n, 128, 128, false)) {
-        const int smem = kWqStages * kWqTileBytes + 8 * NS * 128 * 4 + 64;
-        cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(wcolmax_tma_kernel<NS>), smem);
-        if (e != cudaSuccess) return e;
-        // row runs sized so that there are >= 2 units per SM (bounded atomic traffic)
-        const int rs = (int)std::max<int64_t>(1, std::min<int64_t>(ti, tj * ti / (2 * (int64_t)num_sms())));
-        const int64_t units = tj * ceil_div(ti, rs);
-        const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms() * 2);
-        wcolmax_tma_kernel<NS><<<(unsigned)grid, 256, smem, st>>>(tm, s, d, n, tj, ti, rs, units, amax);
-        done = true;
-      }
-    }
-    if (!done) wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax);
+    wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax);
   }
   { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, rcp, NS * n, (float)qmax); }
   {
     ProfScope ps_("wquant", st);
-    static const bool v1 = getenv("MASQ_WQUANT_V1") != nullptr;    // measurement switch
+    static const bool v1q = getenv("MASQ_WQUANT_V1") != nullptr;   // measurement switch
     bool done = false;
-    if constexpr (sizeof(WT) == 2) {
+    if constexpr (sizeof(WT) == 2) {                     // 3-4 sets: the TMA-fed quantizer, full width
       CUtensorMap tm;
       const int64_t tj = ceil_div(n, 128), ti = ceil_div(d, 128);
-      if (!v1 && make_tmap_2d(&tm, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, n, n, 128, 128, false)) {
+      if (!v1q && make_tmap_2d(&tm, w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, n, n, 128, 128, false)) {
         cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(wquant_tma_kernel<NS>), kWqSmem);
         if (e != cudaSuccess) return e;
         const int64_t grid = std::min<int64_t>(tj * ti, (int64_t)num_sms() * 2);
         wquant_tma_kernel<NS><<<(unsigned)grid, 256, kWqSmem, st>>>(tm, s, d, n, qmin, qmax, rcp, qw, dw, tj,
-                                                                     tj * ti);
+                                                                     tj * ti, n);
         done = true;
       }
     }
