@@ -449,7 +449,13 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
                                   __byte_perm(__float_as_uint(t2), __float_as_uint(t3), 0x0040), 0x5410);
       if (fmaxf(fmax3(fabsf(e0), fabsf(e1), fabsf(e2)), fabsf(e3)) > kLim)
         word = quant4_exact_ool(a, b, __ldg(dw + (int64_t)k * ss + jb + e), rcv[e], qmin, qmax);
-      tile[tx * CPT + e][ty] = word;
+      // word index swizzled by bits 5-6 of the row (XOR with 0/4/8/12, keeping 4-word groups
+      // contiguous for the 16-byte reads below): rows tx * CPT + e of the even / odd tx then fall
+      // in distinct banks (a plain 33-word stride maps rows 0, 32, 64, 96 to one bank: 4-way conflicts)
+      {
+        const int row = tx * CPT + e;
+        tile[row][ty ^ (((row >> 5) & 3) << 2)] = word;
+      }
     }
     __syncthreads();
     // write JT rows (j) x 128 bytes (i): 8 threads per row, 16 bytes each
@@ -458,7 +464,7 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
       const int jr = q * 32 + (threadIdx.x >> 3), part = threadIdx.x & 7;
       const int64_t j = j0 + jr, i = i0 + part * 16;
       if (j < n && i < d) {
-        const uint32_t* t = &tile[jr][part * 4];
+        const uint32_t* t = &tile[jr][(part * 4) ^ (((jr >> 5) & 3) << 2)];
         *reinterpret_cast<uint4*>(qw + ((int64_t)k * ss + j) * d + i) = make_uint4(t[0], t[1], t[2], t[3]);
       }
     }

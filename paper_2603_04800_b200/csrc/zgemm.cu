@@ -23,6 +23,10 @@ using namespace sm100;
 namespace {
 constexpr int ZT = 192;
 constexpr int XCH = 128 * 128;       // A chunk: 128 rows x 64 bf16
+// ksub (kernel argument): 64-column sub-blocks per ring stage; two adjacent SWIZZLE_128B boxes
+// give 256-byte row segments of X per stage (one box alone reads 128 B per row at a d * 2-byte
+// stride); one when a stage of two would not leave two ring stages (large ranks)
+constexpr int KSUB_MAX = 2;
 constexpr int SMEM_CAP = 200 * 1024;
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -37,7 +41,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
              const __grid_constant__ CUtensorMap tmB, const uint8_t* __restrict__ ids, int T, int d, int n_mod,
              int rpad, int per, int a_planes, uint32_t tmem_cols, int stages,
              const uint32_t* __restrict__ tile_mask, uint16_t* __restrict__ Z, float* __restrict__ zpart,
-             int splits, int pair) {
+             int splits, int pair, int ksub) {
   const int mt = blockIdx.x;
   const int m0 = 1 + blockIdx.y * per;
   const int m1 = min(m0 + per, n_mod);           // exclusive
@@ -71,7 +75,8 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   const int N = per * rpad;                      // accumulator columns (= B box rows)
   const bool combined = 2 * N <= 256;            // [hi; lo] planes as one B operand
   const int BB = N * 128;                        // one B plane chunk
-  const int SB = ((a_planes * XCH + 2 * BB) + 1023) & ~1023;
+  const int SBS = a_planes * XCH + 2 * BB;       // one 64-column sub-block of a stage
+  const int SB = ((ksub * SBS) + 1023) & ~1023;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -96,7 +101,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   const uint32_t tmem = *tslot;
   // split-K (small T): CTA z takes k-chunks [kc0, kc1) and writes an f32 partial; a combine kernel
   // adds the partials in split order
-  const int nk_all = (d + 63) / 64;
+  const int nk_all = (d + 64 * ksub - 1) / (64 * ksub);
   const int kc0 = (int)((int64_t)nk_all * blockIdx.z / splits);
   const int kc1 = (int)((int64_t)nk_all * (blockIdx.z + 1) / splits);
   const int nk = kc1 - kc0;
@@ -107,13 +112,18 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
       uint32_t st = 0, ph = 0;
       for (int kc = kc0; kc < kc1; ++kc) {
         mbar_wait(&empty[st], ph ^ 1u);
-        mbar_expect_tx(&full[st], a_planes * XCH + 2 * BB);
-        uint8_t* base = smem + st * SB;
-        tma_load_2d(base, &tmA0, &full[st], kc * 64, mt * 128);
-        if (a_planes == 2) tma_load_2d(base + XCH, &tmA1, &full[st], kc * 64, mt * 128);
-        uint8_t* bb = base + a_planes * XCH;
-        tma_load_2d(bb, &tmB, &full[st], kc * 64, (m0 - 1) * rpad);
-        tma_load_2d(bb + BB, &tmB, &full[st], kc * 64, lo_row0 + (m0 - 1) * rpad);
+        mbar_expect_tx(&full[st], ksub * SBS);
+#pragma unroll
+        for (int sb = 0; sb < KSUB_MAX; ++sb) {
+          if (sb >= ksub) break;
+          const int col = (kc * ksub + sb) * 64;         // past d: TMA zero-fills the whole box
+          uint8_t* base = smem + st * SB + sb * SBS;
+          tma_load_2d(base, &tmA0, &full[st], col, mt * 128);
+          if (a_planes == 2) tma_load_2d(base + XCH, &tmA1, &full[st], col, mt * 128);
+          uint8_t* bb = base + a_planes * XCH;
+          tma_load_2d(bb, &tmB, &full[st], col, (m0 - 1) * rpad);
+          tma_load_2d(bb + BB, &tmB, &full[st], col, lo_row0 + (m0 - 1) * rpad);
+        }
         if (++st == (uint32_t)stages) { st = 0; ph ^= 1u; }
       }
     }
@@ -129,14 +139,18 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&full[st], ph);
         tc_fence_after();
-        const uint32_t base = smem_u32(smem + st * SB);
-        const uint32_t bh = base + a_planes * XCH, bl = bh + BB;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bh + k * 32), idesc, (kc | k) != 0);
-          if (!combined) mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bl + k * 32), idesc, 1u);
-          if (a_planes == 2)
-            mma_bf16(tmem, umma_desc_sw128(base + XCH + k * 32), umma_desc_sw128(bh + k * 32), idesc, 1u);
+        for (int sb = 0; sb < KSUB_MAX; ++sb) {
+          if (sb >= ksub) break;
+          const uint32_t base = smem_u32(smem + st * SB + sb * SBS);
+          const uint32_t bh = base + a_planes * XCH, bl = bh + BB;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bh + k * 32), idesc, (kc | sb | k) != 0);
+            if (!combined) mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bl + k * 32), idesc, 1u);
+            if (a_planes == 2)
+              mma_bf16(tmem, umma_desc_sw128(base + XCH + k * 32), umma_desc_sw128(bh + k * 32), idesc, 1u);
+          }
         }
         mma_commit(&empty[st]);
         if (++st == (uint32_t)stages) { st = 0; ph ^= 1u; }
@@ -381,16 +395,16 @@ __global__ void __launch_bounds__(256) zcombine_kernel(const float* __restrict__
 }  // namespace
 
 int zgemm_splits(int64_t T, int64_t d) {
-  const int64_t tiles = ceil_div(T, 128), nk = ceil_div(d, 64);
+  const int64_t tiles = ceil_div(T, 128), nk = ceil_div(d, 64 * KSUB_MAX);
   static const int env_sp = [] {                         // measurement knob: forced split count
     const char* e = getenv("MASQ_ZGEMM_SPLITS");
     return e ? atoi(e) : 0;
   }();
-  if (env_sp > 0) return (int)std::max<int64_t>(1, std::min<int64_t>(env_sp, nk / 4));
+  if (env_sp > 0) return (int)std::max<int64_t>(1, std::min<int64_t>(env_sp, nk / 2));
   if (tiles <= 0 || tiles * 2 > num_sms()) return 1;     // enough tiles to fill the GPU
   int64_t sp = num_sms() / tiles;
   sp = std::min<int64_t>(sp, 16);
-  sp = std::min<int64_t>(sp, nk / 4);                    // >= 4 k-chunks per split
+  sp = std::min<int64_t>(sp, nk / 2);                    // >= 2 k-chunks (256 columns) per split
   return (int)std::max<int64_t>(sp, 1);
 }
 
@@ -437,7 +451,16 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   ok &= make_tmap_2d(&tb, L1s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)2 * n_nt * rpad, d, d, (uint32_t)N, 64,
                      true);
   if (!ok) return cudaErrorInvalidValue;
-  const int SB = ((a_planes * XCH + 2 * N * 128) + 1023) & ~1023;
+  const int SBS = a_planes * XCH + 2 * N * 128;
+  // measured (c3 step): two sub-blocks per stage make the pair-mode CTAs 1 per SM and lose
+  // (zgemm 0.26 -> 0.36 ms per step), so one is the default
+  int ksub = 1;
+  static const int env_ks = [] {                         // measurement knob: sub-blocks per stage
+    const char* e = getenv("MASQ_ZGEMM_KSUB");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_ks >= 1 && env_ks <= KSUB_MAX) ksub = env_ks;
+  const int SB = ((ksub * SBS) + 1023) & ~1023;
   // cluster-pair split-K (two K halves per 128-row tile, reduced through DSMEM) when the tiles
   // alone leave SMs idle but no global split is taken: 3 stages so two CTAs fit per SM
   static const bool no_pair = [] {
@@ -446,7 +469,7 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
   }();
   const int64_t tiles = ceil_div(T, 128);
   const bool pair = !no_pair && zpart != nullptr && zgemm_splits(T, d) == 1 && a_planes == 1 && 2 * N <= 256 &&
-                    tiles <= num_sms() && ceil_div(d, 64) >= 8;
+                    tiles <= num_sms() && ceil_div(d, 64 * KSUB_MAX) >= 4;
   int stages = (SMEM_CAP - 2048) / SB;
   stages = stages > 8 ? 8 : stages;
   if (pair) stages = std::min(stages, 3);
@@ -480,11 +503,11 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
       cfg.attrs = at;
       cfg.numAttrs = 1;
       e = cudaLaunchKernelEx(&cfg, zgemm_kernel, ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
-                             stages, tile_mask, Z, (float*)nullptr, 2, 1);
+                             stages, tile_mask, Z, (float*)nullptr, 2, 1, ksub);
       if (e != cudaSuccess) return e;
     } else {
       zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
-                                           stages, tile_mask, Z, zpart, splits, 0);
+                                           stages, tile_mask, Z, zpart, splits, 0, ksub);
     }
   }
   if (splits > 1 && !pair) {

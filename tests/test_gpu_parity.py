@@ -51,6 +51,14 @@ def max_abs_norm(a, b):
     return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-300))
 
 
+def max_abs_norm_per_modality(a, b, ids):
+    """max over modalities of the max-abs error normalised by THAT modality's max |b| (image
+    outputs are ~20x text outputs: a global normalisation would check text rows ~20x looser)."""
+    a = np.asarray(a, np.float64)
+    return max(float(np.abs(a[ids == m] - b[ids == m]).max() / max(np.abs(b[ids == m]).max(), 1e-300))
+               for m in np.unique(ids))
+
+
 CASES = {
     # name: (config, overrides)
     "c1": ("c1", {}),
@@ -174,7 +182,7 @@ def test_forward_parity(name, use_cmc):
     L1o = list(c["L1"]) if L1 is not None else None
     L2o = list(c["L2"]) if L2 is not None else None
     Yo = O.linear_forward(c["X"], c["ids"], so, qwo, dwo, c["abits"], L1o, L2o, rows=rows)
-    assert max_abs_norm(Y[rows], Yo) <= TOL_Y
+    assert max_abs_norm_per_modality(Y[rows], Yo, c["ids"][rows]) <= TOL_Y
 
 
 @pytest.mark.parametrize("r", [64, 192])
@@ -189,7 +197,7 @@ def test_forward_c3_gate_cmc_sampled(r):
     m.check()
     rows = sample_rows(c["ids"], n_random=128)
     Yo = O.linear_forward(c["X"], c["ids"], so, qwo, dwo, 8, list(c["L1"]), list(c["L2"]), rows=rows)
-    assert max_abs_norm(Y.cpu().numpy()[rows], Yo) <= TOL_Y
+    assert max_abs_norm_per_modality(Y.cpu().numpy()[rows], Yo, c["ids"][rows]) <= TOL_Y
 
 
 def test_forward_shuffled_ids_three_modalities():
@@ -199,7 +207,7 @@ def test_forward_shuffled_ids_three_modalities():
     _, _, so, qwo, dwo = oracle_state(c)
     Y = m.linear_forward(bf(c["X"]), tt(c["ids"]), tt(so), tt(qwo), tt(dwo), 8, 8, bf(c["L1"]), bf(c["L2"]))
     Yo = O.linear_forward(c["X"], c["ids"], so, qwo, dwo, 8, list(c["L1"]), list(c["L2"]))
-    assert max_abs_norm(Y.cpu().numpy(), Yo) <= TOL_Y
+    assert max_abs_norm_per_modality(Y.cpu().numpy(), Yo, c["ids"]) <= TOL_Y
 
 
 def test_forward_column_shard_matches_full():
@@ -235,7 +243,7 @@ def test_reference_output():
     Yr = m.reference_output(bf(c["X"]), bf(c["W"])).cpu().numpy()
     rows = sample_rows(c["ids"])
     Yo = O.reference_output(c["X"], c["W"], rows=rows)
-    assert max_abs_norm(Yr[rows], Yo) <= 1e-5
+    assert max_abs_norm_per_modality(Yr[rows], Yo, c["ids"][rows]) <= 1e-5
 
 
 @pytest.mark.parametrize("name", ["c1", "ragged3", "c3_qkv"])
@@ -311,7 +319,7 @@ def test_forward_f32_input_with_cmc():
     qxo, dxo = O.quantize_activations(Xf, c["ids"], so, 8)
     assert np.array_equal(qx.cpu().numpy(), qxo) and np.array_equal(dx.cpu().numpy(), dxo)
     Yo = O.linear_forward(Xf, c["ids"], so, qwo, dwo, 8, list(c["L1"]), list(c["L2"]))
-    assert max_abs_norm(Y.cpu().numpy(), Yo) <= TOL_Y
+    assert max_abs_norm_per_modality(Y.cpu().numpy(), Yo, c["ids"]) <= TOL_Y
 
 
 def test_forward_max_tokens_sampled():
@@ -334,7 +342,7 @@ def test_forward_max_tokens_sampled():
     rows = np.concatenate([np.arange(0, 256), np.arange(T - 256, T),
                            np.random.Generator(np.random.PCG64(7)).choice(T, 512, replace=False)])
     Yo = O.linear_forward(X, ids, so, qwo, dwo, 8, [L1[0]], [L2[0]], rows=rows)
-    assert max_abs_norm(Y.cpu().numpy()[rows], Yo) <= TOL_Y
+    assert max_abs_norm_per_modality(Y.cpu().numpy()[rows], Yo, ids[rows]) <= TOL_Y
     qxo, _ = O.quantize_activations(O.decode(X)[rows], ids[rows], so, 8)
     assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), O.int_gemm(qxo, qwo))
 
@@ -360,7 +368,7 @@ def test_eight_modalities_end_to_end():
     assert np.array_equal(qwg.cpu().numpy(), qw) and np.array_equal(dwg.cpu().numpy(), dw)
     Y = m.linear_forward(bf(X), tt(ids), sg, qwg, dwg, 8, 8, bf(L1), bf(L2)).cpu().numpy()
     Yo = O.linear_forward(X, ids, s, qw, dw, 8, list(L1), list(L2))
-    assert max_abs_norm(Y, Yo) <= TOL_Y
+    assert max_abs_norm_per_modality(Y, Yo, ids) <= TOL_Y
     Yref = m.reference_output(bf(X), bf(W))
     sums, counts, loss = m.calib_loss(bf(X), tt(ids), sg, bf(W), 8, 8, Yref)
     so, co, lo = O.calib_loss(X, ids, s, W, 8, 8)
