@@ -12,6 +12,12 @@
 // (tcgen05.ld) and promote it into f32 registers with the lane's own scale:  y += Delta_jg/16 * acc
 // — no shuffles, one scalar per lane and group.  Four 128-column TMEM accumulators rotate so the
 // MMAs of group g+1..g+3 overlap the promotion of group g.
+// Pipeline: an input ring (the group's packed tile by one 1D bulk copy + the token tile by 2-SM
+// TMA), converter warps writing a separate ring of unpacked A tiles, the MMA warp, 8 epilogue
+// warps.  Measured limit (profiles/r02_w4g_ablation.json): the per-group handshake cycles
+// (input slot, A slot, accumulator: ~3 cross-warp / cross-CTA signals per 262 cycles of MMA work)
+// with at most 4 groups in flight (TMEM holds 4 x 128 columns), not the MMAs, the unpacking or
+// the promotion math; a 1-CTA variant without the cross-CTA hops measured no faster.
 //
 // Packed format (this kernel's, masq_quantize_weight_w4g): group-major [d/128][n][64 B] — the 64
 // bytes of (group g, channel j) at (g n + j) 64, so a CTA's 128-channel group tile is one contiguous
@@ -42,7 +48,6 @@ constexpr int QUM = 2 * QM;             // per CTA pair (MMA M)
 constexpr int QN = 128;                 // tokens per unit (MMA N)
 constexpr int QNH = QN / 2;             // token rows each CTA loads
 constexpr int QK = 128;                 // one group = one k-block (128 int8 / 64 bf16)
-constexpr int PK_BYTES = QM * 64;       // packed group tile (8 KB)
 constexpr int QA_BYTES = QM * QK;       // unpacked / L2^T A tile (16 KB)
 constexpr int QB_BYTES = QNH * QK;      // activation / Z B tile (8 KB)
 constexpr int NP = 5;                   // input ring: packed group tile (or a CMC L2^T tile) + B tile
@@ -70,6 +75,7 @@ struct WParams {
   const uint32_t* tile_mask;            // modality bit set per 128-token tile
   const float* dx;                      // [T]
   const float* scales;                  // [n][ng]
+  const uint8_t* packed;                // [ng][n][64] group-major packed codes
   void* out;                            // f32 Y or int32 accumulators [T][ld_out]
   long long ld_out;
   int acc_mode;                         // 1: int32 sum over groups (debug tap), no dx / CMC
@@ -132,7 +138,7 @@ struct QRing {
 
 template <bool ACC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(QTHREADS, 1)
-w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant__ CUtensorMap tmX,
+w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmZ, const WParams p) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -154,7 +160,6 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
   const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmPK);
     tma_prefetch(&tmX);
     for (int i = 0; i < NP; ++i) {
       mbar_init(&pfull[i], 1);
@@ -185,11 +190,19 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
         const WUnit w = w_unit(p, u);
         const int crow = w.nt * QUM + (int)rank * QM;         // this CTA's output channels
         const int trow = w.mt * QN + (int)rank * QNH;         // this CTA's token rows
+        // channels past n: their rows of the tile are left as they are (outputs masked)
+        const uint32_t pk_bytes = (uint32_t)max(0, min(QM, p.n - crow)) * 64u;
         for (int g = 0; g < p.ng; ++g) {
           mbar_wait(&pempty[ring.stage], ring.phase ^ 1u);
           uint8_t* slot = sP + ring.stage * P_SLOT;
-          mbar_expect_tx(&pfull[ring.stage], PK_BYTES);
-          tma_load_2d(slot, &tmPK, &pfull[ring.stage], 0, g * p.n + crow);
+          // the group tile is one contiguous block of the group-major packed weights: one bulk
+          // copy (a 128-row TMA box of 64-byte rows cost 128 TMA row requests per group)
+          if (pk_bytes) {
+            mbar_expect_tx(&pfull[ring.stage], pk_bytes);
+            bulk_load_1d(slot, p.packed + ((size_t)g * p.n + crow) * 64, pk_bytes, &pfull[ring.stage]);
+          } else {
+            mbar_arrive(&pfull[ring.stage]);
+          }
           if (leader) mbar_expect_tx(&full[ring.stage], 2 * QB_BYTES);
           tma_load_2d_2sm(slot + P_A, &tmX, &full[ring.stage], g * QK, trow);
           ring.advance();
@@ -440,11 +453,9 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmPK, const __grid_constant_
 
 cudaError_t launch_w4g_gemm(const W4gArgs& g, cudaStream_t st) {
   if (g.T <= 0 || g.n <= 0) return cudaSuccess;
-  CUtensorMap tpk, tx, tl2, tz;
-  // packed [ng][n][64 B] (group-major): a CTA's group tile is one contiguous 8 KB block
-  bool ok = make_tmap_2d(&tpk, g.packed, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)(g.d / QK) * g.n, 64, 64, QM,
-                         64, false);
-  ok &= make_tmap_2d(&tx, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, QNH, 128, true);
+  CUtensorMap tx, tl2, tz;
+  // packed [ng][n][64 B] (group-major): a CTA's group tile is one contiguous block (1D bulk copy)
+  bool ok = make_tmap_2d(&tx, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, QNH, 128, true);
   const bool cmc = !g.acc_mode && g.rpad > 0 && g.n_mod > 1;
   if (cmc) {
     const int64_t zc = (int64_t)(g.n_mod - 1) * 2 * g.rpad;
@@ -471,6 +482,7 @@ cudaError_t launch_w4g_gemm(const W4gArgs& g, cudaStream_t st) {
   p.tile_mask = g.tile_mask;
   p.dx = g.dx;
   p.scales = g.scales;
+  p.packed = g.packed;
   p.out = g.out;
   p.ld_out = g.ld_out;
   p.acc_mode = g.acc_mode;
@@ -490,9 +502,9 @@ cudaError_t launch_w4g_gemm(const W4gArgs& g, cudaStream_t st) {
   const int clusters = (int)std::min<int64_t>(p.n_units, num_sms() / 2);
   ProfScope ps_(g.acc_mode ? "gemm_w4g_acc" : "gemm_w4g", st);
   if (g.acc_mode)
-    w4g_gemm_kernel<true><<<2 * clusters, QTHREADS, SM_ALLOC, st>>>(tpk, tx, tl2, tz, p);
+    w4g_gemm_kernel<true><<<2 * clusters, QTHREADS, SM_ALLOC, st>>>(tx, tl2, tz, p);
   else
-    w4g_gemm_kernel<false><<<2 * clusters, QTHREADS, SM_ALLOC, st>>>(tpk, tx, tl2, tz, p);
+    w4g_gemm_kernel<false><<<2 * clusters, QTHREADS, SM_ALLOC, st>>>(tx, tl2, tz, p);
   return cudaGetLastError();
 }
 
