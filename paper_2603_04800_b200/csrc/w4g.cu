@@ -80,7 +80,8 @@ struct WParams {
   long long ld_out;
   int acc_mode;                         // 1: int32 sum over groups (debug tap), no dx / CMC
   int exp;                              // measurement knob (MASQ_W4G_EXP): 1 skip promotion, 2 skip unpack,
-                                        // 4 skip the TMEM loads, 8 skip the MMAs
+                                        // 4 skip the TMEM loads, 8 skip the MMAs, 16 skip the converters'
+                                        // proxy fences, 32 skip the converters' shared stores
 };
 
 
@@ -302,7 +303,7 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
         uint4 xin[KCH];
 #pragma unroll
         for (int k = 0; k < KCH; ++k) xin[k] = (p.exp & 2) ? make_uint4(0, 0, 0, 0) : src[tid + k * 32 * CONV_WARPS];
-        fence_proxy_async_smem();                               // the reads before the slot's TMA refill
+        if (!(p.exp & 16)) fence_proxy_async_smem();            // the reads before the slot's TMA refill
         __syncwarp();
         if (lane == 0) mbar_arrive(&pempty[ring.stage]);        // packed bytes consumed
 #pragma unroll
@@ -315,6 +316,7 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
           const uint4 hi = make_uint4(x.x & 0xF0F0F0F0u, x.y & 0xF0F0F0F0u, x.z & 0xF0F0F0F0u, x.w & 0xF0F0F0F0u);
           const uint32_t d0 = dstA + row * QK + (((2u * c) ^ (row & 7u)) << 4);
           const uint32_t d1 = dstA + row * QK + (((2u * c + 1u) ^ (row & 7u)) << 4);
+          if (p.exp & 32) continue;
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d0), "r"(lo.x), "r"(lo.y), "r"(lo.z),
                        "r"(lo.w)
                        : "memory");
@@ -322,7 +324,7 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
                        "r"(hi.w)
                        : "memory");
         }
-        fence_proxy_async_smem();
+        if (!(p.exp & 16)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&aready[aring.stage], 0);
         ring.advance();
