@@ -404,16 +404,24 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
                                                  int64_t jb, bool colok, const float* __restrict__ s, int64_t d,
                                                  int64_t n, int qmin, int qmax, const float* __restrict__ rcp,
                                                  int8_t* __restrict__ qw, const float* __restrict__ dw,
-                                                 uint32_t (*tile)[33], int64_t ss) {
+                                                 uint32_t (*tiles)[33], int64_t ss, uint32_t& par) {
   constexpr int JT = 8 * CPT;
+  // the row factors of every set are loaded up front (their latency overlaps the first set's math)
+  float sis[NS][4];
 #pragma unroll
-  for (int k = 0; k < NS; ++k) {
-    float si[4];
+  for (int k = 0; k < NS; ++k)
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int64_t i = i0 + 4 * ty + r;
-      si[r] = i < d ? __ldg(s + (int64_t)k * d + i) : 0.f;
+      sis[k][r] = i < d ? __ldg(s + (int64_t)k * d + i) : 0.f;
     }
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    // two code tiles used alternately: the barrier after writing one also orders every thread's
+    // reads of the other (from the previous set or tile), so one __syncthreads per set suffices
+    uint32_t (*tile)[33] = tiles + (par & 1u) * JT;
+    ++par;
+    const float* si = sis[k];
     float rcv[CPT];
     if (colok) {
       const float4* r4 = reinterpret_cast<const float4*>(rcp + (int64_t)k * ss + jb);
@@ -468,7 +476,6 @@ __device__ __forceinline__ void wquant_tile_sets(const float (&f)[4][CPT], int64
         *reinterpret_cast<uint4*>(qw + ((int64_t)k * ss + j) * d + i) = make_uint4(t[0], t[1], t[2], t[3]);
       }
     }
-    __syncthreads();
   }
 }
 
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __r
   constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
   constexpr int LPT = CPT / V;                  // loads per row per thread
   constexpr int JT = 8 * CPT;                   // tile columns
-  __shared__ __align__(16) uint32_t tile[JT][33];   // [j][i/4] packed codes (+1 word pad)
+  __shared__ __align__(16) uint32_t tile[2 * JT][33];   // 2 x [j][i/4] packed codes (+1 word pad)
   const int64_t i0 = (int64_t)blockIdx.y * 128, j0 = (int64_t)blockIdx.x * JT;
   const int tx = threadIdx.x & 7;               // column group: j = j0 + 8*tx + e
   const int ty = threadIdx.x >> 3;              // rows 4*ty .. 4*ty+3 of the tile
@@ -505,7 +512,8 @@ __global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __r
       for (int e = 0; e < V; ++e) f[r][l * V + e] = g[e];
     }
   }
-  wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile, n);
+  uint32_t par = 0;
+  wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile, n, par);
 }
 
 // TMA-fed persistent variant (bf16 W): 128 x 128 tiles of W stream through a shared-memory ring
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __r
 #endif
 constexpr int kWqStages = MASQ_WQ_STAGES;
 constexpr int kWqTileBytes = 128 * 128 * 2;
-constexpr int kWqSmem = kWqStages * kWqTileBytes + 128 * 33 * 4 + 64;
+constexpr int kWqSmem = kWqStages * kWqTileBytes + 2 * 128 * 33 * 4 + 64;
 template <int NS>
 __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constant__ CUtensorMap tmW,
                                                             const float* __restrict__ s, int64_t d, int64_t n,
@@ -526,8 +534,9 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
   constexpr int CPT = 16;
   extern __shared__ __align__(128) uint8_t wsm[];
   uint8_t* ring = wsm;
-  uint32_t (*tile)[33] = reinterpret_cast<uint32_t(*)[33]>(wsm + kWqStages * kWqTileBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + kWqStages * kWqTileBytes + 128 * 33 * 4);
+  uint32_t (*tile)[33] = reinterpret_cast<uint32_t(*)[33]>(wsm + kWqStages * kWqTileBytes);   // 2 x 128 rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + kWqStages * kWqTileBytes + 2 * 128 * 33 * 4);
+  uint32_t par = 0;
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   auto issue = [&](int64_t t, int st) {                // thread 0: tile t -> stage st
     const int64_t jt = t % tiles_j, it = t / tiles_j;
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
       if (tn < ntiles) issue(tn, st);
     }
     if (++st == kWqStages) { st = 0; ph ^= 1u; }
-    wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile, ss);
+    wquant_tile_sets<NS, CPT>(f, i0, j0, tx, ty, jb, colok, s, d, n, qmin, qmax, rcp, qw, dw, tile, ss, par);
   }
 }
 
@@ -587,7 +596,7 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
 // crosses unit boundaries); thread (tx, ty) keeps max_i |s_k[i] w_ij| of its 16 columns over its
 // 4 rows per tile in registers; at a unit's end: shuffle + smem reduce over ty, then atomicMax.
 template <int NS>
-__global__ void __launch_bounds__(256, 2) wcolmax_tma_kernel(const __grid_constant__ CUtensorMap tmW,
+__global__ void __launch_bounds__(256, NS <= 2 ? 2 : 1) wcolmax_tma_kernel(const __grid_constant__ CUtensorMap tmW,
                                                              const float* __restrict__ s, int64_t d, int64_t n,
                                                              int64_t tiles_j, int64_t tiles_i, int rs,
                                                              int64_t units, uint32_t* __restrict__ amax, int64_t ss) {
@@ -1400,10 +1409,11 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   strips = (int)ceil_div(d, rows);
   constexpr int CPT = NS == 1 ? 8 : 16;            // measured: 16 columns per thread pays off for >= 2 sets
   dim3 g1(gx, strips), g2((unsigned)ceil_div(n, 8 * CPT), (unsigned)ceil_div(d, 128));
-  if constexpr (sizeof(WT) == 2 && NS <= 2) {
-    // bf16 W: the TMA-fed column maxima and quantization kernels, one column panel of W at a time,
-    // the panel sized to stay L2-resident between the two passes (pass 2 then reads W from L2:
-    // one HBM read of W in total instead of two)
+  if constexpr (sizeof(WT) == 2 && NS <= 3) {
+    // bf16 W, 1-3 sets: the TMA-fed column maxima and quantization kernels.  Optionally one
+    // column panel of W at a time, sized to stay L2-resident between the two passes
+    // (MASQ_WQ_PANEL_MB; off by default: measured slower, the panel launches' tails cost more than
+    // the saved HBM read)
     static const bool v1 = getenv("MASQ_WCOLMAX_V1") != nullptr || getenv("MASQ_WQUANT_V1") != nullptr;
     static const int64_t panel_bytes = [] {
       const char* e = getenv("MASQ_WQ_PANEL_MB");                   // measurement knob (0: no panels)
@@ -1429,7 +1439,8 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
           // row runs sized so that there are >= 2 units per SM (bounded atomic traffic)
           const int rs = (int)std::max<int64_t>(1, std::min<int64_t>(ti, tj * ti / (2 * (int64_t)num_sms())));
           const int64_t units = tj * ceil_div(ti, rs);
-          const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms() * 2);
+          // 3 sets: one CTA per SM (the running maxima of 3 sets need the registers of two)
+          const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms() * (NS <= 2 ? 2 : 1));
           wcolmax_tma_kernel<NS><<<(unsigned)grid, 256, smem_c, st>>>(tm, s, d, pc, tj, ti, rs, units, amax + c0, n);
         }
         {
