@@ -1330,7 +1330,10 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
   double acc[kMaxMod];
 #pragma unroll
   for (int m = 0; m < kMaxMod; ++m) acc[m] = 0.0;
+  // (unrolled: 8 iterations' loads in flight per thread; the single CTA was load-latency bound)
+#pragma unroll 8
   for (int64_t u = threadIdx.x; u < n_extra; u += 512) acc[0] += extra[u];   // text loss from the forward
+#pragma unroll 8
   for (int64_t u = threadIdx.x; u < n_units; u += 512) {         // fixed assignment -> deterministic
     const uint32_t m = tile_mod[u / num_n];
     if (m >= (uint32_t)n_mod) continue;
