@@ -30,7 +30,8 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     case MASQ_OP_CMC_GRAM:
     case MASQ_OP_CMC_FACTORS: {
       if (op != MASQ_OP_CMC_FACTORS) {
-        // tensor-core Gram (gram.cu): routing, the bf16 hi/lo planes of X S^-1, fp32 partial tiles
+        // exact tensor-core Gram (gram.cu): routing, channel maxima / exponents, the three int8
+        // slice planes of X S^-1 (transposed), f64 partial tiles
         const int64_t Tg = grouped_rows(T, n_mod);
         L.inv_s = take(sizeof(float) * n_mod * d);
         L.perm = take(sizeof(int32_t) * (Tg + route_scratch_ints(T)));

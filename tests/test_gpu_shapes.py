@@ -93,6 +93,51 @@ def test_calib_layer_at_bench_shape(cfg, name, d, n):
     assert abs(float(loss.cpu()[0]) - lo) <= TOL_L * abs(lo)
 
 
+@pytest.mark.parametrize("name", ["qkv", "o", "gate_up", "down"])
+def test_calib_layer_c3_full_batch(name):
+    """The c3 linears at the bench's own batch, 16384 tokens, i.e. in exactly the launch
+    configuration bench.py times (e.g. the CMC first factor's cluster-pair DSMEM split-K path,
+    which smaller batches do not take): weight codes / scales bit-exact, int32 accumulators
+    bit-exact and Y per modality <= 1e-3 on sampled rows (first / last tiles of 12 modality
+    segments + 128 random rows), X W on the same rows <= 1e-4.  (The loss, a sum over every row,
+    is checked against the oracle at 4096 tokens above.)"""
+    d, n = {k: (dd, nn) for k, dd, nn in synth.LAYER_LINEARS["c3"]}[name]
+    c = synth.config_inputs("c3", d=d, n=n, layer=11 + [x[0] for x in synth.LAYER_LINEARS["c3"]].index(name))
+    assert c["T"] == 16384
+    m = M()
+    X, W, ids = bf(c["X"]), bf(c["W"]), tt(c["ids"])
+    L1, L2 = bf(c["L1"]), bf(c["L2"])
+    R, cnt = m.calibrate_stats(X, ids, 2)
+    s = m.init_factors(R, cnt, W)
+    Ro, co = O.calibrate_stats(c["X"], c["ids"], 2)
+    so = O.init_factors(Ro, co, c["W"])
+    assert np.array_equal(s.cpu().numpy(), so)
+    qt = torch.empty(n, d, dtype=torch.int8, device="cuda")
+    dt = torch.empty(n, dtype=torch.float32, device="cuda")
+    Y, Yref, sums, counts, loss = m.calib_layer(X, ids, s, W, 4, 8, L1, L2, qw_text=qt, dw_text=dt)
+    m.check()
+    qwo, dwo = O.quantize_weight(c["W"], so[0], 4)
+    assert np.array_equal(qt.cpu().numpy(), qwo) and np.array_equal(dt.cpu().numpy(), dwo)
+    assert np.array_equal(counts.cpu().numpy(), co)
+    rows = sample_rows(c["ids"], n_random=128)
+    ids_r = c["ids"][rows]
+    rt = torch.from_numpy(rows).cuda()
+    Yh = Y[rt].cpu().numpy()                  # gather on the device (Y is 2.5 GB at gate_up)
+    Yrh = Yref[rt].cpu().numpy()
+    del Y, Yref
+    acc = m.linear_forward(X, ids, s, qt, dt, 4, 8, acc_debug=True)
+    acch = acc[rt].cpu().numpy().astype(np.int64)
+    del acc
+    torch.cuda.empty_cache()
+    qxo, _ = O.quantize_activations(O.decode(c["X"])[rows], ids_r, so, 8)
+    assert np.array_equal(acch, O.int_gemm(qxo, qwo))
+    Yo = O.linear_forward(c["X"], c["ids"], so, qwo, dwo, 8, list(c["L1"]), list(c["L2"]), rows=rows)
+    errs = per_modality_err(Yh, Yo, ids_r)
+    assert max(errs.values()) <= TOL_Y, errs
+    errs_r = per_modality_err(Yrh, O.reference_output(c["X"], c["W"], rows=rows), ids_r)
+    assert max(errs_r.values()) <= 1e-4, errs_r
+
+
 def test_stats_d11008_three_modalities():
     """c2's down-projection input width (11008), 3 modalities, the whole 4096-token batch."""
     c = synth.config_inputs("c2", d=11008, n=2048)
