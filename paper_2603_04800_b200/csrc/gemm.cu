@@ -25,7 +25,13 @@
 // (rank 0) issues the MMAs and multicasts its commits to both CTAs; each CTA's TMEM holds its
 // 128 rows x 256 columns.
 //
-// Roles per CTA (320 threads, 1 CTA per SM, grid = 2 x min(#units, #SMs / 2)):
+// Optionally (CL = 4, MASQ_GEMM_CL) a cluster holds two such pairs working on adjacent n-tiles of
+// the same 256-row m-unit: the A tile is then identical for both pairs, and the CTA of rank r in
+// each pair TMA-loads half of it (64 rows) multicast into the rank-r CTAs of both pairs, so each
+// SM reads 24 KB per k-block from L2 instead of 32 KB.  Every stage slot is then shared by the
+// two pairs: the MMA commits that free it multicast to all four CTAs (empty barrier count 2).
+//
+// Roles per CTA (320 threads, 1 CTA per SM, grid = CL x min(#work items, active clusters)):
 //   warp 0 lane 0 : TMA producer  (both CTAs; 6-stage ring of 16 KB A + 16 KB B)
 //   warp 1        : TMEM allocation (both CTAs); lane 0 of the leader issues the MMAs
 //   warps 2..9    : epilogue      (warp w owns TMEM lane quarter w%4 and column half (w-2)/4:
@@ -74,17 +80,18 @@ constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * NSTG * STG_BYTES;
 constexpr int SMEM_USED = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr int kCmcDefer = 4;
-constexpr int kRasterGroupDefault = 16;
+constexpr int kRasterL2MB = 32;                      // L2 budget of a raster group's B panels
+constexpr int kRasterGroupMin = 16;                  // n-tiles per raster group, at least
 constexpr uint32_t IDESC_I8 = idesc_i8(UM, BN);
 constexpr uint32_t IDESC_BF16 = idesc_bf16(UM, BN);
 constexpr uint32_t IDESC_BF16_BMN = idesc_bf16(UM, BN) | (1u << 16);   // B MN-major (X.W reads W as stored)
-constexpr uint16_t kBoth = 0x3;
 static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
 
 struct Params {
   int mode;
   int T, n, d;
   int num_m, num_n, num_kb, n_units;  // num_m = 256-row units
+  int num_np, n_items;                // n-tile groups of the cluster's pairs, work items (m-unit x group)
   int n_tiles128;                     // forward: entries of the 128-row modality mask
   int group;                          // raster: n-tiles per group swept over all m-units
   int n_mod;
@@ -110,28 +117,33 @@ struct Unit {
   uint32_t mask;
 };
 
-__device__ __forceinline__ bool decode_unit(const Params& p, int u, Unit& w) {
+// work item u -> (m-unit, n-tile group); pair `pair` of the cluster takes n-tile NP * group + pair
+// (an n-tile >= num_n runs the k-loop for its partner's shared A stages and stores nothing)
+template <int NP>
+__device__ __forceinline__ bool decode_unit(const Params& p, int u, int pair, Unit& w) {
+  int ntp;
   if (p.group > 0) {
-    // grouped raster: p.group consecutive n-tiles swept over all m-units
+    // grouped raster: p.group consecutive n-tile groups swept over all m-units
     const int per_group = p.group * p.num_m;
     const int g = u / per_group;
     const int rem = u - g * per_group;
     const int nt0 = g * p.group;
-    const int gsz = min(p.group, p.num_n - nt0);
+    const int gsz = min(p.group, p.num_np - nt0);
     w.mt = rem / gsz;
-    w.nt = nt0 + (rem - w.mt * gsz);
+    ntp = nt0 + (rem - w.mt * gsz);
   } else {
     // m-grouped raster (-p.group consecutive m-units swept over all n-tiles): the A panels of the
     // group stay in L2 while B streams once per group
     const int gm = -p.group;
-    const int per_group = gm * p.num_n;
+    const int per_group = gm * p.num_np;
     const int g = u / per_group;
     const int rem = u - g * per_group;
     const int mt0 = g * gm;
     const int gsz = min(gm, p.num_m - mt0);
-    w.nt = rem / gsz;
-    w.mt = mt0 + (rem - w.nt * gsz);
+    ntp = rem / gsz;
+    w.mt = mt0 + (rem - ntp * gsz);
   }
+  w.nt = NP * ntp + pair;
   w.m = 0;
   if (p.mode == kModeLoss || p.mode == kModeAlpha || p.mode == kModeAlphaI8) {
     w.mask = p.tile_mask[w.mt];
@@ -157,8 +169,8 @@ struct Ring {
   }
 };
 
-template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+template <int MODE, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1)
 masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmZ,
                  const __grid_constant__ CUtensorMap tmL2, const Params p) {
@@ -169,7 +181,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint8_t* smB = smem + SMEM_B;
   uint8_t* smS = smem + SMEM_STG;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);  // leader's is used
-  uint64_t* empty = full + STAGES;      // both: multicast MMA commit frees the stage
+  uint64_t* empty = full + STAGES;      // all: the multicast MMA commits of every pair free the stage
   uint64_t* tfull = empty + STAGES;     // [2] both: accumulator ready
   uint64_t* tempty = tfull + 2;         // [2] leader's: both epilogues drained the buffer
   uint64_t* conv = tempty + 2;          // [2] leader's: both epilogues wrote y_base back (CMC)
@@ -179,15 +191,22 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
+  constexpr int NP = CL / 2;             // CTA pairs per cluster
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u;      // rank within the pair
+  const int pair = (int)(crank >> 1);
   const bool leader = rank == 0;
+  const uint32_t lead_cta = crank & ~1u;
+  const uint16_t pmask = (uint16_t)(0x3u << (2 * pair));          // this pair's CTAs
+  const uint16_t all_mask = (uint16_t)((1u << CL) - 1u);
+  const uint16_t a_mask = (uint16_t)(NP == 2 ? ((1u << rank) | (1u << (2 + rank))) : 0u);   // rank-r CTA of each pair
   const int cid = (int)cluster_id_x(), ncl = (int)ncluster_x();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (MODE != kModeLoss && MODE != kModeAlpha && MODE != kModeAlphaI8) tma_prefetch(&tmY);
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NP); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * EPI_WARPS);
@@ -198,7 +217,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
   if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
   tc_fence_before();
-  cluster_sync();                       // barriers of both CTAs initialised before any remote use
+  cluster_sync();                       // barriers of all CTAs initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -207,8 +226,9 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   constexpr bool kAlpha = MODE == kModeAlpha || MODE == kModeAlphaI8;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer (both CTAs)
+    {
+      // ------------------------------------------------------------ TMA producer (all CTAs)
+      // warp-wide loop (uniform state), one elected lane issues each stage's copies
       // A streams through (evict-first); B is re-read by every m-unit of the raster group (evict-last)
       // (int8 modes: default policy measured as fast or faster)
       const uint64_t pol_a = MODE == kModeRef ? policy_evict_first() : policy_evict_normal();
@@ -216,41 +236,56 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       Ring ring;
       bool pend = false;
       Unit pu{};
-      auto stage_arm = [&]() {
-        mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+      auto arm = [&]() {                  // elected lane: the leader's barrier expects the stage's bytes
         if (leader) mbar_expect_tx(&full[ring.stage], 2 * (A_BYTES + B_BYTES));
+      };
+      // A side: CL = 2 loads its 128 rows; CL = 4 loads half of them into both pairs (multicast)
+      auto load_a = [&](const CUtensorMap* tm, int c0, int arow, uint64_t pol) {
+        if (NP == 2) {
+          tma_load_2d_2sm_mc_hint(smA + ring.stage * A_BYTES + pair * (A_BYTES / 2), tm, &full[ring.stage], c0,
+                                  arow + pair * (BM / 2), a_mask, pol);
+        } else {
+          tma_load_2d_2sm_hint(smA + ring.stage * A_BYTES, tm, &full[ring.stage], c0, arow, pol);
+        }
       };
       auto load_cmc = [&](const Unit& w) {
         for (int mm = 1; mm < p.n_mod; ++mm) {
           if (!((w.mask >> mm) & 1u)) continue;
           for (int kb = 0; kb < p.cmc_kb; ++kb) {
-            stage_arm();
-            tma_load_2d_2sm(smA + ring.stage * A_BYTES, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64,
-                            w.mt * UM + (int)rank * BM);
-            tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmL2, &full[ring.stage], kb * 64,
-                            (mm - 1) * p.n + w.nt * BN + (int)rank * BNH);
+            mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+            if (elect_one()) {
+              arm();
+              load_a(&tmZ, (mm - 1) * 2 * p.rpad + kb * 64, w.mt * UM + (int)rank * BM, policy_evict_normal());
+              tma_load_2d_2sm(smB + ring.stage * B_BYTES, &tmL2, &full[ring.stage], kb * 64,
+                              (mm - 1) * p.n + w.nt * BN + (int)rank * BNH);
+            }
+            __syncwarp();
             ring.advance();
           }
         }
       };
-      for (int u = cid; u < p.n_units; u += ncl) {
+      for (int u = cid; u < p.n_items; u += ncl) {
         Unit w;
-        if (!decode_unit(p, u, w)) continue;
+        if (!decode_unit<NP>(p, u, pair, w)) continue;
         const int brow = (kGrouped ? w.m * p.n : 0) + w.nt * BN + (int)rank * BNH;
         const int arow = w.mt * UM + (int)rank * BM;
         const int defer_at = min(p.cmc_defer, p.num_kb - 1);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
-          stage_arm();
-          tma_load_2d_2sm_hint(smA + ring.stage * A_BYTES, &tmA, &full[ring.stage], kb * KELEMS, arow, pol_a);
-          if (MODE == kModeRef) {
-            // W [d x n] as stored: two 64(n) x 64(k) boxes -> MN-major B tile [n-half][k][64 n]
-            tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], brow, kb * KELEMS, pol_b);
-            tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES + B_BYTES / 2, &tmB, &full[ring.stage], brow + 64,
-                                 kb * KELEMS, pol_b);
-          } else {
-            tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow, pol_b);
+          mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
+          if (elect_one()) {
+            arm();
+            load_a(&tmA, kb * KELEMS, arow, pol_a);
+            if (MODE == kModeRef) {
+              // W [d x n] as stored: two 64(n) x 64(k) boxes -> MN-major B tile [n-half][k][64 n]
+              tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], brow, kb * KELEMS, pol_b);
+              tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES + B_BYTES / 2, &tmB, &full[ring.stage], brow + 64,
+                                   kb * KELEMS, pol_b);
+            } else {
+              tma_load_2d_2sm_hint(smB + ring.stage * B_BYTES, &tmB, &full[ring.stage], kb * KELEMS, brow, pol_b);
+            }
           }
+          __syncwarp();
           ring.advance();
         }
         if (unit_has_cmc(p, w)) { pend = true; pu = w; }
@@ -259,8 +294,10 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
       // ------------------------------------------------------------ MMA issuer (leader CTA)
+      // the whole warp runs the loop (its state stays warp-uniform, in uniform registers); one
+      // elected lane issues each k-block's MMAs and the commit that tracks them
       Ring ring;
       uint32_t local = 0, cmc_cnt[2] = {0u, 0u};   // conv/cmcd phases count CMC uses per buffer
       bool pend = false;
@@ -275,20 +312,24 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int kb = 0; kb < p.cmc_kb; ++kb) {
             mbar_wait(&full[ring.stage], ring.phase);
             tc_fence_after();
+            if (elect_one()) {
+              const uint64_t ad = umma_desc_sw128(a0 + ring.stage * A_BYTES);
+              const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              mma_bf16_2sm(tmem_base + buf * BN, umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32),
-                           umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32), IDESC_BF16, 1u);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_2sm(tmem_base + buf * BN, ad + 2 * k, bd + 2 * k, IDESC_BF16, 1u);
+              mma_commit_2sm(&empty[ring.stage], all_mask);
             }
-            mma_commit_2sm(&empty[ring.stage], kBoth);
+            __syncwarp();
             ring.advance();
           }
         }
-        mma_commit_2sm(&cmcd[buf], kBoth);
+        if (elect_one()) mma_commit_2sm(&cmcd[buf], pmask);
+        __syncwarp();
       };
-      for (int u = cid; u < p.n_units; u += ncl) {
+      for (int u = cid; u < p.n_items; u += ncl) {
         Unit w;
-        if (!decode_unit(p, u, w)) continue;
+        if (!decode_unit<NP>(p, u, pair, w)) continue;
         const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
         ++local;
         mbar_wait(&tempty[buf], ph ^ 1u);
@@ -299,24 +340,29 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (pend && kb == defer_at) { issue_cmc(pu, pbuf, pph); pend = false; }
           mbar_wait(&full[ring.stage], ring.phase);
           tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = umma_desc_sw128(a0 + ring.stage * A_BYTES + k * 32);
+          if (elect_one()) {
+            // descriptor start addresses advance by 16-byte units: +32 B per K step (K-major),
+            // +2048 B per 16 K rows (MN-major B of X.W)
+            const uint64_t ad = umma_desc_sw128(a0 + ring.stage * A_BYTES);
             if (MODE == kModeRef) {
-              const uint64_t bd = umma_desc_sw128_mn(b0 + ring.stage * B_BYTES + k * 2048, B_BYTES / 2);
-              mma_bf16_2sm(dtm, ad, bd, IDESC_BF16_BMN, (kb | k) != 0);
-            } else if (MODE == kModeAlpha) {
-              const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
-              mma_bf16_2sm(dtm, ad, bd, IDESC_BF16, (kb | k) != 0);
+              const uint64_t bd = umma_desc_sw128_mn(b0 + ring.stage * B_BYTES, B_BYTES / 2);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) mma_bf16_2sm(dtm, ad + 2 * k, bd + 128 * k, IDESC_BF16_BMN, (kb | k) != 0);
             } else {
-              const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES + k * 32);
-              mma_i8_2sm(dtm, ad, bd, IDESC_I8, (kb | k) != 0);
+              const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (MODE == kModeAlpha) mma_bf16_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_BF16, (kb | k) != 0);
+                else mma_i8_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_I8, (kb | k) != 0);
+              }
             }
+            mma_commit_2sm(&empty[ring.stage], all_mask);
           }
-          mma_commit_2sm(&empty[ring.stage], kBoth);
+          __syncwarp();
           ring.advance();
         }
-        mma_commit_2sm(&tfull[buf], kBoth);
+        if (elect_one()) mma_commit_2sm(&tfull[buf], pmask);
+        __syncwarp();
         if (unit_has_cmc(p, w)) {
           pend = true;
           pu = w;
@@ -337,9 +383,10 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint32_t nst = 0;                                   // Y chunks this warp has staged so far
     uint32_t local = 0, cmc_cnt[2] = {0u, 0u};
     const uint64_t pol_y = policy_evict_first();          // Y is written once, never re-read here
-    for (int u = cid; u < p.n_units; u += ncl) {
+    for (int u = cid; u < p.n_items; u += ncl) {
       Unit w;
-      if (!decode_unit(p, u, w)) continue;
+      if (!decode_unit<NP>(p, u, pair, w)) continue;
+      const bool real = w.nt < p.num_n;                  // false: partner-only n-tile past the edge
       const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
       ++local;
       const int row0 = w.mt * UM + (int)rank * BM + (int)q * 32;
@@ -432,7 +479,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&conv[buf], 0);
+        if (lane == 0) mbar_arrive_cluster(&conv[buf], lead_cta);
         mbar_wait(&cmcd[buf], cmc_cnt[buf] & 1u);
         ++cmc_cnt[buf];
         tc_fence_after();
@@ -497,7 +544,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // combine the 8 epilogue warps in a fixed order -> one partial per (unit, CTA)
         if (lane == 0) red[ew] = part;
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-        if (ew == 0 && lane == 0) {
+        if (ew == 0 && lane == 0 && real) {
           double tot = 0.0;
 #pragma unroll
           for (int e = 0; e < EPI_WARPS; ++e) tot += red[e];
@@ -526,7 +573,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
         if (MODE == kModeAlphaI8) part *= dxr;                      // the row step e_t
-        if (row < p.T) p.apart[(size_t)row * p.apart_ld + p.apart_off + 2 * w.nt + (ew >> 2)] = part;
+        if (row < p.T && real) p.apart[(size_t)row * p.apart_ld + p.apart_off + 2 * w.nt + (ew >> 2)] = part;
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -545,7 +592,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int o = 16; o > 0; o >>= 1) tpart += __shfl_xor_sync(0xffffffffu, tpart, o);
         if (lane == 0) red[ew] = tpart;
         asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-        if (ew == 0 && lane == 0) {
+        if (ew == 0 && lane == 0 && real) {
           double tot = 0.0;
 #pragma unroll
           for (int e = 0; e < EPI_WARPS; ++e) tot += red[e];
@@ -555,32 +602,89 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
+      if (lane == 0) mbar_arrive_cluster(&tempty[buf], lead_cta);
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
   }
 
   tc_fence_before();
-  cluster_sync();                       // both CTAs done with TMEM and with each other's barriers
+  cluster_sync();                       // all CTAs done with TMEM and with each other's barriers
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_2sm(tmem_base, 512);
   }
 }
 
-template <int MODE>
+// co-resident clusters of CL CTAs for this kernel (4-CTA clusters need two TPCs of one GPC, so
+// fewer than #SMs / 4 may fit); cached per (mode, CL, device)
+template <int MODE, int CL>
+int active_clusters() {
+  static int cached[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = cached[dev & 15];
+  if (c == 0) {
+    int n = 0;
+    if (CL == 2) {
+      n = num_sms() / 2;
+    } else {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(CL * (num_sms() / CL));
+      cfg.blockDim = dim3(THREADS);
+      cfg.dynamicSmemBytes = SMEM_ALLOC;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, masq_gemm_kernel<MODE, CL>, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = num_sms() / CL;
+      }
+      n = std::min(n, num_sms() / CL);
+    }
+    c = n;
+    if (getenv("MASQ_GEMM_VERBOSE")) fprintf(stderr, "[masq] gemm mode %d: %d active clusters of %d CTAs\n", MODE, n, CL);
+  }
+  return c;
+}
+
+template <int MODE, int CL>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
-                        const CUtensorMap& l2, const Params& p, int clusters, cudaStream_t st) {
+                        const CUtensorMap& l2, const Params& p, int max_cl, cudaStream_t st) {
   {
-    cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(masq_gemm_kernel<MODE>), SMEM_ALLOC);
+    cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(masq_gemm_kernel<MODE, CL>), SMEM_ALLOC);
     if (e != cudaSuccess) return e;
   }
+  const int clusters = (int)std::min<int64_t>(p.n_items, std::min(max_cl, active_clusters<MODE, CL>()));
   static const char* const kNames[6] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha",
                                         "gemm_alpha_i8"};
   ProfScope ps_(kNames[MODE], st);
-  masq_gemm_kernel<MODE><<<2 * clusters, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
+  masq_gemm_kernel<MODE, CL><<<CL * clusters, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
   return cudaGetLastError();
+}
+
+// MASQ_GEMM_CL (measurement knob): 2 = one CTA pair per cluster, 4 = two pairs sharing the A tile
+int gemm_cluster_size(int mode) {
+  static const int env = [] {
+    const char* e = getenv("MASQ_GEMM_CL");
+    return e ? atoi(e) : 0;
+  }();
+  if (env == 2 || env == 4) return env;
+  // measured (tools/cl_ab.sh): 4-CTA clusters fit 33 per GPU (132 SMs) against 74 pairs (148 SMs);
+  // the multicast saves L2 reads but the 16 idle SMs cost more (2-8% slower at every c3 shape)
+  (void)mode;
+  return 2;
+}
+
+template <int MODE>
+cudaError_t launch_cl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
+                      const CUtensorMap& l2, const Params& p, int cl, int max_pairs, cudaStream_t st) {
+  if (cl == 4) return launch_mode<MODE, 4>(a, b, y, z, l2, p, std::max(1, max_pairs / 2), st);
+  return launch_mode<MODE, 2>(a, b, y, z, l2, p, max_pairs, st);
 }
 }  // namespace
 
@@ -618,16 +722,18 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   if (g.T <= 0 || g.n <= 0) return cudaSuccess;
   CUtensorMap ta, tb, ty, tz, tl2;
   const bool bf = g.mode == kModeRef || g.mode == kModeAlpha;
+  const int cl = gemm_cluster_size(g.mode);
+  const int abox = cl == 4 ? BM / 2 : BM;              // A rows per TMA box (CL = 4: half, multicast)
   bool ok = true;
   if (g.mode == kModeAlpha) {
-    ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
+    ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, abox, 64, true);
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.b_rows, g.d, g.d, BNH, 64, true);
   } else if (bf) {
-    ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, BM, 64, true);
+    ok &= make_tmap_2d(&ta, g.xbf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, g.d, g.ld_x, abox, 64, true);
     // B = W [d x n] row-major (MN-major for the MMA): box 64 (n) x 64 (k)
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.d, g.n, g.n, 64, 64, true);
   } else {
-    ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, BM, 128, true);
+    ok &= make_tmap_2d(&ta, g.qx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.T, g.d, g.d, abox, 128, true);
     ok &= make_tmap_2d(&tb, g.b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.b_rows, g.d, g.d, BNH, 128, true);
   }
   if (g.mode != kModeLoss && g.mode != kModeAlpha && g.mode != kModeAlphaI8) {
@@ -638,7 +744,7 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   const bool cmc = g.mode == kModeFwd && g.rpad > 0;
   if (cmc) {
     const int64_t zc = (int64_t)(g.n_mod - 1) * 2 * g.rpad;
-    ok &= make_tmap_2d(&tz, g.z, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, zc, zc, BM, 64, true);
+    ok &= make_tmap_2d(&tz, g.z, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.T, zc, zc, abox, 64, true);
     ok &= make_tmap_2d(&tl2, g.l2t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)(g.n_mod - 1) * g.n,
                        2 * g.rpad, 2 * g.rpad, BNH, 64, true);
   } else {
@@ -656,6 +762,8 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
   p.num_n = (int)ceil_div(g.n, BN);
   p.num_kb = (int)ceil_div(g.d, bf ? 64 : 128);
   p.n_units = p.num_m * p.num_n;
+  p.num_np = (int)ceil_div(p.num_n, cl / 2);
+  p.n_items = p.num_m * p.num_np;
   p.n_tiles128 = (int)ceil_div(g.T, kTileM);
   {
     static int env_group = -1000;
@@ -663,7 +771,26 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
       const char* e = getenv("MASQ_RASTER_GROUP");         // tuning knob (measurement only;
       env_group = e ? atoi(e) : 0;                          // < 0: m-grouped with -value m-units)
     }
-    p.group = env_group != 0 ? env_group : kRasterGroupDefault;
+    if (env_group != 0) {
+      p.group = env_group;
+    } else {
+      // n-tiles per raster group: at least 16, more when more B panels (256 columns x K) fit an
+      // L2 budget (the group's B stays resident while every m-unit streams past it; A is re-read
+      // once per group); groups balanced in size.  Measured (tools/elect_ab.sh, l2mb_sweep.sh):
+      // the budget helps the 18-tile qkv (one int8 group, +5%), fewer than 16 tiles per group
+      // loses at the deep-K down projection even with less DRAM traffic.
+      // MASQ_RASTER_L2MB: budget knob (measurement only)
+      static const int env_mb = [] {
+        const char* e = getenv("MASQ_RASTER_L2MB");
+        return e ? atoi(e) : 0;
+      }();
+      const double budget = (env_mb > 0 ? env_mb : kRasterL2MB) * 1048576.0;
+      const double panel = (double)BN * (double)g.d * (bf ? 2.0 : 1.0);
+      const int gmax = std::max(kRasterGroupMin, (int)(budget / panel));
+      const int ngroups = (int)ceil_div(p.num_n, gmax);
+      p.group = (int)ceil_div(p.num_n, ngroups);
+    }
+    if (p.group > 0) p.group = std::max(1, (int)ceil_div(p.group, cl / 2));   // in n-tile groups of the cluster
   }
   p.n_mod = g.n_mod;
   p.dx = g.dx;
@@ -700,15 +827,14 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     const char* e = getenv("MASQ_GEMM_CLUSTERS");
     return e ? atoi(e) : 0;
   }();
-  const int max_cl = env_cl > 0 ? std::min(env_cl, num_sms() / 2) : num_sms() / 2;
-  const int clusters = (int)std::min<int64_t>(p.n_units, max_cl);
+  const int max_pairs = env_cl > 0 ? std::min(env_cl, num_sms() / 2) : num_sms() / 2;
   switch (g.mode) {
-    case kModeFwd: return launch_mode<kModeFwd>(ta, tb, ty, tz, tl2, p, clusters, st);
-    case kModeAcc: return launch_mode<kModeAcc>(ta, tb, ty, tz, tl2, p, clusters, st);
-    case kModeLoss: return launch_mode<kModeLoss>(ta, tb, ty, tz, tl2, p, clusters, st);
-    case kModeRef: return launch_mode<kModeRef>(ta, tb, ty, tz, tl2, p, clusters, st);
-    case kModeAlpha: return launch_mode<kModeAlpha>(ta, tb, ty, tz, tl2, p, clusters, st);
-    case kModeAlphaI8: return launch_mode<kModeAlphaI8>(ta, tb, ty, tz, tl2, p, clusters, st);
+    case kModeFwd: return launch_cl<kModeFwd>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
+    case kModeAcc: return launch_cl<kModeAcc>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
+    case kModeLoss: return launch_cl<kModeLoss>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
+    case kModeRef: return launch_cl<kModeRef>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
+    case kModeAlpha: return launch_cl<kModeAlpha>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
+    case kModeAlphaI8: return launch_cl<kModeAlphaI8>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
     default: return cudaErrorInvalidValue;
   }
 }

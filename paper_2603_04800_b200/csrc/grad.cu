@@ -124,7 +124,8 @@ gradgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
+      // warp-wide loops (uniform state); one elected lane issues copies / MMAs
       uint32_t st = 0, ph = 0, local = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         int m, it, jt, k0, nkb;
@@ -133,29 +134,35 @@ gradgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (nkb == 0) continue;
         // the tile of Q(S_m W) for the epilogue: rows j (m*n + jt*256 ..), bytes i (it*128 ..)
         mbar_wait(qempty, (local & 1u) ^ 1u);
-        mbar_expect_tx(qfull, QW_BYTES);
-        tma_load_2d(qws, &tmQW, qfull, it * GM, m * p.n + jt * GN);
+        if (elect_one()) {
+          mbar_expect_tx(qfull, QW_BYTES);
+          tma_load_2d(qws, &tmQW, qfull, it * GM, m * p.n + jt * GN);
+        }
+        __syncwarp();
         ++local;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[st], ph ^ 1u);
-          mbar_expect_tx(&full[st], STAGE);
-          uint8_t* base = smem + st * STAGE;
-          const int t = k0 + kb * GK;
+          if (elect_one()) {
+            mbar_expect_tx(&full[st], STAGE);
+            uint8_t* base = smem + st * STAGE;
+            const int t = k0 + kb * GK;
 #pragma unroll
-          for (int pl = 0; pl < NPL; ++pl)
+            for (int pl = 0; pl < NPL; ++pl)
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-              tma_load_2d(base + pl * APL + h * (APL / 2), &tmA, &full[st], it * GM + h * 64, pl * p.Tg + t);
+              for (int h = 0; h < 2; ++h)
+                tma_load_2d(base + pl * APL + h * (APL / 2), &tmA, &full[st], it * GM + h * 64, pl * p.Tg + t);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            tma_load_2d(base + NPL * APL + q * (BPL / 4), &tmB, &full[st], jt * GN + q * 64, t);
+            for (int q = 0; q < 4; ++q)
+              tma_load_2d(base + NPL * APL + q * (BPL / 4), &tmB, &full[st], jt * GN + q * 64, t);
+          }
+          __syncwarp();
           if (++st == GSTAGES) { st = 0; ph ^= 1u; }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       uint32_t st = 0, ph = 0, local = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         int m, it, jt, k0, nkb;
@@ -168,18 +175,23 @@ gradgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
-          const uint32_t base = smem_u32(smem + st * STAGE);
+          if (elect_one()) {
+            const uint32_t base = smem_u32(smem + st * STAGE);
+            const uint64_t bd = umma_desc_sw128_mn(base + NPL * APL, BPL / 4);
+            const uint64_t a0d = umma_desc_sw128_mn(base, APL / 2), a1d = umma_desc_sw128_mn(base + APL, APL / 2);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t bd = umma_desc_sw128_mn(base + NPL * APL + kk * 2048, BPL / 4);
-            const uint32_t acc0 = (kb | kk) != 0;
-            mma_bf16(tmem, umma_desc_sw128_mn(base + 0 * APL + kk * 2048, APL / 2), bd, IDESC_G, acc0);
-            mma_bf16(tmem + GN, umma_desc_sw128_mn(base + 1 * APL + kk * 2048, APL / 2), bd, IDESC_G, acc0);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t acc0 = (kb | kk) != 0;
+              mma_bf16(tmem, a0d + 128 * kk, bd + 128 * kk, IDESC_G, acc0);
+              mma_bf16(tmem + GN, a1d + 128 * kk, bd + 128 * kk, IDESC_G, acc0);
+            }
+            mma_commit(&empty[st]);
           }
-          mma_commit(&empty[st]);
+          __syncwarp();
           if (++st == GSTAGES) { st = 0; ph ^= 1u; }
         }
-        mma_commit(tfull);
+        if (elect_one()) mma_commit(tfull);
+        __syncwarp();
       }
     }
     __syncwarp();

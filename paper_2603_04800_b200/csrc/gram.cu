@@ -132,29 +132,33 @@ cmc_gram_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------------------ TMA producer
+      // (warp-wide loops with uniform state; one elected lane issues copies / MMAs)
       uint32_t st = 0, ph = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Work w = decode(p, u);
         if (!w.live) continue;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[st], ph ^ 1u);
-          mbar_expect_tx(&full[st], RSTAGE);
-          uint8_t* base = smem + st * RSTAGE;
-          const int t = w.k0 + kb * RK;
+          if (elect_one()) {
+            mbar_expect_tx(&full[st], RSTAGE);
+            uint8_t* base = smem + st * RSTAGE;
+            const int t = w.k0 + kb * RK;
 #pragma unroll
-          for (int s = 0; s < NSL; ++s) {
-            tma_load_2d(base + s * A_SL, &tmA, &full[st], t, s * p.d + w.it * RM);
-            tma_load_2d(base + NSL * A_SL + s * B_SL, &tmB, &full[st], t, s * p.d + w.jt * RN);
+            for (int s = 0; s < NSL; ++s) {
+              tma_load_2d(base + s * A_SL, &tmA, &full[st], t, s * p.d + w.it * RM);
+              tma_load_2d(base + NSL * A_SL + s * B_SL, &tmB, &full[st], t, s * p.d + w.jt * RN);
+            }
           }
+          __syncwarp();
           if (++st == RSTAGES) { st = 0; ph ^= 1u; }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------------------ MMA issuer
       uint32_t st = 0, ph = 0, local = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
@@ -169,24 +173,30 @@ cmc_gram_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[st], ph);
           tc_fence_after();
-          const uint32_t base = smem_u32(smem + st * RSTAGE);
+          if (elect_one()) {
+            const uint32_t base = smem_u32(smem + st * RSTAGE);
+            const uint64_t ad = umma_desc_sw128(base), bd = umma_desc_sw128(base + NSL * A_SL);
 #pragma unroll
-          for (int kk = 0; kk < RK / 32; ++kk) {
+            for (int kk = 0; kk < RK / 32; ++kk) {
 #pragma unroll
-            for (int s = 0; s < NSL; ++s) {
+              for (int s = 0; s < NSL; ++s) {
 #pragma unroll
-              for (int s2 = 0; s2 < NSL; ++s2) {
-                const int lv = s + s2;
-                mma_i8(tmem + lv * RN, umma_desc_sw128(base + s * A_SL + kk * 32),
-                       umma_desc_sw128(base + NSL * A_SL + s2 * B_SL + kk * 32), IDESC_R, fresh[lv] ? 0u : 1u);
-                fresh[lv] = false;
+                for (int s2 = 0; s2 < NSL; ++s2) {
+                  const int lv = s + s2;
+                  mma_i8(tmem + lv * RN, ad + (s * A_SL + kk * 32) / 16, bd + (s2 * B_SL + kk * 32) / 16, IDESC_R,
+                         (fresh[lv] && kk == 0 && s == (lv < NSL ? 0 : lv - (NSL - 1))) ? 0u : 1u);
+                }
               }
             }
+            mma_commit(&empty[st]);
           }
-          mma_commit(&empty[st]);
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < NLV; ++k) fresh[k] = false;
           if (++st == RSTAGES) { st = 0; ph ^= 1u; }
         }
-        mma_commit(tfull);
+        if (elect_one()) mma_commit(tfull);
+        __syncwarp();
       }
     }
     __syncwarp();

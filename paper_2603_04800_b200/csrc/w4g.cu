@@ -184,8 +184,9 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ---------------------------------------------------------------- TMA producer (both CTAs)
+      // warp-wide loop, one elected lane issues the copies
       QRing<NP> ring;
       for (int u = cid; u < p.n_units; u += ncl) {
         const WUnit w = w_unit(p, u);
@@ -195,17 +196,20 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
         const uint32_t pk_bytes = (uint32_t)max(0, min(QM, p.n - crow)) * 64u;
         for (int g = 0; g < p.ng; ++g) {
           mbar_wait(&pempty[ring.stage], ring.phase ^ 1u);
-          uint8_t* slot = sP + ring.stage * P_SLOT;
-          // the group tile is one contiguous block of the group-major packed weights: one bulk
-          // copy (a 128-row TMA box of 64-byte rows cost 128 TMA row requests per group)
-          if (pk_bytes) {
-            mbar_expect_tx(&pfull[ring.stage], pk_bytes);
-            bulk_load_1d(slot, p.packed + ((size_t)g * p.n + crow) * 64, pk_bytes, &pfull[ring.stage]);
-          } else {
-            mbar_arrive(&pfull[ring.stage]);
+          if (elect_one()) {
+            uint8_t* slot = sP + ring.stage * P_SLOT;
+            // the group tile is one contiguous block of the group-major packed weights: one bulk
+            // copy (a 128-row TMA box of 64-byte rows cost 128 TMA row requests per group)
+            if (pk_bytes) {
+              mbar_expect_tx(&pfull[ring.stage], pk_bytes);
+              bulk_load_1d(slot, p.packed + ((size_t)g * p.n + crow) * 64, pk_bytes, &pfull[ring.stage]);
+            } else {
+              mbar_arrive(&pfull[ring.stage]);
+            }
+            if (leader) mbar_expect_tx(&full[ring.stage], 2 * QB_BYTES);
+            tma_load_2d_2sm(slot + P_A, &tmX, &full[ring.stage], g * QK, trow);
           }
-          if (leader) mbar_expect_tx(&full[ring.stage], 2 * QB_BYTES);
-          tma_load_2d_2sm(slot + P_A, &tmX, &full[ring.stage], g * QK, trow);
+          __syncwarp();
           ring.advance();
         }
         if (w.cmc) {
@@ -213,11 +217,14 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
             if (!((w.mask >> mm) & 1u)) continue;
             for (int kb = 0; kb < p.cmc_kb; ++kb) {
               mbar_wait(&pempty[ring.stage], ring.phase ^ 1u);
-              uint8_t* slot = sP + ring.stage * P_SLOT;
-              mbar_arrive(&pfull[ring.stage]);                  // CMC slot: the converters only release it
-              if (leader) mbar_expect_tx(&full[ring.stage], 2 * (QA_BYTES + QB_BYTES));
-              tma_load_2d_2sm(slot, &tmL2, &full[ring.stage], kb * 64, (mm - 1) * p.n + crow);
-              tma_load_2d_2sm(slot + P_A, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64, trow);
+              if (elect_one()) {
+                uint8_t* slot = sP + ring.stage * P_SLOT;
+                mbar_arrive(&pfull[ring.stage]);                // CMC slot: the converters only release it
+                if (leader) mbar_expect_tx(&full[ring.stage], 2 * (QA_BYTES + QB_BYTES));
+                tma_load_2d_2sm(slot, &tmL2, &full[ring.stage], kb * 64, (mm - 1) * p.n + crow);
+                tma_load_2d_2sm(slot + P_A, &tmZ, &full[ring.stage], (mm - 1) * 2 * p.rpad + kb * 64, trow);
+              }
+              __syncwarp();
               ring.advance();
             }
           }
@@ -226,8 +233,9 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
       // ---------------------------------------------------------------- MMA issuer (leader CTA)
+      // warp-wide loop (uniform state), one elected lane issues the MMAs and their commits
       QRing<NP> ring;
       QRing<NA> aring;
       uint32_t acnt = 0;                // accumulator buffers used so far
@@ -241,16 +249,19 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
           mbar_wait(&full[ring.stage], ring.phase);
           mbar_wait(&aready[aring.stage], aring.phase);
           tc_fence_after();
-          const uint32_t dtm = tmem_base + buf * QN;
-          const uint32_t ab = a0 + aring.stage * QA_BYTES, bb = p0 + ring.stage * P_SLOT + P_A;
-          if (!(p.exp & 8)) {
+          if (elect_one()) {
+            const uint32_t dtm = tmem_base + buf * QN;
+            const uint64_t ad = umma_desc_sw128(a0 + aring.stage * QA_BYTES);
+            const uint64_t bd = umma_desc_sw128(p0 + ring.stage * P_SLOT + P_A);
+            if (!(p.exp & 8)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_i8_2sm(dtm, umma_desc_sw128(ab + k * 32), umma_desc_sw128(bb + k * 32), IDESC_Q, k != 0);
+              for (int k = 0; k < 4; ++k) mma_i8_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_Q, k != 0);
+            }
+            mma_commit_2sm(&pempty[ring.stage], kPair);
+            mma_commit_2sm(&aempty[aring.stage], kPair);
+            mma_commit_2sm(&tfull[buf], kPair);
           }
-          mma_commit_2sm(&pempty[ring.stage], kPair);
-          mma_commit_2sm(&aempty[aring.stage], kPair);
-          mma_commit_2sm(&tfull[buf], kPair);
+          __syncwarp();
           ring.advance();
           aring.advance();
         }
@@ -266,18 +277,20 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
             for (int kb = 0; kb < p.cmc_kb; ++kb) {
               mbar_wait(&full[ring.stage], ring.phase);
               tc_fence_after();
-              const uint32_t ab = p0 + ring.stage * P_SLOT, bb = ab + P_A;
+              if (elect_one()) {
+                const uint64_t ad = umma_desc_sw128(p0 + ring.stage * P_SLOT);
+                const uint64_t bd = umma_desc_sw128(p0 + ring.stage * P_SLOT + P_A);
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                mma_bf16_2sm(dtm, umma_desc_sw128(ab + k * 32), umma_desc_sw128(bb + k * 32), IDESC_QC,
-                             first ? 0u : 1u);
-                first = false;
+                for (int k = 0; k < 4; ++k) mma_bf16_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_QC, (first && k == 0) ? 0u : 1u);
+                mma_commit_2sm(&pempty[ring.stage], kPair);
               }
-              mma_commit_2sm(&pempty[ring.stage], kPair);
+              __syncwarp();
+              first = false;
               ring.advance();
             }
           }
-          mma_commit_2sm(&tfull[buf], kPair);
+          if (elect_one()) mma_commit_2sm(&tfull[buf], kPair);
+          __syncwarp();
         }
       }
     }

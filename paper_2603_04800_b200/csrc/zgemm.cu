@@ -108,28 +108,32 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   const int lo_row0 = (n_mod - 1) * rpad;        // lo plane starts after the hi plane
 
   if (warp == 0) {
-    if (lane == 0) {
+    // warp-wide loops (uniform state); one elected lane issues the copies / MMAs
+    {
       uint32_t st = 0, ph = 0;
       for (int kc = kc0; kc < kc1; ++kc) {
         mbar_wait(&empty[st], ph ^ 1u);
-        mbar_expect_tx(&full[st], ksub * SBS);
+        if (elect_one()) {
+          mbar_expect_tx(&full[st], ksub * SBS);
 #pragma unroll
-        for (int sb = 0; sb < KSUB_MAX; ++sb) {
-          if (sb >= ksub) break;
-          const int col = (kc * ksub + sb) * 64;         // past d: TMA zero-fills the whole box
-          uint8_t* base = smem + st * SB + sb * SBS;
-          tma_load_2d(base, &tmA0, &full[st], col, mt * 128);
-          if (a_planes == 2) tma_load_2d(base + XCH, &tmA1, &full[st], col, mt * 128);
-          uint8_t* bb = base + a_planes * XCH;
-          tma_load_2d(bb, &tmB, &full[st], col, (m0 - 1) * rpad);
-          tma_load_2d(bb + BB, &tmB, &full[st], col, lo_row0 + (m0 - 1) * rpad);
+          for (int sb = 0; sb < KSUB_MAX; ++sb) {
+            if (sb >= ksub) break;
+            const int col = (kc * ksub + sb) * 64;         // past d: TMA zero-fills the whole box
+            uint8_t* base = smem + st * SB + sb * SBS;
+            tma_load_2d(base, &tmA0, &full[st], col, mt * 128);
+            if (a_planes == 2) tma_load_2d(base + XCH, &tmA1, &full[st], col, mt * 128);
+            uint8_t* bb = base + a_planes * XCH;
+            tma_load_2d(bb, &tmB, &full[st], col, (m0 - 1) * rpad);
+            tma_load_2d(bb + BB, &tmB, &full[st], col, lo_row0 + (m0 - 1) * rpad);
+          }
         }
+        __syncwarp();
         if (++st == (uint32_t)stages) { st = 0; ph ^= 1u; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       // B = [L1'hi ; L1'lo] (2N rows, the two TMA boxes are contiguous): one N = 2N MMA per
       // k-step accumulates X.L1'hi into columns [0, N) and X.L1'lo into [N, 2N); the epilogue
       // adds the halves
@@ -139,23 +143,27 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&full[st], ph);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int sb = 0; sb < KSUB_MAX; ++sb) {
-          if (sb >= ksub) break;
-          const uint32_t base = smem_u32(smem + st * SB + sb * SBS);
-          const uint32_t bh = base + a_planes * XCH, bl = bh + BB;
+          for (int sb = 0; sb < KSUB_MAX; ++sb) {
+            if (sb >= ksub) break;
+            const uint32_t base = smem_u32(smem + st * SB + sb * SBS);
+            const uint64_t ad = umma_desc_sw128(base), ad2 = umma_desc_sw128(base + XCH);
+            const uint64_t bdh = umma_desc_sw128(base + a_planes * XCH), bdl = umma_desc_sw128(base + a_planes * XCH + BB);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bh + k * 32), idesc, (kc | sb | k) != 0);
-            if (!combined) mma_bf16(tmem, umma_desc_sw128(base + k * 32), umma_desc_sw128(bl + k * 32), idesc, 1u);
-            if (a_planes == 2)
-              mma_bf16(tmem, umma_desc_sw128(base + XCH + k * 32), umma_desc_sw128(bh + k * 32), idesc, 1u);
+            for (int k = 0; k < 4; ++k) {
+              mma_bf16(tmem, ad + 2 * k, bdh + 2 * k, idesc, (kc | sb | k) != 0);
+              if (!combined) mma_bf16(tmem, ad + 2 * k, bdl + 2 * k, idesc, 1u);
+              if (a_planes == 2) mma_bf16(tmem, ad2 + 2 * k, bdh + 2 * k, idesc, 1u);
+            }
           }
+          mma_commit(&empty[st]);
         }
-        mma_commit(&empty[st]);
+        __syncwarp();
         if (++st == (uint32_t)stages) { st = 0; ph ^= 1u; }
       }
-      mma_commit(done);
+      if (elect_one()) mma_commit(done);
+      __syncwarp();
     }
     __syncwarp();
   } else {
