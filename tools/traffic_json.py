@@ -5,16 +5,18 @@ over the launches of each kernel, keyed by the names bench.py's kernel table use
 usage: python tools/traffic_json.py <traffic.csv> <out.json>
 """
 import csv
+import re
 import io
 import json
 import sys
 from collections import defaultdict
 
-NAMES = [("masq_gemm_kernel<0>", "gemm_fwd"), ("masq_gemm_kernel<2>", "gemm_loss"), ("masq_gemm_kernel<3>", "gemm_ref"),
+NAMES = [(r"masq_gemm_kernel<(\(int\))?0[,>]", "gemm_fwd"), (r"masq_gemm_kernel<(\(int\))?2[,>]", "gemm_loss"),
+         (r"masq_gemm_kernel<(\(int\))?3[,>]", "gemm_ref"), (r"masq_gemm_kernel<(\(int\))?5[,>]", "gemm_alpha_i8"),
          ("aquant_bf16_kernel", "aquant"), ("aquant_row_kernel", "aquant"), ("stats_kernel", "stats"),
          ("init_kernel", "init"), ("wcolmax_tma_kernel", "wcolmax"), ("wquant_tma_kernel", "wquant"),
          ("wcolmax_kernel", "wcolmax"), ("wquant_kernel", "wquant"), ("route_scatter_kernel", "route"),
-         ("pad_rows_kernel", "pad_rows"), ("gather_rows_kernel", "gather_rows"), ("zgemm_kernel", "zgemm"),
+         ("pad_rows_kernel", "pad_rows"), ("gather_rows_kernel", "gather_rows"), ("zgemm_kernel", "zgemm"), ("wq1_kernel", "wquant1"),
          ("route_kernel", "route")]
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -34,7 +36,7 @@ def main(src, dst):
     agg = defaultdict(list)
     for i, b in per.items():
         for pat, key in NAMES:
-            if pat in names[i]:
+            if re.search(pat, names[i]):
                 agg[key].append(b)
                 break
     out = {k: sum(v) / len(v) for k, v in agg.items()}
