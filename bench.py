@@ -1000,8 +1000,6 @@ def main():
                              for e in L), "GB/s", peaks["hbm"]),
         "wcolmax": ("hbm", sum(2.0 * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),      # one W read, N_MOD sets
         "wquant": ("hbm", sum((2.0 + N_MOD) * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),
-        # the one-pass A3 kernel: one W read (2 B) + N_MOD code sets (1 B each) per weight
-        "wquant1": ("hbm", sum((2.0 + N_MOD) * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),
         "init": ("hbm", sum(2.0 * e["d"] * e["n"] for e in L), "GB/s", peaks["hbm"]),
     }
     total_kernel_ms = sum(v["ms"] for v in kern.values())

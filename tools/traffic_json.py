@@ -16,7 +16,7 @@ NAMES = [(r"masq_gemm_kernel<(\(int\))?0[,>]", "gemm_fwd"), (r"masq_gemm_kernel<
          ("aquant_bf16_kernel", "aquant"), ("aquant_row_kernel", "aquant"), ("stats_kernel", "stats"),
          ("init_kernel", "init"), ("wcolmax_tma_kernel", "wcolmax"), ("wquant_tma_kernel", "wquant"),
          ("wcolmax_kernel", "wcolmax"), ("wquant_kernel", "wquant"), ("route_scatter_kernel", "route"),
-         ("pad_rows_kernel", "pad_rows"), ("gather_rows_kernel", "gather_rows"), ("zgemm_kernel", "zgemm"), ("wq1_kernel", "wquant1"),
+         ("pad_rows_kernel", "pad_rows"), ("gather_rows_kernel", "gather_rows"), ("zgemm_kernel", "zgemm"),
          ("route_kernel", "route")]
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
