@@ -168,6 +168,12 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
     default:
       break;
   }
+  // stream-K scratch of the forward / X.W GEMMs (after the op's own regions)
+  if (op == MASQ_OP_FORWARD || op == MASQ_OP_LAYER || op == MASQ_OP_REFERENCE ||
+      (self_ref && (op == MASQ_OP_LOSS || op == MASQ_OP_LOSS_GRAD))) {
+    L.skpart = take(gemm_sk_part_bytes());
+    L.skflag = take(gemm_sk_flag_bytes());
+  }
   // last, so every other offset is the same with and without the flag
   if (self_ref && (op == MASQ_OP_LOSS || op == MASQ_OP_LOSS_GRAD)) L.yref = take(sizeof(float) * (size_t)T * n);
   L.total = off;
@@ -183,6 +189,12 @@ inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) 
 inline cudaStream_t S(masq_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 inline uint8_t* W8(void* ws, size_t off) { return static_cast<uint8_t*>(ws) + off; }
 inline uint32_t* status_of(void* ws) { return static_cast<uint32_t*>(ws); }
+// the stream-K scratch of a GEMM whose workspace layout has one
+inline void set_sk(GemmArgs& g, void* ws, const WsLayout& L) {
+  if (L.skpart == 0 || L.skflag == 0) return;
+  g.sk_part = reinterpret_cast<uint32_t*>(W8(ws, L.skpart));
+  g.sk_flag = reinterpret_cast<uint32_t*>(W8(ws, L.skflag));
+}
 // MASQ_DEBUG=1 in the environment prints the failing call and the CUDA error to stderr
 static bool masq_debug_on() {
   static int on = -1;
@@ -352,6 +364,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   if (dbg && dbg->qx) MASQ_CK(cudaMemcpyAsync(dbg->qx, qx, (size_t)T * d, cudaMemcpyDeviceToDevice, st));
   if (dbg && dbg->dx) MASQ_CK(cudaMemcpyAsync(dbg->dx, dx, sizeof(float) * T, cudaMemcpyDeviceToDevice, st));
   GemmArgs g{};
+  set_sk(g, ws, L);
   g.mode = use_acc ? kModeAcc : kModeFwd;
   g.T = T;
   g.n = d_out;
@@ -454,6 +467,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   }
   // A8 target first: the forward's epilogue reads it for the text rows
   GemmArgs gr{};
+  set_sk(gr, ws, L);
   gr.mode = kModeRef;
   gr.T = T;
   gr.n = d_out;
@@ -471,6 +485,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   double* fpart = reinterpret_cast<double*>(W8(ws, L.fpart));
   const int64_t fwd_units = ceil_div(T, kUnitM) * num_n;
   GemmArgs g{};
+  set_sk(g, ws, L);
   g.mode = kModeFwd;
   g.T = T;
   g.n = d_out;
@@ -539,6 +554,7 @@ masq_status masq_reference_output(const void* X, int64_t ld_x, const void* W, in
   const WsLayout L = ws_layout(MASQ_OP_REFERENCE, T, d, d_out, 1, 0);
   MASQ_TRY(check_ws(ws, ws_bytes, L));
   GemmArgs g{};
+  set_sk(g, ws, L);
   g.mode = kModeRef;
   g.T = T;
   g.n = d_out;
@@ -591,6 +607,7 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
     MASQ_TRY(check_ws(ws, ws_bytes, Ls));
     float* yr = reinterpret_cast<float*>(W8(ws, Ls.yref));
     GemmArgs gr{};
+    set_sk(gr, ws, Ls);
     gr.mode = kModeRef;
     gr.T = T;
     gr.n = d_out;

@@ -80,6 +80,12 @@ constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * NSTG * STG_BYTES;
 constexpr int SMEM_USED = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_USED + 1024;
 constexpr int kCmcDefer = 4;
+constexpr int kSkMinKb = 4;                          // stream-K: k-blocks per segment, at least
+constexpr int kSkMaxSeg = 4;                         // stream-K: segments per remainder unit, at most
+// stream-K only for deep K: the owner's fix-up (waiting for and adding up to 3 partial tiles) costs
+// more than the tail it removes at 28 (int8) / 56 (bf16) k-blocks and pays at 148 / 296 (measured,
+// tools/sk_ab.sh: d = 18944 forward -12% at 4k tokens, -4% at 16k; d = 3584 +4-15%)
+constexpr int kSkMinUnitKb = 64;
 constexpr int kRasterL2MB = 32;                      // L2 budget of a raster group's B panels
 constexpr int kRasterGroupMin = 16;                  // n-tiles per raster group, at least
 constexpr uint32_t IDESC_I8 = idesc_i8(UM, BN);
@@ -110,6 +116,11 @@ struct Params {
   const uint8_t* ids;          // fwd with fwd_loss: modality id per row (text rows feed the loss)
   int fwd_loss;                // fwd: sum |y - yref| over text rows into partials[unit][rank]
   int skip_m0;                 // loss: skip the text units (their loss comes from the forward)
+  // stream-K remainder: work items n_full.. are the sk_R units past the last full wave, their
+  // sk_R * num_kb k-blocks cut into ranges of sk_per over pairs 0 .. sk_pairs-1
+  int n_full, sk_R, sk_per, sk_pairs;
+  uint32_t* sk_part;           // [pair][CTA][128 rows][256 cols] 32-bit partial accumulators
+  uint32_t* sk_flag;           // [pair][CTA] partial posted (zeroed before the launch)
 };
 
 struct Unit {
@@ -158,6 +169,52 @@ __device__ __forceinline__ bool decode_unit(const Params& p, int u, int pair, Un
   }
   return true;
 }
+// a cluster's work item: a whole unit, or (stream-K) a k-block segment of a remainder unit
+struct Item {
+  int u;                       // work item index (decode_unit)
+  int kb0, kb1;                // k-block range
+  int kind;                    // 0 whole unit; 1 owner: adds the partials of pairs c_lo..c_hi; 2 partial
+  int c_lo, c_hi;
+};
+constexpr int kItemWhole = 0, kItemOwner = 1, kItemPart = 2;
+// item i of cluster cid: whole units cid, cid + ncl, ... below n_full, then the (<= 2) segments
+// of its stream-K range [cid * sk_per, (cid + 1) * sk_per) of the remainder's k-blocks; a pair's
+// first segment may continue a unit another pair owns (kind 2), any later one starts a unit at
+// k-block 0 (its owner).  Every role walks the same sequence.
+__device__ __forceinline__ bool get_item(const Params& p, int cid, int ncl, int i, Item& it) {
+  const int n1 = p.n_full > cid ? (p.n_full - cid + ncl - 1) / ncl : 0;
+  if (i < n1) {
+    it.u = cid + i * ncl;
+    it.kb0 = 0;
+    it.kb1 = p.num_kb;
+    it.kind = kItemWhole;
+    return true;
+  }
+  const int j = i - n1;
+  if (p.sk_R == 0 || cid >= p.sk_pairs || j > 1) return false;
+  const long long tot = (long long)p.sk_R * p.num_kb;
+  const long long g0 = (long long)cid * p.sk_per;
+  const long long g1 = g0 + p.sk_per < tot ? g0 + p.sk_per : tot;
+  if (g0 >= g1) return false;
+  const int r = (int)(g0 / p.num_kb) + j;
+  const long long us = (long long)r * p.num_kb, ue = us + p.num_kb;
+  const long long a = g0 > us ? g0 : us, b = g1 < ue ? g1 : ue;
+  if (a >= b) return false;
+  it.u = p.n_full + r;
+  it.kb0 = (int)(a - us);
+  it.kb1 = (int)(b - us);
+  if (it.kb0 > 0) {
+    it.kind = kItemPart;
+  } else {
+    long long cl = (ue - 1) / p.sk_per;
+    if (cl > p.sk_pairs - 1) cl = p.sk_pairs - 1;
+    it.kind = cl > cid ? kItemOwner : kItemWhole;
+    it.c_lo = cid + 1;
+    it.c_hi = (int)cl;
+  }
+  return true;
+}
+
 __device__ __forceinline__ bool unit_has_cmc(const Params& p, const Unit& w) {
   return p.mode == kModeFwd && p.rpad > 0 && (w.mask & ~1u) != 0u;
 }
@@ -264,14 +321,15 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
         }
       };
-      for (int u = cid; u < p.n_items; u += ncl) {
+      Item it;
+      for (int i = 0; get_item(p, cid, ncl, i, it); ++i) {
         Unit w;
-        if (!decode_unit<NP>(p, u, pair, w)) continue;
+        if (!decode_unit<NP>(p, it.u, pair, w)) continue;
         const int brow = (kGrouped ? w.m * p.n : 0) + w.nt * BN + (int)rank * BNH;
         const int arow = w.mt * UM + (int)rank * BM;
-        const int defer_at = min(p.cmc_defer, p.num_kb - 1);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          if (pend && kb == defer_at) { load_cmc(pu); pend = false; }
+        const int defer_at = min(p.cmc_defer, it.kb1 - it.kb0 - 1);
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
+          if (pend && kb - it.kb0 == defer_at) { load_cmc(pu); pend = false; }
           mbar_wait(&empty[ring.stage], ring.phase ^ 1u);
           if (elect_one()) {
             arm();
@@ -288,7 +346,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           __syncwarp();
           ring.advance();
         }
-        if (unit_has_cmc(p, w)) { pend = true; pu = w; }
+        if (it.kind != kItemPart && unit_has_cmc(p, w)) { pend = true; pu = w; }
       }
       if (pend) load_cmc(pu);
     }
@@ -327,17 +385,18 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (elect_one()) mma_commit_2sm(&cmcd[buf], pmask);
         __syncwarp();
       };
-      for (int u = cid; u < p.n_items; u += ncl) {
+      Item it;
+      for (int i = 0; get_item(p, cid, ncl, i, it); ++i) {
         Unit w;
-        if (!decode_unit<NP>(p, u, pair, w)) continue;
+        if (!decode_unit<NP>(p, it.u, pair, w)) continue;
         const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
         ++local;
         mbar_wait(&tempty[buf], ph ^ 1u);
         tc_fence_after();
         const uint32_t dtm = tmem_base + buf * BN;
-        const int defer_at = min(p.cmc_defer, p.num_kb - 1);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          if (pend && kb == defer_at) { issue_cmc(pu, pbuf, pph); pend = false; }
+        const int defer_at = min(p.cmc_defer, it.kb1 - it.kb0 - 1);
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
+          if (pend && kb - it.kb0 == defer_at) { issue_cmc(pu, pbuf, pph); pend = false; }
           mbar_wait(&full[ring.stage], ring.phase);
           tc_fence_after();
           if (elect_one()) {
@@ -347,13 +406,15 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             if (MODE == kModeRef) {
               const uint64_t bd = umma_desc_sw128_mn(b0 + ring.stage * B_BYTES, B_BYTES / 2);
 #pragma unroll
-              for (int k = 0; k < 4; ++k) mma_bf16_2sm(dtm, ad + 2 * k, bd + 128 * k, IDESC_BF16_BMN, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_2sm(dtm, ad + 2 * k, bd + 128 * k, IDESC_BF16_BMN, (kb != it.kb0 || k != 0) ? 1u : 0u);
             } else {
               const uint64_t bd = umma_desc_sw128(b0 + ring.stage * B_BYTES);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                if (MODE == kModeAlpha) mma_bf16_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_BF16, (kb | k) != 0);
-                else mma_i8_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_I8, (kb | k) != 0);
+                const uint32_t acc = (kb != it.kb0 || k != 0) ? 1u : 0u;
+                if (MODE == kModeAlpha) mma_bf16_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_BF16, acc);
+                else mma_i8_2sm(dtm, ad + 2 * k, bd + 2 * k, IDESC_I8, acc);
               }
             }
             mma_commit_2sm(&empty[ring.stage], all_mask);
@@ -363,7 +424,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         if (elect_one()) mma_commit_2sm(&tfull[buf], pmask);
         __syncwarp();
-        if (unit_has_cmc(p, w)) {
+        if (it.kind != kItemPart && unit_has_cmc(p, w)) {
           pend = true;
           pu = w;
           pbuf = buf;
@@ -383,9 +444,10 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint32_t nst = 0;                                   // Y chunks this warp has staged so far
     uint32_t local = 0, cmc_cnt[2] = {0u, 0u};
     const uint64_t pol_y = policy_evict_first();          // Y is written once, never re-read here
-    for (int u = cid; u < p.n_items; u += ncl) {
+    Item it;
+    for (int i = 0; get_item(p, cid, ncl, i, it); ++i) {
       Unit w;
-      if (!decode_unit<NP>(p, u, pair, w)) continue;
+      if (!decode_unit<NP>(p, it.u, pair, w)) continue;
       const bool real = w.nt < p.num_n;                  // false: partner-only n-tile past the edge
       const uint32_t buf = local & 1u, ph = (local >> 1) & 1u;
       ++local;
@@ -432,6 +494,64 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_wait(&tfull[buf], ph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN + c0 * 32;
+      if (it.kind == kItemPart) {
+        // stream-K partial: the raw 32-bit accumulators of this CTA's 128 rows go to the pair's
+        // slot; the owner of the unit adds them (int32 exactly; f32 in a fixed order)
+        // slot layout [warp][chunk][j][lane][4]: each 16-byte store of a warp covers 512
+        // contiguous bytes (the owner reads it back the same way)
+        uint4* dst = reinterpret_cast<uint4*>(p.sk_part) + ((size_t)(cid * 2 + (int)rank) * EPI_WARPS + ew) * 4 * 8 * 32 + lane;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= nch) break;
+          uint32_t v[32];
+          tmem_ld32(taddr + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dst[(c * 8 + j) * 32] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[buf], lead_cta);
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], 1;" ::"l"(p.sk_flag + cid * 2 + (int)rank) : "memory");
+        continue;
+      }
+      if (it.kind == kItemOwner) {                       // the later segments' partials are posted
+        if (lane == 0)
+          for (int pc = it.c_lo; pc <= it.c_hi; ++pc) {
+            const uint32_t* fl = p.sk_flag + pc * 2 + (int)rank;
+            uint32_t v = 0;
+            const long long t0 = clock64();
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+              if (clock64() - t0 > 8000000000LL) __trap();
+            } while (v == 0u);
+          }
+        __syncwarp();
+      }
+      // owner: + the posted partials of pairs c_lo..c_hi (same rows / columns), in that order
+      auto add_parts = [&](uint32_t (&v)[32], int c) {
+        if (it.kind != kItemOwner) return;
+        for (int pc = it.c_lo; pc <= it.c_hi; ++pc) {
+          const uint4* s4 = reinterpret_cast<const uint4*>(p.sk_part) +
+                            ((size_t)(pc * 2 + (int)rank) * EPI_WARPS + ew) * 4 * 8 * 32 + c * 8 * 32 + lane;
+          uint4 pa[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) pa[j] = __ldcg(s4 + j * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 a = pa[j];
+            const uint32_t x[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint32_t& t = v[4 * j + e];
+              t = MODE == kModeRef ? __float_as_uint(__uint_as_float(t) + __uint_as_float(x[e])) : t + x[e];
+            }
+          }
+        }
+      };
 
       auto dequant = [&](uint32_t (&v)[32], int c) {
 #pragma unroll
@@ -473,6 +593,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
+          add_parts(v, c);
           dequant(v, c);
           tmem_st32(taddr + c * 32, v);
         }
@@ -581,6 +702,7 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint32_t v[32];
           tmem_ld32(taddr + c * 32, v);
           tmem_wait_ld();
+          add_parts(v, c);
           if (MODE == kModeFwd) dequant(v, c);
           if (MODE == kModeFwd && tl) text_loss(v, c);
           store_chunk(v, c);
@@ -654,12 +776,38 @@ int active_clusters() {
 
 template <int MODE, int CL>
 cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
-                        const CUtensorMap& l2, const Params& p, int max_cl, cudaStream_t st) {
+                        const CUtensorMap& l2, Params p, int max_cl, bool sk_ok, cudaStream_t st) {
   {
     cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(masq_gemm_kernel<MODE, CL>), SMEM_ALLOC);
     if (e != cudaSuccess) return e;
   }
-  const int clusters = (int)std::min<int64_t>(p.n_items, std::min(max_cl, active_clusters<MODE, CL>()));
+  const int avail = std::min(max_cl, active_clusters<MODE, CL>());
+  int clusters = (int)std::min<int64_t>(p.n_items, avail);
+  p.n_full = p.n_items;
+  p.sk_R = p.sk_per = p.sk_pairs = 0;
+  if (sk_ok && CL == 2 && p.num_kb >= kSkMinUnitKb) {
+    // stream-K remainder: when the units past the last full wave would leave more than a quarter
+    // of the pairs idle, their k-blocks are spread over all pairs instead (segments of >= kSkMinKb)
+    const int W = p.n_items / avail, R = p.n_items - W * avail;
+    if (R > 0 && 4 * R <= 3 * avail) {
+      // segment length: an even share of the remainder over all pairs, but at least kSkMinKb and
+      // at most kSkMaxSeg segments per unit (the owner adds the others' partials one by one);
+      // below one unit (a pair holds at most two segments)
+      const long long tot = (long long)R * p.num_kb;
+      long long per = ceil_div(tot, (long long)avail);
+      per = std::max<long long>(per, kSkMinKb);
+      per = std::max<long long>(per, ceil_div((long long)p.num_kb, (long long)kSkMaxSeg));
+      if (per < p.num_kb) {
+        p.sk_per = (int)per;
+        p.sk_pairs = (int)ceil_div(tot, (long long)p.sk_per);
+        p.sk_R = R;
+        p.n_full = W * avail;
+        clusters = avail;
+        cudaError_t e = cudaMemsetAsync(p.sk_flag, 0, sizeof(uint32_t) * 2 * p.sk_pairs, st);
+        if (e != cudaSuccess) return e;
+      }
+    }
+  }
   static const char* const kNames[6] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha",
                                         "gemm_alpha_i8"};
   ProfScope ps_(kNames[MODE], st);
@@ -682,11 +830,14 @@ int gemm_cluster_size(int mode) {
 
 template <int MODE>
 cudaError_t launch_cl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const CUtensorMap& z,
-                      const CUtensorMap& l2, const Params& p, int cl, int max_pairs, cudaStream_t st) {
-  if (cl == 4) return launch_mode<MODE, 4>(a, b, y, z, l2, p, std::max(1, max_pairs / 2), st);
-  return launch_mode<MODE, 2>(a, b, y, z, l2, p, max_pairs, st);
+                      const CUtensorMap& l2, const Params& p, int cl, int max_pairs, bool sk_ok, cudaStream_t st) {
+  if (cl == 4) return launch_mode<MODE, 4>(a, b, y, z, l2, p, std::max(1, max_pairs / 2), false, st);
+  return launch_mode<MODE, 2>(a, b, y, z, l2, p, max_pairs, sk_ok, st);
 }
 }  // namespace
+
+size_t gemm_sk_part_bytes() { return (size_t)(num_sms() / 2) * 2 * BM * BN * sizeof(uint32_t); }
+size_t gemm_sk_flag_bytes() { return (size_t)(num_sms() / 2) * 2 * sizeof(uint32_t); }
 
 int gemm_epilogue_warps() { return 2; }   // loss partial slots per unit (one per CTA of the pair)
 
@@ -828,13 +979,21 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     return e ? atoi(e) : 0;
   }();
   const int max_pairs = env_cl > 0 ? std::min(env_cl, num_sms() / 2) : num_sms() / 2;
+  static const bool sk_off = [] {                          // MASQ_STREAMK=0: measurement switch
+    const char* e = getenv("MASQ_STREAMK");
+    return e && e[0] == '0';
+  }();
+  const bool sk_ok = !sk_off && g.sk_part != nullptr && g.sk_flag != nullptr &&
+                     (g.mode == kModeFwd || g.mode == kModeAcc || g.mode == kModeRef);
+  p.sk_part = g.sk_part;
+  p.sk_flag = g.sk_flag;
   switch (g.mode) {
-    case kModeFwd: return launch_cl<kModeFwd>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
-    case kModeAcc: return launch_cl<kModeAcc>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
-    case kModeLoss: return launch_cl<kModeLoss>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
-    case kModeRef: return launch_cl<kModeRef>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
-    case kModeAlpha: return launch_cl<kModeAlpha>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
-    case kModeAlphaI8: return launch_cl<kModeAlphaI8>(ta, tb, ty, tz, tl2, p, cl, max_pairs, st);
+    case kModeFwd: return launch_cl<kModeFwd>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
+    case kModeAcc: return launch_cl<kModeAcc>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
+    case kModeLoss: return launch_cl<kModeLoss>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
+    case kModeRef: return launch_cl<kModeRef>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
+    case kModeAlpha: return launch_cl<kModeAlpha>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
+    case kModeAlphaI8: return launch_cl<kModeAlphaI8>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -42,6 +42,8 @@ struct WsLayout {
   size_t ids0 = 0, dpart = 0;
   // fused layer call: token-order codes next to the grouped ones
   size_t qx_tok = 0, dx_tok = 0, fpart = 0, ipos = 0, zpart = 0;
+  // stream-K partials / flags of the forward and X.W GEMMs
+  size_t skpart = 0, skflag = 0;
 };
 // f32_x: the forward needs bf16 hi/lo planes of X for the CMC GEMM
 WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, int32_t r, bool f32_x = true);
@@ -170,8 +172,15 @@ struct GemmArgs {
   const uint8_t* ids;
   int fwd_loss = 0;
   int skip_m0 = 0;
+  // stream-K remainder (kModeFwd / Acc / Ref; optional, nullptr = off): the units past the last
+  // full wave are split along K over all CTA pairs; sk_part holds the non-owner partial
+  // accumulators (gemm_sk_bytes), sk_flag one ready flag per (pair, CTA)
+  uint32_t* sk_part = nullptr;
+  uint32_t* sk_flag = nullptr;
 };
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t st);
+size_t gemm_sk_part_bytes();   // workspace for GemmArgs::sk_part (device-independent upper bound)
+size_t gemm_sk_flag_bytes();
 int gemm_epilogue_warps();
 
 // ---------------------------------------------------------------- N1 gradient (grad.cu)

@@ -96,7 +96,7 @@ def test_every_workspace_op_has_a_layout(so):
     flag = ops.pop("MASQ_OP_SELF_REF")
     assert len(ops) >= 14
     T, d, n, M, r = 4096, 1024, 2048, 2, 64
-    stateless = {"MASQ_OP_STATS", "MASQ_OP_INIT", "MASQ_OP_REFERENCE"}   # only the status word
+    stateless = {"MASQ_OP_STATS", "MASQ_OP_INIT"}   # only the status word (REFERENCE: + stream-K scratch)
     cpu_only_unknown = {"MASQ_OP_CMC", "MASQ_OP_CMC_FACTORS"}   # need the eigensolver's query (GPU)
     for name, op in ops.items():
         size = L.masq_workspace_size(op, T, d, n, M, r)

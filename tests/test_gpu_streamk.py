@@ -1,0 +1,44 @@
+"""GPU parity of the GEMM's stream-K remainder (gemm.cu: the 256 x 256 units past the last full
+wave of CTA pairs are split along K over the pairs; the unit's owner adds the other segments'
+partial accumulators — int32 exactly, f32 in a fixed order — before its epilogue).  Deep-K shapes
+only take that path (>= 64 k-blocks per unit).  The checked rows include every row of the
+remainder units (the last m-units of the raster), so each split unit is compared in full:
+  * int32 accumulators bit-exact against the oracle's integer GEMM (A6);
+  * Y <= 1e-3 max-abs-normalised per modality (CMC included);
+  * X W (masq_reference_output) <= 1e-4 per modality against f64 (reading Q16).
+Cases: c3 down 18944 -> 3584 at 4096 tokens (2 remainder units of 4 segments) and c2 down
+11008 -> 2048 at 4096 tokens (54 remainder units, segments crossing unit boundaries)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from test_gpu_parity import M, bf, sample_rows, tt
+from test_gpu_shapes import per_modality_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,d,n,tail_rows", [("c3", 18944, 3584, 256), ("c2", 11008, 2048, 1792)])
+def test_streamk_remainder_units(cfg, d, n, tail_rows):
+    c = synth.config_inputs(cfg, d=d, n=n, T=4096, layer=4)
+    m = M()
+    T, n_mod, wb, ab, r = c["T"], c["n_mod"], c["wbits"], c["abits"], c["r"]
+    Ro, co = O.calibrate_stats(c["X"], c["ids"], n_mod)
+    so = O.init_factors(Ro, co, c["W"])
+    qwo, dwo = O.quantize_weight(c["W"], so[0], wb)
+    X, ids = bf(c["X"]), tt(c["ids"])
+    rows = np.union1d(sample_rows(c["ids"], n_random=64), np.arange(T - tail_rows, T))
+    acc = m.linear_forward(X, ids, tt(so), tt(qwo), tt(dwo), wb, ab, acc_debug=True).cpu().numpy()
+    qxo, _ = O.quantize_activations(O.decode(c["X"])[rows], c["ids"][rows], so, ab)
+    assert np.array_equal(acc[rows].astype(np.int64), O.int_gemm(qxo, qwo))
+    L1 = bf(c["L1"]) if r else None
+    L2 = bf(c["L2"]) if r else None
+    Y = m.linear_forward(X, ids, tt(so), tt(qwo), tt(dwo), wb, ab, L1, L2).cpu().numpy()
+    m.check()
+    Yo = O.linear_forward(c["X"], c["ids"], so, qwo, dwo, ab, list(c["L1"]) if r else None,
+                          list(c["L2"]) if r else None, rows=rows)
+    assert max(per_modality_err(Y[rows], Yo, c["ids"][rows]).values()) <= 1e-3
+    Yr = m.reference_output(X, bf(c["W"])).cpu().numpy()
+    Yro = O.decode(c["X"])[rows].astype(np.float64) @ O.decode(c["W"]).astype(np.float64)
+    assert max(per_modality_err(Yr[rows], Yro, c["ids"][rows]).values()) <= 1e-4
