@@ -14,10 +14,11 @@
 // MMAs of group g+1..g+3 overlap the promotion of group g.
 // Pipeline: an input ring (the group's packed tile by one 1D bulk copy + the token tile by 2-SM
 // TMA), converter warps writing a separate ring of unpacked A tiles, the MMA warp, 8 epilogue
-// warps.  Measured limit (profiles/r02_w4g_ablation.json): the per-group handshake cycles
-// (input slot, A slot, accumulator: ~3 cross-warp / cross-CTA signals per 262 cycles of MMA work)
-// with at most 4 groups in flight (TMEM holds 4 x 128 columns), not the MMAs, the unpacking or
-// the promotion math; a 1-CTA variant without the cross-CTA hops measured no faster.
+// warps.  Measured limit (profiles/r02b_w4g_trace.txt, pipeline clock stamps): each epilogue warp
+// may only read its sub-partition's TMEM lane quarter, the two converter warps load sub-partitions
+// 2 and 3, and the epilogue warps there release each accumulator 2-3 groups late, so the MMA warp
+// (which needs all 32 releases) keeps ~1 group of slack out of 4 accumulators; spreading the
+// unpacking over all sub-partitions measured slower (register caps, fences on the critical path).
 //
 // Packed format (this kernel's, masq_quantize_weight_w4g): group-major [d/128][n][64 B] — the 64
 // bytes of (group g, channel j) at (g n + j) 64, so a CTA's 128-channel group tile is one contiguous
