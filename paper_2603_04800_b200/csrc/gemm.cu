@@ -119,6 +119,7 @@ struct Params {
   // stream-K remainder: work items n_full.. are the sk_R units past the last full wave, their
   // sk_R * num_kb k-blocks cut into ranges of sk_per over pairs 0 .. sk_pairs-1
   int n_full, sk_R, sk_per, sk_pairs;
+  int policy;                  // X.W operand L2 hints: bit 0 A evict_first, bit 1 B evict_last
   uint32_t* sk_part;           // [pair][CTA][128 rows][256 cols] 32-bit partial accumulators
   uint32_t* sk_flag;           // [pair][CTA] partial posted (zeroed before the launch)
 };
@@ -288,8 +289,8 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       // warp-wide loop (uniform state), one elected lane issues each stage's copies
       // A streams through (evict-first); B is re-read by every m-unit of the raster group (evict-last)
       // (int8 modes: default policy measured as fast or faster)
-      const uint64_t pol_a = MODE == kModeRef ? policy_evict_first() : policy_evict_normal();
-      const uint64_t pol_b = MODE == kModeRef ? policy_evict_last() : policy_evict_normal();
+      const uint64_t pol_a = (MODE == kModeRef && (p.policy & 1)) ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_b = (MODE == kModeRef && (p.policy & 2)) ? policy_evict_last() : policy_evict_normal();
       Ring ring;
       bool pend = false;
       Unit pu{};
@@ -987,6 +988,15 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
                      (g.mode == kModeFwd || g.mode == kModeAcc || g.mode == kModeRef);
   p.sk_part = g.sk_part;
   p.sk_flag = g.sk_flag;
+  // X.W L2 hints: A (X) evict_first keeps the raster group's B panels (evict_last) resident at
+  // d = 3584; at deep K the A tile of a k-block is re-read by the other units of the wave after
+  // it was evicted: there A keeps the normal policy (tools/refpol_sweep.sh, profiles/
+  // r02b_refpol_sweep.txt: down projection 1.578 -> 1.506 ms, DRAM reads 6.39 -> 4.00 GB)
+  static const int env_pol = [] {                          // MASQ_REF_POLICY: measurement knob
+    const char* e = getenv("MASQ_REF_POLICY");
+    return e ? atoi(e) : -1;
+  }();
+  p.policy = env_pol >= 0 ? env_pol : (p.num_kb >= 128 ? 2 : 3);
   switch (g.mode) {
     case kModeFwd: return launch_cl<kModeFwd>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
     case kModeAcc: return launch_cl<kModeAcc>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
