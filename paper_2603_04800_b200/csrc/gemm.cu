@@ -287,10 +287,10 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     {
       // ------------------------------------------------------------ TMA producer (all CTAs)
       // warp-wide loop (uniform state), one elected lane issues each stage's copies
-      // A streams through (evict-first); B is re-read by every m-unit of the raster group (evict-last)
-      // (int8 modes: default policy measured as fast or faster)
-      const uint64_t pol_a = (MODE == kModeRef && (p.policy & 1)) ? policy_evict_first() : policy_evict_normal();
-      const uint64_t pol_b = (MODE == kModeRef && (p.policy & 2)) ? policy_evict_last() : policy_evict_normal();
+      // L2 hints per mode and depth (p.policy, set on the host): B is re-read by every m-unit of the
+      // raster group (evict_last); A evict_first only for X.W at d = 3584
+      const uint64_t pol_a = (p.policy & 1) ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol_b = (p.policy & 2) ? policy_evict_last() : policy_evict_normal();
       Ring ring;
       bool pend = false;
       Unit pu{};
@@ -996,7 +996,14 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t st) {
     const char* e = getenv("MASQ_REF_POLICY");
     return e ? atoi(e) : -1;
   }();
-  p.policy = env_pol >= 0 ? env_pol : (p.num_kb >= 128 ? 2 : 3);
+  // int8 GEMMs: B evict_last, A normal measured best or tied at every c3 shape (1-1.5%,
+  // tools/i8pol_sweep.sh, profiles/r02b_i8pol_sweep.txt)
+  static const int env_pol8 = [] {                         // MASQ_I8_POLICY: the same for the int8 GEMMs
+    const char* e = getenv("MASQ_I8_POLICY");
+    return e ? atoi(e) : 2;
+  }();
+  if (g.mode == kModeRef) p.policy = env_pol >= 0 ? env_pol : (p.num_kb >= 128 ? 2 : 3);
+  else p.policy = env_pol8;
   switch (g.mode) {
     case kModeFwd: return launch_cl<kModeFwd>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
     case kModeAcc: return launch_cl<kModeAcc>(ta, tb, ty, tz, tl2, p, cl, max_pairs, sk_ok, st);
