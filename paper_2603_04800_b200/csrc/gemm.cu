@@ -30,10 +30,21 @@
 // each pair TMA-loads half of it (64 rows) multicast into the rank-r CTAs of both pairs, so each
 // SM reads 24 KB per k-block from L2 instead of 32 KB.  Every stage slot is then shared by the
 // two pairs: the MMA commits that free it multicast to all four CTAs (empty barrier count 2).
+// Measured 2-8% slower than CL = 2 on this part (only 33 four-CTA clusters are co-resident:
+// 132 SMs), so CL = 2 is the default.
+//
+// Work items: whole units in a raster order (groups of >= 16 n-tiles swept over all m-units), and
+// for deep K (>= 64 k-blocks) a stream-K remainder: the units past the last full wave of pairs
+// are cut along K into <= 4 segments over the pairs; a segment that does not start at k-block 0
+// writes its raw accumulators to the workspace and releases a flag, and the unit's owner (the
+// pair holding k-block 0) adds them before its normal epilogue.
 //
 // Roles per CTA (320 threads, 1 CTA per SM, grid = CL x min(#work items, active clusters)):
-//   warp 0 lane 0 : TMA producer  (both CTAs; 6-stage ring of 16 KB A + 16 KB B)
-//   warp 1        : TMEM allocation (both CTAs); lane 0 of the leader issues the MMAs
+//   warp 0        : TMA producer  (all CTAs; 6-stage ring of 16 KB A + 16 KB B; one elect.sync lane
+//                   issues each stage's copies)
+//   warp 1        : TMEM allocation (all CTAs); in the leader the whole warp runs the MMA loop and
+//                   one elect.sync lane issues the MMAs and commits (warp-uniform operands: no
+//                   per-operand R2UR waterfalls, profiles/r02b_mma_issue.md)
 //   warps 2..9    : epilogue      (warp w owns TMEM lane quarter w%4 and column half (w-2)/4:
 //                                  tcgen05.ld 32x32b -> dequant -> swizzled smem -> TMA store)
 // TMEM holds two 256-column accumulators (512 columns) so the epilogue of unit i overlaps the
