@@ -190,9 +190,12 @@ struct Item {
 };
 constexpr int kItemWhole = 0, kItemOwner = 1, kItemPart = 2;
 // item i of cluster cid: whole units cid, cid + ncl, ... below n_full, then the (<= 2) segments
-// of its stream-K range [cid * sk_per, (cid + 1) * sk_per) of the remainder's k-blocks; a pair's
-// first segment may continue a unit another pair owns (kind 2), any later one starts a unit at
-// k-block 0 (its owner).  Every role walks the same sequence.
+// of its stream-K range [cid * sk_per, (cid + 1) * sk_per) of the remainder's k-blocks, the later
+// segment first.  A unit's owner is the pair holding its LAST k-block; it waits for the partials
+// of the lower pairs c_lo..cid-1 holding its earlier k-blocks.  A pair's partial segment comes
+// before its owner segment and never waits, and lower cluster ids are dispatched first, so the
+// waits form no cycle and no chain, even when only some clusters are resident (another kernel
+// on another stream holding SMs).  Every role walks the same sequence.
 __device__ __forceinline__ bool get_item(const Params& p, int cid, int ncl, int i, Item& it) {
   const int n1 = p.n_full > cid ? (p.n_full - cid + ncl - 1) / ncl : 0;
   if (i < n1) {
@@ -208,21 +211,25 @@ __device__ __forceinline__ bool get_item(const Params& p, int cid, int ncl, int 
   const long long g0 = (long long)cid * p.sk_per;
   const long long g1 = g0 + p.sk_per < tot ? g0 + p.sk_per : tot;
   if (g0 >= g1) return false;
-  const int r = (int)(g0 / p.num_kb) + j;
+  // the range's segments in reverse order: a second segment (the start of the next unit, never
+  // its last k-block: a partial) first, so partials are posted before any owner waits
+  const int r0 = (int)(g0 / p.num_kb);
+  const bool two = g1 > (long long)(r0 + 1) * p.num_kb;
+  if (j > (two ? 1 : 0)) return false;
+  const int r = r0 + ((two && j == 0) ? 1 : 0);
   const long long us = (long long)r * p.num_kb, ue = us + p.num_kb;
   const long long a = g0 > us ? g0 : us, b = g1 < ue ? g1 : ue;
   if (a >= b) return false;
   it.u = p.n_full + r;
   it.kb0 = (int)(a - us);
   it.kb1 = (int)(b - us);
-  if (it.kb0 > 0) {
+  if (it.kb1 < p.num_kb) {
     it.kind = kItemPart;
   } else {
-    long long cl = (ue - 1) / p.sk_per;
-    if (cl > p.sk_pairs - 1) cl = p.sk_pairs - 1;
-    it.kind = cl > cid ? kItemOwner : kItemWhole;
-    it.c_lo = cid + 1;
-    it.c_hi = (int)cl;
+    const int c0 = (int)(us / p.sk_per);                 // the pair holding the unit's k-block 0
+    it.kind = c0 < cid ? kItemOwner : kItemWhole;
+    it.c_lo = c0;
+    it.c_hi = cid - 1;
   }
   return true;
 }
