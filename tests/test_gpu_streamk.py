@@ -6,8 +6,9 @@ remainder units (the last m-units of the raster), so each split unit is compared
   * int32 accumulators bit-exact against the oracle's integer GEMM (PAPER.md:177-185, A6);
   * Y <= 1e-3 max-abs-normalised per modality (CMC included);
   * X W (masq_reference_output) <= 1e-4 per modality against f64 (reading Q16).
-Cases: c3 down 18944 -> 3584 at 4096 tokens (2 remainder units of 4 segments) and c2 down
-11008 -> 2048 at 4096 tokens (54 remainder units, segments crossing unit boundaries)."""
+Cases: c3 down 18944 -> 3584 at 4096 tokens (2 remainder units of 4 segments), c2 down
+11008 -> 2048 at 4096 tokens (54 remainder units, segments crossing unit boundaries), and two
+ragged deep-K shapes (T and n not multiples of the 256 x 256 unit)."""
 import numpy as np
 import pytest
 
@@ -19,9 +20,11 @@ from test_gpu_shapes import per_modality_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cfg,d,n,tail_rows", [("c3", 18944, 3584, 256), ("c2", 11008, 2048, 1792)])
-def test_streamk_remainder_units(cfg, d, n, tail_rows):
-    c = synth.config_inputs(cfg, d=d, n=n, T=4096, layer=4)
+@pytest.mark.parametrize("cfg,d,n,T,tail_rows", [("c3", 18944, 3584, 4096, 256), ("c2", 11008, 2048, 4096, 1792),
+                                                ("c3", 16384, 2080, 3000, 952), ("c2", 8192, 1120, 2777, 800)])
+def test_streamk_remainder_units(cfg, d, n, T, tail_rows):
+    """(the last two: ragged T and n — partial m-units and a partial last n-tile inside split units)"""
+    c = synth.config_inputs(cfg, d=d, n=n, T=T, layer=4)
     m = M()
     T, n_mod, wb, ab, r = c["T"], c["n_mod"], c["wbits"], c["abits"], c["r"]
     Ro, co = O.calibrate_stats(c["X"], c["ids"], n_mod)
