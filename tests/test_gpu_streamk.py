@@ -45,3 +45,34 @@ def test_streamk_remainder_units(cfg, d, n, T, tail_rows):
     Yr = m.reference_output(X, bf(c["W"])).cpu().numpy()
     Yro = O.decode(c["X"])[rows].astype(np.float64) @ O.decode(c["W"]).astype(np.float64)
     assert max(per_modality_err(Yr[rows], Yro, c["ids"][rows]).values()) <= 1e-4
+
+
+def test_streamk_concurrent_streams():
+    """Two deep-K stream-K GEMM calls on two CUDA streams at once (separate workspaces), repeated:
+    their clusters compete for SMs, so each kernel may be only partly resident while its owners
+    wait for partials; the waits go only to lower, earlier-dispatched clusters, so both complete.
+    Results equal the same calls run alone (int32 accumulators: bit-identical)."""
+    import torch
+    m = M()
+    c = synth.config_inputs("c3", d=18944, n=3584, T=4096, layer=5)
+    Ro, co = O.calibrate_stats(c["X"], c["ids"], 2)
+    so = O.init_factors(Ro, co, c["W"])
+    qwo, dwo = O.quantize_weight(c["W"], so[0], 4)
+    X, ids, s, qw, dw = bf(c["X"]), tt(c["ids"]), tt(so), tt(qwo), tt(dwo)
+    want = m.linear_forward(X, ids, s, qw, dw, 4, 8, acc_debug=True)
+    wref = m.reference_output(X, bf(c["W"]))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    wss = [m.Workspace(X.device), m.Workspace(X.device)]
+    outs = []
+    for it in range(4):
+        for k in range(2):
+            with torch.cuda.stream(streams[k]):
+                if (it + k) % 2 == 0:
+                    outs.append(("acc", m.linear_forward(X, ids, s, qw, dw, 4, 8, acc_debug=True, ws=wss[k])))
+                else:
+                    outs.append(("ref", m.reference_output(X, bf(c["W"]), ws=wss[k])))
+    torch.cuda.synchronize()
+    m.check()
+    for kind, o in outs:
+        assert torch.equal(o, want if kind == "acc" else wref), kind
