@@ -390,20 +390,18 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * QN + h * 64;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          uint32_t v[32];
-          if (!(p.exp & 4)) {
-            tmem_ld32(taddr + half * 32, v);
-            tmem_wait_ld();
-          } else {
+        // both 32-column halves loaded before one wait (the accumulator is released to the MMA
+        // warp a tcgen05.ld round trip earlier)
+        uint32_t v2[2][32];
+        tmem_ld32(taddr, v2[0]);
+        tmem_ld32(taddr + 32, v2[1]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
 #pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = (uint32_t)k;
-          }
-          if (half == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
-          }
+        for (int half = 0; half < 2; ++half) {
+          const uint32_t (&v)[32] = v2[half];
           if constexpr (ACC) {
 #pragma unroll
             for (int k = 0; k < 32; ++k) yi[half * 32 + k] += ((int)v[k]) >> 4;
