@@ -302,6 +302,16 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
     // t takes chunks q = t + 64 k (row q / 4, chunk q % 4): a warp's loads cover 512 contiguous bytes
     // and its swizzled stores hit distinct banks (no shared-memory bank conflicts)
     const uint32_t tid = (warp - 2) * 32 + lane;
+    // this thread's store offsets in an A slot: chunk c of row r -> 16-byte units 2c ^ (r & 7)
+    // (low nibbles) and that ^ 1 (high nibbles); the swizzle depends only on the row
+    constexpr int KCH = (QM * 4) / (32 * CONV_WARPS);
+    uint32_t aoff[KCH];
+#pragma unroll
+    for (int k = 0; k < KCH; ++k) {
+      const uint32_t q = tid + k * 32 * CONV_WARPS;
+      const uint32_t row = q >> 2, c = q & 3u;
+      aoff[k] = row * QK + (((2u * c) ^ (row & 7u)) << 4);
+    }
     QRing<NP> ring;
     QRing<NA> aring;
     for (int u = cid; u < p.n_units; u += ncl) {
@@ -313,23 +323,16 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
         const uint32_t dstA = smem_u32(sA + aring.stage * QA_BYTES);
         // all loads first (the stores below are asm with a memory clobber, which would otherwise
         // serialise every load behind the previous chunk's stores)
-        constexpr int KCH = (QM * 4) / (32 * CONV_WARPS);
         uint4 xin[KCH];
 #pragma unroll
         for (int k = 0; k < KCH; ++k) xin[k] = (p.exp & 2) ? make_uint4(0, 0, 0, 0) : src[tid + k * 32 * CONV_WARPS];
-        if (!(p.exp & 16)) fence_proxy_async_smem();            // the reads before the slot's TMA refill
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pempty[ring.stage]);        // packed bytes consumed
 #pragma unroll
         for (int k = 0; k < KCH; ++k) {
-          const uint32_t q = tid + k * 32 * CONV_WARPS;
-          const uint32_t row = q >> 2, c = q & 3u;
           const uint4 x = xin[k];
           const uint4 lo = make_uint4((x.x << 4) & 0xF0F0F0F0u, (x.y << 4) & 0xF0F0F0F0u,
                                       (x.z << 4) & 0xF0F0F0F0u, (x.w << 4) & 0xF0F0F0F0u);
           const uint4 hi = make_uint4(x.x & 0xF0F0F0F0u, x.y & 0xF0F0F0F0u, x.z & 0xF0F0F0F0u, x.w & 0xF0F0F0F0u);
-          const uint32_t d0 = dstA + row * QK + (((2u * c) ^ (row & 7u)) << 4);
-          const uint32_t d1 = dstA + row * QK + (((2u * c + 1u) ^ (row & 7u)) << 4);
+          const uint32_t d0 = dstA + aoff[k], d1 = dstA + (aoff[k] ^ 16u);
           if (p.exp & 32) continue;
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d0), "r"(lo.x), "r"(lo.y), "r"(lo.z),
                        "r"(lo.w)
@@ -338,6 +341,11 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
                        "r"(hi.w)
                        : "memory");
         }
+        // the packed bytes were consumed by the stores above (their values are in the stored
+        // words), so the input slot is released without a proxy fence of its own; the A slot's
+        // generic stores are fenced for the MMA's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[ring.stage]);
         if (!(p.exp & 16)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&aready[aring.stage], 0);
