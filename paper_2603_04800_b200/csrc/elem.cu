@@ -287,13 +287,26 @@ __global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ R, 
       if (count[m] == 0) atomicOr(status, kStEmptyModality);
   }
   if (i >= d) return;
-  float wm = 0.f;
-  for (int64_t j = (int64_t)lane * V; j < n; j += 32 * V) {
+  // 4 independent 16-byte loads in flight per lane (one per iteration left the warp latency-bound:
+  // 512 B in flight per row)
+  float wq[4] = {0.f, 0.f, 0.f, 0.f};
+  int64_t j = (int64_t)lane * V;
+  for (; j + 3 * 32 * V < n; j += 4 * 32 * V) {
+    float f[4][V];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Vec<WT>::load(W + i * n + j + u * 32 * V, f[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < V; ++e) wq[u] = fmaxf(wq[u], fabsf(f[u][e]));
+  }
+  for (; j < n; j += 32 * V) {
     float f[V];
     Vec<WT>::load(W + i * n + j, f);
 #pragma unroll
-    for (int e = 0; e < V; ++e) wm = fmaxf(wm, fabsf(f[e]));
+    for (int e = 0; e < V; ++e) wq[0] = fmaxf(wq[0], fabsf(f[e]));
   }
+  float wm = fmaxf(fmaxf(wq[0], wq[1]), fmaxf(wq[2], wq[3]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
   if (lane < n_mod) {
