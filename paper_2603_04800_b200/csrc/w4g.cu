@@ -55,7 +55,12 @@ constexpr int NP = 5;                   // input ring: packed group tile (or a C
 constexpr int NA = 5;                   // unpacked A ring (the converters' output)
 constexpr int NBUF = 4;                 // 128-column TMEM accumulators
 constexpr int CONV_WARPS = 2;
-constexpr int EPI_WARPS = 8;
+#ifndef MASQ_W4G_EPI
+#define MASQ_W4G_EPI 8
+#endif
+constexpr int EPI_WARPS = MASQ_W4G_EPI;         // 4 TMEM lane quarters x (EPI_WARPS / 4) column groups
+constexpr int EPI_COLS = QN / (EPI_WARPS / 4);   // token columns per epilogue warp
+constexpr int EPI_CH = EPI_COLS / 32;           // 32-column tcgen05.ld chunks per warp
 constexpr int QTHREADS = 64 + 32 * (CONV_WARPS + EPI_WARPS);
 constexpr int P_A = QA_BYTES;           // input slot: 16 KB region (packed uses 8 KB, CMC A 16 KB) ...
 constexpr int P_SLOT = P_A + QB_BYTES;  // ... + the 8 KB B tile
@@ -366,9 +371,9 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
     }
   } else {
     // ------------------------------------------------------------------ epilogue (both CTAs)
-    const uint32_t e = warp - 2 - CONV_WARPS;           // 0..7
+    const uint32_t e = warp - 2 - CONV_WARPS;           // 0 .. EPI_WARPS-1
     const uint32_t q = warp & 3u;                       // TMEM lane quarter
-    const int h = (int)(e >> 2);                        // column half: tokens [64h, 64h + 64)
+    const int h = (int)(e >> 2);                        // column group: tokens [EPI_COLS h, EPI_COLS (h + 1))
     uint32_t acnt = 0;
     for (int u = cid; u < p.n_units; u += ncl) {
       const WUnit w = w_unit(p, u);
@@ -380,12 +385,12 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
       // the magic-number add (IADD: bits of 1.5 * 2^23 + acc, exact) and FADD2 (- 1.5 * 2^23,
       // exact), then FFMA2 into y — one ALU and one FMA-pipe operation per element (I2FP, the
       // conversion instruction, issues at a quarter of the ALU rate and bound this loop)
-      int yi[ACC ? 64 : 1];
-      uint64_t y2[ACC ? 1 : 32];
+      int yi[ACC ? EPI_COLS : 1];
+      uint64_t y2[ACC ? 1 : EPI_COLS / 2];
 #pragma unroll
-      for (int k = 0; k < (ACC ? 64 : 1); ++k) yi[k] = 0;
+      for (int k = 0; k < (ACC ? EPI_COLS : 1); ++k) yi[k] = 0;
 #pragma unroll
-      for (int k = 0; k < (ACC ? 1 : 32); ++k) y2[k] = 0ull;
+      for (int k = 0; k < (ACC ? 1 : EPI_COLS / 2); ++k) y2[k] = 0ull;
       const uint64_t magic2 = w2_pack(0x4B400000u, 0x4B400000u);
       float sc_next = jv ? __ldg(scp) : 0.f;
       for (int g = 0; g < p.ng; ++g) {
@@ -396,19 +401,18 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
         if (g + 1 < p.ng) sc_next = jv ? __ldg(scp + g + 1) : 0.f;
         mbar_wait(&tfull[buf], bph);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * QN + h * 64;
-#pragma unroll
-        // both 32-column halves loaded before one wait (the accumulator is released to the MMA
+        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * QN + h * EPI_COLS;
+        // every 32-column chunk loaded before one wait (the accumulator is released to the MMA
         // warp a tcgen05.ld round trip earlier)
-        uint32_t v2[2][32];
-        tmem_ld32(taddr, v2[0]);
-        tmem_ld32(taddr + 32, v2[1]);
+        uint32_t v2[EPI_CH][32];
+#pragma unroll
+        for (int ch = 0; ch < EPI_CH; ++ch) tmem_ld32(taddr + ch * 32, v2[ch]);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < EPI_CH; ++half) {
           const uint32_t (&v)[32] = v2[half];
           if constexpr (ACC) {
 #pragma unroll
@@ -422,43 +426,41 @@ w4g_gemm_kernel(const __grid_constant__ CUtensorMap tmX,
           }
         }
       }
-      float y[ACC ? 1 : 64];
+      float y[ACC ? 1 : EPI_COLS];
       if constexpr (!ACC) {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) w2_unpack(y2[k], y[2 * k], y[2 * k + 1]);
+        for (int k = 0; k < EPI_COLS / 2; ++k) w2_unpack(y2[k], y[2 * k], y[2 * k + 1]);
       }
-      const int t0 = w.mt * QN + h * 64;
+      const int t0 = w.mt * QN + h * EPI_COLS;
       if constexpr (ACC) {
         int32_t* out = static_cast<int32_t*>(p.out);
 #pragma unroll
-        for (int k = 0; k < 64; ++k)
+        for (int k = 0; k < EPI_COLS; ++k)
           if (jv && t0 + k < p.T) out[(size_t)(t0 + k) * p.ld_out + j] = yi[k];
       } else {
 #pragma unroll
-        for (int k = 0; k < 64; ++k) y[k] *= (t0 + k < p.T) ? __ldg(p.dx + t0 + k) : 0.f;
+        for (int k = 0; k < EPI_COLS; ++k) y[k] *= (t0 + k < p.T) ? __ldg(p.dx + t0 + k) : 0.f;
         if (w.cmc) {
           const uint32_t buf = acnt % NBUF, bph = (acnt / NBUF) & 1u;
           ++acnt;
           mbar_wait(&tfull[buf], bph);
           tc_fence_after();
-          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * QN + h * 64;
+          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * QN + h * EPI_COLS;
+          uint32_t v2[EPI_CH][32];
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            uint32_t v[32];
-            tmem_ld32(taddr + half * 32, v);
-            tmem_wait_ld();
-            if (half == 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
-            }
+          for (int ch = 0; ch < EPI_CH; ++ch) tmem_ld32(taddr + ch * 32, v2[ch]);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
 #pragma unroll
-            for (int k = 0; k < 32; ++k) y[half * 32 + k] += __uint_as_float(v[k]);
-          }
+          for (int ch = 0; ch < EPI_CH; ++ch)
+#pragma unroll
+            for (int k = 0; k < 32; ++k) y[ch * 32 + k] += __uint_as_float(v2[ch][k]);
         }
         float* out = static_cast<float*>(p.out);
 #pragma unroll
-        for (int k = 0; k < 64; ++k)
+        for (int k = 0; k < EPI_COLS; ++k)
           if (jv && t0 + k < p.T) out[(size_t)(t0 + k) * p.ld_out + j] = y[k];
       }
     }
