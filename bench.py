@@ -61,6 +61,8 @@ def parse():
                          "duration is its own, which the per-kernel table and roofline need; the line also carries an "
                          "'overlapped' block timing the same step on 2 streams, where one linear's HBM-bound kernels "
                          "run beside another's GEMM; c4/c4s use 2)")
+    ap.add_argument("--nvtx", action="store_true",
+                    help="NVTX ranges around the step's phases (stats / per-linear calib_layer), for ncu --nvtx filters")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one captured CUDA graph (N=1; measured slower here: the launch "
                          "gaps are ~2%% of the step and the captured profiler event nodes cost more)")
@@ -703,14 +705,26 @@ def main():
     side_all = [torch.cuda.Stream(device=dev) for _ in range(nside)]
     wss = [ws] + [M.Workspace(dev) for _ in range(nside - 1)]
 
+    nvtx_on = bool(getattr(args, "nvtx", False))
+
+    def rng(name):
+        if nvtx_on:
+            torch.cuda.nvtx.range_push(name)
+
+    def rng_end():
+        if nvtx_on:
+            torch.cuda.nvtx.range_pop()
+
     def step(X_override=None, ids_override=None, nstreams=None):
         nstreams = max(1, args.streams if nstreams is None else nstreams)
         side = side_all[:nstreams] if nstreams > 1 else []
         idt = ids if ids_override is None else ids_override
+        rng("A1 stats + exchange")
         for li, e in enumerate(L):
             X = e["X"] if X_override is None else X_override[li]
             M.calibrate_stats(X, idt, N_MOD, R=Rv[li], count=Cbuf[li], reset=True, ws=ws)
         P.reduce_stats([Rbuf], Cbuf)                    # one batched exchange per step (max is order-free)
+        rng_end()
         main = torch.cuda.current_stream()
         if side:
             ready = torch.cuda.Event()
@@ -721,11 +735,13 @@ def main():
             if side:
                 side[k].wait_event(ready)
             with torch.cuda.stream(side[k] if side else main):
+                rng(f"linear {e['name']} (A2-A8)")
                 s = M.init_factors(Rv[li], Cbuf[li], e["W"], ws=wss[k])
                 e["s"] = s
                 # A3 (every modality's weight codes, one W read) + A4-A7 forward + A8 target and loss
                 M.calib_layer(X, idt, s, e["W"], WBITS, ABITS, e["L1"], e["L2"], Y=e["Y"], Yref=e["Yref"],
                               sums=Sbuf[li], counts=Nbuf[li], loss=losses[li:li + 1], ws=wss[k])
+                rng_end()
         for st_ in side:                                 # join before the exchange / the step's end
             main.wait_stream(st_)
         if world > 1:
