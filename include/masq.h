@@ -81,9 +81,9 @@ typedef enum masq_dtype { MASQ_F32 = 0, MASQ_BF16 = 1 } masq_dtype;
 typedef void* masq_stream;      /* cudaStream_t */
 
 /* Workspace queries: op is one of the MASQ_OP_* values.  The layouts of the calls that run the
- * forward or X W GEMM (FORWARD, LAYER, REFERENCE, LOSS | SELF_REF) include the GEMM's stream-K
- * scratch: one 256 x 256 32-bit partial tile and two flags per CTA pair of the device (~19 MB on
- * 148 SMs). */
+ * forward or X W GEMM (FORWARD, LAYER, REFERENCE, LOSS | SELF_REF) include, for deep K (d >= 8192
+ * for the int8 forward, d >= 4096 for X W), the GEMM's stream-K scratch: one 256 x 256 32-bit
+ * partial tile and two flags per CTA pair of the device (~19 MB on 148 SMs). */
 enum {
   MASQ_OP_STATS = 0, MASQ_OP_INIT = 1, MASQ_OP_QWEIGHT = 2, MASQ_OP_QACT = 3,
   MASQ_OP_FORWARD = 4, MASQ_OP_LOSS = 5, MASQ_OP_REFERENCE = 6, MASQ_OP_LOSS_GRAD = 7,

@@ -96,7 +96,7 @@ def test_every_workspace_op_has_a_layout(so):
     flag = ops.pop("MASQ_OP_SELF_REF")
     assert len(ops) >= 14
     T, d, n, M, r = 4096, 1024, 2048, 2, 64
-    stateless = {"MASQ_OP_STATS", "MASQ_OP_INIT"}   # only the status word (REFERENCE: + stream-K scratch)
+    stateless = {"MASQ_OP_STATS", "MASQ_OP_INIT", "MASQ_OP_REFERENCE"}   # only the status word (at d < 4096)
     cpu_only_unknown = {"MASQ_OP_CMC", "MASQ_OP_CMC_FACTORS"}   # need the eigensolver's query (GPU)
     for name, op in ops.items():
         size = L.masq_workspace_size(op, T, d, n, M, r)
@@ -106,6 +106,10 @@ def test_every_workspace_op_has_a_layout(so):
             assert size >= 256, name
         else:
             assert size > 4096, (name, size)
+    # deep K: the GEMM's stream-K scratch (partial tiles + flags) joins the layouts that run it
+    assert L.masq_workspace_size(ops["MASQ_OP_REFERENCE"], T, 4096, n, 1, 0) > (1 << 20)
+    assert L.masq_workspace_size(ops["MASQ_OP_FORWARD"], T, 8192, n, M, r) > \
+        L.masq_workspace_size(ops["MASQ_OP_FORWARD"], T, 8192 - 128, n, M, r) + (1 << 20)
     # the self-reference flag appends the loss target X W (f32 [T x n]) to the loss layouts
     for name in ("MASQ_OP_LOSS", "MASQ_OP_LOSS_GRAD"):
         base = L.masq_workspace_size(ops[name], T, d, n, M, 0)
