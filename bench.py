@@ -1044,7 +1044,7 @@ def main():
                                + (" x2 (INT8/bf16 nominal ratio)" if dom != "gemm_ref" else ""),
                 "avg_launch_ms": kern[dom]["ms"] / kern[dom]["launches"]}
     fwd = kinfo.get("gemm_fwd", {})
-    fwd_call_ms = sum(kinfo.get(k, {}).get("ms_per_step", 0.0) for k in ("inv", "aquant", "transpose", "l1_fold",
+    fwd_call_ms = sum(kinfo.get(k, {}).get("ms_per_step", 0.0) for k in ("inv", "aquant", "transpose", "l1_fold", "cmc_pack",
                                                                           "zgemm", "gemm_fwd"))
     linear = {
         "tops_gemm_kernel": fwd.get("achieved"),
@@ -1058,7 +1058,7 @@ def main():
         "int8_ceiling_cublas": int8_ceiling,
         "frac_int8_ceiling_cublas_gemm_kernel": (fwd.get("achieved") / int8_ceiling["tops"])
         if (fwd.get("achieved") and int8_ceiling and int8_ceiling.get("tops")) else None,
-        "note": "algorithmic 2*T*d*n ops of the 4 linears; forward = inv + aquant + L1/L2 pack + zgemm + gemm_fwd "
+        "note": "algorithmic 2*T*d*n ops of the 4 linears; forward = inv + aquant + L1/L2 pack (cmc_pack) + zgemm + gemm_fwd "
                 "(the activation codes are computed once per step and shared with the loss)",
     }
     launches = int(sum(v["launches"] for v in kern.values())) * (args.steps // K)   # over the timed region

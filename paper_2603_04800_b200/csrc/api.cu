@@ -385,8 +385,8 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
-    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t, st));
-    MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
+    MASQ_CK(launch_cmc_pack(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t,
+                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, st));
     if (xt == MASQ_BF16) {
       MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     } else {
@@ -511,8 +511,8 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
-    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t, st));
-    MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
+    MASQ_CK(launch_cmc_pack(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t,
+                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, st));
     MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     g.rpad = rp;
     g.z = z;
@@ -1016,8 +1016,8 @@ masq_status masq_linear_forward_w4g(const void* X, masq_dtype xt, int64_t ld_x, 
     uint16_t* l1t = reinterpret_cast<uint16_t*>(W8(ws, L.l1t));
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
-    MASQ_CK(launch_l1_fold(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t, st));
-    MASQ_CK(launch_pack_l2(static_cast<const uint16_t*>(L2), ld_l2, n_mod - 1, d_out, r, rp, l2t, st));
+    MASQ_CK(launch_cmc_pack(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t,
+                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, st));
     if (xt == MASQ_BF16) {
       MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st,
                            reinterpret_cast<float*>(W8(ws, L.zpart))));

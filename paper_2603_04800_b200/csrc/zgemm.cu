@@ -422,6 +422,83 @@ size_t zgemm_part_bytes(int64_t T, int64_t d, int n_mod, int rpad) {
   return sizeof(float) * (size_t)sp * ceil_div(T, 128) * 128 * (n_mod - 1) * rpad;
 }
 
+// the CMC factor packing of a forward call in one launch: blocks [0, g1) fold L1 as l1_fold_kernel,
+// blocks [g1, ...) transpose L2^m [r x n] into L2t rows m*n + j, columns k and rpad + k (the
+// [L2^T ; L2^T] operand of the GEMM's CMC k-blocks).  Both read only the factors, not X.
+__global__ void cmc_pack_kernel(const uint16_t* __restrict__ L1, const float* __restrict__ s_f, int64_t d, int r,
+                                int rpad, int n_nt, uint16_t* __restrict__ L1s, int g1x, int g1y,
+                                const uint16_t* __restrict__ L2, int64_t ld_l2, int64_t n, uint16_t* __restrict__ L2t,
+                                int g2x, int g2y) {
+  __shared__ float t[32][33];
+  const int g1 = g1x * g1y * n_nt;
+  int b = blockIdx.x;
+  if (b < g1) {
+    const int mb = b / (g1x * g1y);
+    b -= mb * g1x * g1y;
+    const int64_t i0 = (int64_t)(b % g1x) * 32;
+    const int k0 = (b / g1x) * 32;
+    const float* sm = s_f + (int64_t)(mb + 1) * d;
+    const uint16_t* src = L1 + (int64_t)mb * d * r;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const int64_t i = i0 + y;
+      const int k = k0 + threadIdx.x;
+      float v = 0.f;
+      if (i < d && k < r) v = __fmul_rn(__uint_as_float((uint32_t)src[i * r + k] << 16), __fdiv_rn(1.0f, sm[i]));
+      t[y][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const int k = k0 + y;
+      const int64_t i = i0 + threadIdx.x;
+      if (k < rpad && i < d) {
+        const float v = t[threadIdx.x][y];
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        const __nv_bfloat16 l = __float2bfloat16_rn(__fsub_rn(v, __bfloat162float(h)));
+        const int64_t row = (int64_t)mb * rpad + k;
+        L1s[row * d + i] = __bfloat16_as_ushort(h);
+        L1s[((int64_t)n_nt * rpad + row) * d + i] = __bfloat16_as_ushort(l);
+      }
+    }
+    return;
+  }
+  b -= g1;
+  const int mb = b / (g2x * g2y);
+  b -= mb * g2x * g2y;
+  const int64_t c0 = (int64_t)(b % g2x) * 32, r0 = (int64_t)(b / g2x) * 32;   // columns j, rows k of L2^m
+  const uint16_t* ib = L2 + (int64_t)mb * r * ld_l2;
+  uint16_t* ob = L2t + (int64_t)mb * n * 2 * rpad;
+  uint16_t (*tt)[33] = reinterpret_cast<uint16_t(*)[33]>(&t[0][0]);
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t rr = r0 + k, c = c0 + threadIdx.x;
+    tt[k][threadIdx.x] = (rr < r && c < n) ? ib[rr * ld_l2 + c] : (uint16_t)0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + k, rr = r0 + threadIdx.x;
+    if (c < n && rr < r) {
+      const uint16_t v = tt[threadIdx.x][k];
+      ob[c * 2 * rpad + rr] = v;
+      ob[c * 2 * rpad + rr + rpad] = v;
+    }
+  }
+}
+
+cudaError_t launch_cmc_pack(const uint16_t* L1, const float* s_f, int64_t d, int r, int rpad, int n_nt, uint16_t* L1s,
+                            const uint16_t* L2, int64_t ld_l2, int64_t n, uint16_t* L2t, cudaStream_t st) {
+  if (r < rpad) {
+    cudaError_t e = cudaMemsetAsync(L1s, 0, sizeof(uint16_t) * 2 * (size_t)n_nt * rpad * d, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L2t, 0, sizeof(uint16_t) * n_nt * n * 2 * rpad, st);
+    if (e != cudaSuccess) return e;
+  }
+  const int g1x = (int)ceil_div(d, 32), g1y = (int)ceil_div(r, 32);
+  const int g2x = (int)ceil_div(n, 32), g2y = (int)ceil_div(r, 32);
+  const int64_t blocks = (int64_t)(g1x * g1y + g2x * g2y) * n_nt;
+  ProfScope ps_("cmc_pack", st);
+  cmc_pack_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(L1, s_f, d, r, rpad, n_nt, L1s, g1x, g1y, L2, ld_l2, n, L2t,
+                                                            g2x, g2y);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_l1_fold(const uint16_t* L1, const float* s_f, int64_t d, int r, int rpad, int n_nt,
                            uint16_t* L1s, cudaStream_t st) {
   if (r < rpad) {
