@@ -539,7 +539,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   gl.skip_m0 = 1;
   MASQ_CK(launch_gemm(gl, st));
   MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st,
-                             fpart, fwd_units * 2));
+                             fpart, fwd_units * 2, partials + tiles * epi, tiles * (16 - epi)));
   if (qw_text) MASQ_CK(cudaMemcpyAsync(qw_text, qw, (size_t)d_out * d, cudaMemcpyDeviceToDevice, st));
   if (dw_text) MASQ_CK(cudaMemcpyAsync(dw_text, dw, sizeof(float) * d_out, cudaMemcpyDeviceToDevice, st));
   return MASQ_OK;
@@ -664,7 +664,8 @@ masq_status loss_core(const void* X, masq_dtype xt, int64_t ld_x, const uint8_t*
   g.partials = partials;
   g.gsign = gsign;
   MASQ_CK(launch_gemm(g, st));
-  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st));
+  MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st,
+                             nullptr, 0, partials + tiles * epi, tiles * (16 - epi)));
   if (grad) {
     uint16_t* planes = reinterpret_cast<uint16_t*>(W8(ws, L.planes));
     double* gpart = reinterpret_cast<double*>(W8(ws, L.gpartial));

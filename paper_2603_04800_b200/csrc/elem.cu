@@ -1376,6 +1376,58 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
   }
 }
 
+// two-level form of loss_reduce_kernel for large unit counts: block b sums a fixed slice of the
+// units (and of the forward's text-loss partials) into bpart[b][m]; one thread then adds the
+// blocks in order — deterministic, and the partial loads spread over the SMs instead of one CTA
+__global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict__ partials, int64_t n_units,
+                                                        int num_n, int epi, const uint32_t* __restrict__ tile_mod,
+                                                        int n_mod, const double* __restrict__ extra, int64_t n_extra,
+                                                        int64_t per_u, int64_t per_e, double* __restrict__ bpart) {
+  __shared__ double red[kMaxMod][256];
+  double acc[kMaxMod];
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) acc[m] = 0.0;
+  const int64_t e0 = (int64_t)blockIdx.x * per_e, e1 = min(n_extra, e0 + per_e);
+#pragma unroll 4
+  for (int64_t u = e0 + threadIdx.x; u < e1; u += 256) acc[0] += extra[u];
+  const int64_t u0 = (int64_t)blockIdx.x * per_u, u1 = min(n_units, u0 + per_u);
+#pragma unroll 4
+  for (int64_t u = u0 + threadIdx.x; u < u1; u += 256) {
+    const uint32_t m = tile_mod[u / num_n];
+    if (m >= (uint32_t)n_mod) continue;
+    double a = 0.0;
+    for (int e = 0; e < epi; ++e) a += partials[u * epi + e];
+#pragma unroll
+    for (int mm = 0; mm < kMaxMod; ++mm)
+      if (mm == (int)m) acc[mm] += a;
+  }
+#pragma unroll
+  for (int m = 0; m < kMaxMod; ++m) red[m][threadIdx.x] = acc[m];
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int m = 0; m < n_mod; ++m) red[m][threadIdx.x] += red[m][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < kMaxMod) bpart[(int64_t)blockIdx.x * kMaxMod + threadIdx.x] = threadIdx.x < n_mod ? red[threadIdx.x][0] : 0.0;
+}
+
+__global__ void loss_blocks_kernel(const double* __restrict__ bpart, int nb, const int64_t* __restrict__ counts_in,
+                                   int n_mod, int64_t n, Lambda8 lam, double* __restrict__ sums,
+                                   int64_t* __restrict__ counts, double* __restrict__ loss) {
+  if (threadIdx.x != 0) return;
+  double L = 0.0;
+  for (int m = 0; m < n_mod; ++m) {
+    double sm = 0.0;
+    for (int b = 0; b < nb; ++b) sm += bpart[(int64_t)b * kMaxMod + m];
+    const int64_t c = counts_in[m];
+    sums[m] = sm;
+    counts[m] = c;
+    if (c > 0) L += (double)lam.v[m] * sm / ((double)c * (double)n);
+  }
+  loss[0] = L;
+}
+
 __global__ void loss_finalize_kernel(const double* sums, const int64_t* counts, Lambda8 lam, int n_mod, int64_t n,
                                      double* loss) {
   double L = 0.0;
@@ -1789,7 +1841,18 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
 cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
                                const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
                                double* sums, int64_t* counts, double* loss, cudaStream_t st, const double* extra,
-                               int64_t n_extra) {
+                               int64_t n_extra, double* scratch, int64_t scratch_cap) {
+  const int64_t items = n_units + n_extra;
+  int nb = (int)std::min<int64_t>(128, ceil_div(items, (int64_t)2048));
+  if (scratch && nb >= 2 && (int64_t)nb * kMaxMod <= scratch_cap) {
+    ProfScope ps2_("loss_reduce", st, 2);
+    const int64_t per_u = ceil_div(n_units, (int64_t)nb), per_e = ceil_div(std::max<int64_t>(n_extra, 1), (int64_t)nb);
+    loss_part_kernel<<<nb, 256, 0, st>>>(partials, n_units, num_n, epi, tile_mod, n_mod, extra, n_extra, per_u, per_e,
+                                         scratch);
+    loss_blocks_kernel<<<1, 32, 0, st>>>(scratch, nb, counts_in, n_mod, n, make_lambda(lambda_host, n_mod), sums,
+                                         counts, loss);
+    return cudaGetLastError();
+  }
   ProfScope ps_("loss_reduce", st);
   loss_reduce_kernel<<<1, 512, 0, st>>>(partials, n_units, num_n, epi, tile_mod, counts_in, n_mod, n,
                                          make_lambda(lambda_host, n_mod), sums, counts, loss, extra, n_extra);

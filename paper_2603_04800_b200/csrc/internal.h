@@ -124,7 +124,9 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
 cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
                                const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
                                double* sums, int64_t* counts, double* loss, cudaStream_t st,
-                               const double* extra = nullptr, int64_t n_extra = 0);
+                               const double* extra = nullptr, int64_t n_extra = 0,
+                               // free doubles after the partials (two-level reduction when large)
+                               double* scratch = nullptr, int64_t scratch_cap = 0);
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st);
 
