@@ -76,3 +76,39 @@ def test_streamk_concurrent_streams():
     m.check()
     for kind, o in outs:
         assert torch.equal(o, want if kind == "acc" else wref), kind
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_streamk_random_deep_k(seed):
+    """Seeded random deep-K problems (d >= 8192: the int8 GEMM's stream-K path; ragged T and n,
+    2-3 modalities, CMC rank 0 / 32 / 64): int32 accumulators of every row of the last 8 m-units
+    plus sampled rows bit-exact, Y <= 1e-3 per modality, X W <= 1e-4 per modality."""
+    g = np.random.Generator(np.random.PCG64(7000 + seed))
+    d = int(g.choice([8192, 12288, 16384]))
+    n = 32 * int(g.integers(8, 100))
+    T = int(g.integers(600, 5000))
+    cfg = "c2" if g.integers(0, 2) else "c3"
+    r = int(g.choice([0, 32, 64])) if cfg == "c3" else 0
+    c = synth.config_inputs(cfg, d=d, n=n, T=T, layer=10 + seed, r=r)
+    m = M()
+    T, n_mod, wb, ab = c["T"], c["n_mod"], c["wbits"], c["abits"]
+    Ro, co = O.calibrate_stats(c["X"], c["ids"], n_mod)
+    if np.any(co == 0):
+        pytest.skip("a modality without tokens at this T")
+    so = O.init_factors(Ro, co, c["W"])
+    qwo, dwo = O.quantize_weight(c["W"], so[0], wb)
+    X, ids = bf(c["X"]), tt(c["ids"])
+    rows = np.union1d(sample_rows(c["ids"], n_random=48), np.arange(max(0, T - 8 * 256), T, 3))
+    acc = m.linear_forward(X, ids, tt(so), tt(qwo), tt(dwo), wb, ab, acc_debug=True).cpu().numpy()
+    qxo, _ = O.quantize_activations(O.decode(c["X"])[rows], c["ids"][rows], so, ab)
+    assert np.array_equal(acc[rows].astype(np.int64), O.int_gemm(qxo, qwo)), (seed, d, n, T)
+    L1 = bf(c["L1"]) if r else None
+    L2 = bf(c["L2"]) if r else None
+    Y = m.linear_forward(X, ids, tt(so), tt(qwo), tt(dwo), wb, ab, L1, L2).cpu().numpy()
+    m.check()
+    Yo = O.linear_forward(c["X"], c["ids"], so, qwo, dwo, ab, list(c["L1"]) if r else None,
+                          list(c["L2"]) if r else None, rows=rows)
+    assert max(per_modality_err(Y[rows], Yo, c["ids"][rows]).values()) <= 1e-3
+    Yr = m.reference_output(X, bf(c["W"])).cpu().numpy()
+    Yro = O.decode(c["X"])[rows].astype(np.float64) @ O.decode(c["W"]).astype(np.float64)
+    assert max(per_modality_err(Yr[rows], Yro, c["ids"][rows]).values()) <= 1e-4
