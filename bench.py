@@ -829,6 +829,29 @@ def main():
     ms_step = ms_total / args.steps
     value = world * T * args.steps / (ms_total / 1e3)
 
+    # ------------------------------------------------------------------ unprofiled (1 stream)
+    # The same K steps again with the library's per-kernel event pairs off: back-to-back launches
+    # of one stream, where a kernel launched with programmatic stream serialization (MASQ_PDL)
+    # runs its prologue while its predecessor drains (an event record between two kernels
+    # serialises them, so the profiled region above cannot show that overlap).
+    unprofiled = None
+    if args.streams == 1:
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        u0.record()
+        for _ in range(args.steps):
+            step()
+        u1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_u = max_over_ranks(u0.elapsed_time(u1))
+        unprofiled = {"streams": 1, "ms_per_step": ms_u / args.steps,
+                      "value": world * T * args.steps / (ms_u / 1e3), "unit": "tokens/s",
+                      "pdl": os.environ.get("MASQ_PDL", "1") != "0",
+                      "note": "same step, same stream, library profiler events off; timed after the main region"}
+
     # ------------------------------------------------------------------ overlapped (2 streams)
     # The same step with the linears on 2 CUDA streams (one linear's HBM-bound kernels beside
     # another's GEMM), timed separately so the per-kernel CUDA-event durations above stay clean.
@@ -1102,6 +1125,7 @@ def main():
         "cuda_graph": use_graph,
         "clocks": clocks,
         "e2e": e2e,
+        "unprofiled": unprofiled,
         "overlapped": overlapped,
         "cpu_baseline": cpu,
         "losses": loss_main,

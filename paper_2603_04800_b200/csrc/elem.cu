@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(128) stats_kernel(const XT* __restrict__ X, in
                                                     int rows_per_strip, float* __restrict__ R,
                                                     unsigned long long* __restrict__ count,
                                                     uint32_t* __restrict__ status) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   constexpr int V = Vec<XT>::N;
   constexpr int U = MASQ_STATS_U;
   constexpr int CH = 128 * V;               // channels per CTA
@@ -263,7 +265,7 @@ cudaError_t stats_dispatch(const XT* X, int64_t ld_x, const uint8_t* ids, int64_
 #define MASQ_STATS_CASE(NM)                                                       \
   case NM: {                                                                      \
     ProfScope ps_("stats", st);                                                   \
-    stats_kernel<XT, NM><<<grid, 128, 0, st>>>(X, ld_x, ids, T, d, rows, R, c, status); \
+    MASQ_LAUNCH(launch_k(stats_kernel<XT, NM>, dim3(grid), dim3(128), 0, st, X, ld_x, ids, T, d, rows, R, c, status)); \
   } break;
     MASQ_STATS_CASE(1) MASQ_STATS_CASE(2) MASQ_STATS_CASE(3) MASQ_STATS_CASE(4)
     MASQ_STATS_CASE(5) MASQ_STATS_CASE(6) MASQ_STATS_CASE(7) MASQ_STATS_CASE(8)
@@ -279,6 +281,8 @@ __global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ R, 
                                                    const WT* __restrict__ W, int64_t d, int64_t n, int n_mod,
                                                    float* __restrict__ s, float* __restrict__ wmax_out,
                                                    uint32_t* __restrict__ status) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   constexpr int V = Vec<WT>::N;
   const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -323,6 +327,8 @@ template <typename WT, int NS>
 __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, const float* __restrict__ s,
                                                       int64_t d, int64_t n, int rows_per_strip,
                                                       uint32_t* __restrict__ amax) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   constexpr int V = Vec<WT>::N;
   constexpr int U = MASQ_WCOLMAX_U;
   __shared__ float ss[NS][256];                       // factors of the current 256-row sub-strip
@@ -389,6 +395,8 @@ __global__ void __launch_bounds__(256) wcolmax_kernel(const WT* __restrict__ W, 
 // column panel [c0, c0 + ncols) of every set k (rows k * ss + j of amax / dw / rcp)
 __global__ void wscale_panel_kernel(const uint32_t* __restrict__ amax, float* __restrict__ dw, float* __restrict__ rcp,
                                     int64_t ncols, int64_t ss, float qmaxf) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= ncols) return;
   const int64_t idx = (int64_t)blockIdx.y * ss + j;
@@ -399,6 +407,8 @@ __global__ void wscale_panel_kernel(const uint32_t* __restrict__ amax, float* __
 
 __global__ void wscale_kernel(const uint32_t* __restrict__ amax, float* __restrict__ dw, float* __restrict__ rcp,
                               int64_t count, float qmaxf) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= count) return;
   const float dv = fmaxf(__fdiv_rn(__uint_as_float(amax[j]), qmaxf), kFloor);
@@ -500,6 +510,8 @@ __global__ void __launch_bounds__(256, MASQ_WQ_MINB) wquant_kernel(const WT* __r
                                                      int64_t d, int64_t n, int qmin, int qmax,
                                                      const float* __restrict__ rcp, int8_t* __restrict__ qw,
                                                      const float* __restrict__ dw) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   constexpr int V = Vec<WT>::N;                 // columns per load (8 bf16 / 4 f32)
   constexpr int LPT = CPT / V;                  // loads per row per thread
   constexpr int JT = 8 * CPT;                   // tile columns
@@ -544,6 +556,8 @@ __global__ void __launch_bounds__(256, 2) wquant_tma_kernel(const __grid_constan
                                                             int qmin, int qmax, const float* __restrict__ rcp,
                                                             int8_t* __restrict__ qw, const float* __restrict__ dw,
                                                             int64_t tiles_j, int64_t ntiles, int64_t ss) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   constexpr int CPT = 16;
   extern __shared__ __align__(128) uint8_t wsm[];
   uint8_t* ring = wsm;
@@ -613,6 +627,8 @@ __global__ void __launch_bounds__(256, NS <= 2 ? 2 : 1) wcolmax_tma_kernel(const
                                                              const float* __restrict__ s, int64_t d, int64_t n,
                                                              int64_t tiles_j, int64_t tiles_i, int rs,
                                                              int64_t units, uint32_t* __restrict__ amax, int64_t ss) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   constexpr int CPT = 16;
   extern __shared__ __align__(128) uint8_t wsm[];
   uint8_t* ring = wsm;
@@ -726,6 +742,8 @@ __global__ void __launch_bounds__(256, NS <= 2 ? 2 : 1) wcolmax_tma_kernel(const
 
 // =============================================================== A4 activation quantization
 __global__ void inv_kernel(const float* __restrict__ s, int64_t count, float* __restrict__ inv) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) inv[i] = __fdiv_rn(1.0f, s[i]);
 }
@@ -880,9 +898,11 @@ __global__ void __launch_bounds__(kAqMaxThreads) aquant_bf16_kernel(
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ uint64_t full[kAqMaxStages];
   __shared__ uint32_t s_red[2][32];
-  // a kernel launched after this one with programmatic stream serialization (the decode GEMM)
-  // may start now; it waits (griddepcontrol.wait) before reading this kernel's outputs
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // launch_k: wait for the previous kernel; a kernel launched after this one with programmatic
+  // stream serialization (the decode GEMM, the forward GEMMs) may start now; it waits
+  // (griddepcontrol.wait) before reading this kernel's outputs
+  sm100::pdl_wait();
+  sm100::pdl_trigger();
   constexpr float kMagic = 12582912.0f;               // 1.5 * 2^23
   constexpr float kLim = 0.5f - 0.000030517578125f;   // 1/2 - 2^-15 (see the proof above)
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;
@@ -1113,6 +1133,8 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
                                                      int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
                                                      int64_t n_tiles, int64_t* __restrict__ counts,
                                                      int32_t* __restrict__ ipos) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ int s_warp[kMaxMod][32];
   __shared__ int s_tot[kMaxMod], s_seg[kMaxMod + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1204,6 +1226,8 @@ __device__ __forceinline__ void route_load8(const uint8_t* __restrict__ ids, int
 
 __global__ void __launch_bounds__(256) route_count_kernel(const uint8_t* __restrict__ ids, int64_t T,
                                                           int32_t* __restrict__ bcnt) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ int s_w[8][kMaxMod];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int m8[8];
@@ -1230,6 +1254,8 @@ __global__ void __launch_bounds__(256) route_scatter_kernel(const uint8_t* __res
                                                             int32_t* __restrict__ perm, uint32_t* __restrict__ tile_mod,
                                                             int64_t n_tiles, int64_t* __restrict__ counts,
                                                             int32_t* __restrict__ ipos) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ int s_tot[kMaxMod], s_off[kMaxMod], s_seg[kMaxMod + 1];
   __shared__ int s_w[8][kMaxMod];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1339,6 +1365,8 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
                                                            int64_t n, Lambda8 lam, double* __restrict__ sums,
                                                            int64_t* __restrict__ counts, double* __restrict__ loss,
                                                            const double* __restrict__ extra, int64_t n_extra) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ double red[kMaxMod][512];
   double acc[kMaxMod];
 #pragma unroll
@@ -1383,6 +1411,8 @@ __global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict
                                                         int num_n, int epi, const uint32_t* __restrict__ tile_mod,
                                                         int n_mod, const double* __restrict__ extra, int64_t n_extra,
                                                         int64_t per_u, int64_t per_e, double* __restrict__ bpart) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ double red[kMaxMod][256];
   double acc[kMaxMod];
 #pragma unroll
@@ -1415,6 +1445,8 @@ __global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict
 __global__ void loss_blocks_kernel(const double* __restrict__ bpart, int nb, const int64_t* __restrict__ counts_in,
                                    int n_mod, int64_t n, Lambda8 lam, double* __restrict__ sums,
                                    int64_t* __restrict__ counts, double* __restrict__ loss) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   if (threadIdx.x != 0) return;
   double L = 0.0;
   for (int m = 0; m < n_mod; ++m) {
@@ -1430,6 +1462,8 @@ __global__ void loss_blocks_kernel(const double* __restrict__ bpart, int nb, con
 
 __global__ void loss_finalize_kernel(const double* sums, const int64_t* counts, Lambda8 lam, int n_mod, int64_t n,
                                      double* loss) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   double L = 0.0;
   for (int m = 0; m < n_mod; ++m)
     if (counts[m] > 0) L += (double)lam.v[m] * sums[m] / ((double)counts[m] * (double)n);
@@ -1458,9 +1492,9 @@ cudaError_t launch_init(const float* R, const int64_t* count, const void* W, mas
   const int grid = (int)ceil_div(d, 8);
   ProfScope ps_("init", st);
   if (wt == MASQ_BF16)
-    init_kernel<<<grid, 256, 0, st>>>(R, count, static_cast<const __nv_bfloat16*>(W), d, n, n_mod, s, wmax, status);
+    MASQ_LAUNCH(launch_k(init_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, R, count, static_cast<const __nv_bfloat16*>(W), d, n, n_mod, s, wmax, status));
   else
-    init_kernel<<<grid, 256, 0, st>>>(R, count, static_cast<const float*>(W), d, n, n_mod, s, wmax, status);
+    MASQ_LAUNCH(launch_k(init_kernel<float>, dim3(grid), dim3(256), 0, st, R, count, static_cast<const float*>(W), d, n, n_mod, s, wmax, status));
   return cudaGetLastError();
 }
 
@@ -1509,18 +1543,18 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
           const int64_t units = tj * ceil_div(ti, rs);
           // 3 sets: one CTA per SM (the running maxima of 3 sets need the registers of two)
           const int64_t grid = std::min<int64_t>(units, (int64_t)num_sms() * (NS <= 2 ? 2 : 1));
-          wcolmax_tma_kernel<NS><<<(unsigned)grid, 256, smem_c, st>>>(tm, s, d, pc, tj, ti, rs, units, amax + c0, n);
+          MASQ_LAUNCH(launch_k(wcolmax_tma_kernel<NS>, dim3((unsigned)grid), dim3(256), smem_c, st, tm, s, d, pc, tj, ti, rs, units, amax + c0, n));
         }
         {
           ProfScope ps_("wscale", st);
-          wscale_panel_kernel<<<dim3((unsigned)ceil_div(pc, 256), NS), 256, 0, st>>>(amax + c0, dw + c0, rcp + c0, pc,
-                                                                                      n, (float)qmax);
+          MASQ_LAUNCH(launch_k(wscale_panel_kernel, dim3(dim3((unsigned)ceil_div(pc, 256), NS)), dim3(256), 0, st, amax + c0, dw + c0, rcp + c0, pc,
+                                                                                      n, (float)qmax));
         }
         {
           ProfScope ps_("wquant", st);
           const int64_t grid = std::min<int64_t>(tj * ti, (int64_t)num_sms() * 2);
-          wquant_tma_kernel<NS><<<(unsigned)grid, 256, kWqSmem, st>>>(tm, s, d, pc, qmin, qmax, rcp + c0, qw + c0 * d,
-                                                                       dw + c0, tj, tj * ti, n);
+          MASQ_LAUNCH(launch_k(wquant_tma_kernel<NS>, dim3((unsigned)grid), dim3(256), kWqSmem, st, tm, s, d, pc, qmin, qmax, rcp + c0, qw + c0 * d,
+                                                                       dw + c0, tj, tj * ti, n));
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -1530,9 +1564,9 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
   }
   {
     ProfScope ps_("wcolmax", st);
-    wcolmax_kernel<WT, NS><<<g1, 256, 0, st>>>(w, s, d, n, rows, amax);
+    MASQ_LAUNCH(launch_k(wcolmax_kernel<WT, NS>, dim3(g1), dim3(256), 0, st, w, s, d, n, rows, amax));
   }
-  { ProfScope ps_("wscale", st); wscale_kernel<<<(unsigned)ceil_div(NS * n, 256), 256, 0, st>>>(amax, dw, rcp, NS * n, (float)qmax); }
+  { ProfScope ps_("wscale", st); MASQ_LAUNCH(launch_k(wscale_kernel, dim3((unsigned)ceil_div(NS * n, 256)), dim3(256), 0, st, amax, dw, rcp, NS * n, (float)qmax)); }
   {
     ProfScope ps_("wquant", st);
     static const bool v1q = getenv("MASQ_WQUANT_V1") != nullptr;   // measurement switch
@@ -1544,12 +1578,12 @@ static cudaError_t wquant_sets(const WT* w, const float* s, int64_t d, int64_t n
         cudaError_t e = set_max_dyn_smem(reinterpret_cast<const void*>(wquant_tma_kernel<NS>), kWqSmem);
         if (e != cudaSuccess) return e;
         const int64_t grid = std::min<int64_t>(tj * ti, (int64_t)num_sms() * 2);
-        wquant_tma_kernel<NS><<<(unsigned)grid, 256, kWqSmem, st>>>(tm, s, d, n, qmin, qmax, rcp, qw, dw, tj,
-                                                                     tj * ti, n);
+        MASQ_LAUNCH(launch_k(wquant_tma_kernel<NS>, dim3((unsigned)grid), dim3(256), kWqSmem, st, tm, s, d, n, qmin, qmax, rcp, qw, dw, tj,
+                                                                     tj * ti, n));
         done = true;
       }
     }
-    if (!done) wquant_kernel<WT, NS, CPT><<<g2, 256, 0, st>>>(w, s, d, n, qmin, qmax, rcp, qw, dw);
+    if (!done) MASQ_LAUNCH(launch_k(wquant_kernel<WT, NS, CPT>, dim3(g2), dim3(256), 0, st, w, s, d, n, qmin, qmax, rcp, qw, dw));
   }
   return cudaGetLastError();
 }
@@ -1588,7 +1622,7 @@ cudaError_t launch_wquant(const void* W, masq_dtype wt, const float* s, int n_se
 
 cudaError_t launch_inv(const float* s, int64_t count, float* inv, cudaStream_t st) {
   ProfScope ps_("inv", st);
-  inv_kernel<<<(unsigned)ceil_div(count, 256), 256, 0, st>>>(s, count, inv);
+  MASQ_LAUNCH(launch_k(inv_kernel, dim3((unsigned)ceil_div(count, 256)), dim3(256), 0, st, s, count, inv));
   return cudaGetLastError();
 }
 
@@ -1657,9 +1691,9 @@ static cudaError_t aquant_bf16_launch(const __nv_bfloat16* X, int64_t ld_x, cons
   const int smem = (int)(S * rowb);
   const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(T_out, (int64_t)num_sms() * per_sm));
   const int64_t rows = ceil_div(T_out, ctas);
-  kern<<<(unsigned)ceil_div(T_out, rows), nthr, smem, st>>>(X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx,
+  MASQ_LAUNCH(launch_k(kern, dim3((unsigned)ceil_div(T_out, rows)), dim3(nthr), smem, st, X, ld_x, ids, d, n_mod, inv_s, qaf, qmin, qmax, qx, dx,
                                                             mask, status, perm, T_out, rows, S, qg, dg, ipos,
-                                                            s_raw);
+                                                            s_raw));
   return cudaGetLastError();
 }
 
@@ -1729,6 +1763,8 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
 __global__ void __launch_bounds__(256) pad_rows_kernel(const int32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ tile_mod, int64_t Tg, int64_t d,
                                                        int m_lo, int8_t* __restrict__ qg, float* __restrict__ dg) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= Tg || __ldg(perm + p) >= 0) return;
@@ -1769,7 +1805,7 @@ cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const
                                        inv_s ? nullptr : s_raw);
   if (e != cudaSuccess) return e;
   ProfScope ps_("pad_rows", st);
-  pad_rows_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(perm, tile_mod, Tg, d, 1, qg, dg);
+  MASQ_LAUNCH(launch_k(pad_rows_kernel, dim3((unsigned)ceil_div(Tg, 8)), dim3(256), 0, st, perm, tile_mod, Tg, d, 1, qg, dg));
   return cudaGetLastError();
 }
 
@@ -1777,6 +1813,8 @@ cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const
 __global__ void __launch_bounds__(256) gather_rows_kernel(const int8_t* __restrict__ qt, const float* __restrict__ dt,
                                                           const int32_t* __restrict__ perm, int64_t Tg, int64_t d,
                                                           int8_t* __restrict__ qg, float* __restrict__ dg) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= Tg) return;
@@ -1790,7 +1828,7 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const int8_t* __restri
 cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t* perm, int64_t Tg, int64_t d, int8_t* qg,
                                float* dg, cudaStream_t st) {
   ProfScope ps_("gather_rows", st);
-  gather_rows_kernel<<<(unsigned)ceil_div(Tg, 8), 256, 0, st>>>(qt, dt, perm, Tg, d, qg, dg);
+  MASQ_LAUNCH(launch_k(gather_rows_kernel, dim3((unsigned)ceil_div(Tg, 8)), dim3(256), 0, st, qt, dt, perm, Tg, d, qg, dg));
   return cudaGetLastError();
 }
 
@@ -1806,12 +1844,12 @@ cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm
     // right after the Tg perm entries (route_scratch_ints)
     int32_t* bcnt = perm + Tg;
     const int64_t nb = route_blocks(T);
-    route_count_kernel<<<(unsigned)nb, 256, 0, st>>>(ids, T, bcnt);
-    route_scatter_kernel<<<(unsigned)nb, 256, 0, st>>>(ids, T, n_mod, bcnt, (int)nb, perm, tile_mod, Tg / kUnitM,
-                                                        counts, ipos);
+    MASQ_LAUNCH(launch_k(route_count_kernel, dim3((unsigned)nb), dim3(256), 0, st, ids, T, bcnt));
+    MASQ_LAUNCH(launch_k(route_scatter_kernel, dim3((unsigned)nb), dim3(256), 0, st, ids, T, n_mod, bcnt, (int)nb, perm, tile_mod, Tg / kUnitM,
+                                                        counts, ipos));
     return cudaGetLastError();
   }
-  route_kernel<<<1, 1024, 0, st>>>(ids, T, n_mod, perm, tile_mod, Tg / kUnitM, counts, ipos);
+  MASQ_LAUNCH(launch_k(route_kernel, dim3(1), dim3(1024), 0, st, ids, T, n_mod, perm, tile_mod, Tg / kUnitM, counts, ipos));
   return cudaGetLastError();
 }
 
@@ -1847,22 +1885,22 @@ cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_
   if (scratch && nb >= 2 && (int64_t)nb * kMaxMod <= scratch_cap) {
     ProfScope ps2_("loss_reduce", st, 2);
     const int64_t per_u = ceil_div(n_units, (int64_t)nb), per_e = ceil_div(std::max<int64_t>(n_extra, 1), (int64_t)nb);
-    loss_part_kernel<<<nb, 256, 0, st>>>(partials, n_units, num_n, epi, tile_mod, n_mod, extra, n_extra, per_u, per_e,
-                                         scratch);
-    loss_blocks_kernel<<<1, 32, 0, st>>>(scratch, nb, counts_in, n_mod, n, make_lambda(lambda_host, n_mod), sums,
-                                         counts, loss);
+    MASQ_LAUNCH(launch_k(loss_part_kernel, dim3(nb), dim3(256), 0, st, partials, n_units, num_n, epi, tile_mod, n_mod, extra, n_extra, per_u, per_e,
+                                         scratch));
+    MASQ_LAUNCH(launch_k(loss_blocks_kernel, dim3(1), dim3(32), 0, st, scratch, nb, counts_in, n_mod, n, make_lambda(lambda_host, n_mod), sums,
+                                         counts, loss));
     return cudaGetLastError();
   }
   ProfScope ps_("loss_reduce", st);
-  loss_reduce_kernel<<<1, 512, 0, st>>>(partials, n_units, num_n, epi, tile_mod, counts_in, n_mod, n,
-                                         make_lambda(lambda_host, n_mod), sums, counts, loss, extra, n_extra);
+  MASQ_LAUNCH(launch_k(loss_reduce_kernel, dim3(1), dim3(512), 0, st, partials, n_units, num_n, epi, tile_mod, counts_in, n_mod, n,
+                                         make_lambda(lambda_host, n_mod), sums, counts, loss, extra, n_extra));
   return cudaGetLastError();
 }
 
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st) {
   ProfScope ps_("loss_finalize", st);
-  loss_finalize_kernel<<<1, 1, 0, st>>>(sums, counts, make_lambda(lambda_host, n_mod), n_mod, n, loss);
+  MASQ_LAUNCH(launch_k(loss_finalize_kernel, dim3(1), dim3(1), 0, st, sums, counts, make_lambda(lambda_host, n_mod), n_mod, n, loss));
   return cudaGetLastError();
 }
 

@@ -296,6 +296,8 @@ masq_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   cluster_sync();                       // barriers of all CTAs initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();                           // the previous kernel's outputs (launch_k) ...
+  pdl_trigger();                        // ... and this grid's TMEM held: the next kernel may start
 
   constexpr int KELEMS = (MODE == kModeRef || MODE == kModeAlpha) ? 64 : 128;
   constexpr bool kGrouped = MODE == kModeLoss || MODE == kModeAlpha || MODE == kModeAlphaI8;
@@ -830,8 +832,7 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   static const char* const kNames[6] = {"gemm_fwd", "gemm_acc", "gemm_loss", "gemm_ref", "gemm_alpha",
                                         "gemm_alpha_i8"};
   ProfScope ps_(kNames[MODE], st);
-  masq_gemm_kernel<MODE, CL><<<CL * clusters, THREADS, SMEM_ALLOC, st>>>(a, b, y, z, l2, p);
-  return cudaGetLastError();
+  return launch_k(masq_gemm_kernel<MODE, CL>, dim3(CL * clusters), dim3(THREADS), SMEM_ALLOC, st, a, b, y, z, l2, p);
 }
 
 // MASQ_GEMM_CL (measurement knob): 2 = one CTA pair per cluster, 4 = two pairs sharing the A tile
@@ -876,6 +877,14 @@ cudaError_t set_max_dyn_smem(const void* func, int bytes) {
   e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) done.push_back({func, dev, bytes});
   return e;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MASQ_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 int num_sms() {

@@ -2,6 +2,7 @@
 // units (elem.cu, gemm.cu, zgemm.cu).  Not part of the public ABI.
 #pragma once
 #include <algorithm>
+#include <utility>
 #include <cstddef>
 #include <cstdint>
 #include <cuda.h>
@@ -51,6 +52,33 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size): the attribute
 // is per device, so one host thread driving several GPUs must set it on each (gemm.cu)
 cudaError_t set_max_dyn_smem(const void* func, int bytes);
+
+// Kernel launch with programmatic stream serialization (MASQ_PDL, default on): the kernel may
+// become resident while the previous kernel of the stream drains, and runs its prologue (barrier
+// init, TMEM allocation, descriptor prefetch) there; every kernel launched this way executes
+// sm100::pdl_wait() in each thread before touching global memory, so stream order holds for all
+// data.  Kernels not launched this way serialise as usual.
+bool pdl_enabled();
+#define MASQ_LAUNCH(call)                      \
+  do {                                         \
+    const cudaError_t le_ = (call);            \
+    if (le_ != cudaSuccess) return le_;        \
+  } while (0)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- opt-in kernel timing (prof.cu)
 // RAII: records a cudaEvent pair around a kernel launch when masq_profile_enable(1) is active.

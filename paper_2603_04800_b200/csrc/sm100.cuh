@@ -310,6 +310,13 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// programmatic dependent launch (kernels launched by launch_k): wait until the previous kernel of
+// the stream has completed and its writes are visible (every thread, before its first global
+// access); let the next kernel of the stream start its own prologue (after this CTA holds all the
+// TMEM it will allocate, so a dependent can never take TMEM this grid still needs)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 

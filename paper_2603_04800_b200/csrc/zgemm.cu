@@ -42,6 +42,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
              int rpad, int per, int a_planes, uint32_t tmem_cols, int stages,
              const uint32_t* __restrict__ tile_mask, uint16_t* __restrict__ Z, float* __restrict__ zpart,
              int splits, int pair, int ksub) {
+  sm100::pdl_wait();     // launch_k: tile_mask / X of the previous kernels
   const int mt = blockIdx.x;
   const int m0 = 1 + blockIdx.y * per;
   const int m1 = min(m0 + per, n_mod);           // exclusive
@@ -99,6 +100,7 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  sm100::pdl_trigger();                          // this CTA's TMEM is held
   // split-K (small T): CTA z takes k-chunks [kc0, kc1) and writes an f32 partial; a combine kernel
   // adds the partials in split order
   const int nk_all = (d + 64 * ksub - 1) / (64 * ksub);
@@ -317,6 +319,8 @@ zgemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ C
 // L1s[p][(m-1)*rpad + k][i] = plane p of inv_s[m][i] * L1^m[i][k] (p = 0 hi, 1 lo); zero for k >= r
 __global__ void l1_fold_kernel(const uint16_t* __restrict__ L1, const float* __restrict__ s_f, int64_t d, int r,
                                int rpad, int n_nt, uint16_t* __restrict__ L1s) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ float t[32][33];
   const int mb = blockIdx.z;                    // non-text modality index (m - 1)
   const int64_t i0 = (int64_t)blockIdx.x * 32;
@@ -348,6 +352,8 @@ __global__ void l1_fold_kernel(const uint16_t* __restrict__ L1, const float* __r
 // f32 X -> bf16 hi / lo planes (exact split to ~2^-17)
 __global__ void split_f32_kernel(const float* __restrict__ X, int64_t ld_x, int64_t T, int64_t d,
                                  uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= T * d) return;
   const int64_t t = idx / d, i = idx - t * d;
@@ -362,6 +368,8 @@ __global__ void __launch_bounds__(256) zcombine_kernel(const float* __restrict__
                                                        const uint8_t* __restrict__ ids, int64_t T, int n_mod,
                                                        int rpad, const uint32_t* __restrict__ tile_mask,
                                                        uint16_t* __restrict__ Z) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   const int nnt = n_mod - 1;
   const int q4 = rpad / 4;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -429,6 +437,8 @@ __global__ void cmc_pack_kernel(const uint16_t* __restrict__ L1, const float* __
                                 int rpad, int n_nt, uint16_t* __restrict__ L1s, int g1x, int g1y,
                                 const uint16_t* __restrict__ L2, int64_t ld_l2, int64_t n, uint16_t* __restrict__ L2t,
                                 int g2x, int g2y) {
+  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
+  sm100::pdl_trigger();
   __shared__ float t[32][33];
   const int g1 = g1x * g1y * n_nt;
   int b = blockIdx.x;
@@ -494,8 +504,8 @@ cudaError_t launch_cmc_pack(const uint16_t* L1, const float* s_f, int64_t d, int
   const int g2x = (int)ceil_div(n, 32), g2y = (int)ceil_div(r, 32);
   const int64_t blocks = (int64_t)(g1x * g1y + g2x * g2y) * n_nt;
   ProfScope ps_("cmc_pack", st);
-  cmc_pack_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(L1, s_f, d, r, rpad, n_nt, L1s, g1x, g1y, L2, ld_l2, n, L2t,
-                                                            g2x, g2y);
+  MASQ_LAUNCH(launch_k(cmc_pack_kernel, dim3((unsigned)blocks), dim3(dim3(32, 8)), 0, st, L1, s_f, d, r, rpad, n_nt, L1s, g1x, g1y, L2, ld_l2, n, L2t,
+                                                            g2x, g2y));
   return cudaGetLastError();
 }
 
@@ -507,7 +517,7 @@ cudaError_t launch_l1_fold(const uint16_t* L1, const float* s_f, int64_t d, int 
   }
   dim3 grid((unsigned)ceil_div(d, 32), (unsigned)ceil_div(r, 32), n_nt), block(32, 8);
   ProfScope ps_("l1_fold", st);
-  l1_fold_kernel<<<grid, block, 0, st>>>(L1, s_f, d, r, rpad, n_nt, L1s);
+  MASQ_LAUNCH(launch_k(l1_fold_kernel, dim3(grid), dim3(block), 0, st, L1, s_f, d, r, rpad, n_nt, L1s));
   return cudaGetLastError();
 }
 
@@ -515,7 +525,7 @@ cudaError_t launch_split_f32(const float* X, int64_t ld_x, int64_t T, int64_t d,
                              cudaStream_t st) {
   const int64_t n = T * d;
   ProfScope ps_("split_f32", st);
-  split_f32_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(X, ld_x, T, d, hi, lo);
+  MASQ_LAUNCH(launch_k(split_f32_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, X, ld_x, T, d, hi, lo));
   return cudaGetLastError();
 }
 
@@ -580,19 +590,21 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
       cfg.blockDim = dim3(ZT);
       cfg.dynamicSmemBytes = (size_t)smem;
       cfg.stream = st;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = 1;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 2;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // as launch_k
+      at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
       e = cudaLaunchKernelEx(&cfg, zgemm_kernel, ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
                              stages, tile_mask, Z, (float*)nullptr, 2, 1, ksub);
       if (e != cudaSuccess) return e;
     } else {
-      zgemm_kernel<<<grid, ZT, smem, st>>>(ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
-                                           stages, tile_mask, Z, zpart, splits, 0, ksub);
+      MASQ_LAUNCH(launch_k(zgemm_kernel, dim3(grid), dim3(ZT), smem, st, ta0, ta1, tb, ids, (int)T, (int)d, n_mod, rpad, per, a_planes, cols,
+                                           stages, tile_mask, Z, zpart, splits, 0, ksub));
     }
   }
   if (splits > 1 && !pair) {
@@ -600,8 +612,8 @@ cudaError_t launch_zgemm(const uint16_t* A0, int64_t ld_a, const uint16_t* A1, c
     if (e != cudaSuccess) return e;
     const int64_t threads = T * n_nt * (rpad / 4);
     ProfScope ps_("zcombine", st);
-    zcombine_kernel<<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(zpart, splits, ceil_div(T, 128) * 128, ids, T,
-                                                                      n_mod, rpad, tile_mask, Z);
+    MASQ_LAUNCH(launch_k(zcombine_kernel, dim3((unsigned)ceil_div(threads, 256)), dim3(256), 0, st, zpart, splits, ceil_div(T, 128) * 128, ids, T,
+                                                                      n_mod, rpad, tile_mask, Z));
   }
   return cudaGetLastError();
 }
