@@ -362,7 +362,8 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
   uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
-  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, mask, status_of(ws), st));
+  // the CMC path's tile masks come from the factor packing below (no zeroing pass, no atomics)
+  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, nullptr, status_of(ws), st));
   if (dbg && dbg->qx) MASQ_CK(cudaMemcpyAsync(dbg->qx, qx, (size_t)T * d, cudaMemcpyDeviceToDevice, st));
   if (dbg && dbg->dx) MASQ_CK(cudaMemcpyAsync(dbg->dx, dx, sizeof(float) * T, cudaMemcpyDeviceToDevice, st));
   GemmArgs g{};
@@ -376,7 +377,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
   g.b_rows = d_out;
   g.dx = dx;
   g.dw = dw;
-  g.tile_mask = mask;
+  g.tile_mask = cmc ? mask : nullptr;
   g.n_mod = n_mod;
   g.out = out;
   g.ld_out = ld_out;
@@ -386,7 +387,7 @@ masq_status masq_linear_forward(const void* X, masq_dtype xt, int64_t ld_x, cons
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
     MASQ_CK(launch_cmc_pack(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t,
-                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, st));
+                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, mod_id, T, n_mod, mask, st));
     if (xt == MASQ_BF16) {
       MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     } else {
@@ -458,11 +459,11 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   MASQ_CK(launch_wquant(W, MASQ_BF16, s, n_mod, d, d_out, wbits, qw, dw, amax, st));
   // the loss GEMM below skips the text units, so only the non-text rows need the grouped copy;
   // the row kernel forms 1/s itself (no inverse-factor launch)
-  const cudaError_t qe = launch_aquant_dual(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, nullptr, abits, qt, dt, mask,
+  const cudaError_t qe = launch_aquant_dual(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, nullptr, abits, qt, dt, nullptr,
                                             status_of(ws), perm, tmod, ipos, Tg, qg, dg, st, s);
   if (qe == cudaErrorNotSupported) {
     MASQ_CK(launch_inv(s, (int64_t)n_mod * d, inv, st));
-    MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, mask, status_of(ws), st));
+    MASQ_CK(launch_aquant(X, MASQ_BF16, ld_x, mod_id, T, d, n_mod, inv, abits, qt, dt, nullptr, status_of(ws), st));
     MASQ_CK(launch_gather_rows(qt, dt, perm, Tg, d, qg, dg, st));
   } else {
     MASQ_CK(qe);
@@ -497,7 +498,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   g.b_rows = d_out;
   g.dx = dt;
   g.dw = dw;
-  g.tile_mask = mask;
+  g.tile_mask = cmc ? mask : nullptr;
   g.n_mod = n_mod;
   g.out = Y;
   g.ld_out = ld_y;
@@ -512,7 +513,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
     MASQ_CK(launch_cmc_pack(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t,
-                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, st));
+                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, mod_id, T, n_mod, mask, st));
     MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st, reinterpret_cast<float*>(W8(ws, L.zpart))));
     g.rpad = rp;
     g.z = z;
@@ -996,7 +997,8 @@ masq_status masq_linear_forward_w4g(const void* X, masq_dtype xt, int64_t ld_x, 
   int8_t* qx = reinterpret_cast<int8_t*>(W8(ws, L.qx));
   float* dx = reinterpret_cast<float*>(W8(ws, L.dx));
   uint32_t* mask = reinterpret_cast<uint32_t*>(W8(ws, L.mask));
-  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, mask, status_of(ws), st));
+  // the CMC path's tile masks come from the factor packing below (no zeroing pass, no atomics)
+  MASQ_CK(quantize_acts(X, xt, ld_x, mod_id, T, d, n_mod, s, inv, abits, qx, dx, nullptr, status_of(ws), st));
   if (dbg && dbg->qx) MASQ_CK(cudaMemcpyAsync(dbg->qx, qx, (size_t)T * d, cudaMemcpyDeviceToDevice, st));
   if (dbg && dbg->dx) MASQ_CK(cudaMemcpyAsync(dbg->dx, dx, sizeof(float) * T, cudaMemcpyDeviceToDevice, st));
   W4gArgs g{};
@@ -1007,7 +1009,7 @@ masq_status masq_linear_forward_w4g(const void* X, masq_dtype xt, int64_t ld_x, 
   g.dx = dx;
   g.packed = packed;
   g.scales = scales;
-  g.tile_mask = mask;
+  g.tile_mask = cmc ? mask : nullptr;
   g.n_mod = n_mod;
   g.out = out;
   g.ld_out = ld_out;
@@ -1018,7 +1020,7 @@ masq_status masq_linear_forward_w4g(const void* X, masq_dtype xt, int64_t ld_x, 
     uint16_t* l2t = reinterpret_cast<uint16_t*>(W8(ws, L.l2t));
     uint16_t* z = reinterpret_cast<uint16_t*>(W8(ws, L.z));
     MASQ_CK(launch_cmc_pack(static_cast<const uint16_t*>(L1), s, d, r, rp, n_mod - 1, l1t,
-                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, st));
+                            static_cast<const uint16_t*>(L2), ld_l2, d_out, l2t, mod_id, T, n_mod, mask, st));
     if (xt == MASQ_BF16) {
       MASQ_CK(launch_zgemm(static_cast<const uint16_t*>(X), ld_x, nullptr, mod_id, T, d, n_mod, l1t, rp, mask, z, st,
                            reinterpret_cast<float*>(W8(ws, L.zpart))));

@@ -341,9 +341,12 @@ cudaError_t launch_range_stats(const float* R, int n_mod, int64_t d, int dominan
 // ---------------------------------------------------------------- CMC first factor (zgemm.cu)
 // L1s planes: [2][(M-1)*rpad][d] bf16, plane 0 = hi, 1 = lo of diag(1/s^m) L1^m (transposed)
 // s: the factors [n_mod][d]; 1/s is formed in the kernel (IEEE division, as inv_kernel)
-// l1_fold + the L2 packing of launch_pack_l2 in one launch (the forward calls' CMC factor packing)
+// l1_fold + the L2 packing of launch_pack_l2 in one launch (the forward calls' CMC factor packing);
+// mask != nullptr: the same launch writes the per-128-row-tile modality bit sets of ids[0, T)
+// (instead of a zeroing pass + the activation quantizer's atomics)
 cudaError_t launch_cmc_pack(const uint16_t* L1, const float* s, int64_t d, int r, int rpad, int n_nt, uint16_t* L1s,
-                            const uint16_t* L2, int64_t ld_l2, int64_t n, uint16_t* L2t, cudaStream_t st);
+                            const uint16_t* L2, int64_t ld_l2, int64_t n, uint16_t* L2t, const uint8_t* ids, int64_t T,
+                            int n_mod, uint32_t* mask, cudaStream_t st);
 cudaError_t launch_l1_fold(const uint16_t* L1, const float* s, int64_t d, int r, int rpad, int n_nt,
                            uint16_t* L1s, cudaStream_t st);
 // f32 X -> bf16 hi / lo planes [T x d]

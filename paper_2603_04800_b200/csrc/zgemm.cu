@@ -436,12 +436,33 @@ size_t zgemm_part_bytes(int64_t T, int64_t d, int n_mod, int rpad) {
 __global__ void cmc_pack_kernel(const uint16_t* __restrict__ L1, const float* __restrict__ s_f, int64_t d, int r,
                                 int rpad, int n_nt, uint16_t* __restrict__ L1s, int g1x, int g1y,
                                 const uint16_t* __restrict__ L2, int64_t ld_l2, int64_t n, uint16_t* __restrict__ L2t,
-                                int g2x, int g2y) {
+                                int g2x, int g2y, const uint8_t* __restrict__ ids, int64_t T, int n_mod,
+                                uint32_t* __restrict__ mask) {
   sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
   sm100::pdl_trigger();
   __shared__ float t[32][33];
   const int g1 = g1x * g1y * n_nt;
+  const int g2 = g2x * g2y * n_nt;
   int b = blockIdx.x;
+  if (b >= g1 + g2) {
+    // the per-128-row-tile modality bit sets the CMC first factor and the GEMM's CMC k-blocks read
+    // (one warp per tile, written whole: no zeroing pass, no atomics); ids >= n_mod set no bit
+    // (the activation quantizer flags them)
+    const int64_t tile = (int64_t)(b - g1 - g2) * 8 + threadIdx.y;
+    if (tile * 128 >= T) return;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t row = tile * 128 + threadIdx.x * 4 + e;
+      if (row < T) {
+        const int m = (int)__ldg(ids + row);
+        if (m < n_mod) bits |= 1u << m;
+      }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (threadIdx.x == 0) mask[tile] = bits;
+    return;
+  }
   if (b < g1) {
     const int mb = b / (g1x * g1y);
     b -= mb * g1x * g1y;
@@ -494,7 +515,8 @@ __global__ void cmc_pack_kernel(const uint16_t* __restrict__ L1, const float* __
 }
 
 cudaError_t launch_cmc_pack(const uint16_t* L1, const float* s_f, int64_t d, int r, int rpad, int n_nt, uint16_t* L1s,
-                            const uint16_t* L2, int64_t ld_l2, int64_t n, uint16_t* L2t, cudaStream_t st) {
+                            const uint16_t* L2, int64_t ld_l2, int64_t n, uint16_t* L2t, const uint8_t* ids, int64_t T,
+                            int n_mod, uint32_t* mask, cudaStream_t st) {
   if (r < rpad) {
     cudaError_t e = cudaMemsetAsync(L1s, 0, sizeof(uint16_t) * 2 * (size_t)n_nt * rpad * d, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(L2t, 0, sizeof(uint16_t) * n_nt * n * 2 * rpad, st);
@@ -502,10 +524,11 @@ cudaError_t launch_cmc_pack(const uint16_t* L1, const float* s_f, int64_t d, int
   }
   const int g1x = (int)ceil_div(d, 32), g1y = (int)ceil_div(r, 32);
   const int g2x = (int)ceil_div(n, 32), g2y = (int)ceil_div(r, 32);
-  const int64_t blocks = (int64_t)(g1x * g1y + g2x * g2y) * n_nt;
+  const int64_t g3 = mask ? ceil_div(ceil_div(T, 128), 8) : 0;
+  const int64_t blocks = (int64_t)(g1x * g1y + g2x * g2y) * n_nt + g3;
   ProfScope ps_("cmc_pack", st);
-  MASQ_LAUNCH(launch_k(cmc_pack_kernel, dim3((unsigned)blocks), dim3(dim3(32, 8)), 0, st, L1, s_f, d, r, rpad, n_nt, L1s, g1x, g1y, L2, ld_l2, n, L2t,
-                                                            g2x, g2y));
+  MASQ_LAUNCH(launch_k(cmc_pack_kernel, dim3((unsigned)blocks), dim3(32, 8), 0, st, L1, s_f, d, r, rpad, n_nt, L1s, g1x,
+                       g1y, L2, ld_l2, n, L2t, g2x, g2y, ids, T, n_mod, mask));
   return cudaGetLastError();
 }
 
