@@ -520,7 +520,8 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
     g.l2t = l2t;
   }
   MASQ_CK(launch_gemm(g, st));
-  MASQ_CK(cudaMemsetAsync(partials, 0, sizeof(double) * tiles * epi, st));
+  // no zeroing of the loss partials: the loss GEMM writes both slots of every unit it runs, and
+  // the units it skips (text, skip_m0; padding) are skipped by the reduction too (m_lo = 1)
   GemmArgs gl{};
   gl.mode = kModeLoss;
   gl.T = Tg;
@@ -540,7 +541,7 @@ masq_status masq_calib_layer(const void* X, int64_t ld_x, const uint8_t* mod_id,
   gl.skip_m0 = 1;
   MASQ_CK(launch_gemm(gl, st));
   MASQ_CK(launch_loss_reduce(partials, tiles, num_n, epi, tmod, cnt, n_mod, d_out, lambda, sums, counts, loss, st,
-                             fpart, fwd_units * 2, partials + tiles * epi, tiles * (16 - epi)));
+                             fpart, fwd_units * 2, partials + tiles * epi, tiles * (16 - epi), 1));
   if (qw_text) MASQ_CK(cudaMemcpyAsync(qw_text, qw, (size_t)d_out * d, cudaMemcpyDeviceToDevice, st));
   if (dw_text) MASQ_CK(cudaMemcpyAsync(dw_text, dw, sizeof(float) * d_out, cudaMemcpyDeviceToDevice, st));
   return MASQ_OK;

@@ -1299,6 +1299,19 @@ __global__ void __launch_bounds__(256) route_scatter_kernel(const uint8_t* __res
     if (lane == 31) s_w[warp][mm] = v;
   }
   __syncthreads();
+  {
+    // padding rows of the grouped layout (each segment's tail up to its 256-row multiple, and the
+    // rows past the last segment) -> -1; the grid covers [0, Tg) in contiguous slices, real rows
+    // are left to the scatter below (disjoint positions), so no zeroing pass is needed
+    const int64_t Tg = n_tiles * kUnitM;
+    const int64_t per = (Tg + gridDim.x - 1) / gridDim.x;
+    const int64_t p0 = (int64_t)b * per, p1 = p0 + per < Tg ? p0 + per : Tg;
+    for (int64_t q = p0 + tid; q < p1; q += blockDim.x) {
+      bool pad = q >= s_seg[n_mod];
+      for (int m = 0; m < n_mod && !pad; ++m) pad = q >= s_seg[m] + s_tot[m] && q < s_seg[m + 1];
+      if (pad) perm[q] = -1;
+    }
+  }
   int pos[kMaxMod];
 #pragma unroll
   for (int mm = 0; mm < kMaxMod; ++mm) {
@@ -1364,7 +1377,7 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
                                                            const int64_t* __restrict__ counts_in, int n_mod,
                                                            int64_t n, Lambda8 lam, double* __restrict__ sums,
                                                            int64_t* __restrict__ counts, double* __restrict__ loss,
-                                                           const double* __restrict__ extra, int64_t n_extra) {
+                                                           const double* __restrict__ extra, int64_t n_extra, int m_lo) {
   sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
   sm100::pdl_trigger();
   __shared__ double red[kMaxMod][512];
@@ -1377,7 +1390,7 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
 #pragma unroll 8
   for (int64_t u = threadIdx.x; u < n_units; u += 512) {         // fixed assignment -> deterministic
     const uint32_t m = tile_mod[u / num_n];
-    if (m >= (uint32_t)n_mod) continue;
+    if (m >= (uint32_t)n_mod || (int)m < m_lo) continue;     // padding units; m_lo: units never written
     double a = 0.0;
     for (int e = 0; e < epi; ++e) a += partials[u * epi + e];
 #pragma unroll
@@ -1410,7 +1423,8 @@ __global__ void __launch_bounds__(512) loss_reduce_kernel(const double* __restri
 __global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict__ partials, int64_t n_units,
                                                         int num_n, int epi, const uint32_t* __restrict__ tile_mod,
                                                         int n_mod, const double* __restrict__ extra, int64_t n_extra,
-                                                        int64_t per_u, int64_t per_e, double* __restrict__ bpart) {
+                                                        int64_t per_u, int64_t per_e, double* __restrict__ bpart,
+                                                        int m_lo) {
   sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
   sm100::pdl_trigger();
   __shared__ double red[kMaxMod][256];
@@ -1424,7 +1438,7 @@ __global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict
 #pragma unroll 4
   for (int64_t u = u0 + threadIdx.x; u < u1; u += 256) {
     const uint32_t m = tile_mod[u / num_n];
-    if (m >= (uint32_t)n_mod) continue;
+    if (m >= (uint32_t)n_mod || (int)m < m_lo) continue;     // padding units; m_lo: units never written
     double a = 0.0;
     for (int e = 0; e < epi; ++e) a += partials[u * epi + e];
 #pragma unroll
@@ -1835,9 +1849,11 @@ cudaError_t launch_gather_rows(const int8_t* qt, const float* dt, const int32_t*
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
                          int64_t* counts, cudaStream_t st, int32_t* ipos) {
   const int64_t Tg = grouped_rows(T, n_mod);
-  cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
-  if (e != cudaSuccess) return e;
   const bool v1 = getenv("MASQ_ROUTE_V1") != nullptr;
+  if (v1) {                                            // the multi-CTA scatter writes the padding itself
+    cudaError_t e = cudaMemsetAsync(perm, 0xFF, sizeof(int32_t) * Tg, st);
+    if (e != cudaSuccess) return e;
+  }
   ProfScope ps_("route", st, v1 ? 1 : 2);
   if (!v1) {
     // two passes over token chunks (per-chunk counts, then scan + scatter); the chunk counts live
@@ -1879,21 +1895,21 @@ cudaError_t launch_transpose_bf16(const uint16_t* W, int64_t d, int64_t n, uint1
 cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_n, int epi, const uint32_t* tile_mod,
                                const int64_t* counts_in, int n_mod, int64_t n, const float* lambda_host,
                                double* sums, int64_t* counts, double* loss, cudaStream_t st, const double* extra,
-                               int64_t n_extra, double* scratch, int64_t scratch_cap) {
+                               int64_t n_extra, double* scratch, int64_t scratch_cap, int m_lo) {
   const int64_t items = n_units + n_extra;
   int nb = (int)std::min<int64_t>(128, ceil_div(items, (int64_t)2048));
   if (scratch && nb >= 2 && (int64_t)nb * kMaxMod <= scratch_cap) {
     ProfScope ps2_("loss_reduce", st, 2);
     const int64_t per_u = ceil_div(n_units, (int64_t)nb), per_e = ceil_div(std::max<int64_t>(n_extra, 1), (int64_t)nb);
     MASQ_LAUNCH(launch_k(loss_part_kernel, dim3(nb), dim3(256), 0, st, partials, n_units, num_n, epi, tile_mod, n_mod, extra, n_extra, per_u, per_e,
-                                         scratch));
+                                         scratch, m_lo));
     MASQ_LAUNCH(launch_k(loss_blocks_kernel, dim3(1), dim3(32), 0, st, scratch, nb, counts_in, n_mod, n, make_lambda(lambda_host, n_mod), sums,
                                          counts, loss));
     return cudaGetLastError();
   }
   ProfScope ps_("loss_reduce", st);
   MASQ_LAUNCH(launch_k(loss_reduce_kernel, dim3(1), dim3(512), 0, st, partials, n_units, num_n, epi, tile_mod, counts_in, n_mod, n,
-                                         make_lambda(lambda_host, n_mod), sums, counts, loss, extra, n_extra));
+                                         make_lambda(lambda_host, n_mod), sums, counts, loss, extra, n_extra, m_lo));
   return cudaGetLastError();
 }
 

@@ -154,7 +154,9 @@ cudaError_t launch_loss_reduce(const double* partials, int64_t n_units, int num_
                                double* sums, int64_t* counts, double* loss, cudaStream_t st,
                                const double* extra = nullptr, int64_t n_extra = 0,
                                // free doubles after the partials (two-level reduction when large)
-                               double* scratch = nullptr, int64_t scratch_cap = 0);
+                               double* scratch = nullptr, int64_t scratch_cap = 0,
+                               // units of modality < m_lo are skipped (their partials never written)
+                               int m_lo = 0);
 cudaError_t launch_loss_finalize(const double* sums, const int64_t* counts, const float* lambda_host, int n_mod,
                                  int64_t n, double* loss, cudaStream_t st);
 
