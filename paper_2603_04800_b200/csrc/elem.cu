@@ -1773,22 +1773,6 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
   return cudaGetLastError();
 }
 
-// padding rows of the grouped copy (perm < 0): zero codes and scale, rows of modality >= m_lo only
-__global__ void __launch_bounds__(256) pad_rows_kernel(const int32_t* __restrict__ perm,
-                                                       const uint32_t* __restrict__ tile_mod, int64_t Tg, int64_t d,
-                                                       int m_lo, int8_t* __restrict__ qg, float* __restrict__ dg) {
-  sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
-  sm100::pdl_trigger();
-  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (p >= Tg || __ldg(perm + p) >= 0) return;
-  const uint32_t tm = __ldg(tile_mod + p / kUnitM);
-  if (tm == 0xFFFFFFFFu || (int)tm < m_lo) return;
-  uint4* out = reinterpret_cast<uint4*>(qg + p * d);
-  for (int64_t c = lane; c < d / 16; c += 32) out[c] = make_uint4(0, 0, 0, 0);
-  if (lane == 0) dg[p] = 0.f;
-}
-
 // A4 of one modality (modality 0, no ids) with 1/s formed in the kernel: the decode path's
 // quantizer in one launch; cudaErrorNotSupported when the TMA row kernel does not apply
 cudaError_t launch_aquant_direct(const void* X, masq_dtype xt, int64_t ld_x, int64_t T, int64_t d, const float* s,
@@ -1817,10 +1801,9 @@ cudaError_t launch_aquant_dual(const void* X, masq_dtype xt, int64_t ld_x, const
   cudaError_t e = aquant_bf16_dispatch(static_cast<const __nv_bfloat16*>(X), ld_x, ids, d, n_mod, inv_s, (float)qmax,
                                        qmin, qmax, qx, dx, mask, status, nullptr, T, st, qg, dg, ipos,
                                        inv_s ? nullptr : s_raw);
-  if (e != cudaSuccess) return e;
-  ProfScope ps_("pad_rows", st);
-  MASQ_LAUNCH(launch_k(pad_rows_kernel, dim3((unsigned)ceil_div(Tg, 8)), dim3(256), 0, st, perm, tile_mod, Tg, d, 1, qg, dg));
-  return cudaGetLastError();
+  // the grouped copy's padding rows (perm < 0) are left as they are: the loss GEMM's epilogue
+  // excludes them (no Yref row, no partial), and their int8 codes cannot fault the integer MMA
+  return e;
 }
 
 // grouped copy of token-order codes: row p of qg = row perm[p] of qt (zeros and dx 0 for padding)
