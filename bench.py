@@ -1052,7 +1052,10 @@ def main():
         kinfo[nm] = ent
     dom = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    # DRAM bytes per launch from an ncu capture of THIS workload's step (c3: ncu_traffic.json;
+    # others: ncu_traffic_<workload>.json), else null
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json" if args.workload == "c3"
+                      else f"ncu_traffic_{args.workload}.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get(dom)
