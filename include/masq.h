@@ -44,6 +44,12 @@
  *    calibration tokens) set a sticky status word inside ws; masq_check()
  *    synchronizes the stream and returns/clears it.  CUDA launch errors ->
  *    MASQ_ERR_CUDA.  Nothing throws across the ABI.
+ *  - Kernels are launched with programmatic stream serialization: a kernel
+ *    may become resident while the previous kernel on the stream drains, but
+ *    touches no global memory before that kernel has completed, so stream
+ *    order holds for every buffer (the caller's and ws).  Environment
+ *    MASQ_PDL=0 (read once per process) launches with plain serialization;
+ *    results are byte-identical either way.
  *  - Limits: d % 16 == 0, d_out % 32 == 0, T >= 0 (T == 0 is a no-op),
  *    bits in [2, 8] (A16 / W16 -> MASQ_ERR_UNSUPPORTED), r % 16 == 0 and
  *    r <= 256 (r == 0 disables CMC), all pointers 16-byte aligned.
