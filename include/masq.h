@@ -49,7 +49,10 @@
  *    touches no global memory before that kernel has completed, so stream
  *    order holds for every buffer (the caller's and ws).  Environment
  *    MASQ_PDL=0 (read once per process) launches with plain serialization;
- *    results are byte-identical either way.
+ *    results are byte-identical either way.  A kernel the caller launches
+ *    right after a call WITH programmatic stream serialization must execute
+ *    griddepcontrol.wait (cudaGridDependencySynchronize) before reading the
+ *    call's outputs, as for any programmatic dependent.
  *  - Limits: d % 16 == 0, d_out % 32 == 0, T >= 0 (T == 0 is a no-op),
  *    bits in [2, 8] (A16 / W16 -> MASQ_ERR_UNSUPPORTED), r % 16 == 0 and
  *    r <= 256 (r == 0 disables CMC), all pointers 16-byte aligned.
