@@ -423,6 +423,10 @@ const char* masq_status_string(masq_status s);
  * all, total_ms[i] is the bracketed time.  Returns -1 on a CUDA error.
  */
 int32_t masq_profile_enable(int32_t on);
+/* Restricts the recording to the kernels reported under `name` (e.g. "gemm_ref"); NULL or ""
+ * records every kernel again.  Every other launch then runs between unbracketed neighbours (no
+ * event record serialising it with them).  Returns 0. */
+int32_t masq_profile_only(const char* name);
 int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms, int64_t* launches);
 
 /* Library identification: "<version> sm_100a". */

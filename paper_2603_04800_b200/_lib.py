@@ -79,6 +79,7 @@ SIGNATURES = {
                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, c_void_p, c_void_p]),
     "masq_check": (c_int32, [c_void_p, c_void_p]),
     "masq_profile_enable": (c_int32, [c_int32]),
+    "masq_profile_only": (c_int32, [ctypes.c_char_p]),
     "masq_profile_collect": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p]),
     "masq_status_string": (ctypes.c_char_p, [c_int32]),
     "masq_version": (ctypes.c_char_p, []),

@@ -21,6 +21,7 @@ struct Rec {
 };
 std::mutex g_mu;
 bool g_on = false;
+std::string g_only;                     // non-empty: record only the scopes of this name
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 
@@ -49,7 +50,7 @@ void record(cudaEvent_t e, cudaStream_t st) {
 
 ProfScope::ProfScope(const char* name, cudaStream_t st, int launches) : name_(name), st_(st), launches_(launches) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (!g_on) return;
+  if (!g_on || (!g_only.empty() && g_only != name)) return;
   a_ = get_event();
   if (a_) record(static_cast<cudaEvent_t>(a_), st_);
 }
@@ -83,6 +84,12 @@ int32_t masq_profile_enable(int32_t on) {
     g_pool.push_back(e);
   }
   return prev;
+}
+
+int32_t masq_profile_only(const char* name) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_only = name ? name : "";
+  return 0;
 }
 
 int32_t masq_profile_collect(int32_t max_entries, char* names, double* total_ms, int64_t* launches) {
