@@ -27,6 +27,10 @@ def test_bench_single_gpu_contract():
     assert KEYS <= set(d), KEYS - set(d)
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
     assert d["roofline"]["bound"] in ("tensor", "hbm") and 0 < d["roofline"]["frac"] < 1.5
+    # the dominant kernel's durations come from the timed region itself (its launches are the only
+    # ones bracketed there); the per-kernel table from the breakdown pass right after
+    assert d["roofline"]["events"] == "timed region" and d["roofline"]["kernel"] in d["kernels"]
+    assert d["kernels_source"].startswith("breakdown pass") and 0 < d["kernel_ms_sum_over_step_ms"] <= 1.05
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
 
 
