@@ -170,7 +170,7 @@ WsLayout ws_layout(int32_t op, int64_t T, int64_t d, int64_t n, int32_t n_mod, i
   }
   // stream-K scratch of the forward / X.W GEMMs (after the op's own regions); only where the
   // GEMM can take the stream-K path (>= 64 k-blocks per unit: d >= 8192 int8, d >= 4096 bf16)
-  const bool sk_i8 = d >= 64 * 128, sk_bf = d >= 64 * 64;
+  const bool sk_i8 = d >= (int64_t)gemm_sk_min_kb() * 128, sk_bf = d >= (int64_t)gemm_sk_min_kb() * 64;
   if ((op == MASQ_OP_FORWARD && sk_i8) || (op == MASQ_OP_LAYER && sk_bf) || (op == MASQ_OP_REFERENCE && sk_bf) ||
       (self_ref && sk_bf && (op == MASQ_OP_LOSS || op == MASQ_OP_LOSS_GRAD))) {
     L.skpart = take(gemm_sk_part_bytes());

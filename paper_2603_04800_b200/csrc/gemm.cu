@@ -97,6 +97,17 @@ constexpr int kSkMaxSeg = 4;                         // stream-K: segments per r
 // more than the tail it removes at 28 (int8) / 56 (bf16) k-blocks and pays at 148 / 296 (measured,
 // tools/sk_ab.sh: d = 18944 forward -12% at 4k tokens, -4% at 16k; d = 3584 +4-15%)
 constexpr int kSkMinUnitKb = 64;
+}  // namespace
+// MASQ_SK_MINKB (measurement knob): the minimum k-blocks per unit for the stream-K remainder
+int gemm_sk_min_kb() {
+  static const int v = [] {
+    const char* e = getenv("MASQ_SK_MINKB");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : kSkMinUnitKb;
+  }();
+  return v;
+}
+namespace {
 constexpr int kRasterL2MB = 32;                      // L2 budget of a raster group's B panels
 constexpr int kRasterGroupMin = 16;                  // n-tiles per raster group, at least
 constexpr uint32_t IDESC_I8 = idesc_i8(UM, BN);
@@ -806,7 +817,7 @@ cudaError_t launch_mode(const CUtensorMap& a, const CUtensorMap& b, const CUtens
   int clusters = (int)std::min<int64_t>(p.n_items, avail);
   p.n_full = p.n_items;
   p.sk_R = p.sk_per = p.sk_pairs = 0;
-  if (sk_ok && CL == 2 && p.num_kb >= kSkMinUnitKb) {
+  if (sk_ok && CL == 2 && p.num_kb >= gemm_sk_min_kb()) {
     // stream-K remainder: when the units past the last full wave would leave more than a quarter
     // of the pairs idle, their k-blocks are spread over all pairs instead (segments of >= kSkMinKb)
     const int W = p.n_items / avail, R = p.n_items - W * avail;

@@ -59,6 +59,7 @@ cudaError_t set_max_dyn_smem(const void* func, int bytes);
 // sm100::pdl_wait() in each thread before touching global memory, so stream order holds for all
 // data.  Kernels not launched this way serialise as usual.
 bool pdl_enabled();
+int gemm_sk_min_kb();   // stream-K: minimum k-blocks per GEMM unit (MASQ_SK_MINKB, default 64)
 #define MASQ_LAUNCH(call)                      \
   do {                                         \
     const cudaError_t le_ = (call);            \
