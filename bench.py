@@ -862,10 +862,8 @@ def main():
         barrier()
 
     # ------------------------------------------------------------------ unprofiled (1 stream)
-    # The same K steps again with the library's per-kernel event pairs off: back-to-back launches
-    # of one stream, where a kernel launched with programmatic stream serialization (MASQ_PDL)
-    # runs its prologue while its predecessor drains (an event record between two kernels
-    # serialises them, so the profiled region above cannot show that overlap).
+    # The same K steps again with no event records at all (the timed region above still brackets
+    # the X W launches for the roofline; an event record between two kernels serialises them).
     unprofiled = None
     if args.streams == 1:
         torch.cuda.synchronize()
@@ -882,7 +880,9 @@ def main():
         unprofiled = {"streams": 1, "ms_per_step": ms_u / args.steps,
                       "value": world * T * args.steps / (ms_u / 1e3), "unit": "tokens/s",
                       "pdl": os.environ.get("MASQ_PDL", "1") != "0",
-                      "note": "same step, same stream, library profiler events off; timed after the main region"}
+                      "note": "same step, same stream, no event records at all (the timed region brackets only the "
+                              "X W launches); run after the breakdown pass, so the GPU's power / thermal state "
+                              "differs from the timed region's"}
 
     # ------------------------------------------------------------------ overlapped (2 streams)
     # The same step with the linears on 2 CUDA streams (one linear's HBM-bound kernels beside
