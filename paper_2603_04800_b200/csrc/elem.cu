@@ -1720,11 +1720,15 @@ static cudaError_t aquant_bf16_dispatch(const __nv_bfloat16* X, int64_t ld_x, co
                                         const int32_t* ipos = nullptr, const float* s_raw = nullptr) {
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (ld_x & 7) || (d & 7)) return cudaErrorNotSupported;  // 16-B rows
   const int64_t ch = d / 8;
-  static const int target = [] {
+  static const int env_cpl = [] {
     const char* e = getenv("MASQ_AQ_CPL");               // measurement knob (chunks per thread)
-    const int v = e ? atoi(e) : 8;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
+    const int v = e ? atoi(e) : 0;
+    return v <= 0 ? 0 : (v > 8 ? 8 : v);
   }();
+  // small T (<= ~55 rows per SM) is latency-bound per row: half the chunks per thread (twice the
+  // threads per row) shortens each row's chain (c5 1k-8k tokens at d = 3584: aquant -5..-15%,
+  // r02c_aqcpl_c5_ab.txt); at 16k tokens 4 and 8 measured even (r02c_aqcpl_step_ab.txt)
+  const int target = env_cpl > 0 ? env_cpl : (T_out <= 8192 ? 4 : 8);
   int64_t nthr = 32 * ceil_div(ch, (int64_t)target * 32);
   if (nthr > kAqMaxThreads) nthr = 32 * ceil_div(ch, 8 * 32);
   if (nthr > kAqMaxThreads) return cudaErrorNotSupported;
