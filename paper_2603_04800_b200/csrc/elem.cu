@@ -283,43 +283,58 @@ cudaError_t stats_dispatch(const XT* X, int64_t ld_x, const uint8_t* ids, int64_
 }
 
 // =============================================================== A2 init
-template <typename WT>
+template <typename WT, int WPR>
 __global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ R, const int64_t* __restrict__ count,
                                                    const WT* __restrict__ W, int64_t d, int64_t n, int n_mod,
                                                    float* __restrict__ s, float* __restrict__ wmax_out,
                                                    uint32_t* __restrict__ status) {
+  // WPR warps share a row (WPR = 1: warp per row, 8 rows per CTA; short d: WPR = 4, 2 rows per
+  // CTA, so even d = 2048 gives ~7 CTAs per SM instead of 1-2 uneven ones)
   sm100::pdl_wait();     // launch_k: the previous kernel's writes are visible
   sm100::pdl_trigger();
   constexpr int V = Vec<WT>::N;
-  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  __shared__ float s_wm[8];
+  const int warp = threadIdx.x >> 5, part = warp % WPR;
+  const int64_t i = (int64_t)blockIdx.x * (8 / WPR) + warp / WPR;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int m = 0; m < n_mod; ++m)
       if (count[m] == 0) atomicOr(status, kStEmptyModality);
   }
+  float wm = 0.f;
+  if (i < d) {
+    // 4 independent 16-byte loads in flight per lane (one per iteration left the warp latency-bound:
+    // 512 B in flight per row); the WPR warps of a row interleave 32 x V-column chunks
+    constexpr int64_t step = (int64_t)WPR * 32 * V;
+    float wq[4] = {0.f, 0.f, 0.f, 0.f};
+    int64_t j = ((int64_t)part * 32 + lane) * V;
+    for (; j + 3 * step < n; j += 4 * step) {
+      float f[4][V];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) Vec<WT>::load(W + i * n + j + u * step, f[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < V; ++e) wq[u] = fmaxf(wq[u], fabsf(f[u][e]));
+    }
+    for (; j < n; j += step) {
+      float f[V];
+      Vec<WT>::load(W + i * n + j, f);
+#pragma unroll
+      for (int e = 0; e < V; ++e) wq[0] = fmaxf(wq[0], fabsf(f[e]));
+    }
+    wm = fmaxf(fmaxf(wq[0], wq[1]), fmaxf(wq[2], wq[3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+  }
+  if (WPR > 1) {
+    if (lane == 0) s_wm[warp] = wm;
+    __syncthreads();
+    if (part != 0) return;
+#pragma unroll
+    for (int k = 1; k < WPR; ++k) wm = fmaxf(wm, s_wm[warp + k]);
+  }
   if (i >= d) return;
-  // 4 independent 16-byte loads in flight per lane (one per iteration left the warp latency-bound:
-  // 512 B in flight per row)
-  float wq[4] = {0.f, 0.f, 0.f, 0.f};
-  int64_t j = (int64_t)lane * V;
-  for (; j + 3 * 32 * V < n; j += 4 * 32 * V) {
-    float f[4][V];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) Vec<WT>::load(W + i * n + j + u * 32 * V, f[u]);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int e = 0; e < V; ++e) wq[u] = fmaxf(wq[u], fabsf(f[u][e]));
-  }
-  for (; j < n; j += 32 * V) {
-    float f[V];
-    Vec<WT>::load(W + i * n + j, f);
-#pragma unroll
-    for (int e = 0; e < V; ++e) wq[0] = fmaxf(wq[0], fabsf(f[e]));
-  }
-  float wm = fmaxf(fmaxf(wq[0], wq[1]), fmaxf(wq[2], wq[3]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
   if (lane < n_mod) {
     const float num = fmaxf(R[(int64_t)lane * d + i], kFloor);
     s[(int64_t)lane * d + i] = __fsqrt_rn(__fdiv_rn(num, fmaxf(wm, kFloor)));
@@ -1510,12 +1525,19 @@ cudaError_t launch_stats(const void* X, masq_dtype xt, int64_t ld_x, const uint8
 
 cudaError_t launch_init(const float* R, const int64_t* count, const void* W, masq_dtype wt, int64_t d, int64_t n,
                         int n_mod, float* s, float* wmax, uint32_t* status, cudaStream_t st) {
-  const int grid = (int)ceil_div(d, 8);
+  // fewer than ~4 warp-per-row CTAs per SM: 4 warps per row (2 rows per CTA)
+  const bool split = ceil_div(d, 8) < 4 * (int64_t)num_sms();
+  const int grid = (int)ceil_div(d, split ? 2 : 8);
   ProfScope ps_("init", st);
-  if (wt == MASQ_BF16)
-    MASQ_LAUNCH(launch_k(init_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, R, count, static_cast<const __nv_bfloat16*>(W), d, n, n_mod, s, wmax, status));
-  else
-    MASQ_LAUNCH(launch_k(init_kernel<float>, dim3(grid), dim3(256), 0, st, R, count, static_cast<const float*>(W), d, n, n_mod, s, wmax, status));
+  if (wt == MASQ_BF16) {
+    const auto* w = static_cast<const __nv_bfloat16*>(W);
+    if (split) MASQ_LAUNCH(launch_k(init_kernel<__nv_bfloat16, 4>, dim3(grid), dim3(256), 0, st, R, count, w, d, n, n_mod, s, wmax, status));
+    else MASQ_LAUNCH(launch_k(init_kernel<__nv_bfloat16, 1>, dim3(grid), dim3(256), 0, st, R, count, w, d, n, n_mod, s, wmax, status));
+  } else {
+    const auto* w = static_cast<const float*>(W);
+    if (split) MASQ_LAUNCH(launch_k(init_kernel<float, 4>, dim3(grid), dim3(256), 0, st, R, count, w, d, n, n_mod, s, wmax, status));
+    else MASQ_LAUNCH(launch_k(init_kernel<float, 1>, dim3(grid), dim3(256), 0, st, R, count, w, d, n, n_mod, s, wmax, status));
+  }
   return cudaGetLastError();
 }
 
