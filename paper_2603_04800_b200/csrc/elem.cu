@@ -1230,7 +1230,7 @@ __global__ void __launch_bounds__(1024) route_kernel(const uint8_t* __restrict__
   }
 }
 
-// ---- multi-CTA routing (same stable counting sort as route_kernel): chunk b of kRouteChunk tokens
+// ---- multi-CTA routing (same stable counting sort as route_kernel): chunk b of route_chunk(T) tokens
 // per CTA, 8 consecutive tokens per thread
 __device__ __forceinline__ void route_load8(const uint8_t* __restrict__ ids, int64_t T, int64_t t0, int (&m)[8]) {
   if (t0 + 8 <= T && (reinterpret_cast<uintptr_t>(ids + t0) & 7) == 0) {
@@ -1253,7 +1253,7 @@ __global__ void __launch_bounds__(256) route_count_kernel(const uint8_t* __restr
   __shared__ int s_w[8][kMaxMod];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int m8[8];
-  route_load8(ids, T, (int64_t)blockIdx.x * kRouteChunk + tid * 8, m8);
+  route_load8(ids, T, (int64_t)blockIdx.x * blockDim.x * 8 + tid * 8, m8);   // chunk = 8 tokens per thread
 #pragma unroll
   for (int mm = 0; mm < kMaxMod; ++mm) {
     int c = 0;
@@ -1266,7 +1266,7 @@ __global__ void __launch_bounds__(256) route_count_kernel(const uint8_t* __restr
   __syncthreads();
   if (tid < kMaxMod) {
     int c = 0;
-    for (int w = 0; w < 8; ++w) c += s_w[w][tid];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += s_w[w][tid];
     bcnt[(int64_t)blockIdx.x * kMaxMod + tid] = c;
   }
 }
@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(256) route_scatter_kernel(const uint8_t* __res
     }
     s_seg[n_mod] = acc;
   }
-  const int64_t t0 = (int64_t)b * kRouteChunk + tid * 8;
+  const int64_t t0 = (int64_t)b * blockDim.x * 8 + tid * 8;
   int m8[8];
   route_load8(ids, T, t0, m8);
   // exclusive prefix of this thread's per-modality counts within the chunk
@@ -1876,8 +1876,9 @@ cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm
     // right after the Tg perm entries (route_scratch_ints)
     int32_t* bcnt = perm + Tg;
     const int64_t nb = route_blocks(T);
-    MASQ_LAUNCH(launch_k(route_count_kernel, dim3((unsigned)nb), dim3(256), 0, st, ids, T, bcnt));
-    MASQ_LAUNCH(launch_k(route_scatter_kernel, dim3((unsigned)nb), dim3(256), 0, st, ids, T, n_mod, bcnt, (int)nb, perm, tile_mod, Tg / kUnitM,
+    const unsigned thr = (unsigned)(route_chunk(T) / 8);
+    MASQ_LAUNCH(launch_k(route_count_kernel, dim3((unsigned)nb), dim3(thr), 0, st, ids, T, bcnt));
+    MASQ_LAUNCH(launch_k(route_scatter_kernel, dim3((unsigned)nb), dim3(thr), 0, st, ids, T, n_mod, bcnt, (int)nb, perm, tile_mod, Tg / kUnitM,
                                                         counts, ipos));
     return cudaGetLastError();
   }

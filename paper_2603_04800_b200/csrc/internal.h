@@ -136,8 +136,10 @@ cudaError_t launch_aquant(const void* X, masq_dtype xt, int64_t ld_x, const uint
 inline int64_t grouped_rows(int64_t T, int n_mod) { return ceil_div(T, kUnitM) * kUnitM + (int64_t)n_mod * kUnitM; }
 // routing scratch: per-chunk modality counts stored after the Tg perm entries (callers size perm
 // as grouped_rows(T, n_mod) + route_scratch_ints(T))
-constexpr int kRouteChunk = 2048;
-inline int64_t route_blocks(int64_t T) { return std::max<int64_t>(1, ceil_div(T, kRouteChunk)); }
+// multi-CTA routing: 8 tokens per thread, 256 threads per CTA (2048 tokens); 64 threads (512
+// tokens) up to 8192 tokens, where the two passes are latency-bound on a handful of CTAs
+inline int64_t route_chunk(int64_t T) { return T <= 8192 ? 512 : 2048; }
+inline int64_t route_blocks(int64_t T) { return std::max<int64_t>(1, ceil_div(T, route_chunk(T))); }
 inline int64_t route_scratch_ints(int64_t T) { return route_blocks(T) * kMaxMod; }
 // counts (optional): per-modality token counts [n_mod] (int64)
 cudaError_t launch_route(const uint8_t* ids, int64_t T, int n_mod, int32_t* perm, uint32_t* tile_mod,
