@@ -477,6 +477,10 @@ def run_c4(args):
                             M.adam_step(th, grads[li], m1, m2, p_ + 1, 1e-2, s_out=svec[li])
             join()
 
+    # the clock sampler starts before the warm-up, so no idle gap precedes the timed region
+    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clk:
+        clk.start()
     for _ in range(max(args.warmup, 1)):
         sweep()
     for w in wss:
@@ -484,10 +488,6 @@ def run_c4(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
-    if clk:
-        clk.start()
-        time.sleep(0.3)
     lib().masq_profile_enable(1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if clk:
@@ -579,16 +579,15 @@ def run_c5(args):
     def fwd():
         M.linear_forward(X, ids, s, qw, dw, WBITS, ABITS, L1, L2s, Y=Y, ws=ws)
 
+    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clk:
+        clk.start()                      # before the warm-up: no idle gap before the timed region
     for _ in range(max(args.warmup, 1)):
         fwd()
     M.check(ws)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
-    if clk:
-        clk.start()
-        time.sleep(0.3)
     lib().masq_profile_enable(1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if clk:
@@ -760,6 +759,12 @@ def main():
         return P.max_over_ranks(x, device=dev)
 
     # ------------------------------------------------------------------ warm-up
+    # the clock sampler starts before the warm-up, so no idle gap (a sleep for the sampler thread
+    # had let the GPU's power budget recover) precedes the timed region: the timed steps follow
+    # the warm-up steps at the sustained, power-capped operating point
+    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 and not args.profile_only else None
+    if clk:
+        clk.start()
     for _ in range(max(args.warmup, 0)):
         step()
     for w in wss:
@@ -773,12 +778,8 @@ def main():
         return 0
 
     # ------------------------------------------------------------------ timed region (device)
-    clk = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     barrier()
     torch.cuda.synchronize()
-    if clk:
-        clk.start()
-        time.sleep(0.3)
     # --graph (N=1): the whole layer step (64 library launches + memsets) is captured once as a
     # CUDA graph and replayed; the library's profiler events are captured with it as external
     # event nodes, so every replay re-times the kernels and the breakdown below is that of the
