@@ -22,7 +22,7 @@ import torch
 
 import oracle as O
 import synth
-from test_gpu_parity import M, bf, sample_rows, tt
+from test_gpu_parity import M, bf, max_abs_norm, sample_rows, tt
 
 pytestmark = pytest.mark.gpu
 
@@ -221,3 +221,38 @@ def test_forward_misaligned_factor_rejected():
     with pytest.raises(m.MasqError) as e:
         m.linear_forward(bf(c["X"]), tt(c["ids"]), s_mis, tt(qwo), tt(dwo), 8, 8)
     assert e.value.status == 4
+
+
+@pytest.mark.parametrize("wbits", [8, 4])
+def test_forward_saturated_accumulators_deep_k(wbits):
+    """the deepest K of the bench (c3 down, d = 18944) with every code at its
+    extreme (|qx| = 127, |qw| = q_max), so |acc| reaches 18944 * 127 * q_max (3.06e8 at W8A8, near
+    2^28; 1.68e7 > 2^24 at W4A8, where the int32 -> f32 conversion of the epilogue rounds): int32
+    accumulators bit-exact (no wrap), Y <= 1e-3 of the f64 oracle.  Rows 0..127 are all +1 and
+    weight columns 0..63 all +1/2, 64..127 all -1/2 (the extreme sums of both signs), the rest
+    random signs; T = 300 and n = 288 leave ragged tails."""
+    T, d, n = 300, 18944, 288
+    g = np.random.Generator(np.random.PCG64(18944 + wbits))
+    xs = np.where(g.random((T, d)) < 0.5, -1.0, 1.0).astype(np.float32)
+    xs[:128] = 1.0
+    ws = np.where(g.random((d, n)) < 0.5, -0.5, 0.5).astype(np.float32)
+    ws[:, :64] = 0.5
+    ws[:, 64:128] = -0.5
+    to_bits = lambda a: (a.view(np.uint32) >> 16).astype(np.uint16)      # exact: +-1, +-1/2
+    Xb, Wb = to_bits(xs), to_bits(ws)
+    ids = np.zeros(T, np.uint8)
+    s = np.ones((1, d), np.float32)
+    m = M()
+    qwo, dwo = O.quantize_weight(Wb, s[0], wbits)
+    assert np.abs(qwo.astype(np.int64)).min() == 2 ** (wbits - 1) - 1
+    qw, dw = m.quantize_weight(bf(Wb), tt(s[0]), wbits)
+    assert np.array_equal(qw.cpu().numpy(), qwo) and np.array_equal(dw.cpu().numpy(), dwo)
+    acc = m.linear_forward(bf(Xb), tt(ids), tt(s), qw, dw, wbits, 8, acc_debug=True).cpu().numpy()
+    qxo, _ = O.quantize_activations(O.decode(Xb), ids, s, 8)
+    ref = O.int_gemm(qxo, qwo)
+    assert np.abs(ref).max() == d * 127 * (2 ** (wbits - 1) - 1)
+    assert np.array_equal(acc.astype(np.int64), ref)
+    Y = m.linear_forward(bf(Xb), tt(ids), tt(s), qw, dw, wbits, 8)
+    m.check()
+    Yo = O.linear_forward(Xb, ids, s, qwo, dwo, 8)
+    assert max_abs_norm(Y.cpu().numpy(), Yo) <= TOL_Y
